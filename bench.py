@@ -1,0 +1,390 @@
+#!/usr/bin/env python3
+"""bench.py — headline benchmark of the CSR SpMM aggregation hot path on B200.
+
+Workload (BASELINE.json configs[3], the configuration the metric is quoted on):
+ogbn-products-shaped power-law graph, N = 2,449,029 nodes, E = 61,859,140
+edges (Chung-Lu alpha = 0.5, ids permuted), F = 100 fp32 features, full-graph
+sum aggregation (the reference's spmm(e, x, nullopt, sum), message_passing.hpp:92).
+A "step" is one full-graph SpMM over the resident graph (the CSC and its plan
+are cached like the reference's EdgeIndex cache and built outside the timed
+region). Synthetic data (no network); X (980 MB) is larger than L2 (126 MB).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun): destination rows are nnz-partitioned across ranks, X is
+row-sharded and all-gathered over NCCL every step (the exchange a multi-layer
+model needs), then each rank aggregates its rows; time = max over ranks.
+`--impl reference` times the reference's own CPU spmm (oracle/_ref, compiled
+in place from /root/reference) on the host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GEdges/s CSR SpMM aggr (frac of HBM BW) + segment_matmul TFLOP/s @1/2/4/8 B200"
+N_NODES, N_EDGES, F = 2_449_029, 61_859_140, 100
+SEED = 0x67726170686D696C  # derive(..) base seed of SURVEY §8d ("graphmil")
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d["hbm_gbs"], d["bf16_tflops"], "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def spmm_bytes(n_dst, e, f, esz=4):
+    """Gather-model algorithmic bytes of one sum SpMM:
+    E*(F*s + 4 col) + N*(8 rowptr + F*s out)."""
+    return e * (f * esz + 4) + n_dst * (8 + f * esz)
+
+
+def make_graph(gm, L, n, e, f, device, stream):
+    src = torch.empty(e, dtype=torch.int64, device=device)
+    dst = torch.empty(e, dtype=torch.int64, device=device)
+    L.check(L.lib().gm_synth_edges(1, SEED, 0, e, n, n, src.data_ptr(), dst.data_ptr(), stream))
+    x = torch.empty(n, f, dtype=torch.float32, device=device)
+    L.check(L.lib().gm_synth_features(SEED, 0, n, f, 0, L.GM_F32, x.data_ptr(), stream))
+    g = gm.EdgeIndex(src, dst, n, n, device=device)
+    return g, x
+
+
+def bench_segment_matmul(gm, L, device):
+    """C3 (OGB-MAG) node-type segment_matmul, K = N = 128, bf16 in/out."""
+    ptr = [0, 736_389, 1_871_038, 1_879_778, 1_939_743]
+    x = torch.randn(ptr[-1], 128, device=device).to(torch.bfloat16)
+    w = (0.05 * torch.randn(4, 128, 128, device=device)).to(torch.bfloat16)
+    try:
+        for _ in range(3):
+            gm.segment_matmul(x, ptr, w)
+        torch.cuda.synchronize()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        reps = 20
+        ev[0].record()
+        for _ in range(reps):
+            gm.segment_matmul(x, ptr, w)
+        ev[1].record()
+        torch.cuda.synchronize()
+        ms = ev[0].elapsed_time(ev[1]) / reps
+    except Exception as exc:  # reported, never silently substituted
+        return {"error": str(exc)[:200]}
+    flops = 2.0 * ptr[-1] * 128 * 128
+    byts = 2.0 * ptr[-1] * 128 * 2 + 4 * 128 * 128 * 2
+    return {"shape": "sum_M=1939743,K=N=128,G=4,bf16", "ms": ms, "tflops": flops / ms / 1e9,
+            "achieved_gbs": byts / ms / 1e6, "bound": "hbm (AI 64 < ridge 251)"}
+
+
+def run_reference_arm(args):
+    """--impl reference: the reference's own CPU spmm<float> on this host."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle.oracle import Reference
+    from paper_2507_16991_b200 import _lib as L
+    if not Reference.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference)"}))
+        return
+    ref = Reference()
+    lib = L.lib()
+    src = np.zeros(N_EDGES, np.int64)
+    dst = np.zeros(N_EDGES, np.int64)
+    lib.gm_synth_edges_host(1, SEED, 0, N_EDGES, N_NODES, N_NODES, src.ctypes.data, dst.ctypes.data)
+    x = np.zeros((N_NODES, F), np.float32)
+    lib.gm_synth_features_host(SEED, 0, N_NODES, F, 0, L.GM_F32, x.ctypes.data)
+    threads = os.cpu_count() or 1
+    # bounded sample: the first 1/4 of destination rows, each step one spmm over it
+    rows = N_NODES // 4
+    secs, edges = ref.bench_spmm(src, dst, N_NODES, N_NODES, x, mean=False, threads=threads,
+                                 rows_limit=rows, warmup=args.warmup, repeat=args.steps)
+    val = edges / secs / 1e9
+    sample = f"dst rows [0,{rows}) of the products graph ({edges} edges), spmm<float> sum"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "GEdges/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "ogbn-products-shaped power-law, sum SpMM, F=100 fp32 (CPU reference)",
+                   "nodes": N_NODES, "edges": N_EDGES, "feats": F},
+        "cpu_baseline": {"value": val, "unit": "GEdges/s", "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": val, "unit": "GEdges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def cpu_baseline_line():
+    """The reference (oracle/_ref) on the host cores, bounded sample (~10 s)."""
+    from oracle.oracle import Reference
+    from paper_2507_16991_b200 import _lib as L
+    if not Reference.available():
+        return None
+    lib = L.lib()
+    src = np.zeros(N_EDGES, np.int64)
+    dst = np.zeros(N_EDGES, np.int64)
+    lib.gm_synth_edges_host(1, SEED, 0, N_EDGES, N_NODES, N_NODES, src.ctypes.data, dst.ctypes.data)
+    x = np.zeros((N_NODES, F), np.float32)
+    lib.gm_synth_features_host(SEED, 0, N_NODES, F, 0, L.GM_F32, x.ctypes.data)
+    threads = os.cpu_count() or 1
+    rows = N_NODES // 4
+    secs, edges = Reference().bench_spmm(src, dst, N_NODES, N_NODES, x, threads=threads, rows_limit=rows,
+                                         warmup=1, repeat=2)
+    return {"value": edges / secs / 1e9, "unit": "GEdges/s", "cores": threads, "kind": "reference",
+            "sample": f"dst rows [0,{rows}) ({edges} edges), reference spmm<float> sum, "
+                      f"{threads} threads over row ranges, mean of 2 after 1 warmup"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+
+    import paper_2507_16991_b200 as gm
+    from paper_2507_16991_b200 import _lib as L
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=device)
+    stream = torch.cuda.current_stream().cuda_stream
+    lib = L.lib()
+
+    g, x = make_graph(gm, L, N_NODES, N_EDGES, F, device, stream)
+    csc = g.to_csc()
+    torch.cuda.synchronize()
+
+    # ---- partition (N > 1): nnz-balanced dst rows, equal-row X shards ----------
+    rowptr_h = csc.rowptr.cpu().numpy()
+    cuts = np.zeros(world + 1, np.int64)
+    L.check(lib.gm_partition_rows_by_nnz(rowptr_h.ctypes.data_as(C.POINTER(C.c_int64)), N_NODES, world,
+                                         cuts.ctypes.data_as(C.POINTER(C.c_int64))))
+    r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
+    local_edges = int(rowptr_h[r1] - rowptr_h[r0])
+    local_csr = csc if world == 1 else csc.row_slice(r0, r1, local_edges)
+    out = torch.empty(N_NODES, F, dtype=torch.float32, device=device)
+    shard = -(-N_NODES // world)
+    x_full = x
+    if world > 1:
+        x_full = torch.zeros(shard * world, F, dtype=torch.float32, device=device)
+        x_full[:N_NODES].copy_(x)
+        x_shard = x_full[rank * shard:(rank + 1) * shard].clone()
+    plan = local_csr.plan()
+    cs = local_csr.c_struct()
+
+    def step():
+        if world > 1:
+            dist.all_gather_into_tensor(x_full, x_shard)
+        L.check(lib.gm_spmm(C.byref(cs), C.byref(plan), L.GM_F32, C.c_void_p(x_full.data_ptr()), F, None,
+                            None, L.GM_SUM, C.c_void_p(out[r0:].data_ptr()), None,
+                            C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t_all0 = torch.cuda.Event(enable_timing=True)
+        t_all1 = torch.cuda.Event(enable_timing=True)
+        t_all0.record()
+        for i in range(args.steps):
+            evs[i][0].record()
+            step()
+            evs[i][1].record()
+        t_all1.record()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+    per_step = [a.elapsed_time(b) for a, b in evs]
+    total_ms = t_all0.elapsed_time(t_all1)
+    if dist:
+        t = torch.tensor([total_ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms = total_ms / args.steps
+    value = N_EDGES / (ms * 1e-3) / 1e9
+
+    hbm, bf16_peak, peak_kind = peaks()
+    # roofline of the dominant launch (one gm_spmm call = light + concurrent hub kernel)
+    call_ms = statistics.mean(per_step) if world == 1 else None
+    roof = None
+    if world == 1:
+        b = spmm_bytes(N_NODES, N_EDGES, F)
+        ach = b / (call_ms * 1e-3) / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "spmm_traffic.json")
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get("dram_bytes_per_call")
+            except Exception:
+                traffic = None
+        roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "traffic": traffic, "peak_kind": peak_kind, "algorithmic_bytes_per_call": b,
+                "unit_of_launch": "one gm_spmm call (warp-window kernel + concurrent hub-row kernel)"}
+
+    # ---- e2e through the public C-ABI with host buffers (N = 1) -----------------
+    e2e = None
+    if world == 1:
+        xh = torch.empty(N_NODES, F, dtype=torch.float32).pin_memory()
+        oh = torch.empty(N_NODES, F, dtype=torch.float32).pin_memory()
+        xh.copy_(x.cpu())
+        xd = torch.empty_like(x)
+        e2e_steps = max(3, min(args.steps, 10))
+
+        def e2e_step():
+            xd.copy_(xh, non_blocking=True)
+            L.check(lib.gm_spmm(C.byref(cs), C.byref(plan), L.GM_F32, C.c_void_p(xd.data_ptr()), F, None,
+                                None, L.GM_SUM, C.c_void_p(out.data_ptr()), None,
+                                C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+            oh.copy_(out, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        a, bev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(e2e_steps):
+            e2e_step()
+        bev.record()
+        torch.cuda.synchronize()
+        ems = a.elapsed_time(bev) / e2e_steps
+        e2e = {"value": N_EDGES / (ems * 1e-3) / 1e9, "unit": "GEdges/s",
+               "h2d_bytes_per_step": N_NODES * F * 4, "d2h_bytes_per_step": N_NODES * F * 4,
+               "ms_per_step": ems}
+
+    secondary = None
+    if world == 1 and not args.no_secondary:
+        secondary = {"segment_matmul_C3": bench_segment_matmul(gm, L, device)}
+        # max + argmax SpMM on the same graph
+        mo = torch.empty(N_NODES, F, dtype=torch.float32, device=device)
+        ma = torch.empty(N_NODES, F, dtype=torch.int32, device=device)
+        for _ in range(2):
+            L.check(lib.gm_spmm(C.byref(cs), C.byref(plan), L.GM_F32, C.c_void_p(x.data_ptr()), F, None, None,
+                                L.GM_MAX, C.c_void_p(mo.data_ptr()), C.c_void_p(ma.data_ptr()), stream))
+        a, bev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(5):
+            L.check(lib.gm_spmm(C.byref(cs), C.byref(plan), L.GM_F32, C.c_void_p(x.data_ptr()), F, None, None,
+                                L.GM_MAX, C.c_void_p(mo.data_ptr()), C.c_void_p(ma.data_ptr()), stream))
+        bev.record()
+        torch.cuda.synchronize()
+        mms = a.elapsed_time(bev) / 5
+        mb = spmm_bytes(N_NODES, N_EDGES, F) + N_NODES * F * 4
+        secondary["max_argmax_spmm"] = {"ms": mms, "gedges_s": N_EDGES / mms / 1e6,
+                                        "frac_hbm": mb / mms / 1e6 / hbm}
+
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline_line()
+        except Exception as exc:
+            cpu = {"error": str(exc)[:200]}
+
+    launches_per_step = 1 + (1 if plan.num_heavy > 0 else 0)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GEdges/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": "ogbn-products-shaped power-law graph (configs[3]), full-graph sum SpMM",
+                       "nodes": N_NODES, "edges": N_EDGES, "feats": F, "graph": "Chung-Lu alpha=0.5",
+                       "parallelism": f"dst-row partition x{world}" + (" + NCCL all-gather of X" if world > 1 else ""),
+                       "l2": "inputs larger than L2 (X = 980 MB)", "heavy_rows": int(plan.num_heavy)},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk.summary(), "secondary": secondary,
+            "per_step_ms": {"min": min(per_step), "median": statistics.median(per_step), "max": max(per_step)},
+        }
+        print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

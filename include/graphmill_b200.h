@@ -1,0 +1,229 @@
+/*
+ * graphmill_b200.h — C-ABI of the B200-native message-passing hot path.
+ *
+ * Drop-in boundary for the reference engine `graphmill` (/root/reference/proj).
+ * Every entry point names the reference interface it replaces (file:line,
+ * relative to /root/reference/proj). Conventions:
+ *   - plain pointers and sizes only; array arguments are DEVICE pointers unless
+ *     the parameter name ends in `_host`;
+ *   - the caller owns every buffer (the library never allocates or frees caller
+ *     memory); scratch comes from caller-supplied workspace with a size query;
+ *   - every call is stream-ordered on `stream` (a cudaStream_t; NULL = legacy
+ *     default stream) and reentrant; no exceptions cross the ABI: a call returns
+ *     a gm_status and gm_last_error() holds a thread-local message shaped like
+ *     the reference's exception text (e.g. "EdgeIndex: src index 7 at position
+ *     3 outside [0, 5)", edge_index.cpp:19-25);
+ *   - indices on the device are int32 for col/perm/argmax (all configured
+ *     graphs have N, E < 2^31; checked) and int64 for rowptr, matching the
+ *     reference's int64 `Index` (tensor.hpp:23) at the boundary arrays keys/values.
+ */
+#ifndef GRAPHMILL_B200_H
+#define GRAPHMILL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GM_API __attribute__((visibility("default")))
+
+typedef void* gm_stream_t; /* cudaStream_t */
+
+typedef enum gm_status {
+  GM_OK = 0,
+  GM_ERR_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument */
+  GM_ERR_OUT_OF_RANGE = 2,     /* reference: std::out_of_range */
+  GM_ERR_CUDA = 3,
+  GM_ERR_UNSUPPORTED = 4,
+  GM_ERR_LOGIC = 5             /* reference: std::logic_error */
+} gm_status;
+
+typedef enum gm_dtype { GM_F32 = 0, GM_F64 = 1, GM_BF16 = 2 } gm_dtype;
+
+/* aggregate.hpp:13 AggKind subset on the hot path. */
+typedef enum gm_reduce { GM_SUM = 0, GM_MEAN = 1, GM_MAX = 2, GM_MIN = 3 } gm_reduce;
+
+/* Thread-local message of the last failing call on this thread. */
+GM_API const char* gm_last_error(void);
+GM_API const char* gm_version(void);
+/* 1 if this build's kernels can run on the current device (sm_100). */
+GM_API int gm_device_supported(void);
+
+/* ------------------------------------------------------------------------ */
+/* Graph structure (L1): edge_index.hpp:22-29 CsrView, edge_index.cpp:45-62  */
+/* ------------------------------------------------------------------------ */
+
+/* Device CSR/CSC view. rowptr[num_rows+1] (int64), col[nnz] and perm[nnz]
+ * (int32, compressed position -> COO position). Same meaning as CsrView. */
+typedef struct gm_csr {
+  int64_t num_rows;
+  int64_t num_cols;
+  int64_t nnz;
+  const int64_t* rowptr;
+  const int32_t* col;
+  const int32_t* perm;
+} gm_csr;
+
+/* Replaces edge_index.cpp:19-25 check_bounds / tensor.hpp:489-495
+ * check_index_range: first position i with ids[i] outside [0, bound).
+ * Returns GM_ERR_OUT_OF_RANGE with message "<prefix> index X at position i
+ * outside [0, bound)". Synchronizes `stream` (the result decides control flow).
+ * workspace >= 64 bytes of device memory. */
+GM_API gm_status gm_check_index_bounds(const int64_t* ids, int64_t len, int64_t bound,
+                                       const char* prefix, void* workspace, gm_stream_t stream);
+
+/* Replaces edge_index.cpp:28-32 first_unsorted (claim verification,
+ * edge_index.cpp:88-95): writes the first position violating non-decreasing
+ * order, or -1, to *pos_host. Synchronizes. workspace >= 64 bytes. */
+GM_API gm_status gm_first_unsorted(const int64_t* keys, int64_t len, int64_t* pos_host,
+                                   void* workspace, gm_stream_t stream);
+
+/* Occurrence counts of ids in [0, n) into deg[n] (int32); ids outside are
+ * skipped (message_passing.hpp:76-78 spmm-mean degree; 441-443 full-array
+ * degrees of gcn_norm). */
+GM_API gm_status gm_degree(const int64_t* ids, int64_t len, int64_t n, int32_t* deg,
+                           gm_stream_t stream);
+
+/* Replaces build_compressed (edge_index.hpp:120-121, edge_index.cpp:45-62):
+ * stable counting sort of (keys, values) into a CSR. Bit-exact: within each
+ * row entries are in ascending COO position; perm[k] = COO position;
+ * col[k] = values[perm[k]]. keys must lie in [0, num_rows) (check first with
+ * gm_check_index_bounds, as EdgeIndex's constructor does). */
+GM_API size_t gm_build_compressed_workspace(int64_t num_edges, int64_t num_rows);
+GM_API gm_status gm_build_compressed(const int64_t* keys, const int64_t* values,
+                                     int64_t num_edges, int64_t num_rows, int64_t* rowptr,
+                                     int32_t* col, int32_t* perm, void* workspace,
+                                     size_t workspace_bytes, gm_stream_t stream);
+
+/* out[k] = in[perm[k]] for nnz elements of dtype: edge values in COO order ->
+ * compressed order (the `w[perm[k]]` lookup of message_passing.hpp:68, done
+ * once and cached instead of per edge). */
+GM_API gm_status gm_permute_edge_values(gm_dtype dtype, const void* in, const int32_t* perm,
+                                        int64_t nnz, void* out, gm_stream_t stream);
+
+/* ------------------------------------------------------------------------ */
+/* Aggregation (L2/L3): spmm, the max path and GCN norm                      */
+/* ------------------------------------------------------------------------ */
+
+/* Scheduling metadata for gm_spmm, computed once per CSR (cache it next to
+ * the CSR like EdgeIndex caches its CsrView, edge_index.hpp:94-103):
+ * destination rows are split into nnz-balanced windows of ~window_edges edges
+ * (win_row[num_windows+1]) for the warp-per-row kernel, and rows longer than
+ * heavy_threshold go to a CTA-per-row pipelined kernel, longest first
+ * (heavy_rows[num_heavy]). Pure scheduling: results do not depend on it. */
+typedef struct gm_spmm_plan {
+  int64_t num_windows;
+  int64_t window_edges;
+  int64_t num_heavy;
+  int64_t heavy_threshold;
+  const int32_t* win_row;
+  const int32_t* heavy_rows;
+} gm_spmm_plan;
+
+GM_API size_t gm_spmm_plan_bytes(int64_t num_rows, int64_t nnz);
+/* Builds the plan into `buffer` (device, gm_spmm_plan_bytes) and fills
+ * *plan_host. Synchronizes once (reads the heavy-row count). */
+GM_API gm_status gm_spmm_plan_build(const gm_csr* csr, void* buffer, size_t buffer_bytes,
+                                    gm_spmm_plan* plan_host, gm_stream_t stream);
+
+/* GCN degree normalisation fused into the SpMM (message_passing.hpp:437-463,
+ * 490-495): per edge (s -> v) the scale is 1 / sqrt(float(deg_src[s]) *
+ * float(deg_dst[v])), exactly as gcn_norm forms it (no rsqrt products). With
+ * self_loops != 0 every row v gets a final term for the self loop (v, v),
+ * which with_self_loops appends after all edges (edge_index.cpp:218-231) and
+ * therefore comes last in CSC order. deg arrays are the effective degrees
+ * (square: din+1 from the FULL dst array; bipartite: dout/din clamped >= 1),
+ * see gm_gcn_degrees. */
+typedef struct gm_gcn_norm {
+  const int32_t* deg_src;
+  const int32_t* deg_dst;
+  int self_loops;
+} gm_gcn_norm;
+
+/* Effective GCN degrees (message_passing.hpp:441-460): square != 0 ->
+ * deg_src = deg_dst = din + 1 (both arrays of length n_dst, may alias);
+ * else deg_src = max(dout, 1) [n_src], deg_dst = max(din, 1) [n_dst].
+ * full_src/full_dst: the base index's FULL arrays (trimmed views normalise
+ * like the untrimmed graph). */
+GM_API gm_status gm_gcn_degrees(const int64_t* full_src, const int64_t* full_dst, int64_t len,
+                                int64_t n_src, int64_t n_dst, int square, int32_t* deg_src,
+                                int32_t* deg_dst, gm_stream_t stream);
+
+/* Replaces spmm (message_passing.hpp:92-169 forward, spmm_forward 47-85) and
+ * the max/min path (message_passing.hpp:508-514 = dst_grouped_order 190-214 +
+ * gather_rows tensor.hpp:499-530 + aggregate aggregate.hpp:197-215), fused:
+ *   out[v] = reduce_{k in row v of csr} scale_k * x[col[k]]
+ * csr: the destination grouping (EdgeIndex::transpose_view()).
+ * x: [csr->num_cols, f] row-major of dtype. out: [csr->num_rows, f].
+ * edge_weight: NULL or per-edge scale in COMPRESSED order (gm_permute_edge_values).
+ * gcn: NULL or fused GCN norm (exclusive with edge_weight).
+ * reduce: SUM, MEAN (sum * (1/deg), deg = row length; message_passing.hpp:76-84),
+ *   MAX/MIN (first element initialises, then strict >/<; empty rows 0).
+ * arg_out: NULL or int32 [num_rows, f]: COO edge id (perm[k]) of the first
+ *   attaining edge, -1 for empty rows (MAX/MIN only; the reference keeps this
+ *   only inside its backward closure, aggregate.hpp:295-308). Requires perm.
+ * Accumulation is fp32 for F32/BF16 (BF16 in, BF16 out, RNE) and fp64 for F64,
+ * sequential per output element in compressed order with no FMA contraction,
+ * i.e. bit-identical to the reference for F32/F64. */
+GM_API gm_status gm_spmm(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype dtype,
+                         const void* x, int64_t f, const void* edge_weight,
+                         const gm_gcn_norm* gcn, gm_reduce reduce, void* out, int32_t* arg_out,
+                         gm_stream_t stream);
+
+/* ------------------------------------------------------------------------ */
+/* segment_matmul (L4): hetero.hpp:134-157 grouped_matmul                    */
+/* ------------------------------------------------------------------------ */
+
+/* out[ptr[g]:ptr[g+1], :] = x[ptr[g]:ptr[g+1], :] @ w[g] for g < groups.
+ * x: [ptr_host[groups], k] row-major BF16; w: [groups, k, n] row-major BF16
+ * (the reference's stacked W[G,F,F'] layout); out: [rows, n] of out_dtype
+ * (GM_BF16 or GM_F32). tcgen05 (UMMA) tensor cores, fp32 accumulation in
+ * TMEM, TMA-fed. ptr_host is a HOST array of groups+1 non-decreasing offsets
+ * (ptr_host[0] = 0). Empty groups produce no rows (0 x n, hetero.hpp:131).
+ * Requires k % 64 == 0, n % 16 == 0, n <= 256, groups <= 256, 16-byte aligned
+ * x/w/out. workspace: gm_segment_matmul_workspace bytes (the K-major copy of w). */
+GM_API size_t gm_segment_matmul_workspace(int64_t groups, int64_t k, int64_t n);
+GM_API gm_status gm_segment_matmul(const void* x, const int64_t* ptr_host, int64_t groups,
+                                   int64_t k, int64_t n, const void* w, gm_dtype out_dtype,
+                                   void* out, void* workspace, size_t workspace_bytes,
+                                   gm_stream_t stream);
+
+/* ------------------------------------------------------------------------ */
+/* Multi-GPU partitioning (north_star: dst-row partition + source all-gather) */
+/* ------------------------------------------------------------------------ */
+
+/* nnz-balanced contiguous destination-row cuts: cuts_host[p] = first row r
+ * with rowptr[r] >= p * nnz / parts (cuts_host[0] = 0, cuts_host[parts] =
+ * num_rows). rowptr_host is a HOST copy of the CSR row pointer. */
+GM_API gm_status gm_partition_rows_by_nnz(const int64_t* rowptr_host, int64_t num_rows,
+                                          int32_t parts, int64_t* cuts_host);
+
+/* ------------------------------------------------------------------------ */
+/* Synthetic inputs (bench/test infrastructure; bit-identical host & device) */
+/* ------------------------------------------------------------------------ */
+
+/* kind 0 = uniform, 1 = power-law (Chung-Lu alpha = 0.5, permuted ids).
+ * Generates edges [first, first+count) of the stream keyed by seed. */
+GM_API gm_status gm_synth_edges(int kind, uint64_t seed, int64_t first, int64_t count,
+                                int64_t n_src, int64_t n_dst, int64_t* src, int64_t* dst,
+                                gm_stream_t stream);
+GM_API void gm_synth_edges_host(int kind, uint64_t seed, int64_t first, int64_t count,
+                                int64_t n_src, int64_t n_dst, int64_t* src, int64_t* dst);
+/* Rows [first_row, first_row+rows) of an f-wide feature matrix, U[-1,1),
+ * written as dtype (BF16 = RNE of the fp32 value). quantize: see synth.h. */
+GM_API gm_status gm_synth_features(uint64_t seed, int64_t first_row, int64_t rows, int64_t f,
+                                   int quantize, gm_dtype dtype, void* x, gm_stream_t stream);
+GM_API void gm_synth_features_host(uint64_t seed, int64_t first_row, int64_t rows, int64_t f,
+                                   int quantize, gm_dtype dtype, void* x);
+/* Edge weights U[0.5, 1.5) for edges [first, first+count). */
+GM_API gm_status gm_synth_weights(uint64_t seed, int64_t first, int64_t count, gm_dtype dtype,
+                                  void* w, gm_stream_t stream);
+GM_API void gm_synth_weights_host(uint64_t seed, int64_t first, int64_t count, gm_dtype dtype,
+                                  void* w);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GRAPHMILL_B200_H */

@@ -1,0 +1,281 @@
+// ref_capi.cpp — C entry points over the UNMODIFIED reference
+// (/root/reference/proj, compiled in place by oracle/Makefile into
+// oracle/_ref/libgraphmill_ref.so). TEST INFRASTRUCTURE ONLY: used to pin the
+// oracle restatement, to generate tests/golden/ fixtures, and as the
+// "reference" CPU arm of bench.py. Every function calls the reference's own
+// public API; nothing here re-implements its arithmetic.
+#include <algorithm>
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <optional>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "graphmill/aggregate.hpp"
+#include "graphmill/edge_index.hpp"
+#include "graphmill/hetero.hpp"
+#include "graphmill/message_passing.hpp"
+
+using namespace graphmill;
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& fn) {
+  try {
+    fn();
+    return 0;
+  } catch (const std::out_of_range& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 3;
+  }
+}
+
+EdgeIndex make_index(const int64_t* src, const int64_t* dst, int64_t e, int64_t n_src,
+                     int64_t n_dst, int undirected) {
+  EdgeIndexClaims claims;
+  if (undirected) claims.is_undirected = true;
+  return EdgeIndex(std::vector<Index>(src, src + e), std::vector<Index>(dst, dst + e), n_src,
+                   n_dst, claims);
+}
+
+template <typename S>
+Tensor<S> make_tensor(const S* p, int64_t rows, int64_t f) {
+  return Tensor<S>::from_data({rows, f}, std::vector<S>(p, p + rows * f));
+}
+
+template <typename S>
+int spmm_impl(const int64_t* src, const int64_t* dst, int64_t e, int64_t n_src, int64_t n_dst,
+              int undirected, const S* x, int64_t f, const S* w, int mean, S* out) {
+  return guarded([&] {
+    NoGradGuard ng;
+    EdgeIndex ei = make_index(src, dst, e, n_src, n_dst, undirected);
+    std::optional<Tensor<S>> wt;
+    if (w) wt = Tensor<S>::from_data({e}, std::vector<S>(w, w + e));
+    Tensor<S> o = spmm(ei, make_tensor(x, n_src, f), wt, mean ? AggKind::mean : AggKind::sum);
+    std::memcpy(out, o.data().data(), sizeof(S) * static_cast<size_t>(n_dst * f));
+  });
+}
+
+// The reference max path (message_passing.hpp:508-514) with argpos recovered
+// from the reference's own backward (aggregate.hpp:295-308): the gradient of
+// sum(out) lands exactly on the first attaining grouped position.
+template <typename S>
+int max_impl(const int64_t* src, const int64_t* dst, int64_t e, int64_t n_src, int64_t n_dst,
+             const S* x, int64_t f, int is_min, S* out, int64_t* arg) {
+  return guarded([&] {
+    EdgeIndex ei = make_index(src, dst, e, n_src, n_dst, 0);
+    auto [order, grouped_dst] = detail::dst_grouped_order(ei, false);
+    std::vector<Index> src_nodes(order.size());
+    for (size_t i = 0; i < order.size(); ++i) src_nodes[i] = ei.src()[static_cast<size_t>(order[i])];
+    Tensor<S> m;
+    {
+      NoGradGuard ng;
+      Tensor<S> g = gather_rows(make_tensor(x, n_src, f), src_nodes);
+      m = Tensor<S>::from_data(g.shape(), std::vector<S>(g.data().begin(), g.data().end()));
+    }
+    m.set_requires_grad(true);
+    Tensor<S> o = aggregate(m, grouped_dst, n_dst, is_min ? AggKind::min : AggKind::max,
+                            AggLayout::sorted_segments);
+    std::memcpy(out, o.data().data(), sizeof(S) * static_cast<size_t>(n_dst * f));
+    std::fill(arg, arg + n_dst * f, int64_t{-1});
+    if (e == 0) return;
+    backward(sum(o));
+    Tensor<S> gm = m.grad();
+    auto gd = gm.data();
+    for (int64_t p = 0; p < e; ++p) {
+      const Index v = grouped_dst[static_cast<size_t>(p)];
+      for (int64_t j = 0; j < f; ++j)
+        if (gd[static_cast<size_t>(p * f + j)] != S(0)) arg[v * f + j] = order[static_cast<size_t>(p)];
+    }
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// edge_index.cpp:45-62
+int ref_build_compressed(const int64_t* keys, const int64_t* values, int64_t e, int64_t num_rows,
+                         int64_t* rowptr, int64_t* col, int64_t* perm) {
+  return guarded([&] {
+    CsrView v = build_compressed(std::span<const Index>(keys, static_cast<size_t>(e)),
+                                 std::span<const Index>(values, static_cast<size_t>(e)), num_rows);
+    std::copy(v.rowptr.begin(), v.rowptr.end(), rowptr);
+    std::copy(v.col.begin(), v.col.end(), col);
+    std::copy(v.perm.begin(), v.perm.end(), perm);
+  });
+}
+
+// EdgeIndex ctor + verify_claims (edge_index.cpp:69-119): status + message.
+int ref_edge_index_check(const int64_t* src, const int64_t* dst, int64_t e, int64_t n_src,
+                         int64_t n_dst, int undirected, int sort_order) {
+  return guarded([&] {
+    EdgeIndexClaims claims;
+    if (undirected) claims.is_undirected = true;
+    if (sort_order == 1) claims.sort_order = SortOrder::by_src;
+    if (sort_order == 2) claims.sort_order = SortOrder::by_dst;
+    EdgeIndex ei(std::vector<Index>(src, src + e), std::vector<Index>(dst, dst + e), n_src, n_dst,
+                 claims);
+  });
+}
+
+// message_passing.hpp:92-169 (forward)
+int ref_spmm_f32(const int64_t* src, const int64_t* dst, int64_t e, int64_t n_src, int64_t n_dst,
+                 int undirected, const float* x, int64_t f, const float* w, int mean, float* out) {
+  return spmm_impl<float>(src, dst, e, n_src, n_dst, undirected, x, f, w, mean, out);
+}
+int ref_spmm_f64(const int64_t* src, const int64_t* dst, int64_t e, int64_t n_src, int64_t n_dst,
+                 int undirected, const double* x, int64_t f, const double* w, int mean,
+                 double* out) {
+  return spmm_impl<double>(src, dst, e, n_src, n_dst, undirected, x, f, w, mean, out);
+}
+
+int ref_max_f32(const int64_t* src, const int64_t* dst, int64_t e, int64_t n_src, int64_t n_dst,
+                const float* x, int64_t f, int is_min, float* out, int64_t* arg) {
+  return max_impl<float>(src, dst, e, n_src, n_dst, x, f, is_min, out, arg);
+}
+int ref_max_f64(const int64_t* src, const int64_t* dst, int64_t e, int64_t n_src, int64_t n_dst,
+                const double* x, int64_t f, int is_min, double* out, int64_t* arg) {
+  return max_impl<double>(src, dst, e, n_src, n_dst, x, f, is_min, out, arg);
+}
+
+// aggregate.hpp:155-215 on edge-level values (a6): kind 0 sum, 1 mean, 2 max, 3 min.
+int ref_aggregate_f32(const float* values, int64_t e, int64_t f, const int64_t* index,
+                      int64_t n, int kind, float* out) {
+  return guarded([&] {
+    NoGradGuard ng;
+    const AggKind k[] = {AggKind::sum, AggKind::mean, AggKind::max, AggKind::min};
+    Tensor<float> o = aggregate(make_tensor(values, e, f),
+                                std::span<const Index>(index, static_cast<size_t>(e)), n, k[kind]);
+    std::memcpy(out, o.data().data(), sizeof(float) * static_cast<size_t>(n * f));
+  });
+}
+
+// GCN fused branch (message_passing.hpp:490-495) after the transform:
+// with_self_loops + gcn_norm + spmm(graph, xw, norm, sum). xw = h @ W given.
+int ref_gcn_aggregate_f32(const int64_t* src, const int64_t* dst, int64_t e, int64_t n,
+                          const float* xw, int64_t f, float* out) {
+  return guarded([&] {
+    NoGradGuard ng;
+    EdgeIndex ei = make_index(src, dst, e, n, n, 0);
+    const EdgeIndex graph = with_self_loops(ei);
+    Tensor<float> norm = detail::gcn_norm<float>(ei, graph, true);
+    Tensor<float> o = spmm(graph, make_tensor(xw, n, f), norm, AggKind::sum);
+    std::memcpy(out, o.data().data(), sizeof(float) * static_cast<size_t>(n * f));
+  });
+}
+
+// Full reference GCN layer forward (message_passing.hpp:600-608, segment_fused):
+// matmul(h, W) + GCN aggregate + bias. Used for the Cora 2-layer parity case.
+int ref_gcn_layer_f32(const int64_t* src, const int64_t* dst, int64_t e, int64_t n,
+                      const float* h, int64_t f_in, const float* wgt, const float* bias,
+                      int64_t f_out, float* out) {
+  return guarded([&] {
+    NoGradGuard ng;
+    EdgeIndex ei = make_index(src, dst, e, n, n, 0);
+    LayerParams<float> p;
+    p.kind = LayerKind::gcn;
+    p.in_dim = f_in;
+    p.out_dim = f_out;
+    p.weights["weight"] = make_tensor(wgt, f_in, f_out);
+    p.weights["bias"] = Tensor<float>::from_data({f_out}, std::vector<float>(bias, bias + f_out));
+    Tensor<float> o = layer_forward(p, ei, make_tensor(h, n, f_in), ExecPath::segment_fused);
+    std::memcpy(out, o.data().data(), sizeof(float) * static_cast<size_t>(n * f_out));
+  });
+}
+
+// hetero.hpp:134-157 over segments of a concatenated x.
+}  // extern "C"
+template <typename S>
+static int gmm_impl(const S* x, const int64_t* ptr, int64_t groups, int64_t k, int64_t n,
+                    const S* w, S* out) {
+  return guarded([&] {
+    NoGradGuard ng;
+    std::vector<Tensor<S>> ins;
+    for (int64_t g = 0; g < groups; ++g)
+      ins.push_back(make_tensor(x + ptr[g] * k, ptr[g + 1] - ptr[g], k));
+    Tensor<S> wt = Tensor<S>::from_data({groups, k, n}, std::vector<S>(w, w + groups * k * n));
+    auto outs = grouped_matmul<S>(ins, wt);
+    for (int64_t g = 0; g < groups; ++g)
+      std::memcpy(out + ptr[g] * n, outs[static_cast<size_t>(g)].data().data(),
+                  sizeof(S) * static_cast<size_t>((ptr[g + 1] - ptr[g]) * n));
+  });
+}
+extern "C" {
+int ref_grouped_matmul_f32(const float* x, const int64_t* ptr, int64_t groups, int64_t k,
+                           int64_t n, const float* w, float* out) {
+  return gmm_impl<float>(x, ptr, groups, k, n, w, out);
+}
+int ref_grouped_matmul_f64(const double* x, const int64_t* ptr, int64_t groups, int64_t k,
+                           int64_t n, const double* w, double* out) {
+  return gmm_impl<double>(x, ptr, groups, k, n, w, out);
+}
+
+// ---------------------------------------------------------------------------
+// CPU arm of bench.py: the reference's own spmm<float> (sum) run by `threads`
+// std::threads, each on the sub-EdgeIndex of a contiguous destination-row
+// range (edges with dst in range, relative COO order kept, dst renumbered), so
+// per-row results and order are those of the single-threaded reference.
+// Sub-indices are built and their CSC caches filled OUTSIDE the timed region
+// (steady state of repeated layer calls, edge_index.hpp:65-71). Returns the
+// mean seconds per repeat over `repeat` timed calls after `warmup`, mirroring
+// time_loop (message_passing.hpp:676-697). rows_limit > 0 restricts the run to
+// the first rows_limit destination rows (a bounded sample); *edges_done gets
+// the number of edges processed per repeat.
+// ---------------------------------------------------------------------------
+int ref_bench_spmm_f32(const int64_t* src, const int64_t* dst, int64_t e, int64_t n_src,
+                       int64_t n_dst, const float* x, int64_t f, int mean, int threads,
+                       int64_t rows_limit, int warmup, int repeat, double* seconds,
+                       int64_t* edges_done) {
+  return guarded([&] {
+    NoGradGuard ng;
+    if (threads < 1) threads = 1;
+    const int64_t rows = rows_limit > 0 ? std::min(rows_limit, n_dst) : n_dst;
+    std::vector<int64_t> cut(static_cast<size_t>(threads) + 1);
+    for (int t = 0; t <= threads; ++t) cut[static_cast<size_t>(t)] = rows * t / threads;
+    std::vector<std::vector<Index>> ssrc(static_cast<size_t>(threads)), sdst(static_cast<size_t>(threads));
+    for (int64_t i = 0; i < e; ++i) {
+      if (dst[i] >= rows) continue;
+      const int t = static_cast<int>(std::upper_bound(cut.begin(), cut.end(), dst[i]) - cut.begin()) - 1;
+      ssrc[static_cast<size_t>(t)].push_back(src[i]);
+      sdst[static_cast<size_t>(t)].push_back(dst[i] - cut[static_cast<size_t>(t)]);
+    }
+    int64_t total = 0;
+    std::vector<EdgeIndex> subs;
+    for (int t = 0; t < threads; ++t) {
+      total += static_cast<int64_t>(ssrc[static_cast<size_t>(t)].size());
+      subs.emplace_back(std::move(ssrc[static_cast<size_t>(t)]), std::move(sdst[static_cast<size_t>(t)]),
+                        n_src, cut[static_cast<size_t>(t) + 1] - cut[static_cast<size_t>(t)]);
+      subs.back().to_csc();
+    }
+    Tensor<float> xt = make_tensor(x, n_src, f);
+    auto run_once = [&] {
+      std::vector<std::thread> pool;
+      for (int t = 0; t < threads; ++t)
+        pool.emplace_back([&, t] {
+          Tensor<float> o = spmm(subs[static_cast<size_t>(t)], xt, std::nullopt,
+                                 mean ? AggKind::mean : AggKind::sum);
+          (void)o;
+        });
+      for (auto& th : pool) th.join();
+    };
+    BenchTiming bt = time_loop(run_once, repeat, warmup);
+    *seconds = bt.mean_ms / 1000.0;
+    *edges_done = total;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,12 @@
+"""graphmill-b200: B200-native (sm_100a) CSR message-passing hot path.
+
+The compute lives in libgraphmill_b200.so (C-ABI, include/graphmill_b200.h);
+`graphmill` mirrors the reference engine's operator API over it.
+"""
+from . import _lib  # noqa: F401
+from .graphmill import (  # noqa: F401
+    CsrView, EdgeIndex, aggregate, build_compressed, gcn_aggregate, gcn_layer, grouped_matmul,
+    neighbor_aggregate, segment_matmul, spmm)
+
+__all__ = ["CsrView", "EdgeIndex", "aggregate", "build_compressed", "gcn_aggregate", "gcn_layer",
+           "grouped_matmul", "neighbor_aggregate", "segment_matmul", "spmm"]

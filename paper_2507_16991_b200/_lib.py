@@ -1,0 +1,128 @@
+"""ctypes binding of the C-ABI in include/graphmill_b200.h.
+
+This is exactly the binding a maintainer of the reference would add on its
+side of the boundary. It loads the in-tree
+``libgraphmill_b200.so`` and fails loudly if it is missing: there is no CPU
+fallback on the product path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgraphmill_b200.so")
+
+GM_OK = 0
+GM_ERR_INVALID_ARGUMENT = 1
+GM_ERR_OUT_OF_RANGE = 2
+GM_ERR_CUDA = 3
+GM_ERR_UNSUPPORTED = 4
+GM_ERR_LOGIC = 5
+
+GM_F32, GM_F64, GM_BF16 = 0, 1, 2
+GM_SUM, GM_MEAN, GM_MAX, GM_MIN = 0, 1, 2, 3
+
+
+class gm_csr(C.Structure):
+    _fields_ = [
+        ("num_rows", C.c_int64),
+        ("num_cols", C.c_int64),
+        ("nnz", C.c_int64),
+        ("rowptr", C.c_void_p),
+        ("col", C.c_void_p),
+        ("perm", C.c_void_p),
+    ]
+
+
+class gm_spmm_plan(C.Structure):
+    _fields_ = [
+        ("num_windows", C.c_int64),
+        ("window_edges", C.c_int64),
+        ("num_heavy", C.c_int64),
+        ("heavy_threshold", C.c_int64),
+        ("win_row", C.c_void_p),
+        ("heavy_rows", C.c_void_p),
+    ]
+
+
+class gm_gcn_norm(C.Structure):
+    _fields_ = [("deg_src", C.c_void_p), ("deg_dst", C.c_void_p), ("self_loops", C.c_int)]
+
+
+# name -> (restype, argtypes); mirrors include/graphmill_b200.h one to one.
+_P = C.c_void_p
+_I64 = C.c_int64
+_U64 = C.c_uint64
+SIGNATURES = {
+    "gm_last_error": (C.c_char_p, []),
+    "gm_version": (C.c_char_p, []),
+    "gm_device_supported": (C.c_int, []),
+    "gm_check_index_bounds": (C.c_int, [_P, _I64, _I64, C.c_char_p, _P, _P]),
+    "gm_first_unsorted": (C.c_int, [_P, _I64, C.POINTER(C.c_int64), _P, _P]),
+    "gm_degree": (C.c_int, [_P, _I64, _I64, _P, _P]),
+    "gm_build_compressed_workspace": (C.c_size_t, [_I64, _I64]),
+    "gm_build_compressed": (C.c_int, [_P, _P, _I64, _I64, _P, _P, _P, _P, C.c_size_t, _P]),
+    "gm_permute_edge_values": (C.c_int, [C.c_int, _P, _P, _I64, _P, _P]),
+    "gm_spmm_plan_bytes": (C.c_size_t, [_I64, _I64]),
+    "gm_spmm_plan_build": (C.c_int, [C.POINTER(gm_csr), _P, C.c_size_t, C.POINTER(gm_spmm_plan), _P]),
+    "gm_gcn_degrees": (C.c_int, [_P, _P, _I64, _I64, _I64, C.c_int, _P, _P, _P]),
+    "gm_spmm": (C.c_int, [C.POINTER(gm_csr), C.POINTER(gm_spmm_plan), C.c_int, _P, _I64, _P,
+                          C.POINTER(gm_gcn_norm), C.c_int, _P, _P, _P]),
+    "gm_segment_matmul_workspace": (C.c_size_t, [_I64, _I64, _I64]),
+    "gm_segment_matmul": (C.c_int, [_P, C.POINTER(C.c_int64), _I64, _I64, _I64, _P, C.c_int, _P,
+                                    _P, C.c_size_t, _P]),
+    "gm_partition_rows_by_nnz": (C.c_int, [C.POINTER(C.c_int64), _I64, C.c_int32,
+                                           C.POINTER(C.c_int64)]),
+    "gm_synth_edges": (C.c_int, [C.c_int, _U64, _I64, _I64, _I64, _I64, _P, _P, _P]),
+    "gm_synth_edges_host": (None, [C.c_int, _U64, _I64, _I64, _I64, _I64, _P, _P]),
+    "gm_synth_features": (C.c_int, [_U64, _I64, _I64, _I64, C.c_int, C.c_int, _P, _P]),
+    "gm_synth_features_host": (None, [_U64, _I64, _I64, _I64, C.c_int, C.c_int, _P]),
+    "gm_synth_weights": (C.c_int, [_U64, _I64, _I64, C.c_int, _P, _P]),
+    "gm_synth_weights_host": (None, [_U64, _I64, _I64, C.c_int, _P]),
+}
+
+
+class GraphmillError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def build(verbose: bool = False) -> str:
+    """Compile the CUDA library in-tree (nvcc, sm_100a)."""
+    cmd = ["make", "-C", os.path.join(_HERE, "csrc"), "-j8"]
+    out = subprocess.run(cmd, capture_output=not verbose, text=True)
+    if out.returncode != 0:
+        raise GraphmillError("building libgraphmill_b200.so failed:\n" + (out.stderr or "")[-4000:])
+    return LIB_PATH
+
+
+def lib():
+    """The loaded C-ABI library (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise GraphmillError(
+                f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+        handle = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def check(status: int, what: str = "") -> None:
+    """Map a gm_status to the reference's exception types."""
+    if status == GM_OK:
+        return
+    msg = lib().gm_last_error().decode()
+    if status == GM_ERR_OUT_OF_RANGE:
+        raise IndexError(msg)          # std::out_of_range
+    if status == GM_ERR_INVALID_ARGUMENT:
+        raise ValueError(msg)          # std::invalid_argument
+    raise GraphmillError(f"{what}: status {status}: {msg}")

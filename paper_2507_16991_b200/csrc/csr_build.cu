@@ -1,0 +1,513 @@
+// csr_build.cu — graph-structure kernels (L1): bounds/claims checks, degree
+// counts and the bit-exact stable CSR/CSC build.
+//
+// build_compressed (edge_index.cpp:45-62) is a stable counting sort: within a
+// row, entries appear in ascending COO position. On the GPU:
+//   1. count   : cnt[key]++ (int32 atomics; exact)
+//   2. scan    : rowptr = exclusive prefix sum (int64), block-partial scan
+//   3. scatter : perm[rowptr[key+1] - atomicSub(&cnt[key], 1)] = i (unstable)
+//   4. restore stability by sorting every row's perm segment ascending (the
+//      values are distinct COO positions, so ascending order IS the stable
+//      order) — warp bitonic for rows <= 32, CTA bitonic in shared memory for
+//      rows <= 4096, chunk-sort + exact rank merge for longer (hub) rows —
+//      and emit col[k] = values[perm[k]] in the same pass.
+// The result is identical to the reference for every input, independent of
+// atomic ordering.
+#include <algorithm>
+#include <climits>
+#include <string>
+
+#include "gm_common.cuh"
+
+namespace gm {
+
+// ---------------------------------------------------------------------------
+// checks and degrees
+// ---------------------------------------------------------------------------
+__global__ void bounds_kernel(const int64_t* __restrict__ ids, int64_t len, int64_t bound,
+                              unsigned long long* __restrict__ first_bad) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < len;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t v = ids[i];
+    if (v < 0 || v >= bound) atomicMin(first_bad, static_cast<unsigned long long>(i));
+  }
+}
+
+__global__ void unsorted_kernel(const int64_t* __restrict__ keys, int64_t len,
+                                unsigned long long* __restrict__ first_bad) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x + 1; i < len;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (keys[i] < keys[i - 1]) atomicMin(first_bad, static_cast<unsigned long long>(i));
+  }
+}
+
+__global__ void degree_kernel(const int64_t* __restrict__ ids, int64_t len, int64_t n,
+                              int32_t* __restrict__ deg) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < len;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t v = ids[i];
+    if (v >= 0 && v < n) atomicAdd(&deg[v], 1);
+  }
+}
+
+__global__ void gcn_finish_kernel(int32_t* __restrict__ deg, int64_t n, int add, int clamp1) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int32_t d = deg[i] + add;
+  if (clamp1 && d < 1) d = 1;
+  deg[i] = d;
+}
+
+static unsigned grid_for(int64_t n, int threads = 256) {
+  const int64_t b = ceil_div(std::max<int64_t>(n, 1), threads);
+  return static_cast<unsigned>(std::min<int64_t>(b, kNumSMs * 32));
+}
+
+// ---------------------------------------------------------------------------
+// exclusive scan of int32 counts into int64 rowptr (3 phases)
+// ---------------------------------------------------------------------------
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ int64_t block_exclusive_scan(int64_t v, int64_t* warp_tot, int64_t* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int64_t inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t n = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += n;
+  }
+  if (lane == 31) warp_tot[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    int64_t t = lane < kScanThreads / 32 ? warp_tot[lane] : 0;
+    int64_t ti = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t n = __shfl_up_sync(0xffffffffu, ti, o);
+      if (lane >= o) ti += n;
+    }
+    if (lane < kScanThreads / 32) warp_tot[lane] = ti - t;
+    if (lane == 31) *total = ti;
+  }
+  __syncthreads();
+  return inc - v + warp_tot[wid];
+}
+
+__global__ void scan_reduce_kernel(const int32_t* __restrict__ cnt, int64_t n,
+                                   int64_t* __restrict__ partial) {
+  __shared__ int64_t wt[kScanThreads / 32];
+  __shared__ int64_t tot;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile;
+  int64_t s = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    const int64_t idx = base + static_cast<int64_t>(threadIdx.x) * kScanItems + i;
+    if (idx < n) s += cnt[idx];
+  }
+  block_exclusive_scan(s, wt, &tot);
+  if (threadIdx.x == 0) partial[blockIdx.x] = tot;
+}
+
+__global__ void scan_partials_kernel(int64_t* __restrict__ partial, int64_t nb) {
+  __shared__ int64_t wt[kScanThreads / 32];
+  __shared__ int64_t tot;
+  int64_t carry = 0;
+  for (int64_t base = 0; base < nb; base += kScanThreads) {
+    const int64_t idx = base + threadIdx.x;
+    const int64_t v = idx < nb ? partial[idx] : 0;
+    const int64_t ex = block_exclusive_scan(v, wt, &tot);
+    if (idx < nb) partial[idx] = carry + ex;
+    __syncthreads();
+    carry += tot;
+    __syncthreads();
+  }
+}
+
+__global__ void scan_down_kernel(const int32_t* __restrict__ cnt, int64_t n,
+                                 const int64_t* __restrict__ partial, int64_t* __restrict__ rowptr) {
+  __shared__ int64_t wt[kScanThreads / 32];
+  __shared__ int64_t tot;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile;
+  int64_t v[kScanItems];
+  int64_t s = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    const int64_t idx = base + static_cast<int64_t>(threadIdx.x) * kScanItems + i;
+    v[i] = idx < n ? cnt[idx] : 0;
+    s += v[i];
+  }
+  int64_t run = block_exclusive_scan(s, wt, &tot) + partial[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    const int64_t idx = base + static_cast<int64_t>(threadIdx.x) * kScanItems + i;
+    if (idx < n) rowptr[idx] = run;
+    run += v[i];
+    if (idx == n - 1) rowptr[n] = run;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// scatter + per-row stabilisation
+// ---------------------------------------------------------------------------
+__global__ void count_kernel(const int64_t* __restrict__ keys, int64_t e, int32_t* __restrict__ cnt) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < e;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    atomicAdd(&cnt[keys[i]], 1);
+}
+
+__global__ void scatter_kernel(const int64_t* __restrict__ keys, int64_t e,
+                               const int64_t* __restrict__ rowptr, int32_t* __restrict__ cnt,
+                               int32_t* __restrict__ perm) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < e;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t k = keys[i];
+    const int32_t c = atomicSub(&cnt[k], 1);
+    perm[rowptr[k + 1] - c] = static_cast<int32_t>(i);
+  }
+}
+
+constexpr int kMedMax = 4096;  // rows up to this length are sorted in one CTA's smem
+constexpr int kSortThreads = 512;
+
+// Warp per row: rows of length <= 32 are sorted in registers (bitonic via
+// shuffles); longer rows are queued for the CTA kernels.
+__global__ void sort_small_kernel(const int64_t* __restrict__ rowptr, int64_t num_rows,
+                                  const int64_t* __restrict__ values, int32_t* __restrict__ perm,
+                                  int32_t* __restrict__ col, int32_t* __restrict__ med_list,
+                                  int32_t* __restrict__ big_list, unsigned int* __restrict__ counters) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = warp; r < num_rows; r += nwarps) {
+    const int64_t kb = rowptr[r];
+    const int64_t len = rowptr[r + 1] - kb;
+    if (len <= 32) {
+      if (len == 0) continue;
+      int32_t v = lane < len ? perm[kb + lane] : INT_MAX;
+      if (len > 1) {
+#pragma unroll
+        for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+          for (int j = k >> 1; j > 0; j >>= 1) {
+            const int32_t o = __shfl_xor_sync(0xffffffffu, v, j);
+            const bool up = (lane & k) == 0;
+            const bool lower = (lane & j) == 0;
+            v = (lower == up) ? min(v, o) : max(v, o);
+          }
+        }
+      }
+      if (lane < len) {
+        perm[kb + lane] = v;
+        col[kb + lane] = static_cast<int32_t>(values[v]);
+      }
+    } else if (lane == 0) {
+      if (len <= kMedMax) med_list[atomicAdd(&counters[0], 1u)] = static_cast<int32_t>(r);
+      else big_list[atomicAdd(&counters[1], 1u)] = static_cast<int32_t>(r);
+    }
+  }
+}
+
+// In-smem bitonic sort of `n` (power of two) int32 keys by kSortThreads threads.
+__device__ void smem_bitonic(int32_t* s, int n) {
+  for (int k = 2; k <= n; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const bool up = (i & k) == 0;
+          const int32_t a = s[i], b = s[ixj];
+          if ((a > b) == up) {
+            s[i] = b;
+            s[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kSortThreads)
+sort_med_kernel(const int64_t* __restrict__ rowptr, const int64_t* __restrict__ values,
+                int32_t* __restrict__ perm, int32_t* __restrict__ col,
+                const int32_t* __restrict__ list, const unsigned int* __restrict__ counters) {
+  __shared__ int32_t s[kMedMax];
+  const unsigned int n_rows = counters[0];
+  for (unsigned int li = blockIdx.x; li < n_rows; li += gridDim.x) {
+    const int64_t r = list[li];
+    const int64_t kb = rowptr[r];
+    const int len = static_cast<int>(rowptr[r + 1] - kb);
+    int p2 = 64;
+    while (p2 < len) p2 <<= 1;
+    for (int i = threadIdx.x; i < p2; i += blockDim.x) s[i] = i < len ? perm[kb + i] : INT_MAX;
+    __syncthreads();
+    smem_bitonic(s, p2);
+    for (int i = threadIdx.x; i < len; i += blockDim.x) {
+      const int32_t v = s[i];
+      perm[kb + i] = v;
+      col[kb + i] = static_cast<int32_t>(values[v]);
+    }
+    __syncthreads();
+  }
+}
+
+// Hub rows: sort kMedMax-chunks in place, then place every element at its
+// exact rank (values are distinct): rank = sum over chunks of lower_bound.
+__global__ void __launch_bounds__(kSortThreads)
+sort_big_kernel(const int64_t* __restrict__ rowptr, const int64_t* __restrict__ values,
+                int32_t* __restrict__ perm, int32_t* __restrict__ col,
+                int32_t* __restrict__ scratch, const int32_t* __restrict__ list,
+                const unsigned int* __restrict__ counters) {
+  __shared__ int32_t s[kMedMax];
+  const unsigned int n_rows = counters[1];
+  for (unsigned int li = blockIdx.x; li < n_rows; li += gridDim.x) {
+    const int64_t r = list[li];
+    const int64_t kb = rowptr[r];
+    const int64_t len = rowptr[r + 1] - kb;
+    const int64_t nch = (len + kMedMax - 1) / kMedMax;
+    for (int64_t c = 0; c < nch; ++c) {
+      const int64_t cb = kb + c * kMedMax;
+      const int clen = static_cast<int>(std::min<int64_t>(kMedMax, len - c * kMedMax));
+      int p2 = 64;
+      while (p2 < clen) p2 <<= 1;
+      for (int i = threadIdx.x; i < p2; i += blockDim.x) s[i] = i < clen ? perm[cb + i] : INT_MAX;
+      __syncthreads();
+      smem_bitonic(s, p2);
+      for (int i = threadIdx.x; i < clen; i += blockDim.x) perm[cb + i] = s[i];
+      __syncthreads();
+    }
+    __threadfence_block();
+    for (int64_t i = threadIdx.x; i < len; i += blockDim.x) {
+      const int32_t v = perm[kb + i];
+      int64_t rank = 0;
+      for (int64_t c = 0; c < nch; ++c) {
+        const int64_t cb = kb + c * kMedMax;
+        int64_t lo = 0, hi = std::min<int64_t>(kMedMax, len - c * kMedMax);
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (perm[cb + mid] < v) lo = mid + 1;
+          else hi = mid;
+        }
+        rank += lo;
+      }
+      scratch[kb + rank] = v;
+    }
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < len; i += blockDim.x) {
+      const int32_t v = scratch[kb + i];
+      perm[kb + i] = v;
+      col[kb + i] = static_cast<int32_t>(values[v]);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void permute_kernel_4(const uint32_t* __restrict__ in, const int32_t* __restrict__ perm,
+                                 int64_t n, uint32_t* __restrict__ out) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = in[perm[i]];
+}
+__global__ void permute_kernel_8(const uint64_t* __restrict__ in, const int32_t* __restrict__ perm,
+                                 int64_t n, uint64_t* __restrict__ out) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = in[perm[i]];
+}
+__global__ void permute_kernel_2(const uint16_t* __restrict__ in, const int32_t* __restrict__ perm,
+                                 int64_t n, uint16_t* __restrict__ out) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = in[perm[i]];
+}
+
+struct BuildWs {
+  int32_t* cnt;
+  int64_t* partial;
+  int32_t* med;
+  int32_t* big;
+  unsigned int* counters;
+  int32_t* scratch;
+  size_t bytes;
+};
+
+static BuildWs build_layout(void* base, int64_t e, int64_t n) {
+  BuildWs w{};
+  unsigned char* p = static_cast<unsigned char*>(base);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    unsigned char* q = p ? p + off : nullptr;
+    off += align_up(std::max<size_t>(bytes, 1), 256);
+    return q;
+  };
+  const int64_t nb = std::max<int64_t>(1, ceil_div(n, kScanTile));
+  w.cnt = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(n)));
+  w.partial = reinterpret_cast<int64_t*>(take(sizeof(int64_t) * static_cast<size_t>(nb)));
+  w.med = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(n)));
+  w.big = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(n)));
+  w.counters = reinterpret_cast<unsigned int*>(take(64));
+  w.scratch = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(e)));
+  w.bytes = off;
+  return w;
+}
+
+}  // namespace gm
+
+using namespace gm;
+
+extern "C" {
+
+GM_API gm_status gm_check_index_bounds(const int64_t* ids, int64_t len, int64_t bound,
+                                       const char* prefix, void* workspace, gm_stream_t stream) {
+  GM_REQUIRE(len >= 0, GM_ERR_INVALID_ARGUMENT, "gm_check_index_bounds: negative length");
+  if (len == 0) return GM_OK;
+  GM_REQUIRE(ids && workspace, GM_ERR_INVALID_ARGUMENT, "gm_check_index_bounds: null pointer");
+  cudaStream_t st = as_stream(stream);
+  auto* first = static_cast<unsigned long long*>(workspace);
+  GM_TRY_CUDA(cudaMemsetAsync(first, 0xff, sizeof(unsigned long long), st));
+  bounds_kernel<<<grid_for(len), 256, 0, st>>>(ids, len, bound, first);
+  GM_CHECK_LAUNCH("bounds_kernel");
+  unsigned long long pos = 0;
+  GM_TRY_CUDA(cudaMemcpyAsync(&pos, first, sizeof(pos), cudaMemcpyDeviceToHost, st));
+  GM_TRY_CUDA(cudaStreamSynchronize(st));
+  if (pos == ~0ull) return GM_OK;
+  int64_t bad = 0;
+  GM_TRY_CUDA(cudaMemcpy(&bad, ids + pos, sizeof(bad), cudaMemcpyDeviceToHost));
+  return fail(GM_ERR_OUT_OF_RANGE, std::string(prefix ? prefix : "") + " index " + std::to_string(bad) +
+                                       " at position " + std::to_string(pos) + " outside [0, " +
+                                       std::to_string(bound) + ")");
+}
+
+GM_API gm_status gm_first_unsorted(const int64_t* keys, int64_t len, int64_t* pos_host,
+                                   void* workspace, gm_stream_t stream) {
+  GM_REQUIRE(pos_host, GM_ERR_INVALID_ARGUMENT, "gm_first_unsorted: null output");
+  *pos_host = -1;
+  if (len < 2) return GM_OK;
+  GM_REQUIRE(keys && workspace, GM_ERR_INVALID_ARGUMENT, "gm_first_unsorted: null pointer");
+  cudaStream_t st = as_stream(stream);
+  auto* first = static_cast<unsigned long long*>(workspace);
+  GM_TRY_CUDA(cudaMemsetAsync(first, 0xff, sizeof(unsigned long long), st));
+  unsorted_kernel<<<grid_for(len), 256, 0, st>>>(keys, len, first);
+  GM_CHECK_LAUNCH("unsorted_kernel");
+  unsigned long long pos = 0;
+  GM_TRY_CUDA(cudaMemcpyAsync(&pos, first, sizeof(pos), cudaMemcpyDeviceToHost, st));
+  GM_TRY_CUDA(cudaStreamSynchronize(st));
+  if (pos != ~0ull) *pos_host = static_cast<int64_t>(pos);
+  return GM_OK;
+}
+
+GM_API gm_status gm_degree(const int64_t* ids, int64_t len, int64_t n, int32_t* deg,
+                           gm_stream_t stream) {
+  GM_REQUIRE(len >= 0 && n >= 0, GM_ERR_INVALID_ARGUMENT, "gm_degree: negative size");
+  if (n == 0) return GM_OK;
+  cudaStream_t st = as_stream(stream);
+  GM_TRY_CUDA(cudaMemsetAsync(deg, 0, sizeof(int32_t) * static_cast<size_t>(n), st));
+  if (len == 0) return GM_OK;
+  degree_kernel<<<grid_for(len), 256, 0, st>>>(ids, len, n, deg);
+  GM_CHECK_LAUNCH("degree_kernel");
+  return GM_OK;
+}
+
+GM_API gm_status gm_gcn_degrees(const int64_t* full_src, const int64_t* full_dst, int64_t len,
+                                int64_t n_src, int64_t n_dst, int square, int32_t* deg_src,
+                                int32_t* deg_dst, gm_stream_t stream) {
+  cudaStream_t st = as_stream(stream);
+  gm_status s = gm_degree(full_dst, len, n_dst, deg_dst, stream);
+  if (s != GM_OK) return s;
+  if (square) {
+    // message_passing.hpp:447: din += 1 for the self loop every node receives
+    if (n_dst > 0) {
+      gcn_finish_kernel<<<static_cast<unsigned>(ceil_div(n_dst, 256)), 256, 0, st>>>(deg_dst, n_dst, 1, 0);
+      GM_CHECK_LAUNCH("gcn_finish_kernel");
+    }
+    if (deg_src != deg_dst && n_dst > 0)
+      GM_TRY_CUDA(cudaMemcpyAsync(deg_src, deg_dst, sizeof(int32_t) * static_cast<size_t>(n_dst),
+                                  cudaMemcpyDeviceToDevice, st));
+    return GM_OK;
+  }
+  // message_passing.hpp:452-460: dout(src), din(dst), each clamped to >= 1
+  s = gm_degree(full_src, len, n_src, deg_src, stream);
+  if (s != GM_OK) return s;
+  if (n_src > 0) {
+    gcn_finish_kernel<<<static_cast<unsigned>(ceil_div(n_src, 256)), 256, 0, st>>>(deg_src, n_src, 0, 1);
+    GM_CHECK_LAUNCH("gcn_finish_kernel");
+  }
+  if (n_dst > 0) {
+    gcn_finish_kernel<<<static_cast<unsigned>(ceil_div(n_dst, 256)), 256, 0, st>>>(deg_dst, n_dst, 0, 1);
+    GM_CHECK_LAUNCH("gcn_finish_kernel");
+  }
+  return GM_OK;
+}
+
+GM_API size_t gm_build_compressed_workspace(int64_t num_edges, int64_t num_rows) {
+  if (num_edges < 0 || num_rows < 0) return 0;
+  return build_layout(nullptr, num_edges, num_rows).bytes;
+}
+
+GM_API gm_status gm_build_compressed(const int64_t* keys, const int64_t* values,
+                                     int64_t num_edges, int64_t num_rows, int64_t* rowptr,
+                                     int32_t* col, int32_t* perm, void* workspace,
+                                     size_t workspace_bytes, gm_stream_t stream) {
+  GM_REQUIRE(num_edges >= 0 && num_rows >= 0, GM_ERR_INVALID_ARGUMENT,
+             "build_compressed: negative size");
+  GM_REQUIRE(num_edges < INT32_MAX && num_rows < INT32_MAX, GM_ERR_INVALID_ARGUMENT,
+             "build_compressed: num_edges and num_rows must be < 2^31 (int32 col/perm)");
+  GM_REQUIRE(rowptr, GM_ERR_INVALID_ARGUMENT, "build_compressed: null rowptr");
+  const BuildWs need = build_layout(nullptr, num_edges, num_rows);
+  GM_REQUIRE(workspace_bytes >= need.bytes && workspace, GM_ERR_INVALID_ARGUMENT,
+             "build_compressed: workspace too small (" + std::to_string(workspace_bytes) + " < " +
+                 std::to_string(need.bytes) + ")");
+  cudaStream_t st = as_stream(stream);
+  if (num_rows == 0) {  // rowptr = {0}
+    GM_TRY_CUDA(cudaMemsetAsync(rowptr, 0, sizeof(int64_t), st));
+    return GM_OK;
+  }
+  const BuildWs w = build_layout(workspace, num_edges, num_rows);
+  GM_TRY_CUDA(cudaMemsetAsync(w.cnt, 0, sizeof(int32_t) * static_cast<size_t>(num_rows), st));
+  GM_TRY_CUDA(cudaMemsetAsync(w.counters, 0, 64, st));
+  if (num_edges > 0) {
+    count_kernel<<<grid_for(num_edges), 256, 0, st>>>(keys, num_edges, w.cnt);
+    GM_CHECK_LAUNCH("count_kernel");
+  }
+  const int64_t nb = ceil_div(num_rows, kScanTile);
+  scan_reduce_kernel<<<static_cast<unsigned>(nb), kScanThreads, 0, st>>>(w.cnt, num_rows, w.partial);
+  GM_CHECK_LAUNCH("scan_reduce_kernel");
+  scan_partials_kernel<<<1, kScanThreads, 0, st>>>(w.partial, nb);
+  GM_CHECK_LAUNCH("scan_partials_kernel");
+  scan_down_kernel<<<static_cast<unsigned>(nb), kScanThreads, 0, st>>>(w.cnt, num_rows, w.partial, rowptr);
+  GM_CHECK_LAUNCH("scan_down_kernel");
+  if (num_edges == 0) return GM_OK;
+  scatter_kernel<<<grid_for(num_edges), 256, 0, st>>>(keys, num_edges, rowptr, w.cnt, perm);
+  GM_CHECK_LAUNCH("scatter_kernel");
+  sort_small_kernel<<<grid_for(num_rows * 32), 256, 0, st>>>(rowptr, num_rows, values, perm, col,
+                                                             w.med, w.big, w.counters);
+  GM_CHECK_LAUNCH("sort_small_kernel");
+  sort_med_kernel<<<kNumSMs * 4, kSortThreads, 0, st>>>(rowptr, values, perm, col, w.med, w.counters);
+  GM_CHECK_LAUNCH("sort_med_kernel");
+  sort_big_kernel<<<kNumSMs, kSortThreads, 0, st>>>(rowptr, values, perm, col, w.scratch, w.big,
+                                                    w.counters);
+  GM_CHECK_LAUNCH("sort_big_kernel");
+  return GM_OK;
+}
+
+GM_API gm_status gm_permute_edge_values(gm_dtype dtype, const void* in, const int32_t* perm,
+                                        int64_t nnz, void* out, gm_stream_t stream) {
+  GM_REQUIRE(nnz >= 0, GM_ERR_INVALID_ARGUMENT, "gm_permute_edge_values: negative nnz");
+  if (nnz == 0) return GM_OK;
+  cudaStream_t st = as_stream(stream);
+  if (dtype == GM_F32)
+    permute_kernel_4<<<grid_for(nnz), 256, 0, st>>>(static_cast<const uint32_t*>(in), perm, nnz,
+                                                    static_cast<uint32_t*>(out));
+  else if (dtype == GM_F64)
+    permute_kernel_8<<<grid_for(nnz), 256, 0, st>>>(static_cast<const uint64_t*>(in), perm, nnz,
+                                                    static_cast<uint64_t*>(out));
+  else
+    permute_kernel_2<<<grid_for(nnz), 256, 0, st>>>(static_cast<const uint16_t*>(in), perm, nnz,
+                                                    static_cast<uint16_t*>(out));
+  GM_CHECK_LAUNCH("permute_kernel");
+  return GM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,660 @@
+// spmm.cu — CSR SpMM aggregation (sum / mean / max / min, optional edge
+// scale or fused GCN norm, optional argmax) for sm_100a.
+//
+// Replaces, bit-exactly for f32/f64:
+//   spmm / detail::spmm_forward     message_passing.hpp:47-85, 92-169
+//   max path (fused, no E x F temp) message_passing.hpp:508-514 ->
+//                                   dst_grouped_order 190-214, gather_rows
+//                                   tensor.hpp:499-530, aggregate 197-215
+//   GCN norm fused into the gather  message_passing.hpp:437-463, 490-495
+//
+// Exactness: every output element is accumulated by ONE thread, sequentially
+// in compressed (CSC) order, with __fadd_rn/__fmul_rn (no FMA contraction) —
+// the reference's `o[j] += w * xi[j]` loop order. Max/min: the first element
+// initialises, then strict compare; ties keep the earlier edge.
+//
+// Scheduling (pure performance, never changes results):
+//   * light rows (deg <= heavy_threshold): a group of LPR lanes owns one
+//     nnz-balanced window of consecutive rows; lanes own VB-byte column
+//     slices, U edges' gathers are in flight per batch (coalesced 128-bit
+//     loads of whole feature rows, L1 no-allocate);
+//   * heavy rows (power-law hubs): one CTA per row, longest first, on a forked
+//     stream so hubs start before the light sweep; the CTA streams the row's
+//     feature rows into a cp.async shared-memory ring (R stages of `se` edges)
+//     while the owning threads accumulate each column in order.
+#include <algorithm>
+#include <vector>
+
+#include "vec.cuh"
+
+namespace gm {
+
+struct SpmmArgs {
+  const int64_t* rowptr;
+  const int32_t* col;
+  const int32_t* perm;
+  const void* x;
+  void* out;
+  int32_t* arg;
+  const void* w;             // per-edge scale (accumulation type), compressed order
+  const int32_t* gdeg_src;   // GCN effective degrees (NULL = no GCN)
+  const int32_t* gdeg_dst;
+  int gcn_self;              // append the (v, v) self-loop term last
+  int mean;
+  int is_min;
+  int64_t num_rows;
+  int64_t f;                 // elements per row
+  int64_t slot_base;         // first VB-byte slot of this column chunk
+  int64_t slot_end;          // one past the last slot of this chunk
+  const int32_t* win_row;
+  int64_t num_windows;
+  int64_t heavy_thr;
+  const int32_t* heavy_rows;
+};
+
+template <typename A>
+__device__ __forceinline__ A gcn_scale(int32_t ds, int32_t dd) {
+  // message_passing.hpp:449-451: S(1) / std::sqrt(S(din[s]) * S(din[d]))
+  return div_rn(A(1), sqrt_rn(mul_rn(static_cast<A>(ds), static_cast<A>(dd))));
+}
+
+// Per-thread accumulator for NV vectors of V elements.
+template <typename A, int NV, int V, bool MAXMIN>
+struct Acc {
+  A v[NV][V];
+  int32_t a[NV][V];
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        v[j][e] = A(0);
+        if (MAXMIN) a[j][e] = -1;
+      }
+  }
+  // One edge's contribution to vector j. `first`: first edge of the row.
+  __device__ __forceinline__ void add(int j, const A* vals, bool scaled, A sc, bool first,
+                                      int is_min, int32_t pm) {
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      const A val = scaled ? mul_rn(vals[e], sc) : vals[e];
+      if (!MAXMIN) {
+        v[j][e] = add_rn(v[j][e], val);
+      } else {
+        const bool better = first || (is_min ? (val < v[j][e]) : (val > v[j][e]));
+        if (better) {
+          v[j][e] = val;
+          a[j][e] = pm;
+        }
+      }
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Light path: LPR lanes per window, NV vectors of VB bytes per lane.
+// ---------------------------------------------------------------------------
+template <typename T, int VB, int NV, int LPR, int U, bool MAXMIN>
+__global__ void __launch_bounds__(256) spmm_light_kernel(const SpmmArgs p) {
+  using VecT = Vec<T, VB>;
+  using A = typename VecT::A;
+  constexpr int V = VecT::V;
+  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t window = gid / LPR;
+  const int sub = static_cast<int>(gid % LPR);
+  if (window >= p.num_windows) return;
+
+  const T* __restrict__ x = static_cast<const T*>(p.x);
+  T* __restrict__ out = static_cast<T*>(p.out);
+  const A* __restrict__ w = static_cast<const A*>(p.w);
+  const bool gcn = p.gdeg_src != nullptr;
+  const bool scaled = gcn || w != nullptr;
+  const bool want_arg = MAXMIN && p.arg != nullptr;
+
+  int64_t slot[NV];
+  bool valid[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    slot[j] = p.slot_base + sub + j * LPR;
+    valid[j] = slot[j] < p.slot_end;
+  }
+
+  const int r0 = p.win_row[window];
+  const int r1 = p.win_row[window + 1];
+  for (int r = r0; r < r1; ++r) {
+    const int64_t kb = p.rowptr[r];
+    const int64_t ke = p.rowptr[r + 1];
+    if (ke - kb > p.heavy_thr) continue;  // the heavy kernel owns this row
+    Acc<A, NV, V, MAXMIN> acc;
+    acc.init();
+    const int32_t dd = gcn ? p.gdeg_dst[r] : 0;
+
+    for (int64_t k = kb; k < ke; k += U) {
+      int32_t c[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) c[u] = (k + u < ke) ? p.col[k + u] : 0;
+      VecT buf[U][NV];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (k + u < ke) {
+          const T* xr = x + static_cast<int64_t>(c[u]) * p.f;
+#pragma unroll
+          for (int j = 0; j < NV; ++j)
+            if (valid[j]) buf[u][j].load_global(xr + slot[j] * V);
+        }
+      A sc[U];
+      int32_t pm[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        sc[u] = A(1);
+        pm[u] = -1;
+        if (k + u < ke) {
+          if (w) sc[u] = w[k + u];
+          else if (gcn) sc[u] = gcn_scale<A>(p.gdeg_src[c[u]], dd);
+          if (want_arg) pm[u] = p.perm[k + u];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (k + u < ke) {
+#pragma unroll
+          for (int j = 0; j < NV; ++j)
+            if (valid[j]) acc.add(j, buf[u][j].v, scaled, sc[u], k + u == kb, p.is_min, pm[u]);
+        }
+    }
+    int64_t cnt = ke - kb;
+    if (gcn && p.gcn_self) {
+      // with_self_loops appends (r, r) after every original edge
+      // (edge_index.cpp:226-229), so it is the last entry of CSC row r.
+      const A sc = gcn_scale<A>(p.gdeg_src[r], dd);
+      const T* xr = x + static_cast<int64_t>(r) * p.f;
+#pragma unroll
+      for (int j = 0; j < NV; ++j)
+        if (valid[j]) {
+          VecT b;
+          b.load_global(xr + slot[j] * V);
+          acc.add(j, b.v, true, sc, cnt == 0, p.is_min, -1);
+        }
+      cnt += 1;
+    }
+    if (!MAXMIN && p.mean && cnt > 0) {
+      const A inv = div_rn(A(1), static_cast<A>(cnt));  // message_passing.hpp:81
+#pragma unroll
+      for (int j = 0; j < NV; ++j)
+#pragma unroll
+        for (int e = 0; e < V; ++e) acc.v[j][e] = mul_rn(acc.v[j][e], inv);
+    }
+    T* orow = out + static_cast<int64_t>(r) * p.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+      if (valid[j]) {
+        VecT::store_global(orow + slot[j] * V, acc.v[j]);
+        if (want_arg) {
+          int32_t* arow = p.arg + static_cast<int64_t>(r) * p.f + slot[j] * V;
+#pragma unroll
+          for (int e = 0; e < V; ++e) arow[e] = acc.a[j][e];
+        }
+      }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Heavy path: one CTA per hub row, cp.async ring of R stages x se edges.
+// ---------------------------------------------------------------------------
+constexpr int kHeavyThreads = 256;
+constexpr int kRing = 4;
+
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem, int bytes) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  if (bytes == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+  else if (bytes == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <typename A>
+__host__ __device__ inline size_t heavy_smem_bytes(int se, int rowb) {
+  size_t b = static_cast<size_t>(kRing) * se * rowb;          // data ring
+  b += static_cast<size_t>(kRing + 1) * se * sizeof(int32_t);  // col ring
+  b += static_cast<size_t>(kRing + 1) * se * sizeof(int32_t);  // perm ring
+  b = (b + 15) / 16 * 16;
+  b += static_cast<size_t>(kRing + 1) * se * sizeof(A);        // scale ring
+  return b;
+}
+
+template <typename T, int VB, int MH, bool MAXMIN>
+__global__ void __launch_bounds__(kHeavyThreads) spmm_heavy_kernel(const SpmmArgs p, int se) {
+  using VecT = Vec<T, VB>;
+  using A = typename VecT::A;
+  constexpr int V = VecT::V;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int nslots = static_cast<int>(p.slot_end - p.slot_base);
+  const int rowb = nslots * VB;
+  unsigned char* data = smem;
+  int32_t* mcol = reinterpret_cast<int32_t*>(smem + static_cast<size_t>(kRing) * se * rowb);
+  int32_t* mperm = mcol + (kRing + 1) * se;
+  size_t off = static_cast<size_t>(kRing) * se * rowb + 2ull * (kRing + 1) * se * sizeof(int32_t);
+  off = (off + 15) / 16 * 16;
+  A* mscale = reinterpret_cast<A*>(smem + off);
+
+  const T* __restrict__ x = static_cast<const T*>(p.x);
+  const A* __restrict__ w = static_cast<const A*>(p.w);
+  const bool gcn = p.gdeg_src != nullptr;
+  const bool scaled = gcn || w != nullptr;
+  const bool want_arg = MAXMIN && p.arg != nullptr;
+  const int t = threadIdx.x;
+
+  const int r = p.heavy_rows[blockIdx.x];
+  const int64_t kb = p.rowptr[r];
+  const int64_t ke = p.rowptr[r + 1];
+  const int64_t deg = ke - kb;
+  const int64_t total = deg + ((gcn && p.gcn_self) ? 1 : 0);
+  const int nst = static_cast<int>((total + se - 1) / se);
+  const int32_t dd = gcn ? p.gdeg_dst[r] : 0;
+  const int gpr = rowb / VB;  // copy granules per feature row (VB bytes each)
+
+  // Register-staged metadata of one stage (threads t < se own edge t).
+  int32_t rc = -1, rp = -1;
+  A rw = A(1);
+  auto load_meta = [&](int q) {
+    const int64_t e = static_cast<int64_t>(q) * se + t;
+    rc = -1;
+    if (t < se && e < total) {
+      if (e < deg) {
+        const int64_t k = kb + e;
+        rc = p.col[k];
+        rp = want_arg ? p.perm[k] : -1;
+        rw = w ? w[k] : A(1);
+      } else {  // the self-loop term
+        rc = r;
+        rp = -1;
+        rw = A(1);
+      }
+    }
+  };
+
+  Acc<A, MH, V, MAXMIN> acc;
+  acc.init();
+  A sc_next = A(1);
+
+  load_meta(0);
+  for (int i = -(kRing - 1); i < nst; ++i) {
+    const int q = i + kRing - 1;  // stage whose copies are issued now
+    if (q < nst && t < se) {
+      const int ms = (q % (kRing + 1)) * se + t;
+      mcol[ms] = rc;
+      mperm[ms] = rp;
+      if (!gcn) mscale[ms] = rw;
+    }
+    if (q + 1 < nst) load_meta(q + 1);
+    __syncthreads();
+    if (q < nst) {
+      const int base_e = q * se;
+      const int n_e = static_cast<int>(min(static_cast<int64_t>(se), total - base_e));
+      const int32_t* cq = mcol + (q % (kRing + 1)) * se;
+      unsigned char* dq = data + static_cast<size_t>(q % kRing) * se * rowb;
+      for (int g = t; g < n_e * gpr; g += kHeavyThreads) {
+        const int e = g / gpr;
+        const int part = g - e * gpr;
+        const T* src = x + static_cast<int64_t>(cq[e]) * p.f + (p.slot_base + part) * V;
+        cp_async(dq + static_cast<size_t>(e) * rowb + part * VB, src, VB);
+      }
+    }
+    cp_async_commit();
+    if (gcn && i + 1 >= 0 && i + 1 < nst && t < se) {
+      const int64_t e = static_cast<int64_t>(i + 1) * se + t;
+      if (e < total) sc_next = gcn_scale<A>(p.gdeg_src[mcol[((i + 1) % (kRing + 1)) * se + t]], dd);
+    }
+    cp_async_wait<kRing - 1>();
+    __syncthreads();
+    if (i >= 0) {
+      const int base_e = i * se;
+      const int n_e = static_cast<int>(min(static_cast<int64_t>(se), total - base_e));
+      const unsigned char* di = data + static_cast<size_t>(i % kRing) * se * rowb;
+      const int mi = (i % (kRing + 1)) * se;
+#pragma unroll
+      for (int m = 0; m < MH; ++m) {
+        const int s = t + m * kHeavyThreads;
+        if (s < nslots) {
+          for (int e = 0; e < n_e; ++e) {
+            VecT v;
+            v.load_shared(reinterpret_cast<const T*>(di + static_cast<size_t>(e) * rowb + s * VB));
+            acc.add(m, v.v, scaled, mscale[mi + e], base_e + e == 0, p.is_min, mperm[mi + e]);
+          }
+        }
+      }
+    }
+    if (gcn && i + 1 >= 0 && i + 1 < nst && t < se) mscale[((i + 1) % (kRing + 1)) * se + t] = sc_next;
+  }
+
+  if (!MAXMIN && p.mean && total > 0) {
+    const A inv = div_rn(A(1), static_cast<A>(total));
+#pragma unroll
+    for (int m = 0; m < MH; ++m)
+#pragma unroll
+      for (int e = 0; e < V; ++e) acc.v[m][e] = mul_rn(acc.v[m][e], inv);
+  }
+  T* orow = static_cast<T*>(p.out) + static_cast<int64_t>(r) * p.f;
+#pragma unroll
+  for (int m = 0; m < MH; ++m) {
+    const int s = t + m * kHeavyThreads;
+    if (s < nslots) {
+      VecT::store_global(orow + (p.slot_base + s) * V, acc.v[m]);
+      if (want_arg) {
+        int32_t* arow = p.arg + static_cast<int64_t>(r) * p.f + (p.slot_base + s) * V;
+#pragma unroll
+        for (int e = 0; e < V; ++e) arow[e] = acc.a[m][e];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Plan: nnz+row balanced windows and the hub list.
+// ---------------------------------------------------------------------------
+constexpr int64_t kWindowCost = 256;    // edges + rows per light window
+constexpr int64_t kHeavyThreshold = 1024;
+
+__global__ void plan_windows_kernel(const int64_t* __restrict__ rowptr, int64_t num_rows,
+                                    int64_t num_windows, int32_t* __restrict__ win_row) {
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g > num_windows) return;
+  if (g == num_windows) {
+    win_row[g] = static_cast<int32_t>(num_rows);
+    return;
+  }
+  // rowptr may be a row slice of a larger CSR: offsets are relative to rowptr[0]
+  const int64_t target = g * kWindowCost + rowptr[0];
+  // first r in [0, num_rows] with rowptr[r] + r >= target
+  int64_t lo = 0, hi = num_rows;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (rowptr[mid] + mid >= target) hi = mid;
+    else lo = mid + 1;
+  }
+  win_row[g] = static_cast<int32_t>(lo);
+}
+
+__global__ void plan_heavy_kernel(const int64_t* __restrict__ rowptr, int64_t num_rows,
+                                  int64_t thr, int64_t cap, unsigned long long* __restrict__ keys,
+                                  unsigned int* __restrict__ count) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= num_rows) return;
+  const int64_t d = rowptr[r + 1] - rowptr[r];
+  if (d > thr) {
+    const unsigned int i = atomicAdd(count, 1u);
+    if (i < cap) keys[i] = (static_cast<unsigned long long>(d) << 32) | static_cast<unsigned long long>(r);
+  }
+}
+
+static int64_t plan_num_windows(int64_t num_rows, int64_t nnz) {
+  return std::max<int64_t>(1, ceil_div(nnz + num_rows, kWindowCost));
+}
+static int64_t plan_heavy_cap(int64_t num_rows, int64_t nnz) {
+  return std::min<int64_t>(num_rows, nnz / kHeavyThreshold + 1);
+}
+
+// ---------------------------------------------------------------------------
+// Launch helpers
+// ---------------------------------------------------------------------------
+struct SideStream {
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  int device = -1;
+};
+static thread_local SideStream t_side;
+
+static gm_status side_stream(SideStream** out) {
+  int dev = 0;
+  GM_TRY_CUDA(cudaGetDevice(&dev));
+  if (t_side.side == nullptr || t_side.device != dev) {
+    GM_TRY_CUDA(cudaStreamCreateWithFlags(&t_side.side, cudaStreamNonBlocking));
+    GM_TRY_CUDA(cudaEventCreateWithFlags(&t_side.fork, cudaEventDisableTiming));
+    GM_TRY_CUDA(cudaEventCreateWithFlags(&t_side.join, cudaEventDisableTiming));
+    t_side.device = dev;
+  }
+  *out = &t_side;
+  return GM_OK;
+}
+
+template <typename K>
+static gm_status ensure_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024)
+    GM_TRY_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(bytes)));
+  return GM_OK;
+}
+
+template <typename T, int VB, bool MAXMIN>
+static gm_status launch_light(const SpmmArgs& p0, int64_t ns, cudaStream_t st) {
+  // chunk columns so a lane holds <= 8 vectors; pick LPR/NV per chunk
+  for (int64_t base = 0; base < ns; base += 256) {
+    SpmmArgs p = p0;
+    p.slot_base = base;
+    p.slot_end = std::min<int64_t>(ns, base + 256);
+    const int64_t slots = p.slot_end - base;
+    int lpr = 32, nv = 1;
+    if (slots <= 4) lpr = 4;
+    else if (slots <= 8) lpr = 8;
+    else if (slots <= 16) lpr = 16;
+    else if (slots <= 32) lpr = 32;
+    else nv = slots <= 64 ? 2 : slots <= 128 ? 4 : 8;
+    const int64_t threads = p.num_windows * lpr;
+    const unsigned grid = static_cast<unsigned>(ceil_div(threads, 256));
+#define GM_LIGHT(LPR_, NV_, U_) \
+  spmm_light_kernel<T, VB, NV_, LPR_, U_, MAXMIN><<<grid, 256, 0, st>>>(p)
+    if (nv == 1) {
+      if (lpr == 4) GM_LIGHT(4, 1, 8);
+      else if (lpr == 8) GM_LIGHT(8, 1, 8);
+      else if (lpr == 16) GM_LIGHT(16, 1, 8);
+      else GM_LIGHT(32, 1, 8);
+    } else if (nv == 2) {
+      GM_LIGHT(32, 2, 4);
+    } else if (nv == 4) {
+      GM_LIGHT(32, 4, 2);
+    } else {
+      GM_LIGHT(32, 8, 1);
+    }
+#undef GM_LIGHT
+    GM_CHECK_LAUNCH("spmm_light_kernel");
+  }
+  return GM_OK;
+}
+
+template <typename T, int VB, bool MAXMIN>
+static gm_status launch_heavy(const SpmmArgs& p0, int64_t num_heavy, int64_t ns, cudaStream_t st) {
+  using A = typename AccOf<T>::type;
+  constexpr int64_t kChunk = 4 * kHeavyThreads;  // slots per column chunk (MH <= 4)
+  for (int64_t base = 0; base < ns; base += kChunk) {
+    SpmmArgs p = p0;
+    p.slot_base = base;
+    p.slot_end = std::min<int64_t>(ns, base + kChunk);
+    const int64_t slots = p.slot_end - base;
+    const int rowb = static_cast<int>(slots * VB);
+    int se = static_cast<int>(std::min<int64_t>(128, std::max<int64_t>(2, 65536 / (kRing * rowb))));
+    const size_t smem = heavy_smem_bytes<A>(se, rowb);
+    const int mh = slots <= kHeavyThreads ? 1 : slots <= 2 * kHeavyThreads ? 2 : 4;
+#define GM_HEAVY(MH_)                                                                    \
+  do {                                                                                   \
+    auto kern = spmm_heavy_kernel<T, VB, MH_, MAXMIN>;                                   \
+    gm_status s_ = ensure_smem(kern, smem);                                              \
+    if (s_ != GM_OK) return s_;                                                          \
+    kern<<<static_cast<unsigned>(num_heavy), kHeavyThreads, smem, st>>>(p, se);          \
+  } while (0)
+    if (mh == 1) GM_HEAVY(1);
+    else if (mh == 2) GM_HEAVY(2);
+    else GM_HEAVY(4);
+#undef GM_HEAVY
+    GM_CHECK_LAUNCH("spmm_heavy_kernel");
+  }
+  return GM_OK;
+}
+
+template <typename T, int VB>
+static gm_status dispatch_vb(const SpmmArgs& p, bool maxmin, bool use_heavy, int64_t num_heavy,
+                             int64_t ns, cudaStream_t st) {
+  if constexpr (VB >= 4) {
+  if (use_heavy) {
+    SideStream* ss = nullptr;
+    gm_status s = side_stream(&ss);
+    if (s != GM_OK) return s;
+    GM_TRY_CUDA(cudaEventRecord(ss->fork, st));
+    GM_TRY_CUDA(cudaStreamWaitEvent(ss->side, ss->fork, 0));
+    s = maxmin ? launch_heavy<T, VB, true>(p, num_heavy, ns, ss->side)
+               : launch_heavy<T, VB, false>(p, num_heavy, ns, ss->side);
+    if (s != GM_OK) return s;
+    GM_TRY_CUDA(cudaEventRecord(ss->join, ss->side));
+    s = maxmin ? launch_light<T, VB, true>(p, ns, st) : launch_light<T, VB, false>(p, ns, st);
+    if (s != GM_OK) return s;
+    GM_TRY_CUDA(cudaStreamWaitEvent(st, ss->join, 0));
+    return GM_OK;
+  }
+  }
+  (void)num_heavy;
+  return maxmin ? launch_light<T, VB, true>(p, ns, st) : launch_light<T, VB, false>(p, ns, st);
+}
+
+}  // namespace gm
+
+using namespace gm;
+
+extern "C" {
+
+GM_API size_t gm_spmm_plan_bytes(int64_t num_rows, int64_t nnz) {
+  if (num_rows < 0 || nnz < 0) return 0;
+  const int64_t g = plan_num_windows(num_rows, nnz);
+  size_t b = align_up(static_cast<size_t>(g + 1) * sizeof(int32_t), 256);
+  b += align_up(static_cast<size_t>(plan_heavy_cap(num_rows, nnz)) * sizeof(int32_t), 256);
+  b += align_up(static_cast<size_t>(plan_heavy_cap(num_rows, nnz)) * sizeof(unsigned long long), 256);
+  b += 256;  // counter
+  return b;
+}
+
+GM_API gm_status gm_spmm_plan_build(const gm_csr* csr, void* buffer, size_t buffer_bytes,
+                                    gm_spmm_plan* plan, gm_stream_t stream) {
+  GM_REQUIRE(csr && plan, GM_ERR_INVALID_ARGUMENT, "gm_spmm_plan_build: null argument");
+  GM_REQUIRE(csr->num_rows >= 0 && csr->nnz >= 0 && csr->num_rows < INT32_MAX && csr->nnz < INT32_MAX,
+             GM_ERR_INVALID_ARGUMENT, "gm_spmm_plan_build: sizes must be in [0, 2^31)");
+  const size_t need = gm_spmm_plan_bytes(csr->num_rows, csr->nnz);
+  GM_REQUIRE(buffer_bytes >= need, GM_ERR_INVALID_ARGUMENT,
+             "gm_spmm_plan_build: buffer too small (" + std::to_string(buffer_bytes) + " < " +
+                 std::to_string(need) + ")");
+  cudaStream_t st = as_stream(stream);
+  const int64_t g = plan_num_windows(csr->num_rows, csr->nnz);
+  const int64_t cap = plan_heavy_cap(csr->num_rows, csr->nnz);
+  unsigned char* b = static_cast<unsigned char*>(buffer);
+  int32_t* win_row = reinterpret_cast<int32_t*>(b);
+  b += align_up(static_cast<size_t>(g + 1) * sizeof(int32_t), 256);
+  int32_t* heavy_rows = reinterpret_cast<int32_t*>(b);
+  b += align_up(static_cast<size_t>(cap) * sizeof(int32_t), 256);
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(b);
+  b += align_up(static_cast<size_t>(cap) * sizeof(unsigned long long), 256);
+  unsigned int* count = reinterpret_cast<unsigned int*>(b);
+
+  plan_windows_kernel<<<static_cast<unsigned>(ceil_div(g + 1, 256)), 256, 0, st>>>(
+      csr->rowptr, csr->num_rows, g, win_row);
+  GM_CHECK_LAUNCH("plan_windows_kernel");
+  GM_TRY_CUDA(cudaMemsetAsync(count, 0, sizeof(unsigned int), st));
+  if (csr->num_rows > 0) {
+    plan_heavy_kernel<<<static_cast<unsigned>(ceil_div(csr->num_rows, 256)), 256, 0, st>>>(
+        csr->rowptr, csr->num_rows, kHeavyThreshold, cap, keys, count);
+    GM_CHECK_LAUNCH("plan_heavy_kernel");
+  }
+  unsigned int n_heavy = 0;
+  GM_TRY_CUDA(cudaMemcpyAsync(&n_heavy, count, sizeof(n_heavy), cudaMemcpyDeviceToHost, st));
+  GM_TRY_CUDA(cudaStreamSynchronize(st));
+  const int64_t nh = std::min<int64_t>(n_heavy, cap);
+  if (nh > 0) {
+    std::vector<unsigned long long> hk(static_cast<size_t>(nh));
+    GM_TRY_CUDA(cudaMemcpyAsync(hk.data(), keys, nh * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    GM_TRY_CUDA(cudaStreamSynchronize(st));
+    std::sort(hk.begin(), hk.end(), [](unsigned long long a, unsigned long long b) { return a > b; });
+    std::vector<int32_t> rows(static_cast<size_t>(nh));
+    for (int64_t i = 0; i < nh; ++i) rows[static_cast<size_t>(i)] = static_cast<int32_t>(hk[static_cast<size_t>(i)] & 0xffffffffull);
+    GM_TRY_CUDA(cudaMemcpyAsync(heavy_rows, rows.data(), nh * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    GM_TRY_CUDA(cudaStreamSynchronize(st));
+  }
+  plan->num_windows = g;
+  plan->window_edges = kWindowCost;
+  plan->num_heavy = nh;
+  plan->heavy_threshold = kHeavyThreshold;
+  plan->win_row = win_row;
+  plan->heavy_rows = heavy_rows;
+  return GM_OK;
+}
+
+GM_API gm_status gm_spmm(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype dtype,
+                         const void* x, int64_t f, const void* edge_weight,
+                         const gm_gcn_norm* gcn, gm_reduce reduce, void* out, int32_t* arg_out,
+                         gm_stream_t stream) {
+  GM_REQUIRE(csr && plan, GM_ERR_INVALID_ARGUMENT, "gm_spmm: null csr/plan");
+  GM_REQUIRE(f >= 0, GM_ERR_INVALID_ARGUMENT, "gm_spmm: negative feature width");
+  GM_REQUIRE(!(edge_weight && gcn), GM_ERR_INVALID_ARGUMENT,
+             "gm_spmm: edge_weight and gcn norm are exclusive");
+  const bool maxmin = reduce == GM_MAX || reduce == GM_MIN;
+  GM_REQUIRE(reduce >= GM_SUM && reduce <= GM_MIN, GM_ERR_INVALID_ARGUMENT, "gm_spmm: bad reduce");
+  GM_REQUIRE(!arg_out || maxmin, GM_ERR_INVALID_ARGUMENT, "gm_spmm: arg_out needs max/min");
+  GM_REQUIRE(!arg_out || csr->perm || csr->nnz == 0, GM_ERR_INVALID_ARGUMENT,
+             "gm_spmm: arg_out needs csr->perm");
+  GM_REQUIRE(!gcn || (gcn->deg_src && gcn->deg_dst), GM_ERR_INVALID_ARGUMENT,
+             "gm_spmm: gcn norm needs both degree arrays");
+  if (csr->num_rows == 0 || f == 0) return GM_OK;
+  GM_REQUIRE(x && out, GM_ERR_INVALID_ARGUMENT, "gm_spmm: null x/out");
+
+  const size_t esz = dtype == GM_F64 ? 8 : dtype == GM_F32 ? 4 : 2;
+  const size_t rowbytes = static_cast<size_t>(f) * esz;
+  const uintptr_t align = reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(out);
+  int vb = 16;
+  while (vb > static_cast<int>(esz) && (rowbytes % vb != 0 || align % vb != 0)) vb >>= 1;
+  GM_REQUIRE(rowbytes % vb == 0 && align % vb == 0, GM_ERR_INVALID_ARGUMENT,
+             "gm_spmm: x/out must be element-aligned");
+  const int64_t ns = static_cast<int64_t>(rowbytes / vb);
+
+  SpmmArgs p{};
+  p.rowptr = csr->rowptr;
+  p.col = csr->col;
+  p.perm = csr->perm;
+  p.x = x;
+  p.out = out;
+  p.arg = arg_out;
+  p.w = edge_weight;
+  p.gdeg_src = gcn ? gcn->deg_src : nullptr;
+  p.gdeg_dst = gcn ? gcn->deg_dst : nullptr;
+  p.gcn_self = gcn ? gcn->self_loops : 0;
+  p.mean = reduce == GM_MEAN;
+  p.is_min = reduce == GM_MIN;
+  p.num_rows = csr->num_rows;
+  p.f = f;
+  p.win_row = plan->win_row;
+  p.num_windows = plan->num_windows;
+  p.heavy_rows = plan->heavy_rows;
+  // cp.async moves >= 4-byte granules: narrower rows keep hubs on the light path
+  const bool use_heavy = plan->num_heavy > 0 && vb >= 4;
+  p.heavy_thr = use_heavy ? plan->heavy_threshold : INT64_MAX;
+  cudaStream_t st = as_stream(stream);
+
+  switch (dtype) {
+    case GM_F32:
+      if (vb == 16) return dispatch_vb<float, 16>(p, maxmin, use_heavy, plan->num_heavy, ns, st);
+      if (vb == 8) return dispatch_vb<float, 8>(p, maxmin, use_heavy, plan->num_heavy, ns, st);
+      return dispatch_vb<float, 4>(p, maxmin, use_heavy, plan->num_heavy, ns, st);
+    case GM_F64:
+      if (vb == 16) return dispatch_vb<double, 16>(p, maxmin, use_heavy, plan->num_heavy, ns, st);
+      return dispatch_vb<double, 8>(p, maxmin, use_heavy, plan->num_heavy, ns, st);
+    case GM_BF16:
+      if (vb == 16) return dispatch_vb<__nv_bfloat16, 16>(p, maxmin, use_heavy, plan->num_heavy, ns, st);
+      if (vb == 8) return dispatch_vb<__nv_bfloat16, 8>(p, maxmin, use_heavy, plan->num_heavy, ns, st);
+      if (vb == 4) return dispatch_vb<__nv_bfloat16, 4>(p, maxmin, use_heavy, plan->num_heavy, ns, st);
+      return dispatch_vb<__nv_bfloat16, 2>(p, maxmin, false, 0, ns, st);
+  }
+  return fail(GM_ERR_INVALID_ARGUMENT, "gm_spmm: unknown dtype");
+}
+
+}  // extern "C"

@@ -1,0 +1,437 @@
+"""Host-side mirror of the reference operator API over the C-ABI.
+
+Names, argument meaning and error behaviour follow the reference graphmill
+engine (/root/reference/proj/include/graphmill/*.hpp) so a test written
+against the reference reads the same here:
+
+    EdgeIndex(src, dst, num_src_nodes, num_dst_nodes, sort_order=, is_undirected=)
+        .to_csr() / .to_csc() / .transpose_view()   edge_index.hpp:43-116
+    build_compressed(keys, values, num_rows)          edge_index.hpp:120-121
+    spmm(e, x, edge_weight, reduce)                   message_passing.hpp:92-169
+    neighbor_aggregate(e, x, kind, ...)               message_passing.hpp:500-514 (sum/mean/max/min)
+    gcn_aggregate(e, xw) / gcn_layer(e, h, W, b)      message_passing.hpp:437-463, 490-499
+    aggregate(values, index, num_groups, kind)        aggregate.hpp:154-215
+    segment_matmul(x, ptr, W) / grouped_matmul(xs, W) hetero.hpp:134-157
+
+Device memory, streams and the collective plumbing come from PyTorch; every
+computation on the path runs in libgraphmill_b200.so. std::invalid_argument
+maps to ValueError, std::out_of_range to IndexError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import torch
+
+from . import _lib as L
+
+_DT = {torch.float32: L.GM_F32, torch.float64: L.GM_F64, torch.bfloat16: L.GM_BF16}
+_KIND = {"sum": L.GM_SUM, "mean": L.GM_MEAN, "max": L.GM_MAX, "min": L.GM_MIN}
+
+
+def _p(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dev_index(a, device) -> torch.Tensor:
+    if isinstance(a, torch.Tensor):
+        return a.to(device=device, dtype=torch.int64).contiguous()
+    return torch.as_tensor(list(a), dtype=torch.int64, device=device)
+
+
+@dataclass
+class CsrView:
+    """Device CSR (edge_index.hpp:22-29): rowptr int64[n+1], col/perm int32[nnz]."""
+
+    rowptr: torch.Tensor
+    col: torch.Tensor
+    perm: torch.Tensor
+    num_cols: int
+    nnz: Optional[int] = None  # edges of these rows (set for row slices of a larger CSR)
+    _plan: Optional[tuple] = field(default=None, repr=False)
+
+    def num_rows(self) -> int:
+        return self.rowptr.numel() - 1
+
+    def num_entries(self) -> int:
+        return self.col.numel() if self.nnz is None else self.nnz
+
+    def row_slice(self, r0: int, r1: int, nnz: int) -> "CsrView":
+        """Rows [r0, r1) sharing col/perm (offsets stay global); nnz = their edge count."""
+        return CsrView(self.rowptr[r0:r1 + 1], self.col, self.perm, self.num_cols, nnz)
+
+    def c_struct(self) -> L.gm_csr:
+        return L.gm_csr(self.num_rows(), self.num_cols, self.num_entries(),
+                        self.rowptr.data_ptr(), self.col.data_ptr(), self.perm.data_ptr())
+
+    def plan(self):
+        """Scheduling metadata (gm_spmm_plan), built once and cached."""
+        if self._plan is None:
+            lib = L.lib()
+            nbytes = lib.gm_spmm_plan_bytes(self.num_rows(), self.num_entries())
+            buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=self.rowptr.device)
+            plan = L.gm_spmm_plan()
+            csr = self.c_struct()
+            L.check(lib.gm_spmm_plan_build(C.byref(csr), _p(buf), nbytes, C.byref(plan), _stream()),
+                    "gm_spmm_plan_build")
+            self._plan = (plan, buf)
+        return self._plan[0]
+
+    def to_host(self):
+        """(rowptr, col, perm) as int64 CPU tensors, the reference's CsrView layout."""
+        return self.rowptr.cpu(), self.col.cpu().long(), self.perm.cpu().long()
+
+
+def build_compressed(keys: torch.Tensor, values: torch.Tensor, num_rows: int,
+                     num_cols: int = 0) -> CsrView:
+    """edge_index.cpp:45-62 on the device (bit-exact stable counting sort)."""
+    lib = L.lib()
+    dev = keys.device
+    e = keys.numel()
+    rowptr = torch.empty(num_rows + 1, dtype=torch.int64, device=dev)
+    col = torch.empty(max(e, 0), dtype=torch.int32, device=dev)
+    perm = torch.empty(max(e, 0), dtype=torch.int32, device=dev)
+    ws_bytes = lib.gm_build_compressed_workspace(e, num_rows)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    L.check(lib.gm_build_compressed(_p(keys), _p(values), e, num_rows, _p(rowptr), _p(col), _p(perm),
+                                    _p(ws), ws_bytes, _stream()), "gm_build_compressed")
+    return CsrView(rowptr, col, perm, num_cols)
+
+
+class EdgeIndex:
+    """COO edge list with verified claims and demand-filled device CSR/CSC
+    caches (edge_index.hpp:43-116). Copies share arrays and caches."""
+
+    def __init__(self, src, dst, num_src_nodes: int, num_dst_nodes: int,
+                 sort_order: Optional[str] = None, is_undirected: Optional[bool] = None,
+                 device: str | torch.device = "cuda"):
+        src_t = _dev_index(src, device)
+        dst_t = _dev_index(dst, device)
+        if src_t.numel() != dst_t.numel():
+            raise ValueError("EdgeIndex: src and dst lengths differ")
+        if num_src_nodes < 0 or num_dst_nodes < 0:
+            raise ValueError("EdgeIndex: negative node count")
+        self._src, self._dst = src_t, dst_t
+        self._num_edges = src_t.numel()
+        self._num_src, self._num_dst = int(num_src_nodes), int(num_dst_nodes)
+        self._cache = _CacheSlot()
+        self._verify_claims(sort_order, is_undirected)
+
+    # -- claims (edge_index.cpp:84-119) --------------------------------------
+    def _verify_claims(self, sort_order, is_undirected):
+        lib = L.lib()
+        ws = torch.empty(64, dtype=torch.uint8, device=self._src.device)
+        L.check(lib.gm_check_index_bounds(_p(self._src), self._num_edges, self._num_src,
+                                          b"EdgeIndex: src", _p(ws), _stream()), "bounds")
+        L.check(lib.gm_check_index_bounds(_p(self._dst), self._num_edges, self._num_dst,
+                                          b"EdgeIndex: dst", _p(ws), _stream()), "bounds")
+        self._sort_order = "unsorted"
+        self._undirected = False
+        if sort_order not in (None, "unsorted"):
+            if sort_order not in ("by_src", "by_dst"):
+                raise ValueError(f"EdgeIndex: unknown sort order {sort_order}")
+            keys = self._src if sort_order == "by_src" else self._dst
+            pos = C.c_int64(-1)
+            L.check(lib.gm_first_unsorted(_p(keys), self._num_edges, C.byref(pos), _p(ws), _stream()),
+                    "first_unsorted")
+            if pos.value >= 0:
+                raise ValueError(f"EdgeIndex: claim {sort_order} violated at position {pos.value}")
+            self._sort_order = sort_order
+        if is_undirected:
+            if self._num_src != self._num_dst:
+                raise ValueError(
+                    "EdgeIndex: is_undirected claim requires num_src_nodes == num_dst_nodes")
+            bad = _first_asymmetric(self._src, self._dst, self._num_src)
+            if bad >= 0:
+                s, d = int(self._src[bad]), int(self._dst[bad])
+                raise ValueError(f"EdgeIndex: is_undirected claim violated at position {bad} "
+                                 f"(edge {s}->{d} lacks a matching reverse)")
+            self._undirected = True
+
+    # -- accessors ---------------------------------------------------------------
+    def src(self) -> torch.Tensor:
+        return self._src[: self._num_edges]
+
+    def dst(self) -> torch.Tensor:
+        return self._dst[: self._num_edges]
+
+    def full_src(self) -> torch.Tensor:
+        return self._src
+
+    def full_dst(self) -> torch.Tensor:
+        return self._dst
+
+    def num_edges(self) -> int:
+        return self._num_edges
+
+    def num_src_nodes(self) -> int:
+        return self._num_src
+
+    def num_dst_nodes(self) -> int:
+        return self._num_dst
+
+    def sort_order(self) -> str:
+        return self._sort_order
+
+    def is_undirected(self) -> bool:
+        return self._undirected
+
+    def is_prefix_view(self) -> bool:
+        return self._num_edges != self._src.numel()
+
+    # -- caches (edge_index.cpp:121-145) -----------------------------------------
+    def _fill_cache(self, by_dst: bool) -> CsrView:
+        slot = self._cache
+        hit = slot.csc if by_dst else slot.csr
+        if hit is not None:
+            return hit
+        keys, vals, n_rows, n_cols = ((self.dst(), self.src(), self._num_dst, self._num_src) if by_dst
+                                      else (self.src(), self.dst(), self._num_src, self._num_dst))
+        built = build_compressed(keys, vals, n_rows, n_cols)
+        with slot.lock:  # compute-then-publish: at most one result wins
+            if by_dst:
+                slot.csc_builds += 1
+                if slot.csc is None:
+                    slot.csc = built
+                return slot.csc
+            slot.csr_builds += 1
+            if slot.csr is None:
+                slot.csr = built
+            return slot.csr
+
+    def to_csr(self) -> CsrView:
+        return self._fill_cache(False)
+
+    def to_csc(self) -> CsrView:
+        return self._fill_cache(True)
+
+    def transpose_view(self) -> CsrView:
+        return self.to_csr() if self._undirected else self.to_csc()
+
+    def has_csr_cache(self) -> bool:
+        return self._cache.csr is not None
+
+    def has_csc_cache(self) -> bool:
+        return self._cache.csc is not None
+
+    def csr_build_count(self) -> int:
+        return self._cache.csr_builds
+
+    def csc_build_count(self) -> int:
+        return self._cache.csc_builds
+
+    def prefix_edges(self, count: int, num_src_nodes: int, num_dst_nodes: int) -> "EdgeIndex":
+        """Zero-copy view of the first `count` edges (edge_index.cpp:201-216)."""
+        if count < 0 or count > self._num_edges:
+            raise IndexError("EdgeIndex: prefix count out of range")
+        view = EdgeIndex.__new__(EdgeIndex)
+        view._src, view._dst = self._src, self._dst
+        view._num_edges = count
+        view._num_src, view._num_dst = num_src_nodes, num_dst_nodes
+        view._sort_order = self._sort_order
+        view._undirected = False
+        view._cache = _CacheSlot()
+        lib = L.lib()
+        ws = torch.empty(64, dtype=torch.uint8, device=self._src.device)
+        L.check(lib.gm_check_index_bounds(_p(view.src()), count, num_src_nodes, b"EdgeIndex: src",
+                                          _p(ws), _stream()), "bounds")
+        L.check(lib.gm_check_index_bounds(_p(view.dst()), count, num_dst_nodes, b"EdgeIndex: dst",
+                                          _p(ws), _stream()), "bounds")
+        return view
+
+
+class _CacheSlot:
+    def __init__(self):
+        self.lock = threading.Lock()
+        self.csr: Optional[CsrView] = None
+        self.csc: Optional[CsrView] = None
+        self.csr_builds = 0
+        self.csc_builds = 0
+
+
+def _first_asymmetric(src: torch.Tensor, dst: torch.Tensor, n: int) -> int:
+    """First COO position whose (u,v) multiplicity differs from (v,u)'s
+    (edge_index.cpp:98-118), via sorted pair keys on the device."""
+    if src.numel() == 0:
+        return -1
+    fwd = src * n + dst
+    rev = dst * n + src
+    sorted_fwd, _ = torch.sort(fwd)
+    cnt_fwd = torch.searchsorted(sorted_fwd, fwd, right=True) - torch.searchsorted(sorted_fwd, fwd)
+    cnt_rev = torch.searchsorted(sorted_fwd, rev, right=True) - torch.searchsorted(sorted_fwd, rev)
+    bad = torch.nonzero(cnt_fwd != cnt_rev)
+    return int(bad[0, 0]) if bad.numel() else -1
+
+
+# ---------------------------------------------------------------------------
+# Aggregation
+# ---------------------------------------------------------------------------
+
+def _run_spmm(grouping: CsrView, x: torch.Tensor, kind: str, w_csr: Optional[torch.Tensor] = None,
+              gcn: Optional[L.gm_gcn_norm] = None, want_arg: bool = False, num_rows: Optional[int] = None):
+    if x.dtype not in _DT:
+        raise ValueError(f"spmm: unsupported dtype {x.dtype}")
+    x = x.contiguous()
+    f = x.shape[1] if x.dim() == 2 else 1
+    rows = grouping.num_rows() if num_rows is None else num_rows
+    out = torch.empty((rows, f) if x.dim() == 2 else (rows,), dtype=x.dtype, device=x.device)
+    arg = torch.empty((rows, f), dtype=torch.int32, device=x.device) if want_arg else None
+    csr = grouping.c_struct()
+    plan = grouping.plan()
+    L.check(L.lib().gm_spmm(C.byref(csr), C.byref(plan), _DT[x.dtype], _p(x), f, _p(w_csr),
+                            C.byref(gcn) if gcn is not None else None, _KIND[kind], _p(out), _p(arg),
+                            _stream()), "gm_spmm")
+    return (out, arg) if want_arg else out
+
+
+def _permute(values: torch.Tensor, perm: torch.Tensor) -> torch.Tensor:
+    out = torch.empty_like(values)
+    L.check(L.lib().gm_permute_edge_values(_DT[values.dtype], _p(values), _p(perm), values.numel(),
+                                           _p(out), _stream()), "permute")
+    return out
+
+
+def spmm(e: EdgeIndex, x: torch.Tensor, edge_weight: Optional[torch.Tensor], reduce: str) -> torch.Tensor:
+    """message_passing.hpp:92-169 forward: out[v] = sum_{(w,v)} weight * x[w] (or mean)."""
+    if reduce not in ("sum", "mean"):
+        raise ValueError("spmm: reduce must be sum or mean")
+    if x.shape[0] != e.num_src_nodes():
+        raise ValueError("spmm: feature rows != num_src_nodes")
+    if edge_weight is not None and edge_weight.numel() != e.num_edges():
+        raise ValueError("spmm: edge weight length != num_edges")
+    w_csr = None
+    if edge_weight is not None:
+        # Undirected + weights: the reference sweeps COO (message_passing.hpp:51-59),
+        # i.e. ascending COO position per destination = CSC order.
+        grouping = e.to_csc() if e.is_undirected() else e.transpose_view()
+        w_csr = _permute(edge_weight.to(_acc_dtype(x.dtype)).contiguous(), grouping.perm)
+    else:
+        grouping = e.transpose_view()
+    return _run_spmm(grouping, x, reduce, w_csr=w_csr, num_rows=e.num_dst_nodes())
+
+
+def _acc_dtype(dt):
+    return torch.float64 if dt == torch.float64 else torch.float32
+
+
+def neighbor_aggregate(e: EdgeIndex, x: torch.Tensor, kind: str,
+                       edge_weight: Optional[torch.Tensor] = None, return_argmax: bool = False):
+    """The fused segment path of layer_neighbor_aggregate (message_passing.hpp:500-514)
+    for identity messages: sum/mean through spmm, max/min through
+    dst_grouped_order + gather_rows + aggregate without the E x F temporary.
+    return_argmax: also the COO edge id of the first attaining edge (-1 if empty)."""
+    if kind not in _KIND:
+        raise ValueError(f"unknown aggregation kind: {kind}")
+    if x.shape[0] != e.num_src_nodes():
+        raise ValueError("propagate: h_src rows != num_src_nodes")
+    grouping = e.transpose_view()
+    w_csr = None
+    if edge_weight is not None:
+        w_csr = _permute(edge_weight.to(_acc_dtype(x.dtype)).contiguous(), grouping.perm)
+    want = return_argmax and kind in ("max", "min")
+    return _run_spmm(grouping, x, kind, w_csr=w_csr, want_arg=want, num_rows=e.num_dst_nodes())
+
+
+def gcn_degrees(e: EdgeIndex, square: bool):
+    """Effective degrees of gcn_norm (message_passing.hpp:437-463) from the FULL arrays."""
+    dev = e.full_dst().device
+    d_dst = torch.empty(e.num_dst_nodes(), dtype=torch.int32, device=dev)
+    d_src = d_dst if square else torch.empty(e.num_src_nodes(), dtype=torch.int32, device=dev)
+    L.check(L.lib().gm_gcn_degrees(_p(e.full_src()), _p(e.full_dst()), e.full_dst().numel(),
+                                   e.num_src_nodes(), e.num_dst_nodes(), int(square), _p(d_src),
+                                   _p(d_dst), _stream()), "gcn_degrees")
+    return d_src, d_dst
+
+
+def gcn_aggregate(e: EdgeIndex, xw: torch.Tensor) -> torch.Tensor:
+    """GCN neighbour side after the transform (message_passing.hpp:490-495):
+    with_self_loops + gcn_norm + spmm(sum), fused into one pass over e's CSC."""
+    square = e.num_src_nodes() == e.num_dst_nodes()
+    d_src, d_dst = gcn_degrees(e, square)
+    gcn = L.gm_gcn_norm(d_src.data_ptr(), d_dst.data_ptr(), int(square))
+    # with_self_loops builds a claim-less index, so its transpose_view is the CSC
+    return _run_spmm(e.to_csc(), xw, "sum", gcn=gcn, num_rows=e.num_dst_nodes())
+
+
+def gcn_layer(e: EdgeIndex, h: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor) -> torch.Tensor:
+    """layer_forward for LayerKind::gcn (message_passing.hpp:490-499, 578): the dense
+    transform is a plain library GEMM (fp32, TF32 off), then the fused aggregate."""
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        xw = h @ weight
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    return gcn_aggregate(e, xw) + bias
+
+
+def aggregate(values: torch.Tensor, index: torch.Tensor, num_groups: int, kind: str) -> torch.Tensor:
+    """aggregate.hpp:154-215 (sum/mean/max/min) for edge-level rows: groups are
+    visited in ascending position, exactly the reference's scatter order."""
+    if kind not in _KIND:
+        raise ValueError(f"unknown aggregation kind: {kind}")
+    index = index.to(dtype=torch.int64).contiguous()
+    if values.shape[0] != index.numel():
+        raise ValueError("aggregate: values rows != index length")
+    lib = L.lib()
+    ws = torch.empty(64, dtype=torch.uint8, device=index.device)
+    L.check(lib.gm_check_index_bounds(_p(index), index.numel(), num_groups, b"aggregate:", _p(ws),
+                                      _stream()), "bounds")
+    positions = torch.arange(index.numel(), dtype=torch.int64, device=index.device)
+    grouping = build_compressed(index, positions, num_groups, index.numel())
+    x = values if values.dim() == 2 else values.reshape(-1, 1)
+    out = _run_spmm(grouping, x, kind, num_rows=num_groups)
+    return out if values.dim() == 2 else out.reshape(-1)
+
+
+# ---------------------------------------------------------------------------
+# Grouped GEMM
+# ---------------------------------------------------------------------------
+
+def segment_matmul(x: torch.Tensor, ptr: Sequence[int], weights: torch.Tensor,
+                   out_dtype: torch.dtype = torch.bfloat16) -> torch.Tensor:
+    """out[ptr[g]:ptr[g+1]] = x[ptr[g]:ptr[g+1]] @ weights[g] (hetero.hpp:134-157),
+    bf16 tensor cores (tcgen05), fp32 accumulation."""
+    if weights.dim() != 3:
+        raise ValueError("grouped_matmul: weights must be [groups, F, F']")
+    groups, k, n = weights.shape
+    if len(ptr) != groups + 1:
+        raise ValueError(f"grouped_matmul: group count mismatch ({len(ptr) - 1} inputs, {groups} weight slabs)")
+    if x.dim() != 2 or x.shape[1] != k:
+        raise ValueError("grouped_matmul: inner dimension mismatch")
+    x = x.to(torch.bfloat16).contiguous()
+    w = weights.to(torch.bfloat16).contiguous()
+    rows = int(ptr[-1])
+    out = torch.empty((rows, n), dtype=out_dtype, device=x.device)
+    ptr_h = (C.c_int64 * (groups + 1))(*[int(p) for p in ptr])
+    lib = L.lib()
+    ws_bytes = lib.gm_segment_matmul_workspace(groups, k, n)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=x.device)
+    L.check(lib.gm_segment_matmul(_p(x), ptr_h, groups, k, n, _p(w), _DT[out_dtype], _p(out), _p(ws),
+                                  ws_bytes, _stream()), "gm_segment_matmul")
+    return out
+
+
+def grouped_matmul(inputs: Sequence[torch.Tensor], weights: torch.Tensor,
+                   out_dtype: torch.dtype = torch.bfloat16):
+    """List form of hetero.hpp:134-157 (validates like the reference)."""
+    if weights.dim() != 3:
+        raise ValueError("grouped_matmul: weights must be [groups, F, F']")
+    groups, k, _ = weights.shape
+    if len(inputs) != groups:
+        raise ValueError(f"grouped_matmul: group count mismatch ({len(inputs)} inputs, {groups} weight slabs)")
+    for g, h in enumerate(inputs):
+        if h.dim() != 2 or h.shape[1] != k:
+            raise ValueError(f"grouped_matmul: group {g} inner dimension mismatch")
+    ptr = [0]
+    for h in inputs:
+        ptr.append(ptr[-1] + h.shape[0])
+    out = segment_matmul(torch.cat(list(inputs), 0), ptr, weights, out_dtype)
+    return [out[ptr[g]:ptr[g + 1]] for g in range(groups)]
