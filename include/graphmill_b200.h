@@ -120,6 +120,10 @@ typedef struct gm_spmm_plan {
   int64_t heavy_threshold;
   const int32_t* win_row;
   const int32_t* heavy_rows;
+  /* The same windows split around heavy rows: (first_row, end_row) pairs of
+   * heavy-free row runs, streamed edge-contiguously by the flat kernel. */
+  int64_t num_light_windows;
+  const int32_t* light_windows;
 } gm_spmm_plan;
 
 GM_API size_t gm_spmm_plan_bytes(int64_t num_rows, int64_t nnz);

@@ -44,6 +44,8 @@ class gm_spmm_plan(C.Structure):
         ("heavy_threshold", C.c_int64),
         ("win_row", C.c_void_p),
         ("heavy_rows", C.c_void_p),
+        ("num_light_windows", C.c_int64),
+        ("light_windows", C.c_void_p),
     ]
 
 

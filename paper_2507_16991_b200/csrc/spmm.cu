@@ -50,6 +50,9 @@ struct SpmmArgs {
   int64_t num_windows;
   int64_t heavy_thr;
   const int32_t* heavy_rows;
+  const int32_t* light_windows;  // (first_row, end_row) pairs, heavy-free
+  int64_t num_light_windows;
+  int flat_ok;                   // heavy rows (if any) are covered by the hub kernel
 };
 
 template <typename A>
@@ -196,6 +199,140 @@ __global__ void __launch_bounds__(256) spmm_light_kernel(const SpmmArgs p) {
         }
       }
   }
+}
+
+
+// ---------------------------------------------------------------------------
+// Flat light path (the hot one): one warp streams a heavy-free window of
+// consecutive rows as ONE contiguous edge range, U edges per batch regardless
+// of row boundaries (no partial batches at row ends). The next batch's col
+// (and weight / perm) entries are prefetched one batch ahead, one per lane,
+// and broadcast by shuffle; row ends are cached 32 at a time across lanes.
+// Accumulation order per output element is unchanged: ascending CSC position.
+// ---------------------------------------------------------------------------
+template <typename T, int VB, int NV, int U, int MODE, bool SCALED>
+__global__ void __launch_bounds__(256, 3) spmm_flat_kernel(const SpmmArgs p) {
+  constexpr bool MAXMIN = MODE == 2;
+  constexpr bool MEAN = MODE == 1;
+  using VecT = Vec<T, VB>;
+  using A = typename VecT::A;
+  using R = typename VecT::R;
+  constexpr int V = VecT::V;
+  constexpr unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (warp >= p.num_light_windows) return;
+
+  const T* __restrict__ x = static_cast<const T*>(p.x);
+  T* __restrict__ out = static_cast<T*>(p.out);
+  const int32_t* __restrict__ col = p.col;
+  const bool want_arg = MAXMIN && p.arg != nullptr;
+
+  int64_t slot[NV];
+  bool valid[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    slot[j] = p.slot_base + lane + j * 32;
+    valid[j] = slot[j] < p.slot_end;
+  }
+
+  const int ra = p.light_windows[2 * warp];
+  const int rb = p.light_windows[2 * warp + 1];
+  const int64_t kbeg = p.rowptr[ra];
+  const int64_t kend = p.rowptr[rb];
+
+  // lane l caches the end of row cbase + l
+  int cbase = ra;
+  int64_t rend_l = (cbase + lane < rb) ? p.rowptr[cbase + 1 + lane] : kend;
+  int row = ra;
+  int64_t row_start = kbeg;
+  int64_t row_end = __shfl_sync(FULL, rend_l, 0);
+
+  Acc<A, NV, V, MAXMIN> acc;
+  acc.init();
+  bool first = true;
+
+  auto flush = [&]() {
+    if (MEAN) {
+      const int64_t cnt = row_end - row_start;
+      if (cnt > 0) {
+        const A inv = div_rn(A(1), static_cast<A>(cnt));  // message_passing.hpp:81
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+#pragma unroll
+          for (int e = 0; e < V; ++e) acc.v[j][e] = mul_rn(acc.v[j][e], inv);
+      }
+    }
+    T* orow = out + static_cast<int64_t>(row) * p.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+      if (valid[j]) {
+        VecT::store_global(orow + slot[j] * V, acc.v[j]);
+        if (want_arg) {
+          int32_t* arow = p.arg + static_cast<int64_t>(row) * p.f + slot[j] * V;
+#pragma unroll
+          for (int e = 0; e < V; ++e) arow[e] = acc.a[j][e];
+        }
+      }
+    acc.init();
+    first = true;
+    ++row;
+    row_start = row_end;
+    if (row < rb) {
+      if (row - cbase >= 32) {
+        cbase = row;
+        rend_l = (cbase + lane < rb) ? p.rowptr[cbase + 1 + lane] : kend;
+      }
+      row_end = __shfl_sync(FULL, rend_l, row - cbase);
+    }
+  };
+
+  int32_t c_next = 0, p_next = -1;
+  A w_next = A(1);
+  auto fetch = [&](int64_t kb) {
+    const int64_t k = kb + lane;
+    if (lane < U && k < kend) {
+      c_next = col[k];
+      if (SCALED) w_next = static_cast<const A*>(p.w)[k];
+      if (MAXMIN) p_next = want_arg ? p.perm[k] : -1;
+    }
+  };
+  fetch(kbeg);
+
+  for (int64_t k0 = kbeg; k0 < kend; k0 += U) {
+    const int32_t c_cur = c_next;
+    const int32_t p_cur = p_next;
+    const A w_cur = w_next;
+    fetch(k0 + U);
+    R buf[U][NV];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int32_t cu = __shfl_sync(FULL, c_cur, u);
+      if (k0 + u < kend) {
+        const T* xr = x + static_cast<int64_t>(cu) * p.f;
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+          if (valid[j]) buf[u][j] = VecT::load_raw(xr + slot[j] * V);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const A sc = SCALED ? __shfl_sync(FULL, w_cur, u) : A(1);
+      const int32_t pm = MAXMIN ? __shfl_sync(FULL, p_cur, u) : -1;
+      if (k0 + u < kend) {
+        while (k0 + u >= row_end) flush();
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+          if (valid[j]) {
+            A vals[V];
+            VecT::unpack(buf[u][j], vals);
+            acc.add(j, vals, SCALED, sc, first, p.is_min, pm);
+          }
+        first = false;
+      }
+    }
+  }
+  while (row < rb) flush();
 }
 
 // ---------------------------------------------------------------------------
@@ -433,7 +570,46 @@ static gm_status ensure_smem(K kernel, size_t bytes) {
 }
 
 template <typename T, int VB, bool MAXMIN>
+static gm_status launch_flat(const SpmmArgs& p0, int64_t ns, cudaStream_t st) {
+  const bool scaled = p0.w != nullptr;
+  // at most 32 accumulator elements per lane: 8 float4, 4 bf16x8, 8 double2
+  constexpr int kV = VB / static_cast<int>(sizeof(T));
+  constexpr int64_t kChunk = 32 * std::min(8, std::max(1, 32 / kV));
+  for (int64_t base = 0; base < ns; base += kChunk) {
+    SpmmArgs p = p0;
+    p.slot_base = base;
+    p.slot_end = std::min<int64_t>(ns, base + kChunk);
+    const int64_t slots = p.slot_end - base;
+    const int nv = slots <= 32 ? 1 : slots <= 64 ? 2 : slots <= 128 ? 4 : 8;
+    const unsigned grid = static_cast<unsigned>(ceil_div(p.num_light_windows * 32, 256));
+    if (grid == 0) continue;
+#define GM_FLAT_M(NV_, U_, M_)                                                       \
+  do {                                                                               \
+    if (scaled) spmm_flat_kernel<T, VB, NV_, U_, M_, true><<<grid, 256, 0, st>>>(p);   \
+    else spmm_flat_kernel<T, VB, NV_, U_, M_, false><<<grid, 256, 0, st>>>(p);         \
+  } while (0)
+#define GM_FLAT(NV_, U_)                               \
+  do {                                                 \
+    if constexpr (MAXMIN) GM_FLAT_M(NV_, U_, 2);       \
+    else if (p.mean) GM_FLAT_M(NV_, U_, 1);            \
+    else GM_FLAT_M(NV_, U_, 0);                        \
+  } while (0)
+    if (nv == 1) GM_FLAT(1, 8);
+    else if (nv == 2) GM_FLAT(2, 4);
+    else if (nv == 4 || kChunk <= 128) GM_FLAT(4, 2);
+    else if constexpr (kChunk > 128) GM_FLAT(8, 1);
+#undef GM_FLAT
+#undef GM_FLAT_M
+    GM_CHECK_LAUNCH("spmm_flat_kernel");
+  }
+  return GM_OK;
+}
+
+template <typename T, int VB, bool MAXMIN>
 static gm_status launch_light(const SpmmArgs& p0, int64_t ns, cudaStream_t st) {
+  // wide rows without the fused GCN term take the flat edge-stream kernel
+  if (p0.gdeg_src == nullptr && ns > 8 && p0.flat_ok)
+    return launch_flat<T, VB, MAXMIN>(p0, ns, st);
   // chunk columns so a lane holds <= 8 vectors; pick LPR/NV per chunk
   for (int64_t base = 0; base < ns; base += 256) {
     SpmmArgs p = p0;
@@ -534,6 +710,7 @@ GM_API size_t gm_spmm_plan_bytes(int64_t num_rows, int64_t nnz) {
   b += align_up(static_cast<size_t>(plan_heavy_cap(num_rows, nnz)) * sizeof(int32_t), 256);
   b += align_up(static_cast<size_t>(plan_heavy_cap(num_rows, nnz)) * sizeof(unsigned long long), 256);
   b += 256;  // counter
+  b += align_up(static_cast<size_t>(2 * (g + plan_heavy_cap(num_rows, nnz))) * sizeof(int32_t), 256);
   return b;
 }
 
@@ -557,6 +734,8 @@ GM_API gm_status gm_spmm_plan_build(const gm_csr* csr, void* buffer, size_t buff
   unsigned long long* keys = reinterpret_cast<unsigned long long*>(b);
   b += align_up(static_cast<size_t>(cap) * sizeof(unsigned long long), 256);
   unsigned int* count = reinterpret_cast<unsigned int*>(b);
+  b += 256;
+  int32_t* light = reinterpret_cast<int32_t*>(b);
 
   plan_windows_kernel<<<static_cast<unsigned>(ceil_div(g + 1, 256)), 256, 0, st>>>(
       csr->rowptr, csr->num_rows, g, win_row);
@@ -569,8 +748,11 @@ GM_API gm_status gm_spmm_plan_build(const gm_csr* csr, void* buffer, size_t buff
   }
   unsigned int n_heavy = 0;
   GM_TRY_CUDA(cudaMemcpyAsync(&n_heavy, count, sizeof(n_heavy), cudaMemcpyDeviceToHost, st));
+  std::vector<int32_t> wr(static_cast<size_t>(g + 1));
+  GM_TRY_CUDA(cudaMemcpyAsync(wr.data(), win_row, (g + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   GM_TRY_CUDA(cudaStreamSynchronize(st));
   const int64_t nh = std::min<int64_t>(n_heavy, cap);
+  std::vector<int32_t> heavy_sorted;
   if (nh > 0) {
     std::vector<unsigned long long> hk(static_cast<size_t>(nh));
     GM_TRY_CUDA(cudaMemcpyAsync(hk.data(), keys, nh * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
@@ -580,6 +762,33 @@ GM_API gm_status gm_spmm_plan_build(const gm_csr* csr, void* buffer, size_t buff
     for (int64_t i = 0; i < nh; ++i) rows[static_cast<size_t>(i)] = static_cast<int32_t>(hk[static_cast<size_t>(i)] & 0xffffffffull);
     GM_TRY_CUDA(cudaMemcpyAsync(heavy_rows, rows.data(), nh * sizeof(int32_t), cudaMemcpyHostToDevice, st));
     GM_TRY_CUDA(cudaStreamSynchronize(st));
+    heavy_sorted = rows;
+    std::sort(heavy_sorted.begin(), heavy_sorted.end());
+  }
+  // heavy-free windows: split every window around the heavy rows inside it
+  std::vector<int32_t> lw;
+  lw.reserve(static_cast<size_t>(2 * (g + nh)));
+  size_t hi = 0;
+  for (int64_t w = 0; w < g; ++w) {
+    int32_t a = wr[static_cast<size_t>(w)];
+    const int32_t bnd = wr[static_cast<size_t>(w) + 1];
+    while (hi < heavy_sorted.size() && heavy_sorted[hi] < a) ++hi;
+    while (hi < heavy_sorted.size() && heavy_sorted[hi] < bnd) {
+      const int32_t h = heavy_sorted[hi++];
+      if (a < h) {
+        lw.push_back(a);
+        lw.push_back(h);
+      }
+      a = h + 1;
+    }
+    if (a < bnd) {
+      lw.push_back(a);
+      lw.push_back(bnd);
+    }
+  }
+  if (!lw.empty()) {
+    GM_TRY_CUDA(cudaMemcpyAsync(light, lw.data(), lw.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    GM_TRY_CUDA(cudaStreamSynchronize(st));
   }
   plan->num_windows = g;
   plan->window_edges = kWindowCost;
@@ -587,6 +796,8 @@ GM_API gm_status gm_spmm_plan_build(const gm_csr* csr, void* buffer, size_t buff
   plan->heavy_threshold = kHeavyThreshold;
   plan->win_row = win_row;
   plan->heavy_rows = heavy_rows;
+  plan->num_light_windows = static_cast<int64_t>(lw.size() / 2);
+  plan->light_windows = light;
   return GM_OK;
 }
 
@@ -635,9 +846,12 @@ GM_API gm_status gm_spmm(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype d
   p.win_row = plan->win_row;
   p.num_windows = plan->num_windows;
   p.heavy_rows = plan->heavy_rows;
+  p.light_windows = plan->light_windows;
+  p.num_light_windows = plan->num_light_windows;
   // cp.async moves >= 4-byte granules: narrower rows keep hubs on the light path
   const bool use_heavy = plan->num_heavy > 0 && vb >= 4;
   p.heavy_thr = use_heavy ? plan->heavy_threshold : INT64_MAX;
+  p.flat_ok = plan->num_heavy == 0 || use_heavy;
   cudaStream_t st = as_stream(stream);
 
   switch (dtype) {

@@ -105,6 +105,17 @@ struct Vec {
   __device__ __forceinline__ void load_shared(const T* p) {
     from_raw(*reinterpret_cast<const R*>(p));
   }
+  // Raw (still packed) gather, widened later at consume time: keeps bf16
+  // batches at half the registers.
+  __device__ static __forceinline__ R load_raw(const T* p) {
+    return ldg_na<R>(reinterpret_cast<const R*>(p));
+  }
+  __device__ static __forceinline__ void unpack(const R& r, A* out) {
+    T tmp[V];
+    memcpy(tmp, &r, VB);
+#pragma unroll
+    for (int i = 0; i < V; ++i) out[i] = widen(tmp[i]);
+  }
   __device__ static __forceinline__ void store_global(T* p, const A* vals) {
     T tmp[V];
 #pragma unroll
