@@ -124,9 +124,17 @@ typedef struct gm_spmm_plan {
    * heavy-free row runs, streamed edge-contiguously by the flat kernel. */
   int64_t num_light_windows;
   const int32_t* light_windows;
+  /* L2 residency hint (B200: 126 MB L2). Per compressed entry, the hotness
+   * class of its source row: floor(4*log2(1 + G)), G = number of source rows
+   * with a strictly larger out-degree. Gathers of rows whose class fits the
+   * l2_hot_bytes budget use an L2 evict_last policy, all others evict_first,
+   * so power-law hub rows stay L2-resident for the whole sweep. The caller
+   * may change l2_hot_bytes between calls (0 disables the hint). */
+  const uint8_t* src_class;
+  int64_t l2_hot_bytes;
 } gm_spmm_plan;
 
-GM_API size_t gm_spmm_plan_bytes(int64_t num_rows, int64_t nnz);
+GM_API size_t gm_spmm_plan_bytes(int64_t num_rows, int64_t num_cols, int64_t nnz);
 /* Builds the plan into `buffer` (device, gm_spmm_plan_bytes) and fills
  * *plan_host. Synchronizes once (reads the heavy-row count). */
 GM_API gm_status gm_spmm_plan_build(const gm_csr* csr, void* buffer, size_t buffer_bytes,

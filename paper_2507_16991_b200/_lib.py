@@ -46,6 +46,8 @@ class gm_spmm_plan(C.Structure):
         ("heavy_rows", C.c_void_p),
         ("num_light_windows", C.c_int64),
         ("light_windows", C.c_void_p),
+        ("src_class", C.c_void_p),
+        ("l2_hot_bytes", C.c_int64),
     ]
 
 
@@ -67,7 +69,7 @@ SIGNATURES = {
     "gm_build_compressed_workspace": (C.c_size_t, [_I64, _I64]),
     "gm_build_compressed": (C.c_int, [_P, _P, _I64, _I64, _P, _P, _P, _P, C.c_size_t, _P]),
     "gm_permute_edge_values": (C.c_int, [C.c_int, _P, _P, _I64, _P, _P]),
-    "gm_spmm_plan_bytes": (C.c_size_t, [_I64, _I64]),
+    "gm_spmm_plan_bytes": (C.c_size_t, [_I64, _I64, _I64]),
     "gm_spmm_plan_build": (C.c_int, [C.POINTER(gm_csr), _P, C.c_size_t, C.POINTER(gm_spmm_plan), _P]),
     "gm_gcn_degrees": (C.c_int, [_P, _P, _I64, _I64, _I64, C.c_int, _P, _P, _P]),
     "gm_spmm": (C.c_int, [C.POINTER(gm_csr), C.POINTER(gm_spmm_plan), C.c_int, _P, _I64, _P,

@@ -23,6 +23,8 @@
 //     feature rows into a cp.async shared-memory ring (R stages of `se` edges)
 //     while the owning threads accumulate each column in order.
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "vec.cuh"
@@ -53,7 +55,51 @@ struct SpmmArgs {
   const int32_t* light_windows;  // (first_row, end_row) pairs, heavy-free
   int64_t num_light_windows;
   int flat_ok;                   // heavy rows (if any) are covered by the hub kernel
+  const uint8_t* src_class;      // per-entry source hotness class (NULL: no L2 hint)
+  int hot_class_limit;           // entries with class < limit gather with evict_last
 };
+
+// L2 eviction-priority policies (createpolicy; PTX ISA "Cache eviction priority hints").
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+template <typename R>
+__device__ __forceinline__ R ldg_hint(const R* p, uint64_t pol);
+template <>
+__device__ __forceinline__ uint4 ldg_hint<uint4>(const uint4* p, uint64_t pol) {
+  uint4 r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p), "l"(pol));
+  return r;
+}
+template <>
+__device__ __forceinline__ uint2 ldg_hint<uint2>(const uint2* p, uint64_t pol) {
+  uint2 r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+      : "=r"(r.x), "=r"(r.y)
+      : "l"(p), "l"(pol));
+  return r;
+}
+template <>
+__device__ __forceinline__ uint32_t ldg_hint<uint32_t>(const uint32_t* p, uint64_t pol) {
+  uint32_t r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
+}
+template <>
+__device__ __forceinline__ unsigned short ldg_hint<unsigned short>(const unsigned short* p, uint64_t pol) {
+  unsigned short r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(r) : "l"(p), "l"(pol));
+  return r;
+}
 
 template <typename A>
 __device__ __forceinline__ A gcn_scale(int32_t ds, int32_t dd) {
@@ -211,7 +257,7 @@ __global__ void __launch_bounds__(256) spmm_light_kernel(const SpmmArgs p) {
 // Accumulation order per output element is unchanged: ascending CSC position.
 // ---------------------------------------------------------------------------
 template <typename T, int VB, int NV, int U, int MODE, bool SCALED>
-__global__ void __launch_bounds__(256, 3) spmm_flat_kernel(const SpmmArgs p) {
+__global__ void __launch_bounds__(256, (MODE == 2 || SCALED || sizeof(T) == 8) ? 3 : 4) spmm_flat_kernel(const SpmmArgs p) {
   constexpr bool MAXMIN = MODE == 2;
   constexpr bool MEAN = MODE == 1;
   using VecT = Vec<T, VB>;
@@ -227,26 +273,29 @@ __global__ void __launch_bounds__(256, 3) spmm_flat_kernel(const SpmmArgs p) {
   T* __restrict__ out = static_cast<T*>(p.out);
   const int32_t* __restrict__ col = p.col;
   const bool want_arg = MAXMIN && p.arg != nullptr;
+  const uint32_t fu = static_cast<uint32_t>(p.f);  // row stride (elements)
 
-  int64_t slot[NV];
+  uint32_t soff[NV];  // element offset of this lane's vector j inside a row
   bool valid[NV];
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
-    slot[j] = p.slot_base + lane + j * 32;
-    valid[j] = slot[j] < p.slot_end;
+    const int64_t sl = p.slot_base + lane + j * 32;
+    valid[j] = sl < p.slot_end;
+    soff[j] = static_cast<uint32_t>(sl * V);
   }
 
+  // Positions fit int32: gm_build_compressed / plan_build require nnz < 2^31.
   const int ra = p.light_windows[2 * warp];
   const int rb = p.light_windows[2 * warp + 1];
-  const int64_t kbeg = p.rowptr[ra];
-  const int64_t kend = p.rowptr[rb];
+  const int32_t kbeg = static_cast<int32_t>(p.rowptr[ra]);
+  const int32_t kend = static_cast<int32_t>(p.rowptr[rb]);
 
   // lane l caches the end of row cbase + l
   int cbase = ra;
-  int64_t rend_l = (cbase + lane < rb) ? p.rowptr[cbase + 1 + lane] : kend;
+  int32_t rend_l = (cbase + lane < rb) ? static_cast<int32_t>(p.rowptr[cbase + 1 + lane]) : kend;
   int row = ra;
-  int64_t row_start = kbeg;
-  int64_t row_end = __shfl_sync(FULL, rend_l, 0);
+  int32_t row_start = kbeg;
+  int32_t row_end = __shfl_sync(FULL, rend_l, 0);
 
   Acc<A, NV, V, MAXMIN> acc;
   acc.init();
@@ -254,7 +303,7 @@ __global__ void __launch_bounds__(256, 3) spmm_flat_kernel(const SpmmArgs p) {
 
   auto flush = [&]() {
     if (MEAN) {
-      const int64_t cnt = row_end - row_start;
+      const int32_t cnt = row_end - row_start;
       if (cnt > 0) {
         const A inv = div_rn(A(1), static_cast<A>(cnt));  // message_passing.hpp:81
 #pragma unroll
@@ -263,13 +312,13 @@ __global__ void __launch_bounds__(256, 3) spmm_flat_kernel(const SpmmArgs p) {
           for (int e = 0; e < V; ++e) acc.v[j][e] = mul_rn(acc.v[j][e], inv);
       }
     }
-    T* orow = out + static_cast<int64_t>(row) * p.f;
+    const uint64_t obase = static_cast<uint64_t>(static_cast<uint32_t>(row)) * fu;
 #pragma unroll
     for (int j = 0; j < NV; ++j)
       if (valid[j]) {
-        VecT::store_global(orow + slot[j] * V, acc.v[j]);
+        VecT::store_global(out + obase + soff[j], acc.v[j]);
         if (want_arg) {
-          int32_t* arow = p.arg + static_cast<int64_t>(row) * p.f + slot[j] * V;
+          int32_t* arow = p.arg + obase + soff[j];
 #pragma unroll
           for (int e = 0; e < V; ++e) arow[e] = acc.a[j][e];
         }
@@ -281,54 +330,85 @@ __global__ void __launch_bounds__(256, 3) spmm_flat_kernel(const SpmmArgs p) {
     if (row < rb) {
       if (row - cbase >= 32) {
         cbase = row;
-        rend_l = (cbase + lane < rb) ? p.rowptr[cbase + 1 + lane] : kend;
+        rend_l = (cbase + lane < rb) ? static_cast<int32_t>(p.rowptr[cbase + 1 + lane]) : kend;
       }
       row_end = __shfl_sync(FULL, rend_l, row - cbase);
     }
   };
 
-  int32_t c_next = 0, p_next = -1;
+  const bool hinted = p.src_class != nullptr;
+  const uint64_t pol_hot = policy_evict_last();
+  const uint64_t pol_cold = policy_evict_first();
+  int32_t c_next = 0, p_next = -1, h_next = 0;
   A w_next = A(1);
-  auto fetch = [&](int64_t kb) {
-    const int64_t k = kb + lane;
+  auto fetch = [&](int32_t kb) {
+    const int32_t k = kb + lane;
     if (lane < U && k < kend) {
       c_next = col[k];
+      if (hinted) h_next = p.src_class[k] < p.hot_class_limit;
       if (SCALED) w_next = static_cast<const A*>(p.w)[k];
       if (MAXMIN) p_next = want_arg ? p.perm[k] : -1;
     }
   };
   fetch(kbeg);
 
-  for (int64_t k0 = kbeg; k0 < kend; k0 += U) {
+  for (int32_t k0 = kbeg; k0 < kend; k0 += U) {
     const int32_t c_cur = c_next;
     const int32_t p_cur = p_next;
+    const int32_t h_cur = h_next;
     const A w_cur = w_next;
     fetch(k0 + U);
+    const int nb = min(U, kend - k0);  // edges in this batch
     R buf[U][NV];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int32_t cu = __shfl_sync(FULL, c_cur, u);
-      if (k0 + u < kend) {
-        const T* xr = x + static_cast<int64_t>(cu) * p.f;
+      const uint32_t cu = static_cast<uint32_t>(__shfl_sync(FULL, c_cur, u));
+      const int32_t hu = __shfl_sync(FULL, h_cur, u);
+      if (u < nb) {
+        const T* xr = x + static_cast<uint64_t>(cu) * fu;
+        if (hinted) {
+          const uint64_t pol = hu ? pol_hot : pol_cold;
 #pragma unroll
-        for (int j = 0; j < NV; ++j)
-          if (valid[j]) buf[u][j] = VecT::load_raw(xr + slot[j] * V);
+          for (int j = 0; j < NV; ++j)
+            if (valid[j]) buf[u][j] = ldg_hint<R>(reinterpret_cast<const R*>(xr + soff[j]), pol);
+        } else {
+#pragma unroll
+          for (int j = 0; j < NV; ++j)
+            if (valid[j]) buf[u][j] = VecT::load_raw(xr + soff[j]);
+        }
       }
     }
+    if (nb == U && k0 + U <= row_end) {
+      // fast path: the whole batch belongs to the current row
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const A sc = SCALED ? __shfl_sync(FULL, w_cur, u) : A(1);
-      const int32_t pm = MAXMIN ? __shfl_sync(FULL, p_cur, u) : -1;
-      if (k0 + u < kend) {
-        while (k0 + u >= row_end) flush();
+      for (int u = 0; u < U; ++u) {
+        const A sc = SCALED ? __shfl_sync(FULL, w_cur, u) : A(1);
+        const int32_t pm = MAXMIN ? __shfl_sync(FULL, p_cur, u) : -1;
 #pragma unroll
         for (int j = 0; j < NV; ++j)
           if (valid[j]) {
             A vals[V];
             VecT::unpack(buf[u][j], vals);
-            acc.add(j, vals, SCALED, sc, first, p.is_min, pm);
+            acc.add(j, vals, SCALED, sc, first && u == 0, p.is_min, pm);
           }
-        first = false;
+      }
+      first = false;
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const A sc = SCALED ? __shfl_sync(FULL, w_cur, u) : A(1);
+        const int32_t pm = MAXMIN ? __shfl_sync(FULL, p_cur, u) : -1;
+        if (u < nb) {
+          while (k0 + u >= row_end) flush();
+#pragma unroll
+          for (int j = 0; j < NV; ++j)
+            if (valid[j]) {
+              A vals[V];
+              VecT::unpack(buf[u][j], vals);
+              acc.add(j, vals, SCALED, sc, first, p.is_min, pm);
+            }
+          first = false;
+        }
       }
     }
   }
@@ -531,6 +611,25 @@ __global__ void plan_heavy_kernel(const int64_t* __restrict__ rowptr, int64_t nu
   }
 }
 
+constexpr int kDegBuckets = 65536;  // out-degrees >= 65535 share the hottest bucket
+
+__global__ void src_degree_kernel(const int32_t* __restrict__ col, int64_t nnz, int32_t* __restrict__ deg) {
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < nnz;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    atomicAdd(&deg[col[k]], 1);
+}
+__global__ void deg_hist_kernel(const int32_t* __restrict__ deg, int64_t n, int32_t* __restrict__ hist) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    atomicAdd(&hist[min(deg[i], kDegBuckets - 1)], 1);
+}
+__global__ void src_class_kernel(const int32_t* __restrict__ col, int64_t nnz, const int32_t* __restrict__ deg,
+                                 const uint8_t* __restrict__ table, uint8_t* __restrict__ cls) {
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < nnz;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    cls[k] = table[min(deg[col[k]], kDegBuckets - 1)];
+}
+
 static int64_t plan_num_windows(int64_t num_rows, int64_t nnz) {
   return std::max<int64_t>(1, ceil_div(nnz + num_rows, kWindowCost));
 }
@@ -703,14 +802,18 @@ using namespace gm;
 
 extern "C" {
 
-GM_API size_t gm_spmm_plan_bytes(int64_t num_rows, int64_t nnz) {
-  if (num_rows < 0 || nnz < 0) return 0;
+GM_API size_t gm_spmm_plan_bytes(int64_t num_rows, int64_t num_cols, int64_t nnz) {
+  if (num_rows < 0 || nnz < 0 || num_cols < 0) return 0;
   const int64_t g = plan_num_windows(num_rows, nnz);
   size_t b = align_up(static_cast<size_t>(g + 1) * sizeof(int32_t), 256);
   b += align_up(static_cast<size_t>(plan_heavy_cap(num_rows, nnz)) * sizeof(int32_t), 256);
   b += align_up(static_cast<size_t>(plan_heavy_cap(num_rows, nnz)) * sizeof(unsigned long long), 256);
   b += 256;  // counter
   b += align_up(static_cast<size_t>(2 * (g + plan_heavy_cap(num_rows, nnz))) * sizeof(int32_t), 256);
+  b += align_up(static_cast<size_t>(num_cols) * sizeof(int32_t), 256);  // source out-degrees
+  b += align_up(kDegBuckets * sizeof(int32_t), 256);                   // degree histogram
+  b += align_up(kDegBuckets, 256);                                     // degree -> class
+  b += align_up(static_cast<size_t>(nnz), 256);                        // per-entry class
   return b;
 }
 
@@ -719,7 +822,7 @@ GM_API gm_status gm_spmm_plan_build(const gm_csr* csr, void* buffer, size_t buff
   GM_REQUIRE(csr && plan, GM_ERR_INVALID_ARGUMENT, "gm_spmm_plan_build: null argument");
   GM_REQUIRE(csr->num_rows >= 0 && csr->nnz >= 0 && csr->num_rows < INT32_MAX && csr->nnz < INT32_MAX,
              GM_ERR_INVALID_ARGUMENT, "gm_spmm_plan_build: sizes must be in [0, 2^31)");
-  const size_t need = gm_spmm_plan_bytes(csr->num_rows, csr->nnz);
+  const size_t need = gm_spmm_plan_bytes(csr->num_rows, csr->num_cols, csr->nnz);
   GM_REQUIRE(buffer_bytes >= need, GM_ERR_INVALID_ARGUMENT,
              "gm_spmm_plan_build: buffer too small (" + std::to_string(buffer_bytes) + " < " +
                  std::to_string(need) + ")");
@@ -736,6 +839,14 @@ GM_API gm_status gm_spmm_plan_build(const gm_csr* csr, void* buffer, size_t buff
   unsigned int* count = reinterpret_cast<unsigned int*>(b);
   b += 256;
   int32_t* light = reinterpret_cast<int32_t*>(b);
+  b += align_up(static_cast<size_t>(2 * (g + cap)) * sizeof(int32_t), 256);
+  int32_t* sdeg = reinterpret_cast<int32_t*>(b);
+  b += align_up(static_cast<size_t>(csr->num_cols) * sizeof(int32_t), 256);
+  int32_t* dhist = reinterpret_cast<int32_t*>(b);
+  b += align_up(kDegBuckets * sizeof(int32_t), 256);
+  uint8_t* dtable = b;
+  b += align_up(kDegBuckets, 256);
+  uint8_t* cls = b;
 
   plan_windows_kernel<<<static_cast<unsigned>(ceil_div(g + 1, 256)), 256, 0, st>>>(
       csr->rowptr, csr->num_rows, g, win_row);
@@ -798,6 +909,41 @@ GM_API gm_status gm_spmm_plan_build(const gm_csr* csr, void* buffer, size_t buff
   plan->heavy_rows = heavy_rows;
   plan->num_light_windows = static_cast<int64_t>(lw.size() / 2);
   plan->light_windows = light;
+
+  // source hotness classes for the L2 residency hint
+  plan->src_class = nullptr;
+  plan->l2_hot_bytes = 0;
+  if (csr->num_cols > 0 && csr->nnz > 0) {
+    GM_TRY_CUDA(cudaMemsetAsync(sdeg, 0, csr->num_cols * sizeof(int32_t), st));
+    GM_TRY_CUDA(cudaMemsetAsync(dhist, 0, kDegBuckets * sizeof(int32_t), st));
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(ceil_div(csr->nnz, 256), kNumSMs * 16));
+    // a row slice's entries start at rowptr[0]
+    int64_t k0 = 0;
+    GM_TRY_CUDA(cudaMemcpyAsync(&k0, csr->rowptr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    GM_TRY_CUDA(cudaStreamSynchronize(st));
+    src_degree_kernel<<<grid, 256, 0, st>>>(csr->col + k0, csr->nnz, sdeg);
+    GM_CHECK_LAUNCH("src_degree_kernel");
+    deg_hist_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(csr->num_cols, 256), kNumSMs * 16)), 256, 0, st>>>(
+        sdeg, csr->num_cols, dhist);
+    GM_CHECK_LAUNCH("deg_hist_kernel");
+    std::vector<int32_t> hist(kDegBuckets);
+    GM_TRY_CUDA(cudaMemcpyAsync(hist.data(), dhist, kDegBuckets * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    GM_TRY_CUDA(cudaStreamSynchronize(st));
+    std::vector<uint8_t> table(kDegBuckets);
+    int64_t greater = 0;  // rows with a strictly larger out-degree
+    for (int d = kDegBuckets - 1; d >= 0; --d) {
+      const double c = std::floor(4.0 * std::log2(1.0 + static_cast<double>(greater)));
+      table[static_cast<size_t>(d)] = static_cast<uint8_t>(std::min(255.0, c));
+      greater += hist[static_cast<size_t>(d)];
+    }
+    GM_TRY_CUDA(cudaMemcpyAsync(dtable, table.data(), kDegBuckets, cudaMemcpyHostToDevice, st));
+    src_class_kernel<<<grid, 256, 0, st>>>(csr->col + k0, csr->nnz, sdeg, dtable, cls + 0);
+    GM_CHECK_LAUNCH("src_class_kernel");
+    GM_TRY_CUDA(cudaStreamSynchronize(st));
+    plan->src_class = cls - k0;  // indexed by global compressed position
+    const char* env = getenv("GM_L2_HOT_MB");
+    plan->l2_hot_bytes = (env ? atoll(env) : 64) << 20;
+  }
   return GM_OK;
 }
 
@@ -852,6 +998,14 @@ GM_API gm_status gm_spmm(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype d
   const bool use_heavy = plan->num_heavy > 0 && vb >= 4;
   p.heavy_thr = use_heavy ? plan->heavy_threshold : INT64_MAX;
   p.flat_ok = plan->num_heavy == 0 || use_heavy;
+  p.src_class = nullptr;
+  p.hot_class_limit = 0;
+  if (plan->src_class && plan->l2_hot_bytes > 0) {
+    // rows that fit the budget: rank < hot_rows  <=>  class < floor(4*log2(1 + hot_rows))
+    const double hot_rows = static_cast<double>(plan->l2_hot_bytes) / static_cast<double>(rowbytes);
+    p.src_class = plan->src_class;
+    p.hot_class_limit = static_cast<int>(std::floor(4.0 * std::log2(1.0 + hot_rows)));
+  }
   cudaStream_t st = as_stream(stream);
 
   switch (dtype) {

@@ -75,7 +75,7 @@ class CsrView:
         """Scheduling metadata (gm_spmm_plan), built once and cached."""
         if self._plan is None:
             lib = L.lib()
-            nbytes = lib.gm_spmm_plan_bytes(self.num_rows(), self.num_entries())
+            nbytes = lib.gm_spmm_plan_bytes(self.num_rows(), self.num_cols, self.num_entries())
             buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=self.rowptr.device)
             plan = L.gm_spmm_plan()
             csr = self.c_struct()
