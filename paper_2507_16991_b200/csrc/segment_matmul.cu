@@ -1,9 +1,496 @@
-// placeholder, replaced by the tcgen05 kernel
+// segment_matmul.cu — grouped GEMM over node-type segments on 5th-gen tensor
+// cores (tcgen05 / TMEM / TMA), sm_100a.
+//
+// Replaces grouped_matmul (hetero.hpp:134-157): for each group g,
+//   out[ptr[g]:ptr[g+1], :] = x[ptr[g]:ptr[g+1], :] @ W[g]        (W: [G, K, N])
+// bf16 operands, fp32 accumulation in TMEM, bf16 or fp32 output.
+//
+// Structure (persistent, one CTA per SM, 6 warps):
+//   warp 0  TMA producer: A k-blocks (128 rows x 64 k, SWIZZLE_128B) into an
+//           S-stage ring; W^T[g] either resident (loaded once per group run)
+//           or streamed per k-block when it does not fit.
+//   warp 1  TMEM allocator + single-thread MMA issuer: tcgen05.mma
+//           kind::f16, M=128, N=BN, K=16 steps; tcgen05.commit releases smem
+//           stages and signals the epilogue. Two TMEM accumulators so the
+//           epilogue of tile i overlaps the MMAs of tile i+1.
+//   warps 2-5 epilogue: tcgen05.ld 32x32b (each warp its TMEM lane quarter =
+//           32 output rows), convert, 16-byte stores of whole row segments;
+//           rows past the group end are masked (tiles never straddle groups).
+// Tiles: (group, 128-row m-tile, BN-column n-tile), group-major, assigned
+// round-robin to CTAs, so each CTA sees groups in non-decreasing order.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <mutex>
+#include <string>
+#include <vector>
+
 #include "gm_common.cuh"
+
+namespace gm {
+namespace gmm {
+
+constexpr int kMaxGroups = 128;
+constexpr int BM = 128;          // UMMA M (cta_group::1)
+constexpr int BK = 64;           // k elements per stage (128 B rows, SWIZZLE_128B)
+constexpr int kThreads = 192;    // 6 warps
+constexpr uint32_t kAStageBytes = BM * BK * 2;  // 16 KB
+
+struct Params {
+  int64_t ptr[kMaxGroups + 1];        // group row offsets
+  int32_t tile_start[kMaxGroups + 1]; // first m-tile id of each group (n-tiles folded in)
+  int32_t groups;
+  int32_t num_tiles;
+  int32_t n_tiles;                    // BN-wide column tiles
+  int32_t k_blocks;                   // K / 64
+  int32_t n;                          // total output columns
+  int32_t bn;                         // columns per tile (<= 256)
+  int32_t out_f32;
+  int32_t stages;
+  int32_t b_resident;
+  uint32_t tmem_cols;
+  void* out;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                            int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// K-major, SWIZZLE_128B smem matrix descriptor: 8-row x 128-byte atoms,
+// atoms 1024 B apart (SBO), LBO unused (1), version 1 (sm_100).
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
+  uint64_t d = static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(1) << 16;
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(2) << 61;
+  return d;
+}
+// Instruction descriptor: bf16 x bf16 -> f32, both K-major, M=128, N=bn.
+__device__ __forceinline__ uint32_t idesc_bf16(int bn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(bn >> 3) << 17) |
+         (static_cast<uint32_t>(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void decode_tile(const Params& P, int t, int& g, int& mt, int& nt) {
+  g = 0;
+  while (g + 1 < P.groups && P.tile_start[g + 1] <= t) ++g;
+  const int local = t - P.tile_start[g];
+  mt = local / P.n_tiles;
+  nt = local - mt * P.n_tiles;
+}
+
+template <int CHUNK>
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v);
+template <>
+__device__ __forceinline__ void tmem_ld32<32>(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+template <>
+__device__ __forceinline__ void tmem_ld32<16>(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ void st_na_v4(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.global.L1::no_allocate.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
+__device__ __forceinline__ uint32_t pack_bf16(uint32_t lo_f32, uint32_t hi_f32) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(lo_f32), __uint_as_float(hi_f32));
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ CUtensorMap map_a,
+                      const __grid_constant__ CUtensorMap map_b) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-B alignment for the SWIZZLE_128B atoms
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int S = P.stages;
+  const uint32_t b_kblock_bytes = static_cast<uint32_t>(P.bn) * BK * 2;
+  unsigned char* a_ring = smem;
+  unsigned char* b_buf = smem + static_cast<size_t>(S) * kAStageBytes;
+  const size_t b_bytes = P.b_resident ? static_cast<size_t>(P.k_blocks) * b_kblock_bytes
+                                      : static_cast<size_t>(S) * b_kblock_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(b_buf + b_bytes);
+  uint64_t* full = bars;              // [S]
+  uint64_t* empty = bars + S;         // [S]
+  uint64_t* tfull = bars + 2 * S;     // [2]
+  uint64_t* tempty = bars + 2 * S + 2;// [2]
+  uint64_t* bfull = bars + 2 * S + 4;
+  uint64_t* bempty = bars + 2 * S + 5;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 6);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+    }
+    mbar_init(bfull, 1);
+    mbar_init(bempty, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(P.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      int cur_g = -1;
+      uint32_t nbload = 0;
+      for (int t = blockIdx.x; t < P.num_tiles; t += gridDim.x) {
+        int g, mt, nt;
+        decode_tile(P, t, g, mt, nt);
+        const int row0 = static_cast<int>(P.ptr[g]) + mt * BM;
+        const int brow0 = g * P.n + nt * P.bn;
+        if (P.b_resident && g != cur_g) {
+          if (nbload > 0) mbar_wait(bempty, (nbload - 1) & 1);
+          mbar_expect_tx(bfull, static_cast<uint32_t>(P.k_blocks) * b_kblock_bytes);
+          for (int kb = 0; kb < P.k_blocks; ++kb)
+            tma_load_2d(b_buf + static_cast<size_t>(kb) * b_kblock_bytes, &map_b, bfull, kb * BK, brow0);
+          cur_g = g;
+          ++nbload;
+        }
+        for (int kb = 0; kb < P.k_blocks; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          if (P.b_resident) {
+            mbar_expect_tx(&full[s], kAStageBytes);
+          } else {
+            mbar_expect_tx(&full[s], kAStageBytes + b_kblock_bytes);
+            tma_load_2d(b_buf + static_cast<size_t>(s) * b_kblock_bytes, &map_b, &full[s], kb * BK, brow0);
+          }
+          tma_load_2d(a_ring + static_cast<size_t>(s) * kAStageBytes, &map_a, &full[s], kb * BK, row0);
+          if (++s == S) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    const uint32_t idesc = idesc_bf16(P.bn);
+    int s = 0;
+    uint32_t ph = 0;
+    int acc = 0;
+    uint32_t aph = 0;
+    int cur_g = -1;
+    uint32_t nbwait = 0;
+    for (int t = blockIdx.x; t < P.num_tiles; t += gridDim.x) {
+      int g, mt, nt;
+      decode_tile(P, t, g, mt, nt);
+      if (P.b_resident && g != cur_g) {
+        mbar_wait(bfull, nbwait & 1);
+        ++nbwait;
+        cur_g = g;
+      }
+      mbar_wait(&tempty[acc], aph ^ 1);
+      tc_fence_after();
+      const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * P.bn);
+      for (int kb = 0; kb < P.k_blocks; ++kb) {
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a_addr = smem_u32(a_ring + static_cast<size_t>(s) * kAStageBytes);
+          const uint32_t b_addr = P.b_resident ? smem_u32(b_buf + static_cast<size_t>(kb) * b_kblock_bytes)
+                                               : smem_u32(b_buf + static_cast<size_t>(s) * b_kblock_bytes);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // advancing 16 bf16 = 32 B inside the 128-B swizzle atom
+            tc_mma(tmem_d, sdesc_sw128(a_addr + k * 32), sdesc_sw128(b_addr + k * 32), idesc,
+                   (kb > 0 || k > 0) ? 1u : 0u);
+          }
+          tc_commit(&empty[s]);  // smem stage free once these MMAs retire
+        }
+        __syncwarp();
+        if (++s == S) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+      if (lane == 0) {
+        tc_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        if (P.b_resident) {
+          const int tn = t + static_cast<int>(gridDim.x);
+          int g2 = -1, m2, n2;
+          if (tn < P.num_tiles) decode_tile(P, tn, g2, m2, n2);
+          if (g2 != g) tc_commit(bempty);  // W^T[g] no longer read by this CTA
+        }
+      }
+      __syncwarp();
+      if (++acc == 2) {
+        acc = 0;
+        aph ^= 1;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int t = blockIdx.x; t < P.num_tiles; t += gridDim.x) {
+      int g, mt, nt;
+      decode_tile(P, t, g, mt, nt);
+      const int64_t grow_end = P.ptr[g + 1];
+      const int64_t row = P.ptr[g] + static_cast<int64_t>(mt) * BM + q * 32 + lane;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * P.bn);
+      const bool live = row < grow_end;
+      for (int c = 0; c < P.bn; c += 32) {
+        uint32_t v[32];
+        const int width = min(32, P.bn - c);
+        if (width == 32) tmem_ld32<32>(tbase + c, v);
+        else tmem_ld32<16>(tbase + c, v);
+        tmem_wait_ld();
+        if (live) {
+          const int64_t col0 = static_cast<int64_t>(nt) * P.bn + c;
+          if (P.out_f32) {
+            float* o = static_cast<float*>(P.out) + row * P.n + col0;
+            for (int i = 0; i < width; i += 4) st_na_v4(o + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
+          } else {
+            __nv_bfloat16* o = static_cast<__nv_bfloat16*>(P.out) + row * P.n + col0;
+            for (int i = 0; i < width; i += 8)
+              st_na_v4(o + i, pack_bf16(v[i], v[i + 1]), pack_bf16(v[i + 2], v[i + 3]),
+                       pack_bf16(v[i + 4], v[i + 5]), pack_bf16(v[i + 6], v[i + 7]));
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        aph ^= 1;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(P.tmem_cols)
+                 : "memory");
+  }
+}
+
+// W[g] [K, N] row-major -> W^T [G*N, K] (K-major B operand)
+__global__ void transpose_w_kernel(const __nv_bfloat16* __restrict__ w, int groups, int k, int n,
+                                   __nv_bfloat16* __restrict__ wt) {
+  const int64_t total = static_cast<int64_t>(groups) * k * n;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t g = i / (static_cast<int64_t>(k) * n);
+    const int64_t rem = i - g * k * n;
+    const int64_t kk = rem / n;
+    const int64_t nn = rem - kk * n;
+    wt[(g * n + nn) * k + kk] = w[i];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+static gm_status make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                          uint32_t box_outer) {
+  EncodeTiledFn fn = encode_fn();
+  GM_REQUIRE(fn, GM_ERR_CUDA, "segment_matmul: cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {inner * 2};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  GM_REQUIRE(r == CUDA_SUCCESS, GM_ERR_CUDA, "segment_matmul: cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+  return GM_OK;
+}
+
+}  // namespace gmm
+}  // namespace gm
+
+using namespace gm;
+
 extern "C" {
-GM_API size_t gm_segment_matmul_workspace(int64_t, int64_t, int64_t) { return 0; }
-GM_API gm_status gm_segment_matmul(const void*, const int64_t*, int64_t, int64_t, int64_t, const void*,
-                                   gm_dtype, void*, void*, size_t, gm_stream_t) {
-  return gm::fail(GM_ERR_UNSUPPORTED, "segment_matmul: not built");
+
+GM_API size_t gm_segment_matmul_workspace(int64_t groups, int64_t k, int64_t n) {
+  if (groups < 0 || k < 0 || n < 0) return 0;
+  return align_up(static_cast<size_t>(groups * k * n) * 2, 256);
 }
+
+GM_API gm_status gm_segment_matmul(const void* x, const int64_t* ptr_host, int64_t groups, int64_t k, int64_t n,
+                                   const void* w, gm_dtype out_dtype, void* out, void* workspace,
+                                   size_t workspace_bytes, gm_stream_t stream) {
+  using namespace gm::gmm;
+  GM_REQUIRE(ptr_host && groups >= 1 && groups <= kMaxGroups, GM_ERR_INVALID_ARGUMENT,
+             "segment_matmul: groups must be in [1, " + std::to_string(kMaxGroups) + "]");
+  GM_REQUIRE(k > 0 && k % BK == 0, GM_ERR_INVALID_ARGUMENT, "segment_matmul: K must be a positive multiple of 64");
+  GM_REQUIRE(n > 0 && n % 16 == 0, GM_ERR_INVALID_ARGUMENT, "segment_matmul: N must be a positive multiple of 16");
+  GM_REQUIRE(out_dtype == GM_BF16 || out_dtype == GM_F32, GM_ERR_INVALID_ARGUMENT,
+             "segment_matmul: out dtype must be bf16 or f32");
+  GM_REQUIRE(ptr_host[0] == 0, GM_ERR_INVALID_ARGUMENT, "segment_matmul: ptr[0] must be 0");
+  for (int64_t g = 0; g < groups; ++g)
+    GM_REQUIRE(ptr_host[g + 1] >= ptr_host[g], GM_ERR_INVALID_ARGUMENT, "segment_matmul: ptr must be non-decreasing");
+  const int64_t rows = ptr_host[groups];
+  GM_REQUIRE(rows < INT32_MAX, GM_ERR_INVALID_ARGUMENT, "segment_matmul: too many rows");
+  if (rows == 0) return GM_OK;
+  GM_REQUIRE(x && w && out, GM_ERR_INVALID_ARGUMENT, "segment_matmul: null pointer");
+  GM_REQUIRE((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(out)) % 16 == 0,
+             GM_ERR_INVALID_ARGUMENT, "segment_matmul: x, w and out must be 16-byte aligned");
+  const size_t need = gm_segment_matmul_workspace(groups, k, n);
+  GM_REQUIRE(workspace && workspace_bytes >= need, GM_ERR_INVALID_ARGUMENT, "segment_matmul: workspace too small");
+  cudaStream_t st = as_stream(stream);
+
+  Params P{};
+  P.groups = static_cast<int32_t>(groups);
+  P.bn = static_cast<int32_t>(std::min<int64_t>(n, 256));
+  while (n % P.bn != 0) P.bn -= 16;
+  P.n_tiles = static_cast<int32_t>(n / P.bn);
+  P.k_blocks = static_cast<int32_t>(k / BK);
+  P.n = static_cast<int32_t>(n);
+  P.out_f32 = out_dtype == GM_F32;
+  P.out = out;
+  int32_t tiles = 0;
+  for (int64_t g = 0; g < groups; ++g) {
+    P.ptr[g] = ptr_host[g];
+    P.tile_start[g] = tiles;
+    tiles += static_cast<int32_t>(ceil_div(ptr_host[g + 1] - ptr_host[g], BM)) * P.n_tiles;
+  }
+  P.ptr[groups] = ptr_host[groups];
+  P.tile_start[groups] = tiles;
+  P.num_tiles = tiles;
+  uint32_t cols = 32;
+  while (cols < static_cast<uint32_t>(2 * P.bn)) cols <<= 1;
+  P.tmem_cols = cols;
+
+  const size_t b_full_bytes = static_cast<size_t>(P.k_blocks) * P.bn * BK * 2;
+  const size_t b_stage_bytes = static_cast<size_t>(P.bn) * BK * 2;
+  P.b_resident = (P.n_tiles == 1 && b_full_bytes <= 64 * 1024) ? 1 : 0;
+  const size_t budget = 227 * 1024 - 1024 - 256;  // alignment slack + barriers
+  int stages;
+  if (P.b_resident) stages = static_cast<int>((budget - b_full_bytes) / kAStageBytes);
+  else stages = static_cast<int>(budget / (kAStageBytes + b_stage_bytes));
+  stages = std::max(2, std::min(stages, 8));
+  P.stages = stages;
+  const size_t smem = 1024 + static_cast<size_t>(stages) * kAStageBytes +
+                      (P.b_resident ? b_full_bytes : static_cast<size_t>(stages) * b_stage_bytes) + 256;
+
+  // K-major copy of the weights: W^T as a [G*N, K] bf16 matrix
+  __nv_bfloat16* wt = static_cast<__nv_bfloat16*>(workspace);
+  transpose_w_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(groups * k * n, 256), 4096)), 256, 0, st>>>(
+      static_cast<const __nv_bfloat16*>(w), static_cast<int>(groups), static_cast<int>(k), static_cast<int>(n), wt);
+  GM_CHECK_LAUNCH("transpose_w_kernel");
+
+  CUtensorMap map_a, map_b;
+  gm_status s = make_map(&map_a, x, static_cast<uint64_t>(k), static_cast<uint64_t>(rows), BK, BM);
+  if (s != GM_OK) return s;
+  s = make_map(&map_b, wt, static_cast<uint64_t>(k), static_cast<uint64_t>(groups * n), BK, static_cast<uint32_t>(P.bn));
+  if (s != GM_OK) return s;
+
+  static std::once_flag attr_once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(attr_once, [] {
+    attr_err = cudaFuncSetAttribute(segment_matmul_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  });
+  GM_TRY_CUDA(attr_err);
+  const unsigned grid = static_cast<unsigned>(std::min<int32_t>(tiles, kNumSMs));
+  segment_matmul_kernel<<<grid, kThreads, smem, st>>>(P, map_a, map_b);
+  GM_CHECK_LAUNCH("segment_matmul_kernel");
+  return GM_OK;
 }
+
+}  // extern "C"

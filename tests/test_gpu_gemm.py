@@ -1,0 +1,96 @@
+"""segment_matmul (tcgen05 grouped GEMM) parity on B200.
+
+Tolerance (stated, bf16 path — SURVEY.md §7.2/§8c): inputs are bf16 (rounded
+on both sides), products are exact in fp32 and accumulate in fp32, so against
+the fp64 oracle on the same rounded inputs
+    |gpu - ref64| <= 1e-5 * sum_k |a_ik b_kj| + 1e-7             (fp32 output)
+    |gpu - ref64| <= 2^-8 * |ref64| + 1e-5 * sum_k |a_ik b_kj|    (bf16 output)
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2507_16991_b200 as gm
+from oracle.oracle import Oracle
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def ref_rows(x, ptr, w, rows):
+    """fp64 reference and |a||b| scale for selected output rows."""
+    x64 = x.double().cpu().numpy()
+    w64 = w.double().cpu().numpy()
+    ptr = np.asarray(ptr)
+    g = np.searchsorted(ptr, rows, side="right") - 1
+    ref = np.einsum("rk,rkn->rn", x64[rows], w64[g])
+    scale = np.einsum("rk,rkn->rn", np.abs(x64[rows]), np.abs(w64[g]))
+    return ref, scale
+
+
+def check(out, x, ptr, w, rows, bf16_out):
+    ref, scale = ref_rows(x, ptr, w, rows)
+    got = out.double().cpu().numpy()[rows]
+    err = np.abs(got - ref)
+    tol = 1e-5 * scale + (2.0 ** -8 * np.abs(ref) if bf16_out else 1e-7)
+    bad = err > tol
+    assert not bad.any(), f"{bad.sum()} elements out of tolerance, max err {err.max():.3e}"
+
+
+def test_golden_ragged_groups_fp32_and_bf16():
+    d = np.load(os.path.join(GOLD, "gemm.npz"))
+    x = torch.from_numpy(d["seg_x"]).cuda().to(torch.bfloat16)  # already bf16-exact
+    w = torch.from_numpy(d["seg_w"]).cuda().to(torch.bfloat16)
+    ptr = [int(v) for v in d["seg_ptr"]]
+    ref = d["seg_out64"]  # the reference's grouped_matmul<double> on the rounded inputs
+    scale = Oracle().segment_matmul(np.abs(d["seg_x"].astype(np.float64)), d["seg_ptr"],
+                                    np.abs(d["seg_w"].astype(np.float64)))
+    for dt in (torch.float32, torch.bfloat16):
+        out = gm.segment_matmul(x, ptr, w, out_dtype=dt).double().cpu().numpy()
+        tol = 1e-5 * scale + (2.0 ** -8 * np.abs(ref) if dt == torch.bfloat16 else 1e-7)
+        assert np.all(np.abs(out - ref) <= tol), dt
+
+
+@pytest.mark.parametrize("k,n", [(64, 16), (128, 128), (128, 48), (192, 256), (256, 64), (512, 512), (1024, 256)])
+def test_shapes_and_ragged_tiles(k, n):
+    torch.manual_seed(k * 1000 + n)
+    ptr = [0, 5, 5, 133, 400, 401, 1031]
+    x = torch.randn(ptr[-1], k, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(len(ptr) - 1, k, n, device="cuda") / k ** 0.5).to(torch.bfloat16)
+    for dt in (torch.float32, torch.bfloat16):
+        out = gm.segment_matmul(x, ptr, w, out_dtype=dt)
+        check(out, x, ptr, w, np.arange(ptr[-1]), dt == torch.bfloat16)
+
+
+def test_ogb_mag_shape_sampled_rows():
+    ptr = [0, 736_389, 1_871_038, 1_879_778, 1_939_743]
+    torch.manual_seed(3)
+    x = torch.randn(ptr[-1], 128, device="cuda").to(torch.bfloat16)
+    w = (0.1 * torch.randn(4, 128, 128, device="cuda")).to(torch.bfloat16)
+    out = gm.segment_matmul(x, ptr, w)
+    rng = np.random.default_rng(0)
+    rows = np.unique(np.concatenate([rng.integers(0, ptr[-1], 4000), np.array(ptr[1:-1]) - 1,
+                                     np.array(ptr[:-1]), [ptr[-1] - 1]]))
+    check(out, x, ptr, w, rows, True)
+
+
+def test_list_form_and_errors():
+    torch.manual_seed(1)
+    w = torch.randn(3, 64, 32, device="cuda").to(torch.bfloat16)
+    hs = [torch.randn(r, 64, device="cuda").to(torch.bfloat16) for r in (1, 7, 3)]
+    outs = gm.grouped_matmul(hs, w, out_dtype=torch.float32)
+    assert [o.shape[0] for o in outs] == [1, 7, 3]
+    for h, o, g in zip(hs, outs, range(3)):
+        want = h.double() @ w[g].double()
+        assert torch.allclose(o.double(), want, rtol=1e-5, atol=1e-5)
+    # empty group -> 0 x F' (test_hetero.cpp:82-92)
+    outs = gm.grouped_matmul([hs[0][:0], hs[1], hs[2]], w)
+    assert outs[0].shape == (0, 32)
+    with pytest.raises(ValueError, match="group count mismatch"):
+        gm.grouped_matmul(hs[:2], w)
+    with pytest.raises(ValueError, match="inner dimension mismatch"):
+        gm.grouped_matmul([hs[0], hs[1], torch.zeros(2, 5, device="cuda")], w)
+    with pytest.raises(ValueError, match="multiple of 64"):
+        gm.segment_matmul(torch.zeros(4, 3, device="cuda"), [0, 4], torch.zeros(1, 3, 16, device="cuda"))
