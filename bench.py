@@ -118,11 +118,15 @@ def make_graph(gm, L, n, e, f, device, stream):
     return g, x
 
 
-def bench_segment_matmul(gm, L, device):
-    """C3 (OGB-MAG) node-type segment_matmul, K = N = 128, bf16 in/out."""
-    ptr = [0, 736_389, 1_871_038, 1_879_778, 1_939_743]
-    x = torch.randn(ptr[-1], 128, device=device).to(torch.bfloat16)
-    w = (0.05 * torch.randn(4, 128, 128, device=device)).to(torch.bfloat16)
+def bench_segment_matmul(gm, L, device, f=128, rows=1_939_743):
+    """Node-type segment_matmul, K = N = f, bf16 in/out. f=128: C3 (OGB-MAG)
+    with the real per-type row counts; larger f: the tensor-bound F-sweep."""
+    if f == 128 and rows == 1_939_743:
+        ptr = [0, 736_389, 1_871_038, 1_879_778, 1_939_743]
+    else:
+        ptr = [0, rows * 38 // 100, rows * 96 // 100, rows * 97 // 100, rows]
+    x = torch.randn(ptr[-1], f, device=device).to(torch.bfloat16)
+    w = (torch.randn(4, f, f, device=device) / f ** 0.5).to(torch.bfloat16)
     try:
         for _ in range(3):
             gm.segment_matmul(x, ptr, w)
@@ -137,10 +141,16 @@ def bench_segment_matmul(gm, L, device):
         ms = ev[0].elapsed_time(ev[1]) / reps
     except Exception as exc:  # reported, never silently substituted
         return {"error": str(exc)[:200]}
-    flops = 2.0 * ptr[-1] * 128 * 128
-    byts = 2.0 * ptr[-1] * 128 * 2 + 4 * 128 * 128 * 2
-    return {"shape": "sum_M=1939743,K=N=128,G=4,bf16", "ms": ms, "tflops": flops / ms / 1e9,
-            "achieved_gbs": byts / ms / 1e6, "bound": "hbm (AI 64 < ridge 251)"}
+    flops = 2.0 * ptr[-1] * f * f
+    byts = 2.0 * ptr[-1] * f * 2 + 4 * f * f * 2
+    hbm, bf16_peak, _ = peaks()
+    ai = flops / byts
+    ceiling = min(bf16_peak, ai * hbm / 1e3)
+    return {"shape": f"sum_M={ptr[-1]},K=N={f},G=4,bf16", "ms": ms, "tflops": flops / ms / 1e9,
+            "frac_tensor_peak": flops / ms / 1e9 / bf16_peak, "achieved_gbs": byts / ms / 1e6,
+            "frac_hbm": byts / ms / 1e6 / hbm, "roofline_ceiling_tflops": ceiling,
+            "frac_roofline": flops / ms / 1e9 / ceiling,
+            "bound": "hbm" if ai * hbm / 1e3 < bf16_peak else "tensor"}
 
 
 def run_reference_arm(args):
@@ -339,7 +349,8 @@ def main():
 
     secondary = None
     if world == 1 and not args.no_secondary:
-        secondary = {"segment_matmul_C3": bench_segment_matmul(gm, L, device)}
+        secondary = {"segment_matmul_C3": bench_segment_matmul(gm, L, device),
+                     "segment_matmul_F1024": bench_segment_matmul(gm, L, device, f=1024, rows=500_000)}
         # max + argmax SpMM on the same graph
         mo = torch.empty(N_NODES, F, dtype=torch.float32, device=device)
         ma = torch.empty(N_NODES, F, dtype=torch.int32, device=device)
