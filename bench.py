@@ -245,26 +245,25 @@ def main():
     torch.cuda.synchronize()
 
     # ---- partition (N > 1): nnz-balanced dst rows, equal-row X shards ----------
+    from paper_2507_16991_b200.dist import allgather_features, make_shard
     rowptr_h = csc.rowptr.cpu().numpy()
-    cuts = np.zeros(world + 1, np.int64)
-    L.check(lib.gm_partition_rows_by_nnz(rowptr_h.ctypes.data_as(C.POINTER(C.c_int64)), N_NODES, world,
-                                         cuts.ctypes.data_as(C.POINTER(C.c_int64))))
-    r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
+    sh = make_shard(rowptr_h, N_NODES, rank, world)
+    r0, r1 = sh.row_begin, sh.row_end
     local_edges = int(rowptr_h[r1] - rowptr_h[r0])
     local_csr = csc if world == 1 else csc.row_slice(r0, r1, local_edges)
     out = torch.empty(N_NODES, F, dtype=torch.float32, device=device)
-    shard = -(-N_NODES // world)
     x_full = x
     if world > 1:
-        x_full = torch.zeros(shard * world, F, dtype=torch.float32, device=device)
-        x_full[:N_NODES].copy_(x)
-        x_shard = x_full[rank * shard:(rank + 1) * shard].clone()
+        x_full = torch.zeros(sh.shard_rows * world, F, dtype=torch.float32, device=device)
+        lo, hi = sh.x_rows()
+        x_shard = torch.zeros(sh.shard_rows, F, dtype=torch.float32, device=device)
+        x_shard[: max(0, min(hi, N_NODES) - lo)].copy_(x[lo:min(hi, N_NODES)])
     plan = local_csr.plan()
     cs = local_csr.c_struct()
 
     def step():
         if world > 1:
-            dist.all_gather_into_tensor(x_full, x_shard)
+            allgather_features(x_shard, sh, out=x_full)
         L.check(lib.gm_spmm(C.byref(cs), C.byref(plan), L.GM_F32, C.c_void_p(x_full.data_ptr()), F, None,
                             None, L.GM_SUM, C.c_void_p(out[r0:].data_ptr()), None,
                             C.c_void_p(torch.cuda.current_stream().cuda_stream)))

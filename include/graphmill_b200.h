@@ -194,9 +194,12 @@ GM_API gm_status gm_spmm(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype d
  * (GM_BF16 or GM_F32). tcgen05 (UMMA) tensor cores, fp32 accumulation in
  * TMEM, TMA-fed. ptr_host is a HOST array of groups+1 non-decreasing offsets
  * (ptr_host[0] = 0). Empty groups produce no rows (0 x n, hetero.hpp:131).
- * Requires k % 64 == 0, n % 16 == 0, n <= 256, groups <= 256, 16-byte aligned
- * x/w/out. workspace: gm_segment_matmul_workspace bytes (the K-major copy of w). */
-GM_API size_t gm_segment_matmul_workspace(int64_t groups, int64_t k, int64_t n);
+ * Any K, N >= 1 and groups <= 128: K % 64 == 0 and N % 16 == 0 run in place
+ * (16-byte aligned x/out); other shapes run zero-padded through the
+ * workspace. N > 256 is tiled in 256-wide column tiles.
+ * workspace: gm_segment_matmul_workspace(rows = ptr_host[groups], ...) bytes
+ * (K-major W^T copy, plus padded x / out for odd shapes). */
+GM_API size_t gm_segment_matmul_workspace(int64_t rows, int64_t groups, int64_t k, int64_t n);
 GM_API gm_status gm_segment_matmul(const void* x, const int64_t* ptr_host, int64_t groups,
                                    int64_t k, int64_t n, const void* w, gm_dtype out_dtype,
                                    void* out, void* workspace, size_t workspace_bytes,

@@ -351,17 +351,40 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
   }
 }
 
-// W[g] [K, N] row-major -> W^T [G*N, K] (K-major B operand)
-__global__ void transpose_w_kernel(const __nv_bfloat16* __restrict__ w, int groups, int k, int n,
+// W[g] [K, N] row-major -> W^T [G*Np, Kp] (K-major B operand), zero-padded
+__global__ void transpose_w_kernel(const __nv_bfloat16* __restrict__ w, int groups, int k, int n, int kp, int np,
                                    __nv_bfloat16* __restrict__ wt) {
-  const int64_t total = static_cast<int64_t>(groups) * k * n;
+  const int64_t total = static_cast<int64_t>(groups) * kp * np;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t g = i / (static_cast<int64_t>(k) * n);
-    const int64_t rem = i - g * k * n;
-    const int64_t kk = rem / n;
-    const int64_t nn = rem - kk * n;
-    wt[(g * n + nn) * k + kk] = w[i];
+    const int64_t g = i / (static_cast<int64_t>(np) * kp);
+    const int64_t rem = i - g * np * kp;
+    const int64_t nn = rem / kp;
+    const int64_t kk = rem - nn * kp;
+    wt[i] = (nn < n && kk < k) ? w[(g * k + kk) * n + nn] : __float2bfloat16_rn(0.f);
+  }
+}
+
+// zero-padded copy of a row-major [rows, c] bf16 matrix into [rows, cp]
+__global__ void pad_cols_kernel(const __nv_bfloat16* __restrict__ a, int64_t rows, int c, int cp,
+                                __nv_bfloat16* __restrict__ b) {
+  const int64_t total = rows * cp;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / cp;
+    const int64_t j = i - r * cp;
+    b[i] = j < c ? a[r * c + j] : __float2bfloat16_rn(0.f);
+  }
+}
+// [rows, np] -> [rows, n] (element size esz)
+__global__ void unpad_cols_kernel(const unsigned char* __restrict__ a, int64_t rows, int n, int np, int esz,
+                                  unsigned char* __restrict__ b) {
+  const int64_t total = rows * n;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / n;
+    const int64_t j = i - r * n;
+    for (int e = 0; e < esz; ++e) b[i * esz + e] = a[(r * np + j) * esz + e];
   }
 }
 
@@ -407,19 +430,26 @@ using namespace gm;
 
 extern "C" {
 
-GM_API size_t gm_segment_matmul_workspace(int64_t groups, int64_t k, int64_t n) {
-  if (groups < 0 || k < 0 || n < 0) return 0;
-  return align_up(static_cast<size_t>(groups * k * n) * 2, 256);
+static int64_t pad_to(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+GM_API size_t gm_segment_matmul_workspace(int64_t rows, int64_t groups, int64_t k, int64_t n) {
+  if (rows < 0 || groups < 0 || k < 0 || n < 0) return 0;
+  const int64_t kp = pad_to(std::max<int64_t>(k, 1), 64), np = pad_to(std::max<int64_t>(n, 1), 16);
+  size_t b = align_up(static_cast<size_t>(groups * kp * np) * 2, 256);  // K-major W^T
+  if (kp != k) b += align_up(static_cast<size_t>(rows * kp) * 2, 256);   // padded x
+  if (np != n) b += align_up(static_cast<size_t>(rows * np) * 4, 256);   // padded out
+  return b;
 }
 
-GM_API gm_status gm_segment_matmul(const void* x, const int64_t* ptr_host, int64_t groups, int64_t k, int64_t n,
-                                   const void* w, gm_dtype out_dtype, void* out, void* workspace,
+GM_API gm_status gm_segment_matmul(const void* x, const int64_t* ptr_host, int64_t groups, int64_t k_in,
+                                   int64_t n_in, const void* w, gm_dtype out_dtype, void* out, void* workspace,
                                    size_t workspace_bytes, gm_stream_t stream) {
   using namespace gm::gmm;
   GM_REQUIRE(ptr_host && groups >= 1 && groups <= kMaxGroups, GM_ERR_INVALID_ARGUMENT,
              "segment_matmul: groups must be in [1, " + std::to_string(kMaxGroups) + "]");
-  GM_REQUIRE(k > 0 && k % BK == 0, GM_ERR_INVALID_ARGUMENT, "segment_matmul: K must be a positive multiple of 64");
-  GM_REQUIRE(n > 0 && n % 16 == 0, GM_ERR_INVALID_ARGUMENT, "segment_matmul: N must be a positive multiple of 16");
+  GM_REQUIRE(k_in > 0 && n_in > 0, GM_ERR_INVALID_ARGUMENT, "segment_matmul: K and N must be positive");
+  // odd shapes run zero-padded (K to 64, N to 16) through the workspace
+  const int64_t k = pad_to(k_in, BK), n = pad_to(n_in, 16);
   GM_REQUIRE(out_dtype == GM_BF16 || out_dtype == GM_F32, GM_ERR_INVALID_ARGUMENT,
              "segment_matmul: out dtype must be bf16 or f32");
   GM_REQUIRE(ptr_host[0] == 0, GM_ERR_INVALID_ARGUMENT, "segment_matmul: ptr[0] must be 0");
@@ -429,11 +459,29 @@ GM_API gm_status gm_segment_matmul(const void* x, const int64_t* ptr_host, int64
   GM_REQUIRE(rows < INT32_MAX, GM_ERR_INVALID_ARGUMENT, "segment_matmul: too many rows");
   if (rows == 0) return GM_OK;
   GM_REQUIRE(x && w && out, GM_ERR_INVALID_ARGUMENT, "segment_matmul: null pointer");
-  GM_REQUIRE((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(out)) % 16 == 0,
-             GM_ERR_INVALID_ARGUMENT, "segment_matmul: x, w and out must be 16-byte aligned");
-  const size_t need = gm_segment_matmul_workspace(groups, k, n);
+  const size_t need = gm_segment_matmul_workspace(rows, groups, k_in, n_in);
   GM_REQUIRE(workspace && workspace_bytes >= need, GM_ERR_INVALID_ARGUMENT, "segment_matmul: workspace too small");
   cudaStream_t st = as_stream(stream);
+  unsigned char* wsp = static_cast<unsigned char*>(workspace);
+  __nv_bfloat16* wt = reinterpret_cast<__nv_bfloat16*>(wsp);
+  wsp += align_up(static_cast<size_t>(groups * k * n) * 2, 256);
+  const void* xk = x;
+  if (k != k_in) {
+    __nv_bfloat16* xp = reinterpret_cast<__nv_bfloat16*>(wsp);
+    wsp += align_up(static_cast<size_t>(rows * k) * 2, 256);
+    pad_cols_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(rows * k, 256), 8192)), 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(x), rows, static_cast<int>(k_in), static_cast<int>(k), xp);
+    GM_CHECK_LAUNCH("pad_cols_kernel");
+    xk = xp;
+  }
+  const size_t esz = out_dtype == GM_F32 ? 4 : 2;
+  void* outk = out;
+  if (n != n_in) {
+    outk = wsp;
+    wsp += align_up(static_cast<size_t>(rows * n) * 4, 256);
+  }
+  GM_REQUIRE((reinterpret_cast<uintptr_t>(xk) | reinterpret_cast<uintptr_t>(outk)) % 16 == 0,
+             GM_ERR_INVALID_ARGUMENT, "segment_matmul: x and out must be 16-byte aligned");
 
   Params P{};
   P.groups = static_cast<int32_t>(groups);
@@ -443,7 +491,7 @@ GM_API gm_status gm_segment_matmul(const void* x, const int64_t* ptr_host, int64
   P.k_blocks = static_cast<int32_t>(k / BK);
   P.n = static_cast<int32_t>(n);
   P.out_f32 = out_dtype == GM_F32;
-  P.out = out;
+  P.out = outk;
   int32_t tiles = 0;
   for (int64_t g = 0; g < groups; ++g) {
     P.ptr[g] = ptr_host[g];
@@ -469,14 +517,14 @@ GM_API gm_status gm_segment_matmul(const void* x, const int64_t* ptr_host, int64
   const size_t smem = 1024 + static_cast<size_t>(stages) * kAStageBytes +
                       (P.b_resident ? b_full_bytes : static_cast<size_t>(stages) * b_stage_bytes) + 256;
 
-  // K-major copy of the weights: W^T as a [G*N, K] bf16 matrix
-  __nv_bfloat16* wt = static_cast<__nv_bfloat16*>(workspace);
+  // K-major copy of the weights: W^T as a zero-padded [G*N, K] bf16 matrix
   transpose_w_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(groups * k * n, 256), 4096)), 256, 0, st>>>(
-      static_cast<const __nv_bfloat16*>(w), static_cast<int>(groups), static_cast<int>(k), static_cast<int>(n), wt);
+      static_cast<const __nv_bfloat16*>(w), static_cast<int>(groups), static_cast<int>(k_in), static_cast<int>(n_in),
+      static_cast<int>(k), static_cast<int>(n), wt);
   GM_CHECK_LAUNCH("transpose_w_kernel");
 
   CUtensorMap map_a, map_b;
-  gm_status s = make_map(&map_a, x, static_cast<uint64_t>(k), static_cast<uint64_t>(rows), BK, BM);
+  gm_status s = make_map(&map_a, xk, static_cast<uint64_t>(k), static_cast<uint64_t>(rows), BK, BM);
   if (s != GM_OK) return s;
   s = make_map(&map_b, wt, static_cast<uint64_t>(k), static_cast<uint64_t>(groups * n), BK, static_cast<uint32_t>(P.bn));
   if (s != GM_OK) return s;
@@ -490,6 +538,12 @@ GM_API gm_status gm_segment_matmul(const void* x, const int64_t* ptr_host, int64
   const unsigned grid = static_cast<unsigned>(std::min<int32_t>(tiles, kNumSMs));
   segment_matmul_kernel<<<grid, kThreads, smem, st>>>(P, map_a, map_b);
   GM_CHECK_LAUNCH("segment_matmul_kernel");
+  if (n != n_in) {
+    unpad_cols_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(rows * n_in, 256), 8192)), 256, 0, st>>>(
+        static_cast<const unsigned char*>(outk), rows, static_cast<int>(n_in), static_cast<int>(n),
+        static_cast<int>(esz), static_cast<unsigned char*>(out));
+    GM_CHECK_LAUNCH("unpad_cols_kernel");
+  }
   return GM_OK;
 }
 

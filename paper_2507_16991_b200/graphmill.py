@@ -215,6 +215,14 @@ class EdgeIndex:
     def transpose_view(self) -> CsrView:
         return self.to_csr() if self._undirected else self.to_csc()
 
+    def _exact_dst_grouping(self) -> CsrView:
+        """Destination grouping for the reference's undirected+weights COO sweep
+        (message_passing.hpp:51-59): cached privately, never published as the
+        CSC cache (the reference never builds one there, test_message_passing.cpp:121)."""
+        if self._cache.exact is None:
+            self._cache.exact = build_compressed(self.dst(), self.src(), self._num_dst, self._num_src)
+        return self._cache.exact
+
     def has_csr_cache(self) -> bool:
         return self._cache.csr is not None
 
@@ -254,6 +262,7 @@ class _CacheSlot:
         self.csc: Optional[CsrView] = None
         self.csr_builds = 0
         self.csc_builds = 0
+        self.exact: Optional[CsrView] = None
 
 
 def _first_asymmetric(src: torch.Tensor, dst: torch.Tensor, n: int) -> int:
@@ -310,7 +319,7 @@ def spmm(e: EdgeIndex, x: torch.Tensor, edge_weight: Optional[torch.Tensor], red
     if edge_weight is not None:
         # Undirected + weights: the reference sweeps COO (message_passing.hpp:51-59),
         # i.e. ascending COO position per destination = CSC order.
-        grouping = e.to_csc() if e.is_undirected() else e.transpose_view()
+        grouping = e._exact_dst_grouping() if e.is_undirected() else e.transpose_view()
         w_csr = _permute(edge_weight.to(_acc_dtype(x.dtype)).contiguous(), grouping.perm)
     else:
         grouping = e.transpose_view()
@@ -412,7 +421,7 @@ def segment_matmul(x: torch.Tensor, ptr: Sequence[int], weights: torch.Tensor,
     out = torch.empty((rows, n), dtype=out_dtype, device=x.device)
     ptr_h = (C.c_int64 * (groups + 1))(*[int(p) for p in ptr])
     lib = L.lib()
-    ws_bytes = lib.gm_segment_matmul_workspace(groups, k, n)
+    ws_bytes = lib.gm_segment_matmul_workspace(rows, groups, k, n)
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=x.device)
     L.check(lib.gm_segment_matmul(_p(x), ptr_h, groups, k, n, _p(w), _DT[out_dtype], _p(out), _p(ws),
                                   ws_bytes, _stream()), "gm_segment_matmul")

@@ -1,0 +1,90 @@
+"""N>1 host logic on CPU: world_size-2 gloo processes run the real partitioner
+(gm_partition_rows_by_nnz from the C-ABI library) and the real exchange
+(all_gather_into_tensor), then aggregate their destination-row slice with the
+oracle restatement (the only CPU stand-in for the device kernel, which cannot
+run here). The concatenated per-rank outputs must equal the single-process
+oracle bit-for-bit — the property that makes the GPU path correct by
+construction (per-row results never depend on the partition)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n, e, f, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.oracle import Oracle
+        from paper_2507_16991_b200 import _lib as L
+        from paper_2507_16991_b200.dist import allgather_features, make_shard
+        lib = L.lib()
+        src = np.zeros(e, np.int64)
+        dst = np.zeros(e, np.int64)
+        lib.gm_synth_edges_host(1, 99, 0, e, n, n, src.ctypes.data, dst.ctypes.data)
+        orc = Oracle()
+        rp, col, perm = orc.build_compressed(dst, src, n)
+        sh = make_shard(rp, n, rank, world)
+        # this rank's X shard (rows it owns), produced locally
+        x = np.zeros((n, f), np.float32)
+        lib.gm_synth_features_host(99, 0, n, f, 1, L.GM_F32, x.ctypes.data)
+        lo, hi = sh.x_rows()
+        shard = np.zeros((sh.shard_rows, f), np.float32)
+        shard[: max(0, min(hi, n) - lo)] = x[lo:min(hi, n)]
+        full = allgather_features(torch.from_numpy(shard), sh).numpy()[:n]
+        assert full.tobytes() == x.tobytes()
+        rows = np.arange(sh.row_begin, sh.row_end)
+        out = orc.spmm(rp, col, perm, full, rows=rows)
+        mx, arg = orc.spmm_max(rp, col, perm, full, rows=rows)
+        q.put((rank, sh.row_begin, sh.row_end, out, mx, arg, int(rp[sh.row_end] - rp[sh.row_begin])))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_partitioned_spmm_matches_single_process(world):
+    n, e, f = 3000, 60000, 12
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, e, f, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = sorted([q.get(timeout=300) for _ in range(world)])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    from oracle.oracle import Oracle
+    from paper_2507_16991_b200 import _lib as L
+    lib = L.lib()
+    src = np.zeros(e, np.int64)
+    dst = np.zeros(e, np.int64)
+    lib.gm_synth_edges_host(1, 99, 0, e, n, n, src.ctypes.data, dst.ctypes.data)
+    x = np.zeros((n, f), np.float32)
+    lib.gm_synth_features_host(99, 0, n, f, 1, L.GM_F32, x.ctypes.data)
+    orc = Oracle()
+    rp, col, perm = orc.build_compressed(dst, src, n)
+    want = orc.spmm(rp, col, perm, x)
+    wmx, warg = orc.spmm_max(rp, col, perm, x)
+    # contiguous, covering, nnz-balanced
+    assert results[0][1] == 0 and results[-1][2] == n
+    for a, b in zip(results, results[1:]):
+        assert a[2] == b[1]
+    loads = [r[6] for r in results]
+    assert max(loads) - min(loads) <= max(rp[1:] - rp[:-1]) + 1
+    got = np.concatenate([r[3] for r in results])
+    assert got.tobytes() == want.tobytes()
+    assert np.concatenate([r[4] for r in results]).tobytes() == wmx.tobytes()
+    assert np.array_equal(np.concatenate([r[5] for r in results]), warg)

@@ -92,5 +92,24 @@ def test_list_form_and_errors():
         gm.grouped_matmul(hs[:2], w)
     with pytest.raises(ValueError, match="inner dimension mismatch"):
         gm.grouped_matmul([hs[0], hs[1], torch.zeros(2, 5, device="cuda")], w)
-    with pytest.raises(ValueError, match="multiple of 64"):
-        gm.segment_matmul(torch.zeros(4, 3, device="cuda"), [0, 4], torch.zeros(1, 3, 16, device="cuda"))
+
+
+
+def test_odd_shapes_pad_internally():
+    # the reference's own test shapes (test_hetero.cpp:61-106): K=3, N=5 / 4 / 2
+    d = np.load(os.path.join(GOLD, "gemm.npz"))
+    for xk, wk, ptr, ok in (("gm_x", "gm_w", [0, 2, 6], "gm_out"), ("gm_empty_x", "gm_empty_w", [0, 0, 2], "gm_empty_out")):
+        x = torch.from_numpy(d[xk]).cuda().to(torch.bfloat16)
+        w = torch.from_numpy(d[wk]).cuda().to(torch.bfloat16)
+        got = gm.segment_matmul(x, ptr, w, out_dtype=torch.float32).double().cpu().numpy()
+        # reference output on the bf16-rounded inputs
+        want = Oracle().segment_matmul(x.double().cpu().numpy(), np.array(ptr), w.double().cpu().numpy())
+        assert np.allclose(got, want, rtol=1e-6, atol=1e-6)
+        # and within bf16 input rounding of the reference's f64 result
+        assert np.allclose(got, d[ok], rtol=2e-2, atol=2e-2)
+    for k, n in ((3, 5), (100, 7), (130, 33)):
+        torch.manual_seed(k + n)
+        ptr = [0, 17, 17, 300]
+        x = torch.randn(ptr[-1], k, device="cuda").to(torch.bfloat16)
+        w = torch.randn(3, k, n, device="cuda").to(torch.bfloat16)
+        check(gm.segment_matmul(x, ptr, w, out_dtype=torch.float32), x, ptr, w, np.arange(ptr[-1]), False)
