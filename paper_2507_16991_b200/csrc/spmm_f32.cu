@@ -1,0 +1,13 @@
+// spmm_f32.cu — float instantiations of the SpMM kernels (split for parallel builds).
+#include "spmm_kernels.cuh"
+
+namespace gm {
+
+gm_status spmm_dispatch_f32(const SpmmArgs& p, bool maxmin, bool use_heavy, int64_t num_heavy, int64_t ns, int vb,
+                            cudaStream_t st) {
+  if (vb == 16) return dispatch_vb<float, 16>(p, maxmin, use_heavy, num_heavy, ns, st);
+  if (vb == 8) return dispatch_vb<float, 8>(p, maxmin, use_heavy, num_heavy, ns, st);
+  return dispatch_vb<float, 4>(p, maxmin, use_heavy, num_heavy, ns, st);
+}
+
+}  // namespace gm

@@ -1,0 +1,830 @@
+// spmm.cu — CSR SpMM aggregation (sum / mean / max / min, optional edge
+// scale or fused GCN norm, optional argmax) for sm_100a.
+//
+// Replaces, bit-exactly for f32/f64:
+//   spmm / detail::spmm_forward     message_passing.hpp:47-85, 92-169
+//   max path (fused, no E x F temp) message_passing.hpp:508-514 ->
+//                                   dst_grouped_order 190-214, gather_rows
+//                                   tensor.hpp:499-530, aggregate 197-215
+//   GCN norm fused into the gather  message_passing.hpp:437-463, 490-495
+//
+// Exactness: every output element is accumulated by ONE thread, sequentially
+// in compressed (CSC) order, with __fadd_rn/__fmul_rn (no FMA contraction) —
+// the reference's `o[j] += w * xi[j]` loop order. Max/min: the first element
+// initialises, then strict compare; ties keep the earlier edge.
+//
+// Scheduling (pure performance, never changes results):
+//   * light rows (deg <= heavy_threshold): a group of LPR lanes owns one
+//     nnz-balanced window of consecutive rows; lanes own VB-byte column
+//     slices, U edges' gathers are in flight per batch (coalesced 128-bit
+//     loads of whole feature rows, L1 no-allocate);
+//   * heavy rows (power-law hubs): one CTA per row, longest first, on a forked
+//     stream so hubs start before the light sweep; the CTA streams the row's
+//     feature rows into a cp.async shared-memory ring (R stages of `se` edges)
+//     while the owning threads accumulate each column in order.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <vector>
+
+#pragma once
+#include "vec.cuh"
+
+namespace gm {
+
+struct SpmmArgs {
+  const int64_t* rowptr;
+  const int32_t* col;
+  const int32_t* perm;
+  const void* x;
+  void* out;
+  int32_t* arg;
+  const void* w;             // per-edge scale (accumulation type), compressed order
+  const int32_t* gdeg_src;   // GCN effective degrees (NULL = no GCN)
+  const int32_t* gdeg_dst;
+  int gcn_self;              // append the (v, v) self-loop term last
+  int mean;
+  int is_min;
+  int64_t num_rows;
+  int64_t f;                 // elements per row
+  int64_t slot_base;         // first VB-byte slot of this column chunk
+  int64_t slot_end;          // one past the last slot of this chunk
+  const int32_t* win_row;
+  int64_t num_windows;
+  int64_t heavy_thr;
+  const int32_t* heavy_rows;
+  const int32_t* light_windows;  // (first_row, end_row) pairs, heavy-free
+  int64_t num_light_windows;
+  int flat_ok;                   // heavy rows (if any) are covered by the hub kernel
+  const uint8_t* src_class;      // per-entry source hotness class (NULL: no L2 hint)
+  int hot_class_limit;           // entries with class < limit gather with evict_last
+};
+
+// L2 eviction-priority policies (createpolicy; PTX ISA "Cache eviction priority hints").
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+template <typename R>
+__device__ __forceinline__ R ldg_hint(const R* p, uint64_t pol);
+template <>
+__device__ __forceinline__ uint4 ldg_hint<uint4>(const uint4* p, uint64_t pol) {
+  uint4 r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p), "l"(pol));
+  return r;
+}
+template <>
+__device__ __forceinline__ uint2 ldg_hint<uint2>(const uint2* p, uint64_t pol) {
+  uint2 r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+      : "=r"(r.x), "=r"(r.y)
+      : "l"(p), "l"(pol));
+  return r;
+}
+template <>
+__device__ __forceinline__ uint32_t ldg_hint<uint32_t>(const uint32_t* p, uint64_t pol) {
+  uint32_t r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
+}
+template <>
+__device__ __forceinline__ unsigned short ldg_hint<unsigned short>(const unsigned short* p, uint64_t pol) {
+  unsigned short r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(r) : "l"(p), "l"(pol));
+  return r;
+}
+
+template <typename A>
+__device__ __forceinline__ A gcn_scale(int32_t ds, int32_t dd) {
+  // message_passing.hpp:449-451: S(1) / std::sqrt(S(din[s]) * S(din[d]))
+  return div_rn(A(1), sqrt_rn(mul_rn(static_cast<A>(ds), static_cast<A>(dd))));
+}
+
+// Per-thread accumulator for NV vectors of V elements.
+template <typename A, int NV, int V, bool MAXMIN>
+struct Acc {
+  A v[NV][V];
+  int32_t a[NV][V];
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        v[j][e] = A(0);
+        if (MAXMIN) a[j][e] = -1;
+      }
+  }
+  // One edge's contribution to vector j. `first`: first edge of the row.
+  __device__ __forceinline__ void add(int j, const A* vals, bool scaled, A sc, bool first,
+                                      int is_min, int32_t pm) {
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      const A val = scaled ? mul_rn(vals[e], sc) : vals[e];
+      if (!MAXMIN) {
+        v[j][e] = add_rn(v[j][e], val);
+      } else {
+        const bool better = first || (is_min ? (val < v[j][e]) : (val > v[j][e]));
+        if (better) {
+          v[j][e] = val;
+          a[j][e] = pm;
+        }
+      }
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Light path: LPR lanes per window, NV vectors of VB bytes per lane.
+// ---------------------------------------------------------------------------
+template <typename T, int VB, int NV, int LPR, int U, bool MAXMIN>
+__global__ void __launch_bounds__(256) spmm_light_kernel(const SpmmArgs p) {
+  using VecT = Vec<T, VB>;
+  using A = typename VecT::A;
+  constexpr int V = VecT::V;
+  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t window = gid / LPR;
+  const int sub = static_cast<int>(gid % LPR);
+  if (window >= p.num_windows) return;
+
+  const T* __restrict__ x = static_cast<const T*>(p.x);
+  T* __restrict__ out = static_cast<T*>(p.out);
+  const A* __restrict__ w = static_cast<const A*>(p.w);
+  const bool gcn = p.gdeg_src != nullptr;
+  const bool scaled = gcn || w != nullptr;
+  const bool want_arg = MAXMIN && p.arg != nullptr;
+
+  int64_t slot[NV];
+  bool valid[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    slot[j] = p.slot_base + sub + j * LPR;
+    valid[j] = slot[j] < p.slot_end;
+  }
+
+  const int r0 = p.win_row[window];
+  const int r1 = p.win_row[window + 1];
+  for (int r = r0; r < r1; ++r) {
+    const int64_t kb = p.rowptr[r];
+    const int64_t ke = p.rowptr[r + 1];
+    if (ke - kb > p.heavy_thr) continue;  // the heavy kernel owns this row
+    Acc<A, NV, V, MAXMIN> acc;
+    acc.init();
+    const int32_t dd = gcn ? p.gdeg_dst[r] : 0;
+
+    for (int64_t k = kb; k < ke; k += U) {
+      int32_t c[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) c[u] = (k + u < ke) ? p.col[k + u] : 0;
+      VecT buf[U][NV];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (k + u < ke) {
+          const T* xr = x + static_cast<int64_t>(c[u]) * p.f;
+#pragma unroll
+          for (int j = 0; j < NV; ++j)
+            if (valid[j]) buf[u][j].load_global(xr + slot[j] * V);
+        }
+      A sc[U];
+      int32_t pm[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        sc[u] = A(1);
+        pm[u] = -1;
+        if (k + u < ke) {
+          if (w) sc[u] = w[k + u];
+          else if (gcn) sc[u] = gcn_scale<A>(p.gdeg_src[c[u]], dd);
+          if (want_arg) pm[u] = p.perm[k + u];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (k + u < ke) {
+#pragma unroll
+          for (int j = 0; j < NV; ++j)
+            if (valid[j]) acc.add(j, buf[u][j].v, scaled, sc[u], k + u == kb, p.is_min, pm[u]);
+        }
+    }
+    int64_t cnt = ke - kb;
+    if (gcn && p.gcn_self) {
+      // with_self_loops appends (r, r) after every original edge
+      // (edge_index.cpp:226-229), so it is the last entry of CSC row r.
+      const A sc = gcn_scale<A>(p.gdeg_src[r], dd);
+      const T* xr = x + static_cast<int64_t>(r) * p.f;
+#pragma unroll
+      for (int j = 0; j < NV; ++j)
+        if (valid[j]) {
+          VecT b;
+          b.load_global(xr + slot[j] * V);
+          acc.add(j, b.v, true, sc, cnt == 0, p.is_min, -1);
+        }
+      cnt += 1;
+    }
+    if (!MAXMIN && p.mean && cnt > 0) {
+      const A inv = div_rn(A(1), static_cast<A>(cnt));  // message_passing.hpp:81
+#pragma unroll
+      for (int j = 0; j < NV; ++j)
+#pragma unroll
+        for (int e = 0; e < V; ++e) acc.v[j][e] = mul_rn(acc.v[j][e], inv);
+    }
+    T* orow = out + static_cast<int64_t>(r) * p.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+      if (valid[j]) {
+        VecT::store_global(orow + slot[j] * V, acc.v[j]);
+        if (want_arg) {
+          int32_t* arow = p.arg + static_cast<int64_t>(r) * p.f + slot[j] * V;
+#pragma unroll
+          for (int e = 0; e < V; ++e) arow[e] = acc.a[j][e];
+        }
+      }
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// Flat light path (the hot one): one warp streams a heavy-free window of
+// consecutive rows as ONE contiguous edge range, U edges per batch regardless
+// of row boundaries (no partial batches at row ends). The next batch's col
+// (and weight / perm) entries are prefetched one batch ahead, one per lane,
+// and broadcast by shuffle; row ends are cached 32 at a time across lanes.
+// Accumulation order per output element is unchanged: ascending CSC position.
+// ---------------------------------------------------------------------------
+// shuffle of a raw vector
+__device__ __forceinline__ uint4 shfl_raw(const uint4& v, int src) {
+  return make_uint4(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src),
+                    __shfl_sync(0xffffffffu, v.z, src), __shfl_sync(0xffffffffu, v.w, src));
+}
+__device__ __forceinline__ uint2 shfl_raw(const uint2& v, int src) {
+  return make_uint2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+__device__ __forceinline__ uint32_t shfl_raw(const uint32_t& v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+__device__ __forceinline__ unsigned short shfl_raw(const unsigned short& v, int src) {
+  return static_cast<unsigned short>(__shfl_sync(0xffffffffu, static_cast<uint32_t>(v), src));
+}
+
+// P > 1 (rows of <= 32/P vector slots): one load instruction fetches P edges
+// (lane l loads slot l % (32/P) of edge l / (32/P)); the owning lanes then
+// take each edge's slice by shuffle, in edge order — same accumulation order.
+template <typename T, int VB, int NV, int U, int MODE, bool SCALED, int P = 1>
+__global__ void __launch_bounds__(256, (SCALED || sizeof(T) == 8) ? 3 : 4) spmm_flat_kernel(const SpmmArgs p) {
+  static_assert(P == 1 || NV == 1, "lane-split loads need one vector per lane");
+  static_assert(U % P == 0, "batch must hold whole load groups");
+  constexpr int SLW = 32 / P;  // lanes per edge in the load phase
+  constexpr bool MAXMIN = MODE == 2;
+  constexpr bool MEAN = MODE == 1;
+  using VecT = Vec<T, VB>;
+  using A = typename VecT::A;
+  using R = typename VecT::R;
+  constexpr int V = VecT::V;
+  constexpr unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (warp >= p.num_light_windows) return;
+
+  const T* __restrict__ x = static_cast<const T*>(p.x);
+  T* __restrict__ out = static_cast<T*>(p.out);
+  const int32_t* __restrict__ col = p.col;
+  const bool want_arg = MAXMIN && p.arg != nullptr;
+  const uint32_t fu = static_cast<uint32_t>(p.f);  // row stride (elements)
+
+  uint32_t soff[NV];  // element offset of this lane's vector j inside a row
+  bool valid[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int64_t sl = p.slot_base + lane + j * 32;
+    valid[j] = sl < p.slot_end;
+    soff[j] = static_cast<uint32_t>(sl * V);
+  }
+  // load-phase slot (P > 1): slot lane % SLW of edge lane / SLW
+  const int64_t lsl = p.slot_base + (lane % SLW);
+  const bool lvalid = lsl < p.slot_end;
+  const uint32_t loff = static_cast<uint32_t>(lsl * V);
+
+  // Positions fit int32: gm_build_compressed / plan_build require nnz < 2^31.
+  const int ra = p.light_windows[2 * warp];
+  const int rb = p.light_windows[2 * warp + 1];
+  const int32_t kbeg = static_cast<int32_t>(p.rowptr[ra]);
+  const int32_t kend = static_cast<int32_t>(p.rowptr[rb]);
+
+  // lane l caches the end of row cbase + l
+  int cbase = ra;
+  int32_t rend_l = (cbase + lane < rb) ? static_cast<int32_t>(p.rowptr[cbase + 1 + lane]) : kend;
+  int row = ra;
+  int32_t row_start = kbeg;
+  int32_t row_end = __shfl_sync(FULL, rend_l, 0);
+
+  Acc<A, NV, V, MAXMIN> acc;
+  acc.init();
+  bool first = true;
+
+  auto flush = [&]() {
+    if (MEAN) {
+      const int32_t cnt = row_end - row_start;
+      if (cnt > 0) {
+        const A inv = div_rn(A(1), static_cast<A>(cnt));  // message_passing.hpp:81
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+#pragma unroll
+          for (int e = 0; e < V; ++e) acc.v[j][e] = mul_rn(acc.v[j][e], inv);
+      }
+    }
+    const uint64_t obase = static_cast<uint64_t>(static_cast<uint32_t>(row)) * fu;
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+      if (valid[j]) {
+        VecT::store_global(out + obase + soff[j], acc.v[j]);
+        if (want_arg) {
+          int32_t* arow = p.arg + obase + soff[j];
+#pragma unroll
+          for (int e = 0; e < V; ++e) arow[e] = acc.a[j][e];
+        }
+      }
+    acc.init();
+    first = true;
+    ++row;
+    row_start = row_end;
+    if (row < rb) {
+      if (row - cbase >= 32) {
+        cbase = row;
+        rend_l = (cbase + lane < rb) ? static_cast<int32_t>(p.rowptr[cbase + 1 + lane]) : kend;
+      }
+      row_end = __shfl_sync(FULL, rend_l, row - cbase);
+    }
+  };
+
+  const bool hinted = p.src_class != nullptr;
+  const uint64_t pol_hot = policy_evict_last();
+  const uint64_t pol_cold = policy_evict_first();
+  int32_t c_next = 0, p_next = -1, h_next = 0;
+  A w_next = A(1);
+  auto fetch = [&](int32_t kb) {
+    const int32_t k = kb + lane;
+    if (lane < U && k < kend) {
+      c_next = col[k];
+      if (hinted) h_next = p.src_class[k] < p.hot_class_limit;
+      if (SCALED) w_next = static_cast<const A*>(p.w)[k];
+      if (MAXMIN) p_next = want_arg ? p.perm[k] : -1;
+    }
+  };
+  fetch(kbeg);
+
+  for (int32_t k0 = kbeg; k0 < kend; k0 += U) {
+    const int32_t c_cur = c_next;
+    const int32_t p_cur = p_next;
+    const int32_t h_cur = h_next;
+    const A w_cur = w_next;
+    fetch(k0 + U);
+    const int nb = min(U, kend - k0);  // edges in this batch
+    R buf[U / P][NV];
+    if constexpr (P == 1) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t cu = static_cast<uint32_t>(__shfl_sync(FULL, c_cur, u));
+        const int32_t hu = __shfl_sync(FULL, h_cur, u);
+        if (u < nb) {
+          const T* xr = x + static_cast<uint64_t>(cu) * fu;
+          if (hinted) {
+            const uint64_t pol = hu ? pol_hot : pol_cold;
+#pragma unroll
+            for (int j = 0; j < NV; ++j)
+              if (valid[j]) buf[u][j] = ldg_hint<R>(reinterpret_cast<const R*>(xr + soff[j]), pol);
+          } else {
+#pragma unroll
+            for (int j = 0; j < NV; ++j)
+              if (valid[j]) buf[u][j] = VecT::load_raw(xr + soff[j]);
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int g = 0; g < U / P; ++g) {
+        const int eb = g * P + lane / SLW;  // edge of this lane's load
+        const uint32_t cu = static_cast<uint32_t>(__shfl_sync(FULL, c_cur, eb));
+        const int32_t hu = __shfl_sync(FULL, h_cur, eb);
+        if (eb < nb && lvalid) {
+          const T* xr = x + static_cast<uint64_t>(cu) * fu;
+          if (hinted) buf[g][0] = ldg_hint<R>(reinterpret_cast<const R*>(xr + loff), hu ? pol_hot : pol_cold);
+          else buf[g][0] = VecT::load_raw(xr + loff);
+        }
+      }
+    }
+    // this lane's slice of edge u (the loads above put it on lane (u%P)*SLW + lane)
+    auto slice = [&](int u, int j) -> R {
+      if constexpr (P == 1) return buf[u][j];
+      else return shfl_raw(buf[u / P][0], (u % P) * SLW + (lane % SLW));
+    };
+    if (nb == U && k0 + U <= row_end) {
+      // fast path: the whole batch belongs to the current row
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const A sc = SCALED ? __shfl_sync(FULL, w_cur, u) : A(1);
+        const int32_t pm = MAXMIN ? __shfl_sync(FULL, p_cur, u) : -1;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          const R r = slice(u, j);
+          if (valid[j]) {
+            A vals[V];
+            VecT::unpack(r, vals);
+            acc.add(j, vals, SCALED, sc, first && u == 0, p.is_min, pm);
+          }
+        }
+      }
+      first = false;
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const A sc = SCALED ? __shfl_sync(FULL, w_cur, u) : A(1);
+        const int32_t pm = MAXMIN ? __shfl_sync(FULL, p_cur, u) : -1;
+        R rs[NV];
+#pragma unroll
+        for (int j = 0; j < NV; ++j) rs[j] = slice(u, j);
+        if (u < nb) {
+          while (k0 + u >= row_end) flush();
+#pragma unroll
+          for (int j = 0; j < NV; ++j)
+            if (valid[j]) {
+              A vals[V];
+              VecT::unpack(rs[j], vals);
+              acc.add(j, vals, SCALED, sc, first, p.is_min, pm);
+            }
+          first = false;
+        }
+      }
+    }
+  }
+  while (row < rb) flush();
+}
+
+// ---------------------------------------------------------------------------
+// Heavy path: one CTA per hub row, cp.async ring of R stages x se edges.
+// ---------------------------------------------------------------------------
+constexpr int kHeavyThreads = 256;
+constexpr int64_t kWideRowBytes = 1024;
+// Experimental: route every wide row through the CTA kernel (GM_WIDE_CTA=1).
+inline bool wide_cta_mode() {
+  static const bool on = [] { const char* e = getenv("GM_WIDE_CTA"); return e && atoi(e) == 1; }();
+  return on;
+}
+// Lane-split loads for narrow rows (experimental; GM_LANE_SPLIT=1 enables).
+inline bool lane_split() {
+  static const bool on = [] { const char* e = getenv("GM_LANE_SPLIT"); return e && atoi(e) != 0; }();
+  return on;
+}
+// 16-edge batches for narrow bf16 rows (experimental; GM_NARROW_U16=1 enables).
+inline bool narrow_u16() {
+  static const bool on = [] { const char* e = getenv("GM_NARROW_U16"); return e && atoi(e) != 0; }();
+  return on;
+}
+// Max vectors per lane in the flat kernel (GM_FLAT_MAX_NV, default 4: wide
+// rows take more column passes with more edges in flight per batch).
+inline int flat_max_nv() {
+  static const int nv = [] { const char* e = getenv("GM_FLAT_MAX_NV"); return e ? atoi(e) : 4; }();
+  return nv;
+}
+constexpr int kRing = 4;
+
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem, int bytes) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  if (bytes == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+  else if (bytes == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <typename A>
+__host__ __device__ inline size_t heavy_smem_bytes(int se, int rowb) {
+  size_t b = static_cast<size_t>(kRing) * se * rowb;          // data ring
+  b += static_cast<size_t>(kRing + 1) * se * sizeof(int32_t);  // col ring
+  b += static_cast<size_t>(kRing + 1) * se * sizeof(int32_t);  // perm ring
+  b = (b + 15) / 16 * 16;
+  b += static_cast<size_t>(kRing + 1) * se * sizeof(A);        // scale ring
+  return b;
+}
+
+template <typename T, int VB, int MH, bool MAXMIN>
+__global__ void __launch_bounds__(kHeavyThreads) spmm_heavy_kernel(const SpmmArgs p, int se) {
+  using VecT = Vec<T, VB>;
+  using A = typename VecT::A;
+  constexpr int V = VecT::V;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int nslots = static_cast<int>(p.slot_end - p.slot_base);
+  const int rowb = nslots * VB;
+  unsigned char* data = smem;
+  int32_t* mcol = reinterpret_cast<int32_t*>(smem + static_cast<size_t>(kRing) * se * rowb);
+  int32_t* mperm = mcol + (kRing + 1) * se;
+  size_t off = static_cast<size_t>(kRing) * se * rowb + 2ull * (kRing + 1) * se * sizeof(int32_t);
+  off = (off + 15) / 16 * 16;
+  A* mscale = reinterpret_cast<A*>(smem + off);
+
+  const T* __restrict__ x = static_cast<const T*>(p.x);
+  const A* __restrict__ w = static_cast<const A*>(p.w);
+  const bool gcn = p.gdeg_src != nullptr;
+  const bool scaled = gcn || w != nullptr;
+  const bool want_arg = MAXMIN && p.arg != nullptr;
+  const int t = threadIdx.x;
+
+  // hub list, or every row (wide-row mode: heavy_rows == NULL)
+  const int r = p.heavy_rows ? p.heavy_rows[blockIdx.x] : static_cast<int>(blockIdx.x);
+  const int64_t kb = p.rowptr[r];
+  const int64_t ke = p.rowptr[r + 1];
+  const int64_t deg = ke - kb;
+  const int64_t total = deg + ((gcn && p.gcn_self) ? 1 : 0);
+  const int nst = static_cast<int>((total + se - 1) / se);
+  const int32_t dd = gcn ? p.gdeg_dst[r] : 0;
+  const int gpr = rowb / VB;  // copy granules per feature row (VB bytes each)
+
+  // Register-staged metadata of one stage (threads t < se own edge t).
+  int32_t rc = -1, rp = -1;
+  A rw = A(1);
+  auto load_meta = [&](int q) {
+    const int64_t e = static_cast<int64_t>(q) * se + t;
+    rc = -1;
+    if (t < se && e < total) {
+      if (e < deg) {
+        const int64_t k = kb + e;
+        rc = p.col[k];
+        rp = want_arg ? p.perm[k] : -1;
+        rw = w ? w[k] : A(1);
+      } else {  // the self-loop term
+        rc = r;
+        rp = -1;
+        rw = A(1);
+      }
+    }
+  };
+
+  Acc<A, MH, V, MAXMIN> acc;
+  acc.init();
+  A sc_next = A(1);
+
+  load_meta(0);
+  for (int i = -(kRing - 1); i < nst; ++i) {
+    const int q = i + kRing - 1;  // stage whose copies are issued now
+    if (q < nst && t < se) {
+      const int ms = (q % (kRing + 1)) * se + t;
+      mcol[ms] = rc;
+      mperm[ms] = rp;
+      if (!gcn) mscale[ms] = rw;
+    }
+    if (q + 1 < nst) load_meta(q + 1);
+    __syncthreads();
+    if (q < nst) {
+      const int base_e = q * se;
+      const int n_e = static_cast<int>(min(static_cast<int64_t>(se), total - base_e));
+      const int32_t* cq = mcol + (q % (kRing + 1)) * se;
+      unsigned char* dq = data + static_cast<size_t>(q % kRing) * se * rowb;
+      for (int g = t; g < n_e * gpr; g += kHeavyThreads) {
+        const int e = g / gpr;
+        const int part = g - e * gpr;
+        const T* src = x + static_cast<int64_t>(cq[e]) * p.f + (p.slot_base + part) * V;
+        cp_async(dq + static_cast<size_t>(e) * rowb + part * VB, src, VB);
+      }
+    }
+    cp_async_commit();
+    if (gcn && i + 1 >= 0 && i + 1 < nst && t < se) {
+      const int64_t e = static_cast<int64_t>(i + 1) * se + t;
+      if (e < total) sc_next = gcn_scale<A>(p.gdeg_src[mcol[((i + 1) % (kRing + 1)) * se + t]], dd);
+    }
+    cp_async_wait<kRing - 1>();
+    __syncthreads();
+    if (i >= 0) {
+      const int base_e = i * se;
+      const int n_e = static_cast<int>(min(static_cast<int64_t>(se), total - base_e));
+      const unsigned char* di = data + static_cast<size_t>(i % kRing) * se * rowb;
+      const int mi = (i % (kRing + 1)) * se;
+#pragma unroll
+      for (int m = 0; m < MH; ++m) {
+        const int s = t + m * kHeavyThreads;
+        if (s < nslots) {
+          for (int e = 0; e < n_e; ++e) {
+            VecT v;
+            v.load_shared(reinterpret_cast<const T*>(di + static_cast<size_t>(e) * rowb + s * VB));
+            acc.add(m, v.v, scaled, mscale[mi + e], base_e + e == 0, p.is_min, mperm[mi + e]);
+          }
+        }
+      }
+    }
+    if (gcn && i + 1 >= 0 && i + 1 < nst && t < se) mscale[((i + 1) % (kRing + 1)) * se + t] = sc_next;
+  }
+
+  if (!MAXMIN && p.mean && total > 0) {
+    const A inv = div_rn(A(1), static_cast<A>(total));
+#pragma unroll
+    for (int m = 0; m < MH; ++m)
+#pragma unroll
+      for (int e = 0; e < V; ++e) acc.v[m][e] = mul_rn(acc.v[m][e], inv);
+  }
+  T* orow = static_cast<T*>(p.out) + static_cast<int64_t>(r) * p.f;
+#pragma unroll
+  for (int m = 0; m < MH; ++m) {
+    const int s = t + m * kHeavyThreads;
+    if (s < nslots) {
+      VecT::store_global(orow + (p.slot_base + s) * V, acc.v[m]);
+      if (want_arg) {
+        int32_t* arow = p.arg + static_cast<int64_t>(r) * p.f + (p.slot_base + s) * V;
+#pragma unroll
+        for (int e = 0; e < V; ++e) arow[e] = acc.a[m][e];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Launch helpers
+// ---------------------------------------------------------------------------
+struct SideStream {
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  int device = -1;
+};
+// One library-owned side stream (+ fork/join events) per host thread (spmm.cu).
+gm_status side_stream(SideStream** out);
+
+template <typename K>
+inline gm_status ensure_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024)
+    GM_TRY_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(bytes)));
+  return GM_OK;
+}
+
+template <typename T, int VB, bool MAXMIN>
+gm_status launch_flat(const SpmmArgs& p0, int64_t ns, cudaStream_t st) {
+  const bool scaled = p0.w != nullptr;
+  // at most 32 accumulator elements per lane: 8 float4, 4 bf16x8, 8 double2
+  constexpr int kV = VB / static_cast<int>(sizeof(T));
+  constexpr int64_t kChunk = 32 * std::min(8, std::max(1, 32 / kV));
+  const int64_t chunk = std::min<int64_t>(kChunk, 32 * std::max(1, flat_max_nv()));
+  for (int64_t base = 0; base < ns; base += chunk) {
+    SpmmArgs p = p0;
+    p.slot_base = base;
+    p.slot_end = std::min<int64_t>(ns, base + chunk);
+    const int64_t slots = p.slot_end - base;
+    const int nv = slots <= 32 ? 1 : slots <= 64 ? 2 : slots <= 128 ? 4 : 8;
+    const unsigned grid = static_cast<unsigned>(ceil_div(p.num_light_windows * 32, 256));
+    if (grid == 0) continue;
+#define GM_FLAT_M(NV_, U_, M_)                                                       \
+  do {                                                                               \
+    if (scaled) spmm_flat_kernel<T, VB, NV_, U_, M_, true><<<grid, 256, 0, st>>>(p);   \
+    else spmm_flat_kernel<T, VB, NV_, U_, M_, false><<<grid, 256, 0, st>>>(p);         \
+  } while (0)
+#define GM_FLAT_MP(U_, P_, M_)                                                                 \
+  do {                                                                                           \
+    if (scaled) spmm_flat_kernel<T, VB, 1, U_, M_, true, P_><<<grid, 256, 0, st>>>(p);           \
+    else spmm_flat_kernel<T, VB, 1, U_, M_, false, P_><<<grid, 256, 0, st>>>(p);                 \
+  } while (0)
+#define GM_FLAT_P(U_, P_)                              \
+  do {                                                 \
+    if constexpr (MAXMIN) GM_FLAT_MP(U_, P_, 2);       \
+    else if (p.mean) GM_FLAT_MP(U_, P_, 1);            \
+    else GM_FLAT_MP(U_, P_, 0);                        \
+  } while (0)
+#define GM_FLAT(NV_, U_)                               \
+  do {                                                 \
+    if constexpr (MAXMIN) GM_FLAT_M(NV_, U_, 2);       \
+    else if (p.mean) GM_FLAT_M(NV_, U_, 1);            \
+    else GM_FLAT_M(NV_, U_, 0);                        \
+  } while (0)
+    if (nv == 1 && slots <= 8 && lane_split()) GM_FLAT_P(16, 4);
+    else if (nv == 1 && slots <= 16 && lane_split()) GM_FLAT_P(16, 2);
+    else if (sizeof(T) == 2 && nv == 1 && slots <= 16 && narrow_u16()) {
+      if constexpr (sizeof(T) == 2) GM_FLAT(1, 16);
+    } else if (nv == 1) GM_FLAT(1, 8);
+    else if (nv == 2) GM_FLAT(2, 4);
+    else if (nv == 4 || kChunk <= 128) GM_FLAT(4, 2);
+    else if constexpr (kChunk > 128) GM_FLAT(8, 1);
+#undef GM_FLAT
+#undef GM_FLAT_M
+#undef GM_FLAT_P
+#undef GM_FLAT_MP
+    GM_CHECK_LAUNCH("spmm_flat_kernel");
+  }
+  return GM_OK;
+}
+
+template <typename T, int VB, bool MAXMIN>
+gm_status launch_light(const SpmmArgs& p0, int64_t ns, cudaStream_t st) {
+  // wide rows without the fused GCN term take the flat edge-stream kernel
+  if (p0.gdeg_src == nullptr && (ns > 8 || lane_split()) && p0.flat_ok)
+    return launch_flat<T, VB, MAXMIN>(p0, ns, st);
+  // chunk columns so a lane holds <= 8 vectors; pick LPR/NV per chunk
+  for (int64_t base = 0; base < ns; base += 256) {
+    SpmmArgs p = p0;
+    p.slot_base = base;
+    p.slot_end = std::min<int64_t>(ns, base + 256);
+    const int64_t slots = p.slot_end - base;
+    int lpr = 32, nv = 1;
+    if (slots <= 4) lpr = 4;
+    else if (slots <= 8) lpr = 8;
+    else if (slots <= 16) lpr = 16;
+    else if (slots <= 32) lpr = 32;
+    else nv = slots <= 64 ? 2 : slots <= 128 ? 4 : 8;
+    const int64_t threads = p.num_windows * lpr;
+    const unsigned grid = static_cast<unsigned>(ceil_div(threads, 256));
+#define GM_LIGHT(LPR_, NV_, U_) \
+  spmm_light_kernel<T, VB, NV_, LPR_, U_, MAXMIN><<<grid, 256, 0, st>>>(p)
+    if (nv == 1) {
+      if (lpr == 4) GM_LIGHT(4, 1, 8);
+      else if (lpr == 8) GM_LIGHT(8, 1, 8);
+      else if (lpr == 16) GM_LIGHT(16, 1, 8);
+      else GM_LIGHT(32, 1, 8);
+    } else if (nv == 2) {
+      GM_LIGHT(32, 2, 4);
+    } else if (nv == 4) {
+      GM_LIGHT(32, 4, 2);
+    } else {
+      GM_LIGHT(32, 8, 1);
+    }
+#undef GM_LIGHT
+    GM_CHECK_LAUNCH("spmm_light_kernel");
+  }
+  return GM_OK;
+}
+
+template <typename T, int VB, bool MAXMIN>
+gm_status launch_heavy(const SpmmArgs& p0, int64_t num_heavy, int64_t ns, cudaStream_t st) {
+  using A = typename AccOf<T>::type;
+  constexpr int64_t kChunk = 4 * kHeavyThreads;  // slots per column chunk (MH <= 4)
+  for (int64_t base = 0; base < ns; base += kChunk) {
+    SpmmArgs p = p0;
+    p.slot_base = base;
+    p.slot_end = std::min<int64_t>(ns, base + kChunk);
+    const int64_t slots = p.slot_end - base;
+    const int rowb = static_cast<int>(slots * VB);
+    int se = static_cast<int>(std::min<int64_t>(128, std::max<int64_t>(2, 65536 / (kRing * rowb))));
+    const size_t smem = heavy_smem_bytes<A>(se, rowb);
+    const int mh = slots <= kHeavyThreads ? 1 : slots <= 2 * kHeavyThreads ? 2 : 4;
+#define GM_HEAVY(MH_)                                                                    \
+  do {                                                                                   \
+    auto kern = spmm_heavy_kernel<T, VB, MH_, MAXMIN>;                                   \
+    gm_status s_ = ensure_smem(kern, smem);                                              \
+    if (s_ != GM_OK) return s_;                                                          \
+    kern<<<static_cast<unsigned>(num_heavy), kHeavyThreads, smem, st>>>(p, se);          \
+  } while (0)
+    if (mh == 1) GM_HEAVY(1);
+    else if (mh == 2) GM_HEAVY(2);
+    else GM_HEAVY(4);
+#undef GM_HEAVY
+    GM_CHECK_LAUNCH("spmm_heavy_kernel");
+  }
+  return GM_OK;
+}
+
+template <typename T, int VB>
+gm_status dispatch_vb(const SpmmArgs& p, bool maxmin, bool use_heavy, int64_t num_heavy,
+                             int64_t ns, cudaStream_t st) {
+  if constexpr (VB >= 4) {
+  // Wide rows (>= 1 KB): every row takes the CTA-per-row cp.async pipeline,
+  // whose in-flight bytes do not cost registers (Reddit-shaped F=602).
+  if (wide_cta_mode() && static_cast<int64_t>(p.f) * static_cast<int64_t>(sizeof(T)) >= kWideRowBytes &&
+      p.num_rows > 0) {
+    SpmmArgs q = p;
+    q.heavy_rows = nullptr;
+    q.heavy_thr = -1;
+    return maxmin ? launch_heavy<T, VB, true>(q, p.num_rows, ns, st) : launch_heavy<T, VB, false>(q, p.num_rows, ns, st);
+  }
+  if (use_heavy) {
+    SideStream* ss = nullptr;
+    gm_status s = side_stream(&ss);
+    if (s != GM_OK) return s;
+    GM_TRY_CUDA(cudaEventRecord(ss->fork, st));
+    GM_TRY_CUDA(cudaStreamWaitEvent(ss->side, ss->fork, 0));
+    s = maxmin ? launch_heavy<T, VB, true>(p, num_heavy, ns, ss->side)
+               : launch_heavy<T, VB, false>(p, num_heavy, ns, ss->side);
+    if (s != GM_OK) return s;
+    GM_TRY_CUDA(cudaEventRecord(ss->join, ss->side));
+    s = maxmin ? launch_light<T, VB, true>(p, ns, st) : launch_light<T, VB, false>(p, ns, st);
+    if (s != GM_OK) return s;
+    GM_TRY_CUDA(cudaStreamWaitEvent(st, ss->join, 0));
+    return GM_OK;
+  }
+  }
+  (void)num_heavy;
+  return maxmin ? launch_light<T, VB, true>(p, ns, st) : launch_light<T, VB, false>(p, ns, st);
+}
+
+
+// Per-dtype dispatch, instantiated in spmm_f32.cu / spmm_f64.cu / spmm_bf16.cu.
+gm_status spmm_dispatch_f32(const SpmmArgs& p, bool maxmin, bool use_heavy, int64_t num_heavy, int64_t ns, int vb,
+                            cudaStream_t st);
+gm_status spmm_dispatch_f64(const SpmmArgs& p, bool maxmin, bool use_heavy, int64_t num_heavy, int64_t ns, int vb,
+                            cudaStream_t st);
+gm_status spmm_dispatch_bf16(const SpmmArgs& p, bool maxmin, bool use_heavy, int64_t num_heavy, int64_t ns, int vb,
+                             cudaStream_t st);
+
+}  // namespace gm

@@ -1,0 +1,132 @@
+"""Throughput of every BASELINE.json config on one B200 (CUDA events, L2
+flushed between timed calls, warmup 3). Prints one JSON object per config.
+
+  C1 Cora-shaped 2-layer GCN forward (fp32, 1433 -> 16 -> 16 -> head 7)
+  C2 Reddit-shaped mean SpMM (F=602 fp32)
+  C3 OGB-MAG segment_matmul (K=N=128 bf16)  [+ per-edge-type mean SpMM at F=128]
+  C4 ogbn-products sum / max+argmax SpMM (F=100 fp32)
+  C5 ogbn-papers100M sum SpMM (F=128 bf16)
+"""
+import ctypes as C
+import json
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2507_16991_b200 as gm  # noqa: E402
+from paper_2507_16991_b200 import _lib as L  # noqa: E402
+
+PEAKS = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+HBM = PEAKS["hbm_gbs"]
+SEED = 0x67726170686D696C
+FLUSH = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+
+def timed(fn, reps=10, warm=3):
+    for _ in range(warm):
+        fn()
+    ts = []
+    for _ in range(reps):
+        FLUSH.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return sum(ts) / len(ts)
+
+
+def graph(kind, n, e, seed=SEED):
+    s = torch.empty(e, dtype=torch.int64, device="cuda")
+    d = torch.empty(e, dtype=torch.int64, device="cuda")
+    L.check(L.lib().gm_synth_edges(kind, seed, 0, e, n, n, s.data_ptr(), d.data_ptr(),
+                                   torch.cuda.current_stream().cuda_stream))
+    return gm.EdgeIndex(s, d, n, n)
+
+
+def feats(n, f, dtype):
+    x = torch.empty(n, f, dtype=dtype, device="cuda")
+    code = {torch.float32: L.GM_F32, torch.bfloat16: L.GM_BF16}[dtype]
+    L.check(L.lib().gm_synth_features(SEED, 0, n, f, 0, code, x.data_ptr(), torch.cuda.current_stream().cuda_stream))
+    return x
+
+
+def spmm_line(name, kind, n, e, f, dtype, reduce):
+    g = graph(kind, n, e)
+    x = feats(n, f, dtype)
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    csc = g.to_csc()
+    t1.record()
+    torch.cuda.synchronize()
+    build_ms = t0.elapsed_time(t1)
+    csc.plan()
+    if reduce in ("max", "min"):
+        ms = timed(lambda: gm.neighbor_aggregate(g, x, reduce, return_argmax=True))
+    else:
+        ms = timed(lambda: gm.spmm(g, x, None, reduce))
+    s = x.element_size()
+    byts = e * (f * s + 4) + n * (8 + f * s) + (n * f * 4 if reduce in ("max", "min") else 0)
+    r = {"config": name, "reduce": reduce, "dtype": str(dtype).split(".")[-1], "nodes": n, "edges": e, "feats": f,
+         "ms": ms, "gedges_s": e / ms / 1e6, "algo_gbs": byts / ms / 1e6, "frac_hbm": byts / ms / 1e6 / HBM,
+         "csc_build_ms": build_ms, "heavy_rows": int(csc.plan().num_heavy)}
+    print(json.dumps(r), flush=True)
+    del g, x, csc
+    torch.cuda.empty_cache()
+    return r
+
+
+def cora():
+    n, e = 2708, 10556
+    g = graph(0, n, e)
+    torch.manual_seed(0)
+    h = torch.randn(n, 1433, device="cuda")
+    w1, w2, wh = (torch.randn(1433, 16, device="cuda") / 38, torch.randn(16, 16, device="cuda") / 4,
+                  torch.randn(16, 7, device="cuda") / 4)
+    b1, b2, bh = torch.zeros(16, device="cuda"), torch.zeros(16, device="cuda"), torch.zeros(7, device="cuda")
+
+    def fwd():
+        z = torch.relu(gm.gcn_layer(g, h, w1, b1))
+        z = gm.gcn_layer(g, z, w2, b2)
+        return z @ wh + bh
+
+    ms = timed(fwd, reps=50)
+    r = {"config": "C1 cora 2-layer GCN forward", "ms": ms, "nodes": n, "edges": e, "feats": 1433,
+         "note": "launch-bound (2 transforms + 2 fused GCN SpMMs + head); parity config"}
+    print(json.dumps(r), flush=True)
+
+
+def mag_gemm():
+    ptr = [0, 736_389, 1_871_038, 1_879_778, 1_939_743]
+    x = torch.randn(ptr[-1], 128, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(4, 128, 128, device="cuda") / 11).to(torch.bfloat16)
+    ms = timed(lambda: gm.segment_matmul(x, ptr, w), reps=20)
+    flops = 2.0 * ptr[-1] * 128 * 128
+    byts = 2.0 * ptr[-1] * 256 + 4 * 128 * 128 * 2
+    r = {"config": "C3 ogb-mag segment_matmul", "ms": ms, "tflops": flops / ms / 1e9,
+         "algo_gbs": byts / ms / 1e6, "frac_hbm": byts / ms / 1e6 / HBM,
+         "frac_tensor": flops / ms / 1e9 / PEAKS["bf16_tflops"]}
+    print(json.dumps(r), flush=True)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["C1", "C2", "C3", "C4", "C5"]
+    if "C1" in which:
+        cora()
+    if "C3" in which:
+        mag_gemm()
+        spmm_line("C3 ogb-mag per-relation mean SpMM (writes, 1.13M->0.74M)", 0, 1_134_649, 7_145_660, 128,
+                  torch.float32, "mean")
+    if "C4" in which:
+        spmm_line("C4 ogbn-products", 1, 2_449_029, 61_859_140, 100, torch.float32, "sum")
+        spmm_line("C4 ogbn-products", 1, 2_449_029, 61_859_140, 100, torch.float32, "max")
+    if "C2" in which:
+        spmm_line("C2 reddit", 1, 232_965, 114_615_892, 602, torch.float32, "mean")
+    if "C5" in which:
+        spmm_line("C5 ogbn-papers100M (1 GPU)", 1, 111_059_956, 1_615_685_872, 128, torch.bfloat16, "sum")
