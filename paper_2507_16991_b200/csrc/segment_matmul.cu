@@ -36,6 +36,8 @@ constexpr int BM = 128;          // UMMA M (cta_group::1)
 constexpr int BK = 64;           // k elements per stage (128 B rows, SWIZZLE_128B)
 constexpr int kThreads = 192;    // 6 warps
 constexpr uint32_t kAStageBytes = BM * BK * 2;  // 16 KB
+constexpr uint32_t kCBoxBytes = 32 * 128;       // 32 rows x 128 B
+constexpr uint32_t kCStageBytes = 4 * 2 * kCBoxBytes;  // 4 warps x double buffer = 32 KB
 
 struct Params {
   int64_t ptr[kMaxGroups + 1];        // group row offsets
@@ -49,6 +51,7 @@ struct Params {
   int32_t out_f32;
   int32_t stages;
   int32_t b_resident;
+  int32_t tma_store;                  // full tiles leave through TMA bulk stores
   uint32_t tmem_cols;
   void* out;
 };
@@ -85,6 +88,22 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
           smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -159,7 +178,7 @@ __device__ __forceinline__ uint32_t pack_bf16(uint32_t lo_f32, uint32_t hi_f32) 
 
 __global__ void __launch_bounds__(kThreads, 1)
 segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ CUtensorMap map_a,
-                      const __grid_constant__ CUtensorMap map_b) {
+                      const __grid_constant__ CUtensorMap map_b, const __grid_constant__ CUtensorMap map_c) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-B alignment for the SWIZZLE_128B atoms
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -169,7 +188,9 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
   unsigned char* b_buf = smem + static_cast<size_t>(S) * kAStageBytes;
   const size_t b_bytes = P.b_resident ? static_cast<size_t>(P.k_blocks) * b_kblock_bytes
                                       : static_cast<size_t>(S) * b_kblock_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(b_buf + b_bytes);
+  // output staging: per epilogue warp two 32-row x 128-byte SWIZZLE_128B boxes
+  unsigned char* c_stage = b_buf + b_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(c_stage + kCStageBytes);
   uint64_t* full = bars;              // [S]
   uint64_t* empty = bars + S;         // [S]
   uint64_t* tfull = bars + 2 * S;     // [2]
@@ -302,33 +323,75 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
   } else {
     // ------------------------------------------------------------ epilogue
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int esz = P.out_f32 ? 4 : 2;
+    const int chunk_cols = 128 / esz;  // columns per 128-byte TMA box
+    unsigned char* my_stage = c_stage + static_cast<size_t>(warp - 2) * 2 * kCBoxBytes;
     int acc = 0;
     uint32_t aph = 0;
+    int nstore = 0;
     for (int t = blockIdx.x; t < P.num_tiles; t += gridDim.x) {
       int g, mt, nt;
       decode_tile(P, t, g, mt, nt);
       const int64_t grow_end = P.ptr[g + 1];
-      const int64_t row = P.ptr[g] + static_cast<int64_t>(mt) * BM + q * 32 + lane;
+      const int64_t row0 = P.ptr[g] + static_cast<int64_t>(mt) * BM;
+      const int64_t row = row0 + q * 32 + lane;
+      const bool full_tile = P.tma_store && row0 + BM <= grow_end;  // else: masked direct stores
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * P.bn);
-      const bool live = row < grow_end;
-      for (int c = 0; c < P.bn; c += 32) {
-        uint32_t v[32];
-        const int width = min(32, P.bn - c);
-        if (width == 32) tmem_ld32<32>(tbase + c, v);
-        else tmem_ld32<16>(tbase + c, v);
-        tmem_wait_ld();
-        if (live) {
-          const int64_t col0 = static_cast<int64_t>(nt) * P.bn + c;
+      if (full_tile) {
+        for (int c = 0; c < P.bn; c += chunk_cols) {
+          // 128 bytes of this lane's row: 32 fp32 or 64 bf16 values
+          uint32_t packed[32];
           if (P.out_f32) {
-            float* o = static_cast<float*>(P.out) + row * P.n + col0;
-            for (int i = 0; i < width; i += 4) st_na_v4(o + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
+            tmem_ld32<32>(tbase + c, packed);
+            tmem_wait_ld();
           } else {
-            __nv_bfloat16* o = static_cast<__nv_bfloat16*>(P.out) + row * P.n + col0;
-            for (int i = 0; i < width; i += 8)
-              st_na_v4(o + i, pack_bf16(v[i], v[i + 1]), pack_bf16(v[i + 2], v[i + 3]),
-                       pack_bf16(v[i + 4], v[i + 5]), pack_bf16(v[i + 6], v[i + 7]));
+            uint32_t v[32];
+            tmem_ld32<32>(tbase + c, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) packed[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
+            tmem_ld32<32>(tbase + c + 32, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) packed[16 + i] = pack_bf16(v[2 * i], v[2 * i + 1]);
+          }
+          const int b = nstore & 1;
+          if (lane == 0 && nstore >= 2) bulk_wait_read<1>();  // buffer b's previous store has read smem
+          __syncwarp();
+          const uint32_t sbase = smem_u32(my_stage + b * kCBoxBytes) + lane * 128;
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch)  // SWIZZLE_128B: 16-B chunk ch lands at ch ^ (row % 8)
+            st_shared_v4(sbase + ((ch ^ (lane & 7)) << 4), packed[4 * ch], packed[4 * ch + 1], packed[4 * ch + 2],
+                         packed[4 * ch + 3]);
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&map_c, my_stage + b * kCBoxBytes, nt * P.bn + c, static_cast<int32_t>(row0 + q * 32));
+            bulk_commit();
+          }
+          ++nstore;
+        }
+      } else {
+        const bool live = row < grow_end;
+        for (int c = 0; c < P.bn; c += 32) {
+          uint32_t v[32];
+          const int width = min(32, P.bn - c);
+          if (width == 32) tmem_ld32<32>(tbase + c, v);
+          else tmem_ld32<16>(tbase + c, v);
+          tmem_wait_ld();
+          if (live) {
+            const int64_t col0 = static_cast<int64_t>(nt) * P.bn + c;
+            if (P.out_f32) {
+              float* o = static_cast<float*>(P.out) + row * P.n + col0;
+              for (int i = 0; i < width; i += 4) st_na_v4(o + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
+            } else {
+              __nv_bfloat16* o = static_cast<__nv_bfloat16*>(P.out) + row * P.n + col0;
+              for (int i = 0; i < width; i += 8)
+                st_na_v4(o + i, pack_bf16(v[i], v[i + 1]), pack_bf16(v[i + 2], v[i + 3]),
+                         pack_bf16(v[i + 4], v[i + 5]), pack_bf16(v[i + 6], v[i + 7]));
+            }
           }
         }
       }
@@ -340,6 +403,8 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
         aph ^= 1;
       }
     }
+    if (lane == 0) bulk_wait_all();  // stores complete before the CTA exits
+    __syncwarp();
   }
 
   tc_fence_before();
@@ -409,14 +474,15 @@ static EncodeTiledFn encode_fn() {
 }
 
 static gm_status make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
-                          uint32_t box_outer) {
+                          uint32_t box_outer, CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                          uint64_t esz = 2) {
   EncodeTiledFn fn = encode_fn();
   GM_REQUIRE(fn, GM_ERR_CUDA, "segment_matmul: cuTensorMapEncodeTiled unavailable");
   const cuuint64_t dims[2] = {inner, outer};
-  const cuuint64_t strides[1] = {inner * 2};
+  const cuuint64_t strides[1] = {inner * esz};
   const cuuint32_t box[2] = {box_inner, box_outer};
   const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+  const CUresult r = fn(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   GM_REQUIRE(r == CUDA_SUCCESS, GM_ERR_CUDA, "segment_matmul: cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
@@ -492,6 +558,7 @@ GM_API gm_status gm_segment_matmul(const void* x, const int64_t* ptr_host, int64
   P.n = static_cast<int32_t>(n);
   P.out_f32 = out_dtype == GM_F32;
   P.out = outk;
+  P.tma_store = (P.bn % (128 / static_cast<int>(out_dtype == GM_F32 ? 4 : 2))) == 0 ? 1 : 0;
   int32_t tiles = 0;
   for (int64_t g = 0; g < groups; ++g) {
     P.ptr[g] = ptr_host[g];
@@ -508,14 +575,14 @@ GM_API gm_status gm_segment_matmul(const void* x, const int64_t* ptr_host, int64
   const size_t b_full_bytes = static_cast<size_t>(P.k_blocks) * P.bn * BK * 2;
   const size_t b_stage_bytes = static_cast<size_t>(P.bn) * BK * 2;
   P.b_resident = (P.n_tiles == 1 && b_full_bytes <= 64 * 1024) ? 1 : 0;
-  const size_t budget = 227 * 1024 - 1024 - 256;  // alignment slack + barriers
+  const size_t budget = 227 * 1024 - 1024 - 256 - kCStageBytes;  // alignment slack, barriers, out staging
   int stages;
   if (P.b_resident) stages = static_cast<int>((budget - b_full_bytes) / kAStageBytes);
   else stages = static_cast<int>(budget / (kAStageBytes + b_stage_bytes));
   stages = std::max(2, std::min(stages, 8));
   P.stages = stages;
   const size_t smem = 1024 + static_cast<size_t>(stages) * kAStageBytes +
-                      (P.b_resident ? b_full_bytes : static_cast<size_t>(stages) * b_stage_bytes) + 256;
+                      (P.b_resident ? b_full_bytes : static_cast<size_t>(stages) * b_stage_bytes) + kCStageBytes + 256;
 
   // K-major copy of the weights: W^T as a zero-padded [G*N, K] bf16 matrix
   transpose_w_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(groups * k * n, 256), 4096)), 256, 0, st>>>(
@@ -528,6 +595,12 @@ GM_API gm_status gm_segment_matmul(const void* x, const int64_t* ptr_host, int64
   if (s != GM_OK) return s;
   s = make_map(&map_b, wt, static_cast<uint64_t>(k), static_cast<uint64_t>(groups * n), BK, static_cast<uint32_t>(P.bn));
   if (s != GM_OK) return s;
+  // output map: [rows, n] of the output dtype, 128-byte x 32-row SWIZZLE_128B boxes
+  CUtensorMap map_c;
+  s = make_map(&map_c, outk, static_cast<uint64_t>(n), static_cast<uint64_t>(rows), 128 / static_cast<uint32_t>(esz),
+               32, out_dtype == GM_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+               static_cast<uint64_t>(esz));
+  if (s != GM_OK) return s;
 
   static std::once_flag attr_once;
   static cudaError_t attr_err = cudaSuccess;
@@ -536,7 +609,7 @@ GM_API gm_status gm_segment_matmul(const void* x, const int64_t* ptr_host, int64
   });
   GM_TRY_CUDA(attr_err);
   const unsigned grid = static_cast<unsigned>(std::min<int32_t>(tiles, kNumSMs));
-  segment_matmul_kernel<<<grid, kThreads, smem, st>>>(P, map_a, map_b);
+  segment_matmul_kernel<<<grid, kThreads, smem, st>>>(P, map_a, map_b, map_c);
   GM_CHECK_LAUNCH("segment_matmul_kernel");
   if (n != n_in) {
     unpad_cols_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(rows * n_in, 256), 8192)), 256, 0, st>>>(
