@@ -184,6 +184,18 @@ GM_API gm_status gm_spmm(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype d
                          const gm_gcn_norm* gcn, gm_reduce reduce, void* out, int32_t* arg_out,
                          gm_stream_t stream);
 
+/* Backward of spmm (message_passing.hpp:119-166). With g the gradient of the
+ * output [n_dst, f]:
+ *   scaled_g = mean ? g / S(max(deg_dst, 1)) : g           gm_scale_rows_div (:128-132)
+ *   dx = gm_spmm(CSR by source, scaled_g, w in CSR order)   transposed product (:133-155)
+ *   dw[i] = sum_j scaled_g[dst[i]][j] * x[src[i]][j]       gm_edge_dot (:156-165)
+ * f32/f64, bit-identical to the reference's closure (sequential order, no FMA). */
+GM_API gm_status gm_scale_rows_div(gm_dtype dtype, const void* in, int64_t rows, int64_t f,
+                                   const int32_t* deg, void* out, gm_stream_t stream);
+GM_API gm_status gm_edge_dot(gm_dtype dtype, const int64_t* src, const int64_t* dst, int64_t num_edges,
+                             const void* a_by_dst, const void* b_by_src, int64_t f, void* out,
+                             gm_stream_t stream);
+
 /* ------------------------------------------------------------------------ */
 /* segment_matmul (L4): hetero.hpp:134-157 grouped_matmul                    */
 /* ------------------------------------------------------------------------ */

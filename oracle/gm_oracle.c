@@ -165,3 +165,37 @@ void or_degree(const int64_t* ids, int64_t len, int64_t n, int64_t* deg) {
   }
 DEFINE_SEGMM(f64, double)
 DEFINE_SEGMM(f32, float)
+
+/* message_passing.hpp:119-166 (the spmm backward closure) */
+#define DEFINE_SPMM_BWD(SUF, S)                                                               \
+  void or_spmm_backward_##SUF(const int64_t* rp, const int64_t* col, const int64_t* perm,     \
+                              int64_t n_src, const int64_t* src, const int64_t* dst,          \
+                              int64_t e, const S* g, const S* x, int64_t f, const S* w,       \
+                              const int64_t* deg, S* dx, S* dw) {                             \
+    /* scaled_g(v, j) = mean ? g / S(max(deg[v], 1)) : g  (:128-132) */                       \
+    for (int64_t u = 0; u < n_src; ++u) {                                                     \
+      S* o = dx + u * f;                                                                      \
+      for (int64_t j = 0; j < f; ++j) o[j] = (S)0;                                            \
+      for (int64_t k = rp[u]; k < rp[u + 1]; ++k) {                                           \
+        const int64_t v = col[k];                                                             \
+        const S coeff = w ? w[perm[k]] : (S)1;                                                \
+        for (int64_t j = 0; j < f; ++j) {                                                     \
+          const S gv = g[v * f + j];                                                          \
+          const S sg = deg ? gv / (S)(deg[v] > 1 ? deg[v] : 1) : gv;                          \
+          o[j] += coeff * sg;                                                                 \
+        }                                                                                     \
+      }                                                                                       \
+    }                                                                                         \
+    if (w && dw)                                                                              \
+      for (int64_t i = 0; i < e; ++i) {                                                       \
+        S acc = (S)0;                                                                         \
+        for (int64_t j = 0; j < f; ++j) {                                                     \
+          const S gv = g[dst[i] * f + j];                                                     \
+          const S sg = deg ? gv / (S)(deg[dst[i]] > 1 ? deg[dst[i]] : 1) : gv;                \
+          acc += sg * x[src[i] * f + j];                                                      \
+        }                                                                                     \
+        dw[i] = acc;                                                                          \
+      }                                                                                       \
+  }
+DEFINE_SPMM_BWD(f32, float)
+DEFINE_SPMM_BWD(f64, double)

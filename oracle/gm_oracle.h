@@ -69,6 +69,20 @@ void or_gcn_norm_f64(const int64_t* base_full_src, const int64_t* base_full_dst,
                      int64_t n_src, int64_t n_dst, const int64_t* g_src, const int64_t* g_dst,
                      int64_t g_len, int square, double* norm);
 
+/* message_passing.hpp:119-166 spmm backward. csr_* : the CSR by SOURCE
+ * (EdgeIndex::to_csr(), :143). g: grad of out [n_dst, f]. deg_dst != NULL
+ * selects mean (scaled_g = g / S(max(deg, 1)), :128-132). w_coo may be NULL.
+ * dx [n_src, f] (:133-155); dw [E] if w_coo && dw (:156-165, sequential in j,
+ * over the COO arrays src/dst). */
+void or_spmm_backward_f32(const int64_t* csr_rowptr, const int64_t* csr_col, const int64_t* csr_perm,
+                          int64_t n_src, const int64_t* src, const int64_t* dst, int64_t num_edges,
+                          const float* g, const float* x, int64_t f, const float* w_coo,
+                          const int64_t* deg_dst, float* dx, float* dw);
+void or_spmm_backward_f64(const int64_t* csr_rowptr, const int64_t* csr_col, const int64_t* csr_perm,
+                          int64_t n_src, const int64_t* src, const int64_t* dst, int64_t num_edges,
+                          const double* g, const double* x, int64_t f, const double* w_coo,
+                          const int64_t* deg_dst, double* dx, double* dw);
+
 /* Occurrence counts of ids in [0, n) (message_passing.hpp:76-78, 441-443). */
 void or_degree(const int64_t* ids, int64_t len, int64_t n, int64_t* deg);
 

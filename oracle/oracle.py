@@ -52,7 +52,8 @@ class Oracle:
         self.lib = C.CDLL(ORACLE_SO)
         for name in ("or_build_compressed", "or_spmm_f32", "or_spmm_f64", "or_spmm_coo_f32",
                      "or_spmm_coo_f64", "or_spmm_max_f32", "or_spmm_max_f64", "or_gcn_norm_f32",
-                     "or_gcn_norm_f64", "or_degree", "or_segment_matmul_f64", "or_segment_matmul_f32"):
+                     "or_gcn_norm_f64", "or_degree", "or_segment_matmul_f64", "or_segment_matmul_f32",
+                     "or_spmm_backward_f32", "or_spmm_backward_f64"):
             getattr(self.lib, name).restype = None
 
     def build_compressed(self, keys, values, num_rows):
@@ -113,6 +114,23 @@ class Oracle:
                                                 _I(n_src), _I(n_dst), _ptr(g_src), _ptr(g_dst),
                                                 _I(g_src.size), C.c_int(int(square)), _ptr(norm))
         return norm
+
+    def spmm_backward(self, src, dst, n_src, n_dst, g, x, w_coo=None, mean=False):
+        """dx, dw of spmm (message_passing.hpp:119-166) via the CSR by source."""
+        src, dst = _i64(src), _i64(dst)
+        g = np.ascontiguousarray(g)
+        x = np.ascontiguousarray(x, dtype=g.dtype)
+        suf = "f64" if g.dtype == np.float64 else "f32"
+        f = g.shape[1]
+        rp, col, perm = self.build_compressed(src, dst, n_src)
+        deg = self.degree(dst, n_dst) if mean else None
+        dx = np.zeros((n_src, f), g.dtype)
+        w = None if w_coo is None else np.ascontiguousarray(w_coo, dtype=g.dtype)
+        dw = np.zeros(src.size, g.dtype) if w is not None else None
+        getattr(self.lib, "or_spmm_backward_" + suf)(
+            _ptr(rp), _ptr(col), _ptr(perm), _I(n_src), _ptr(src), _ptr(dst), _I(src.size), _ptr(g), _ptr(x),
+            _I(f), _ptr(w), _ptr(deg), _ptr(dx), _ptr(dw))
+        return dx, dw
 
     def degree(self, ids, n):
         deg = np.zeros(n, np.int64)
@@ -190,6 +208,20 @@ class Reference:
             _ptr(src), _ptr(dst), _I(src.size), _I(n_src), _I(n_dst), C.c_int(int(undirected)), _ptr(x), _I(f),
             _ptr(wa), C.c_int(int(mean)), _ptr(out)))
         return out
+
+    def spmm_backward(self, src, dst, n_src, n_dst, x, g, w=None, mean=False, undirected=False):
+        x = np.ascontiguousarray(x)
+        g = np.ascontiguousarray(g, dtype=x.dtype)
+        suf = "f64" if x.dtype == np.float64 else "f32"
+        src, dst = _i64(src), _i64(dst)
+        f = x.shape[1]
+        dx = np.zeros((n_src, f), x.dtype)
+        wa = None if w is None else np.ascontiguousarray(w, dtype=x.dtype)
+        dw = None if w is None else np.zeros(src.size, x.dtype)
+        self._check(getattr(self.lib, "ref_spmm_backward_" + suf)(
+            _ptr(src), _ptr(dst), _I(src.size), _I(n_src), _I(n_dst), C.c_int(int(undirected)), _ptr(x), _I(f),
+            _ptr(wa), C.c_int(int(mean)), _ptr(g), _ptr(dx), _ptr(dw)))
+        return dx, dw
 
     def max_path(self, src, dst, n_src, n_dst, x, is_min=False):
         x = np.ascontiguousarray(x)

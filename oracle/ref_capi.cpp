@@ -101,9 +101,54 @@ int max_impl(const int64_t* src, const int64_t* dst, int64_t e, int64_t n_src, i
   });
 }
 
+// spmm backward through the reference's own tape: loss = sum(mul(spmm(e, x, w), G)),
+// so the gradient entering spmm's closure is exactly G (test_message_passing.cpp:92-105).
+template <typename S>
+int spmm_bwd_impl(const int64_t* src, const int64_t* dst, int64_t e, int64_t n_src, int64_t n_dst, int undirected,
+                  const S* x, int64_t f, const S* w, int mean, const S* G, S* dx, S* dw) {
+  return guarded([&] {
+    EdgeIndex ei = make_index(src, dst, e, n_src, n_dst, undirected);
+    Tensor<S> xt = make_tensor(x, n_src, f);
+    xt.set_requires_grad(true);
+    std::optional<Tensor<S>> wt;
+    if (w) {
+      wt = Tensor<S>::from_data({e}, std::vector<S>(w, w + e));
+      wt->set_requires_grad(true);
+    }
+    Tensor<S> out = spmm(ei, xt, wt, mean ? AggKind::mean : AggKind::sum);
+    Tensor<S> coeff = make_tensor(G, n_dst, f);
+    backward(sum(mul(out, coeff)));
+    if (xt.has_grad()) {
+      Tensor<S> gx = xt.grad();
+      std::memcpy(dx, gx.data().data(), sizeof(S) * static_cast<size_t>(n_src * f));
+    } else {
+      std::fill(dx, dx + n_src * f, S(0));
+    }
+    if (w && dw) {
+      if (wt->has_grad()) {
+        Tensor<S> gw = wt->grad();
+        std::memcpy(dw, gw.data().data(), sizeof(S) * static_cast<size_t>(e));
+      } else {
+        std::fill(dw, dw + e, S(0));
+      }
+    }
+  });
+}
+
 }  // namespace
 
 extern "C" {
+
+int ref_spmm_backward_f32(const int64_t* src, const int64_t* dst, int64_t e, int64_t n_src, int64_t n_dst,
+                          int undirected, const float* x, int64_t f, const float* w, int mean, const float* G,
+                          float* dx, float* dw) {
+  return spmm_bwd_impl<float>(src, dst, e, n_src, n_dst, undirected, x, f, w, mean, G, dx, dw);
+}
+int ref_spmm_backward_f64(const int64_t* src, const int64_t* dst, int64_t e, int64_t n_src, int64_t n_dst,
+                          int undirected, const double* x, int64_t f, const double* w, int mean, const double* G,
+                          double* dx, double* dw) {
+  return spmm_bwd_impl<double>(src, dst, e, n_src, n_dst, undirected, x, f, w, mean, G, dx, dw);
+}
 
 const char* ref_last_error() { return g_err.c_str(); }
 

@@ -74,6 +74,8 @@ SIGNATURES = {
     "gm_gcn_degrees": (C.c_int, [_P, _P, _I64, _I64, _I64, C.c_int, _P, _P, _P]),
     "gm_spmm": (C.c_int, [C.POINTER(gm_csr), C.POINTER(gm_spmm_plan), C.c_int, _P, _I64, _P,
                           C.POINTER(gm_gcn_norm), C.c_int, _P, _P, _P]),
+    "gm_scale_rows_div": (C.c_int, [C.c_int, _P, _I64, _I64, _P, _P, _P]),
+    "gm_edge_dot": (C.c_int, [C.c_int, _P, _P, _I64, _P, _P, _I64, _P, _P]),
     "gm_segment_matmul_workspace": (C.c_size_t, [_I64, _I64, _I64, _I64]),
     "gm_segment_matmul": (C.c_int, [_P, C.POINTER(C.c_int64), _I64, _I64, _I64, _P, C.c_int, _P,
                                     _P, C.c_size_t, _P]),

@@ -1,0 +1,106 @@
+// backward.cu — pieces of the spmm backward (message_passing.hpp:119-166)
+// that are not themselves an SpMM:
+//   gm_scale_rows_div : scaled_g(v, j) = g[v][j] / S(max(deg[v], 1))   (:128-132)
+//   gm_edge_dot       : dw[i] = sum_j scaled_g(dst[i], j) * x[src[i], j] (:156-165)
+// dx itself is gm_spmm over the CSR by source (the transposed product, :143-152).
+// All arithmetic is IEEE round-to-nearest with no contraction, in the
+// reference's order (sequential in j), so results are bit-identical.
+#include <algorithm>
+
+#include "vec.cuh"
+
+namespace gm {
+
+template <typename S>
+__global__ void scale_rows_div_kernel(const S* __restrict__ in, int64_t rows, int64_t f,
+                                      const int32_t* __restrict__ deg, S* __restrict__ out) {
+  const int64_t total = rows * f;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / f;
+    const int32_t d = deg[r] > 1 ? deg[r] : 1;
+    out[i] = div_rn(in[i], static_cast<S>(d));
+  }
+}
+
+// One thread per edge, COO order (coalesced src/dst/dw); both rows are read
+// sequentially by the thread (L1-cached: each 128-B line serves its next loads).
+template <typename S>
+__global__ void __launch_bounds__(256) edge_dot_kernel(const int64_t* __restrict__ src, const int64_t* __restrict__ dst,
+                                                       int64_t e, const S* __restrict__ a, const S* __restrict__ b,
+                                                       int64_t f, S* __restrict__ out) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < e;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const S* ar = a + dst[i] * f;
+    const S* br = b + src[i] * f;
+    S acc = S(0);
+    int64_t j = 0;
+    if constexpr (sizeof(S) == 4) {
+      if ((f & 3) == 0) {
+        const float4* a4 = reinterpret_cast<const float4*>(ar);
+        const float4* b4 = reinterpret_cast<const float4*>(br);
+#pragma unroll 4
+        for (int64_t q = 0; q < f / 4; ++q) {
+          const float4 u = __ldg(a4 + q), v = __ldg(b4 + q);
+          acc = add_rn(acc, mul_rn(u.x, v.x));
+          acc = add_rn(acc, mul_rn(u.y, v.y));
+          acc = add_rn(acc, mul_rn(u.z, v.z));
+          acc = add_rn(acc, mul_rn(u.w, v.w));
+        }
+        j = f;
+      }
+    }
+    for (; j < f; ++j) acc = add_rn(acc, mul_rn(__ldg(ar + j), __ldg(br + j)));
+    out[i] = acc;
+  }
+}
+
+static unsigned grid_of(int64_t n) {
+  return static_cast<unsigned>(std::min<int64_t>(std::max<int64_t>(ceil_div(n, 256), 1), kNumSMs * 32));
+}
+
+}  // namespace gm
+
+using namespace gm;
+
+extern "C" {
+
+GM_API gm_status gm_scale_rows_div(gm_dtype dtype, const void* in, int64_t rows, int64_t f, const int32_t* deg,
+                                   void* out, gm_stream_t stream) {
+  GM_REQUIRE(rows >= 0 && f >= 0, GM_ERR_INVALID_ARGUMENT, "gm_scale_rows_div: negative size");
+  GM_REQUIRE(dtype == GM_F32 || dtype == GM_F64, GM_ERR_INVALID_ARGUMENT, "gm_scale_rows_div: f32/f64 only");
+  if (rows == 0 || f == 0) return GM_OK;
+  cudaStream_t st = as_stream(stream);
+  if (dtype == GM_F32)
+    scale_rows_div_kernel<float><<<grid_of(rows * f), 256, 0, st>>>(static_cast<const float*>(in), rows, f, deg,
+                                                                    static_cast<float*>(out));
+  else
+    scale_rows_div_kernel<double><<<grid_of(rows * f), 256, 0, st>>>(static_cast<const double*>(in), rows, f, deg,
+                                                                     static_cast<double*>(out));
+  GM_CHECK_LAUNCH("scale_rows_div_kernel");
+  return GM_OK;
+}
+
+GM_API gm_status gm_edge_dot(gm_dtype dtype, const int64_t* src, const int64_t* dst, int64_t num_edges,
+                             const void* a_by_dst, const void* b_by_src, int64_t f, void* out, gm_stream_t stream) {
+  GM_REQUIRE(num_edges >= 0 && f >= 0, GM_ERR_INVALID_ARGUMENT, "gm_edge_dot: negative size");
+  GM_REQUIRE(dtype == GM_F32 || dtype == GM_F64, GM_ERR_INVALID_ARGUMENT, "gm_edge_dot: f32/f64 only");
+  if (num_edges == 0) return GM_OK;
+  cudaStream_t st = as_stream(stream);
+  if (dtype == GM_F32) {
+    GM_REQUIRE(reinterpret_cast<uintptr_t>(a_by_dst) % 16 == 0 && reinterpret_cast<uintptr_t>(b_by_src) % 16 == 0,
+               GM_ERR_INVALID_ARGUMENT, "gm_edge_dot: 16-byte aligned rows required");
+    edge_dot_kernel<float><<<grid_of(num_edges), 256, 0, st>>>(src, dst, num_edges, static_cast<const float*>(a_by_dst),
+                                                               static_cast<const float*>(b_by_src), f,
+                                                               static_cast<float*>(out));
+  } else {
+    edge_dot_kernel<double><<<grid_of(num_edges), 256, 0, st>>>(src, dst, num_edges,
+                                                                static_cast<const double*>(a_by_dst),
+                                                                static_cast<const double*>(b_by_src), f,
+                                                                static_cast<double*>(out));
+  }
+  GM_CHECK_LAUNCH("edge_dot_kernel");
+  return GM_OK;
+}
+
+}  // extern "C"

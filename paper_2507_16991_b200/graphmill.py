@@ -9,6 +9,7 @@ against the reference reads the same here:
     build_compressed(keys, values, num_rows)          edge_index.hpp:120-121
     spmm(e, x, edge_weight, reduce)                   message_passing.hpp:92-169
     neighbor_aggregate(e, x, kind, ...)               message_passing.hpp:500-514 (sum/mean/max/min)
+    spmm_backward(e, x, w, reduce, grad_out)          message_passing.hpp:119-166 (dx, dw)
     gcn_aggregate(e, xw) / gcn_layer(e, h, W, b)      message_passing.hpp:437-463, 490-499
     aggregate(values, index, num_groups, kind)        aggregate.hpp:154-215
     segment_matmul(x, ptr, W) / grouped_matmul(xs, W) hetero.hpp:134-157
@@ -324,6 +325,39 @@ def spmm(e: EdgeIndex, x: torch.Tensor, edge_weight: Optional[torch.Tensor], red
     else:
         grouping = e.transpose_view()
     return _run_spmm(grouping, x, reduce, w_csr=w_csr, num_rows=e.num_dst_nodes())
+
+
+def spmm_backward(e: EdgeIndex, x: torch.Tensor, edge_weight: Optional[torch.Tensor], reduce: str,
+                  grad_out: torch.Tensor):
+    """Backward of spmm (message_passing.hpp:119-166): (dx, dw). dx is the
+    transposed product over the CSR-by-source cache (:143), dw the per-edge
+    dot product (:156-165); mean divides the gradient by max(deg, 1) (:128-132).
+    dw is None without an edge weight. f32/f64, bit-identical to the reference."""
+    if reduce not in ("sum", "mean"):
+        raise ValueError("spmm: reduce must be sum or mean")
+    if x.dtype not in (torch.float32, torch.float64):
+        raise ValueError("spmm_backward: f32/f64 only")
+    lib = L.lib()
+    g = grad_out.to(x.dtype).contiguous()
+    f = g.shape[1]
+    if reduce == "mean":
+        deg = torch.empty(e.num_dst_nodes(), dtype=torch.int32, device=g.device)
+        L.check(lib.gm_degree(_p(e.dst()), e.num_edges(), e.num_dst_nodes(), _p(deg), _stream()), "degree")
+        gs = torch.empty_like(g)
+        L.check(lib.gm_scale_rows_div(_DT[x.dtype], _p(g), g.shape[0], f, _p(deg), _p(gs), _stream()), "scale")
+    else:
+        gs = g
+    csr = e.to_csr()
+    w_csr = None
+    if edge_weight is not None:
+        w_csr = _permute(edge_weight.to(x.dtype).contiguous(), csr.perm)
+    dx = _run_spmm(csr, gs, "sum", w_csr=w_csr, num_rows=e.num_src_nodes())
+    dw = None
+    if edge_weight is not None:
+        dw = torch.empty(e.num_edges(), dtype=x.dtype, device=x.device)
+        L.check(lib.gm_edge_dot(_DT[x.dtype], _p(e.src()), _p(e.dst()), e.num_edges(), _p(gs), _p(x.contiguous()),
+                                f, _p(dw), _stream()), "edge_dot")
+    return dx, dw
 
 
 def _acc_dtype(dt):

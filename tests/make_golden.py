@@ -126,6 +126,24 @@ def spmm_fixtures(ref: Reference) -> dict:
     # bf16-rounded inputs, fp32 reference accumulate (output rounding done by the test)
     bx = bf16_round(rng.uniform(-1, 1, (n, 16)))
     d.update(hub_bf16_x=bx, hub_bf16_out=ref.spmm(hs, ht, n, n, bx, None, False))
+    # spmm gradients (test_message_passing.cpp:92-105): graph salt 64, coeff 65, x 66, w 67,
+    # loss = sum(spmm * coeff) -> the gradient entering spmm's closure is coeff
+    bs, bd = refrng.random_graph(8, 20, 64)
+    coeff = refrng.random_tensor((8, 3), 65)
+    bx = refrng.random_tensor((8, 3), 66)
+    bw = refrng.random_tensor((20,), 67)
+    d.update(bwd_src=bs, bwd_dst=bd, bwd_g=coeff, bwd_x=bx, bwd_w=bw)
+    for mean in (0, 1):
+        dx, dw = ref.spmm_backward(bs, bd, 8, 8, bx, coeff, bw, bool(mean))
+        d[f"bwd_dx_m{mean}"], d[f"bwd_dw_m{mean}"] = dx, dw
+        dx0, _ = ref.spmm_backward(bs, bd, 8, 8, bx, coeff, None, bool(mean))
+        d[f"bwd_dx_unweighted_m{mean}"] = dx0
+    # larger f32 backward on the uniform graph
+    ug = rng.uniform(-1, 1, (300, 7)).astype(np.float32)
+    d.update(uni_g=ug)
+    for mean in (0, 1):
+        dx, dw = ref.spmm_backward(d["uni_src"], d["uni_dst"], 300, 300, d["uni_x"], ug, d["uni_w"], bool(mean))
+        d[f"uni_bwd_dx_m{mean}"], d[f"uni_bwd_dw_m{mean}"] = dx, dw
     # GCN edge cases: test_message_passing.cpp:188-207 (edgeless -> identity norm)
     ex = refrng.random_tensor((4, 3), 74, dtype=np.float32)
     d.update(gcn_edgeless_x=ex, gcn_edgeless_out=ref.gcn_aggregate(np.zeros(0), np.zeros(0), 4, ex))
