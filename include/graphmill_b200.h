@@ -196,6 +196,16 @@ GM_API gm_status gm_edge_dot(gm_dtype dtype, const int64_t* src, const int64_t* 
                              const void* a_by_dst, const void* b_by_src, int64_t f, void* out,
                              gm_stream_t stream);
 
+/* Heterogeneous combine (hetero.hpp:338-343 InterCombine::sum, then
+ * layer_update hetero.hpp:362 / message_passing.hpp:579-580 for SAGE):
+ *   out = ((((parts[0] + parts[1]) + ...) + self_term) + bias)   fp32, in this
+ * order; parts are the per-edge-type results for one destination node type in
+ * sorted canonical edge-type order (host array of <= 8 device pointers, each
+ * [rows, f]); self_term [rows, f] and bias [f] may be NULL. */
+GM_API gm_status gm_hetero_combine(const float* const* parts, int32_t n_parts, const float* self_term,
+                                   const float* bias, int64_t rows, int64_t f, float* out,
+                                   gm_stream_t stream);
+
 /* ------------------------------------------------------------------------ */
 /* segment_matmul (L4): hetero.hpp:134-157 grouped_matmul                    */
 /* ------------------------------------------------------------------------ */

@@ -274,6 +274,21 @@ class Reference:
             _ptr(x), _ptr(_i64(ptr)), _I(g), _I(k), _I(n), _ptr(w), _ptr(out)))
         return out
 
+    def hetero_sage(self, node_ptr, h, et_src, et_dst, e_ptr, src, dst, w_neigh, w_self, bias):
+        """to_hetero(sage) + hetero_propagate(sum), node types n<i>, edge types (n<s>, r<i>, n<d>)."""
+        h = np.ascontiguousarray(h, dtype=np.float32)
+        f_in = h.shape[1]
+        f_out = w_self.shape[2]
+        out = np.zeros((h.shape[0], f_out), np.float32)
+        i32 = lambda a: np.ascontiguousarray(a, dtype=np.int32)  # noqa: E731
+        f32 = lambda a: np.ascontiguousarray(a, dtype=np.float32)  # noqa: E731
+        es, ed = i32(et_src), i32(et_dst)
+        self._check(self.lib.ref_hetero_sage_f32(
+            C.c_int32(len(node_ptr) - 1), _ptr(_i64(node_ptr)), _ptr(h), _I(f_in), _I(f_out), C.c_int32(len(es)),
+            _ptr(es), _ptr(ed), _ptr(_i64(e_ptr)), _ptr(_i64(src)), _ptr(_i64(dst)), _ptr(f32(w_neigh)),
+            _ptr(f32(w_self)), _ptr(f32(bias)), _ptr(out)))
+        return out
+
     def bench_spmm(self, src, dst, n_src, n_dst, x, mean=False, threads=1, rows_limit=0, warmup=1,
                    repeat=3):
         """Reference spmm<float> timed by its own time_loop over `threads` row ranges."""

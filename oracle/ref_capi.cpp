@@ -150,6 +150,57 @@ int ref_spmm_backward_f64(const int64_t* src, const int64_t* dst, int64_t e, int
   return spmm_bwd_impl<double>(src, dst, e, n_src, n_dst, undirected, x, f, w, mean, G, dx, dw);
 }
 
+// to_hetero(sage) + hetero_propagate(InterCombine::sum), segment_fused
+// (hetero.hpp:217-365) with caller-given weights. Node types "n<i>" (ptr over a
+// concatenated h), edge types (n<s>, r<i>, n<d>); outputs concatenated like h.
+int ref_hetero_sage_f32(int32_t n_types, const int64_t* node_ptr, const float* h, int64_t f_in, int64_t f_out,
+                        int32_t n_et, const int32_t* et_src, const int32_t* et_dst, const int64_t* e_ptr,
+                        const int64_t* src, const int64_t* dst, const float* w_neigh, const float* w_self,
+                        const float* bias, float* out) {
+  return guarded([&] {
+    NoGradGuard ng;
+    HeteroGraph<float> g;
+    std::map<std::string, Tensor<float>> hm;
+    HeteroModel<float> model;
+    model.kind = LayerKind::sage;
+    model.in_dim = f_in;
+    model.out_dim = f_out;
+    model.combine = InterCombine::sum;
+    auto name = [](int i) { return "n" + std::to_string(i); };
+    for (int t = 0; t < n_types; ++t) {
+      Tensor<float> ht = make_tensor(h + node_ptr[t] * f_in, node_ptr[t + 1] - node_ptr[t], f_in);
+      g.add_node_type(name(t), ht);
+      hm[name(t)] = ht;
+      LayerParams<float> up;
+      up.kind = LayerKind::sage;
+      up.in_dim = f_in;
+      up.out_dim = f_out;
+      up.weights["w_self"] = make_tensor(w_self + t * f_in * f_out, f_in, f_out);
+      up.weights["bias"] = Tensor<float>::from_data({f_out}, std::vector<float>(bias + t * f_out, bias + (t + 1) * f_out));
+      model.node_update[name(t)] = up;
+    }
+    for (int i = 0; i < n_et; ++i) {
+      EdgeType et{name(et_src[i]), "r" + std::to_string(i), name(et_dst[i])};
+      const int64_t a = e_ptr[i], b = e_ptr[i + 1];
+      g.add_edge_type(et, EdgeIndex(std::vector<Index>(src + a, src + b), std::vector<Index>(dst + a, dst + b),
+                                    node_ptr[et_src[i] + 1] - node_ptr[et_src[i]],
+                                    node_ptr[et_dst[i] + 1] - node_ptr[et_dst[i]]));
+      LayerParams<float> rp;
+      rp.kind = LayerKind::sage;
+      rp.in_dim = f_in;
+      rp.out_dim = f_out;
+      rp.aggregation = AggregationSpec<float>::simple(AggKind::mean);
+      rp.weights["w_neigh"] = make_tensor(w_neigh + i * f_in * f_out, f_in, f_out);
+      model.replicas[et] = rp;
+    }
+    auto res = hetero_propagate(g, model, hm, ExecPath::segment_fused);
+    for (int t = 0; t < n_types; ++t) {
+      const Tensor<float>& o = res.at(name(t));
+      std::memcpy(out + node_ptr[t] * f_out, o.data().data(), sizeof(float) * static_cast<size_t>(o.numel()));
+    }
+  });
+}
+
 const char* ref_last_error() { return g_err.c_str(); }
 
 // edge_index.cpp:45-62

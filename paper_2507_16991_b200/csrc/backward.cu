@@ -104,3 +104,49 @@ GM_API gm_status gm_edge_dot(gm_dtype dtype, const int64_t* src, const int64_t* 
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// hetero combine (hetero.hpp:338-343 InterCombine::sum + layer_update :579-580):
+//   out = ((((p0 + p1) + ...) + p_{n-1}) + self) + bias      (fp32, this order)
+// ---------------------------------------------------------------------------
+namespace gm {
+struct CombineArgs {
+  const float* parts[8];
+  int n_parts;
+  const float* self;
+  const float* bias;
+  int64_t rows;
+  int64_t f;
+  float* out;
+};
+__global__ void hetero_combine_kernel(const CombineArgs a) {
+  const int64_t total = a.rows * a.f;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float acc = a.n_parts > 0 ? a.parts[0][i] : 0.0f;
+    for (int p = 1; p < a.n_parts; ++p) acc = __fadd_rn(acc, a.parts[p][i]);
+    if (a.self) acc = __fadd_rn(acc, a.self[i]);
+    if (a.bias) acc = __fadd_rn(acc, a.bias[i % a.f]);
+    a.out[i] = acc;
+  }
+}
+}  // namespace gm
+
+extern "C" GM_API gm_status gm_hetero_combine(const float* const* parts, int32_t n_parts, const float* self_term,
+                                              const float* bias, int64_t rows, int64_t f, float* out,
+                                              gm_stream_t stream) {
+  using namespace gm;
+  GM_REQUIRE(n_parts >= 0 && n_parts <= 8, GM_ERR_INVALID_ARGUMENT, "gm_hetero_combine: at most 8 parts");
+  if (rows == 0 || f == 0) return GM_OK;
+  CombineArgs a{};
+  for (int p = 0; p < n_parts; ++p) a.parts[p] = parts[p];
+  a.n_parts = n_parts;
+  a.self = self_term;
+  a.bias = bias;
+  a.rows = rows;
+  a.f = f;
+  a.out = out;
+  hetero_combine_kernel<<<grid_of(rows * f), 256, 0, as_stream(stream)>>>(a);
+  GM_CHECK_LAUNCH("hetero_combine_kernel");
+  return GM_OK;
+}

@@ -1,0 +1,84 @@
+"""Heterogeneous (RGCN-shaped) layer on B200: the reference's
+``to_hetero(sage)`` + ``hetero_propagate`` with ``InterCombine::sum``
+(hetero.hpp:217-365), composed from the hot-path kernels:
+
+  1. per edge type (sorted canonical order, hetero.hpp:294-300):
+       agg_et = spmm(e_et, h[src_type], mean)               exact fp32 (gm_spmm)
+  2. neighbour projection for ALL edge types at once:
+       P = segment_matmul(cat(agg_et), stack(w_neigh_et))  tcgen05 grouped GEMM
+     (message_passing.hpp:520, one matmul per edge type in the reference)
+  3. self projection for ALL node types at once:
+       S = segment_matmul(cat(h_nt), stack(w_self_nt))     tcgen05 grouped GEMM
+     (layer_update message_passing.hpp:579-580, one matmul per node type)
+  4. out_nt = ((sum_et P_et) + S_nt) + bias_nt              gm_hetero_combine,
+     in the reference's add order (hetero.hpp:338-343, :362)
+
+Steps 1 and 4 are bit-exact; 2 and 3 run bf16 operands with fp32
+accumulation (the segment_matmul tolerance, tests/test_gpu_gemm.py).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Dict, Tuple
+
+import torch
+
+from . import _lib as L
+from .graphmill import EdgeIndex, _stream, segment_matmul, spmm
+
+EdgeKey = Tuple[str, str, str]  # (src, rel, dst) — EdgeType
+
+
+def canonical(et: EdgeKey) -> str:
+    """EdgeType::canonical (hetero.hpp:16-22): src__rel__dst."""
+    return f"{et[0]}__{et[1]}__{et[2]}"
+
+
+def hetero_sage_layer(edges: Dict[EdgeKey, EdgeIndex], h: Dict[str, torch.Tensor],
+                      w_neigh: Dict[EdgeKey, torch.Tensor], w_self: Dict[str, torch.Tensor],
+                      bias: Dict[str, torch.Tensor]) -> Dict[str, torch.Tensor]:
+    node_types = sorted(h)                       # std::map order
+    edge_types = sorted(edges, key=canonical)    # EdgeType::operator< (canonical)
+    for nt in node_types:
+        if nt not in w_self or nt not in bias:
+            raise ValueError(f"hetero_propagate: model lacks update params for type {nt}")
+    for et in edge_types:
+        if et[0] not in h or et[2] not in h:
+            raise ValueError(f"hetero_propagate: missing node type {et[0] if et[0] not in h else et[2]}")
+        if et not in w_neigh:
+            raise ValueError(f"hetero_propagate: model lacks a replica for edge type {canonical(et)}")
+    f_out = next(iter(w_self.values())).shape[1]
+    dev = next(iter(h.values())).device
+
+    # 1. per-edge-type mean aggregation (exact)
+    aggs = [spmm(edges[et], h[et[0]], None, "mean") for et in edge_types]
+    # 2. one grouped GEMM over edge types (tcgen05)
+    parts_by_dst: Dict[str, list] = {nt: [] for nt in node_types}
+    if edge_types:
+        ptr = [0]
+        for a in aggs:
+            ptr.append(ptr[-1] + a.shape[0])
+        proj = segment_matmul(torch.cat(aggs, 0), ptr, torch.stack([w_neigh[et] for et in edge_types]),
+                              out_dtype=torch.float32)
+        for i, et in enumerate(edge_types):
+            parts_by_dst[et[2]].append(proj[ptr[i]:ptr[i + 1]])
+    # 3. one grouped GEMM over node types (tcgen05)
+    nptr = [0]
+    for nt in node_types:
+        nptr.append(nptr[-1] + h[nt].shape[0])
+    selfp = segment_matmul(torch.cat([h[nt] for nt in node_types], 0), nptr,
+                           torch.stack([w_self[nt] for nt in node_types]), out_dtype=torch.float32)
+    # 4. combine in the reference's order
+    out = {}
+    lib = L.lib()
+    for i, nt in enumerate(node_types):
+        rows = h[nt].shape[0]
+        o = torch.empty(rows, f_out, dtype=torch.float32, device=dev)
+        parts = [p.contiguous() for p in parts_by_dst[nt]]
+        arr = (C.c_void_p * max(1, len(parts)))(*[p.data_ptr() for p in parts])
+        s = selfp[nptr[i]:nptr[i + 1]]
+        b = bias[nt].to(torch.float32).contiguous()
+        L.check(lib.gm_hetero_combine(arr, len(parts), C.c_void_p(s.data_ptr()), C.c_void_p(b.data_ptr()),
+                                      rows, f_out, C.c_void_p(o.data_ptr()), _stream()), "gm_hetero_combine")
+        out[nt] = o
+    return out

@@ -172,10 +172,37 @@ def gemm_fixtures(ref: Reference) -> dict:
     return d
 
 
+def hetero_fixtures(ref: Reference) -> dict:
+    """to_hetero(sage) + hetero_propagate(sum) (hetero.hpp:217-365), 3 node types,
+    4 edge types (one self-relation, one node type with two incoming relations,
+    one node type with none)."""
+    rng = np.random.default_rng(77)
+    counts = [300, 500, 20, 9]  # n3 has no incoming edge type
+    node_ptr = np.concatenate([[0], np.cumsum(counts)])
+    f_in, f_out = 64, 32
+    h = rng.uniform(-1, 1, (node_ptr[-1], f_in)).astype(np.float32)
+    ets = [(1, 0, 3000), (0, 0, 2000), (0, 2, 800), (1, 2, 500)]
+    src, dst, e_ptr = [], [], [0]
+    for s_t, d_t, e in ets:
+        src.append(rng.integers(0, counts[s_t], e))
+        dst.append(rng.integers(0, counts[d_t], e))
+        e_ptr.append(e_ptr[-1] + e)
+    src, dst = np.concatenate(src), np.concatenate(dst)
+    w_neigh = rng.uniform(-0.125, 0.125, (len(ets), f_in, f_out)).astype(np.float32)
+    w_self = rng.uniform(-0.125, 0.125, (len(counts), f_in, f_out)).astype(np.float32)
+    bias = rng.uniform(-0.1, 0.1, (len(counts), f_out)).astype(np.float32)
+    et_src = np.array([e[0] for e in ets], np.int32)
+    et_dst = np.array([e[1] for e in ets], np.int32)
+    out = ref.hetero_sage(node_ptr, h, et_src, et_dst, e_ptr, src, dst, w_neigh, w_self, bias)
+    return dict(node_ptr=node_ptr, h=h, et_src=et_src, et_dst=et_dst, e_ptr=np.array(e_ptr), src=src, dst=dst,
+                w_neigh=w_neigh, w_self=w_self, bias=bias, out=out)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     ref = Reference()
-    for name, fn in (("csr", csr_fixtures), ("spmm", spmm_fixtures), ("gemm", gemm_fixtures)):
+    for name, fn in (("csr", csr_fixtures), ("spmm", spmm_fixtures), ("gemm", gemm_fixtures),
+                     ("hetero", hetero_fixtures)):
         data = fn(ref)
         path = os.path.join(OUT, f"{name}.npz")
         np.savez_compressed(path, **data)
