@@ -237,6 +237,38 @@ GM_API gm_status gm_segment_matmul(const void* x, const int64_t* ptr_host, int64
 GM_API gm_status gm_partition_rows_by_nnz(const int64_t* rowptr_host, int64_t num_rows,
                                           int32_t parts, int64_t* cuts_host);
 
+/* Stable split of a (row-slice) CSR into num_blocks source blocks, for the
+ * exchange-overlapped multi-GPU aggregation ("local CSR per GPU
+ * is 2-D blocked by source shard"): entry k of row r moves to block
+ * b = src_block[col[k]] with column src_col[col[k]] (e.g. the row inside the
+ * peer shard / exchange chunk that will hold that source) and keeps perm[k].
+ * Inside each (block, row) entries keep their compressed order, so each
+ * block is itself a valid compressed view of the same rows.
+ * Outputs: rowptr_out [num_blocks][num_rows+1] (block b's view is
+ * {rowptr_out + b*(num_rows+1), col_out, perm_out}, offsets into the shared
+ * col_out/perm_out arrays of csr->nnz entries). src_block/src_col are device
+ * arrays of csr->num_cols entries; src_block values in [0, num_blocks). */
+GM_API size_t gm_csr_split_blocks_workspace(int64_t num_rows, int32_t num_blocks);
+GM_API gm_status gm_csr_split_blocks(const gm_csr* csr, const int32_t* src_block, const int32_t* src_col,
+                                     int32_t num_blocks, int64_t* rowptr_out, int32_t* col_out,
+                                     int32_t* perm_out, void* workspace, size_t workspace_bytes,
+                                     gm_stream_t stream);
+
+/* Continue an aggregation over another block of the same destination rows
+ * (gm_csr_split_blocks): every row starts from the current out (and, for
+ * MAX/MIN, arg_out) contents and accumulates this block's entries in
+ * compressed order. MAX/MIN break ties on the smaller COO id (arg_out
+ * required), so the value and argmax equal the single-pass result exactly for
+ * NaN-free inputs whatever the block order; SUM continues the running sum (one
+ * re-association per block boundary: within the fp32 tolerance, not
+ * bit-identical). reduce = MEAN finalises: sum, then * (1 / mean_deg[row])
+ * with mean_deg the FULL row degrees (earlier blocks run as SUM). F32/F64 for
+ * SUM/MEAN (BF16 would round between blocks); any dtype for MAX/MIN. */
+GM_API gm_status gm_spmm_accumulate(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype dtype,
+                                    const void* x, int64_t f, const void* edge_weight, gm_reduce reduce,
+                                    const int32_t* mean_deg, void* out, int32_t* arg_out,
+                                    gm_stream_t stream);
+
 /* ------------------------------------------------------------------------ */
 /* Synthetic inputs (bench/test infrastructure; bit-identical host & device) */
 /* ------------------------------------------------------------------------ */

@@ -353,11 +353,166 @@ static BuildWs build_layout(void* base, int64_t e, int64_t n) {
   return w;
 }
 
+// ---------------------------------------------------------------------------
+// Stable split of a CSR's entries into source blocks (multi-GPU overlap):
+// entry k of row r goes to block src_block[col[k]] with column src_col[col[k]];
+// inside every (block, row) the entries keep their compressed order.
+// ---------------------------------------------------------------------------
+constexpr int kSplitWarps = 8;
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__global__ void __launch_bounds__(kSplitWarps * 32)
+split_count_kernel(const int64_t* __restrict__ rowptr, int64_t rows, const int32_t* __restrict__ col,
+                   const int32_t* __restrict__ src_block, int32_t* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * kSplitWarps;
+  for (int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < rows; r += nw) {
+    const int64_t kb = rowptr[r], ke = rowptr[r + 1];
+    for (int64_t k0 = kb; k0 < ke; k0 += 32) {
+      const int64_t k = k0 + lane;
+      const int b = k < ke ? src_block[col[k]] : -1;
+      const unsigned peers = __match_any_sync(0xffffffffu, b);
+      if (b >= 0 && (peers & lanemask_lt()) == 0) atomicAdd(&cnt[static_cast<int64_t>(b) * rows + r], __popc(peers));
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kSplitWarps * 32)
+split_scatter_kernel(const int64_t* __restrict__ rowptr, int64_t rows, const int32_t* __restrict__ col,
+                     const int32_t* __restrict__ perm, const int32_t* __restrict__ src_block,
+                     const int32_t* __restrict__ src_col, int32_t nb, const int64_t* __restrict__ off,
+                     int32_t* __restrict__ col_out, int32_t* __restrict__ perm_out) {
+  extern __shared__ int32_t cursors[];
+  const int lane = threadIdx.x & 31;
+  int32_t* cur = cursors + (threadIdx.x >> 5) * nb;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * kSplitWarps;
+  for (int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < rows; r += nw) {
+    for (int i = lane; i < nb; i += 32) cur[i] = 0;
+    __syncwarp();
+    const int64_t kb = rowptr[r], ke = rowptr[r + 1];
+    for (int64_t k0 = kb; k0 < ke; k0 += 32) {
+      const int64_t k = k0 + lane;
+      int32_t c = 0;
+      int b = -1;
+      if (k < ke) {
+        c = col[k];
+        b = src_block[c];
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, b);
+      const int rank = __popc(peers & lanemask_lt());
+      const int base = b >= 0 ? cur[b] : 0;
+      __syncwarp();
+      if (b >= 0) {
+        const int64_t pos = off[static_cast<int64_t>(b) * rows + r] + base + rank;
+        col_out[pos] = src_col[c];
+        perm_out[pos] = perm[k];
+        if (rank == 0) cur[b] = base + __popc(peers);
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// rowptr_out[b][r] = off[b * rows + r] for r in [0, rows] (the scan's last
+// entry closes the last block).
+__global__ void split_rowptr_kernel(const int64_t* __restrict__ off, int64_t rows, int64_t nb,
+                                    int64_t* __restrict__ rowptr_out) {
+  const int64_t n = nb * (rows + 1);
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = i / (rows + 1), r = i - b * (rows + 1);
+    rowptr_out[i] = off[b * rows + r];
+  }
+}
+
+struct SplitWs {
+  int32_t* cnt;
+  int64_t* partial;
+  int64_t* off;
+  size_t bytes;
+};
+
+static SplitWs split_layout(void* base, int64_t rows, int64_t nb) {
+  SplitWs w{};
+  unsigned char* p = static_cast<unsigned char*>(base);
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    unsigned char* q = p ? p + o : nullptr;
+    o += align_up(std::max<size_t>(bytes, 1), 256);
+    return q;
+  };
+  const int64_t n = rows * nb;
+  w.cnt = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(n)));
+  w.partial = reinterpret_cast<int64_t*>(take(sizeof(int64_t) * static_cast<size_t>(std::max<int64_t>(1, ceil_div(n, kScanTile)))));
+  w.off = reinterpret_cast<int64_t*>(take(sizeof(int64_t) * static_cast<size_t>(n + 1)));
+  w.bytes = o;
+  return w;
+}
+
 }  // namespace gm
 
 using namespace gm;
 
 extern "C" {
+
+GM_API size_t gm_csr_split_blocks_workspace(int64_t num_rows, int32_t num_blocks) {
+  if (num_rows < 0 || num_blocks < 1) return 0;
+  return split_layout(nullptr, num_rows, num_blocks).bytes;
+}
+
+GM_API gm_status gm_csr_split_blocks(const gm_csr* csr, const int32_t* src_block, const int32_t* src_col,
+                                     int32_t num_blocks, int64_t* rowptr_out, int32_t* col_out,
+                                     int32_t* perm_out, void* workspace, size_t workspace_bytes,
+                                     gm_stream_t stream) {
+  GM_REQUIRE(csr, GM_ERR_INVALID_ARGUMENT, "gm_csr_split_blocks: null csr");
+  GM_REQUIRE(num_blocks >= 1 && num_blocks <= 1024, GM_ERR_INVALID_ARGUMENT,
+             "gm_csr_split_blocks: num_blocks must be in [1, 1024]");
+  GM_REQUIRE(csr->num_rows >= 0 && csr->nnz >= 0, GM_ERR_INVALID_ARGUMENT, "gm_csr_split_blocks: negative size");
+  GM_REQUIRE(csr->nnz == 0 || csr->perm, GM_ERR_INVALID_ARGUMENT, "gm_csr_split_blocks: csr->perm required");
+  GM_REQUIRE(rowptr_out, GM_ERR_INVALID_ARGUMENT, "gm_csr_split_blocks: null rowptr_out");
+  const int64_t rows = csr->num_rows;
+  const SplitWs need = split_layout(nullptr, rows, num_blocks);
+  GM_REQUIRE(workspace && workspace_bytes >= need.bytes, GM_ERR_INVALID_ARGUMENT,
+             "gm_csr_split_blocks: workspace too small (" + std::to_string(workspace_bytes) + " < " +
+                 std::to_string(need.bytes) + ")");
+  cudaStream_t st = as_stream(stream);
+  if (rows == 0) {
+    GM_TRY_CUDA(cudaMemsetAsync(rowptr_out, 0, sizeof(int64_t) * static_cast<size_t>(num_blocks), st));
+    return GM_OK;
+  }
+  const SplitWs w = split_layout(workspace, rows, num_blocks);
+  const int64_t n = rows * num_blocks;
+  GM_TRY_CUDA(cudaMemsetAsync(w.cnt, 0, sizeof(int32_t) * static_cast<size_t>(n), st));
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(ceil_div(rows, kSplitWarps), kNumSMs * 16));
+  if (csr->nnz > 0) {
+    split_count_kernel<<<grid, kSplitWarps * 32, 0, st>>>(csr->rowptr, rows, csr->col, src_block, w.cnt);
+    GM_CHECK_LAUNCH("split_count_kernel");
+  }
+  const int64_t nbk = ceil_div(n, kScanTile);
+  scan_reduce_kernel<<<static_cast<unsigned>(nbk), kScanThreads, 0, st>>>(w.cnt, n, w.partial);
+  GM_CHECK_LAUNCH("scan_reduce_kernel");
+  scan_partials_kernel<<<1, kScanThreads, 0, st>>>(w.partial, nbk);
+  GM_CHECK_LAUNCH("scan_partials_kernel");
+  scan_down_kernel<<<static_cast<unsigned>(nbk), kScanThreads, 0, st>>>(w.cnt, n, w.partial, w.off);
+  GM_CHECK_LAUNCH("scan_down_kernel");
+  if (csr->nnz > 0) {
+    const size_t smem = sizeof(int32_t) * kSplitWarps * static_cast<size_t>(num_blocks);
+    if (smem > 48 * 1024)
+      GM_TRY_CUDA(cudaFuncSetAttribute(split_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem)));
+    split_scatter_kernel<<<grid, kSplitWarps * 32, smem, st>>>(csr->rowptr, rows, csr->col, csr->perm, src_block,
+                                                               src_col, num_blocks, w.off, col_out, perm_out);
+    GM_CHECK_LAUNCH("split_scatter_kernel");
+  }
+  split_rowptr_kernel<<<grid_for(num_blocks * (rows + 1)), 256, 0, st>>>(w.off, rows, num_blocks, rowptr_out);
+  GM_CHECK_LAUNCH("split_rowptr_kernel");
+  return GM_OK;
+}
 
 GM_API gm_status gm_check_index_bounds(const int64_t* ids, int64_t len, int64_t bound,
                                        const char* prefix, void* workspace, gm_stream_t stream) {

@@ -262,10 +262,10 @@ GM_API gm_status gm_spmm_plan_build(const gm_csr* csr, void* buffer, size_t buff
   return GM_OK;
 }
 
-GM_API gm_status gm_spmm(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype dtype,
-                         const void* x, int64_t f, const void* edge_weight,
-                         const gm_gcn_norm* gcn, gm_reduce reduce, void* out, int32_t* arg_out,
-                         gm_stream_t stream) {
+static gm_status spmm_impl(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype dtype,
+                           const void* x, int64_t f, const void* edge_weight,
+                           const gm_gcn_norm* gcn, gm_reduce reduce, void* out, int32_t* arg_out,
+                           int accum, const int32_t* mean_deg, gm_stream_t stream) {
   GM_REQUIRE(csr && plan, GM_ERR_INVALID_ARGUMENT, "gm_spmm: null csr/plan");
   GM_REQUIRE(f >= 0, GM_ERR_INVALID_ARGUMENT, "gm_spmm: negative feature width");
   GM_REQUIRE(!(edge_weight && gcn), GM_ERR_INVALID_ARGUMENT,
@@ -302,6 +302,8 @@ GM_API gm_status gm_spmm(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype d
   p.gcn_self = gcn ? gcn->self_loops : 0;
   p.mean = reduce == GM_MEAN;
   p.is_min = reduce == GM_MIN;
+  p.accum = accum;
+  p.mean_deg = mean_deg;
   p.num_rows = csr->num_rows;
   p.f = f;
   p.win_row = plan->win_row;
@@ -329,6 +331,27 @@ GM_API gm_status gm_spmm(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype d
     case GM_BF16: return spmm_dispatch_bf16(p, maxmin, use_heavy && vb >= 4, plan->num_heavy, ns, vb, st);
   }
   return fail(GM_ERR_INVALID_ARGUMENT, "gm_spmm: unknown dtype");
+}
+
+GM_API gm_status gm_spmm(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype dtype,
+                         const void* x, int64_t f, const void* edge_weight,
+                         const gm_gcn_norm* gcn, gm_reduce reduce, void* out, int32_t* arg_out,
+                         gm_stream_t stream) {
+  return spmm_impl(csr, plan, dtype, x, f, edge_weight, gcn, reduce, out, arg_out, 0, nullptr, stream);
+}
+
+GM_API gm_status gm_spmm_accumulate(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype dtype,
+                                    const void* x, int64_t f, const void* edge_weight, gm_reduce reduce,
+                                    const int32_t* mean_deg, void* out, int32_t* arg_out,
+                                    gm_stream_t stream) {
+  const bool maxmin = reduce == GM_MAX || reduce == GM_MIN;
+  GM_REQUIRE(dtype != GM_BF16 || maxmin, GM_ERR_INVALID_ARGUMENT,
+             "gm_spmm_accumulate: bf16 sum/mean would round between blocks (use gm_spmm on the gathered x)");
+  GM_REQUIRE(!maxmin || arg_out, GM_ERR_INVALID_ARGUMENT,
+             "gm_spmm_accumulate: max/min needs the running arg_out (ties break on COO id)");
+  GM_REQUIRE(reduce != GM_MEAN || mean_deg, GM_ERR_INVALID_ARGUMENT,
+             "gm_spmm_accumulate: mean needs the full-row degrees");
+  return spmm_impl(csr, plan, dtype, x, f, edge_weight, nullptr, reduce, out, arg_out, 1, mean_deg, stream);
 }
 
 }  // extern "C"

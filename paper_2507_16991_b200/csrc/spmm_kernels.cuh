@@ -58,6 +58,12 @@ struct SpmmArgs {
   int flat_ok;                   // heavy rows (if any) are covered by the hub kernel
   const uint8_t* src_class;      // per-entry source hotness class (NULL: no L2 hint)
   int hot_class_limit;           // entries with class < limit gather with evict_last
+  // Seeded (blocked) accumulation: every row starts from the current out (and
+  // arg) contents instead of 0 / the first element; max/min ties then break
+  // on the smaller COO id, which reproduces "first attaining edge" across
+  // source blocks (multi-GPU exchange overlap, dist.py).
+  int accum;
+  const int32_t* mean_deg;       // MEAN denominators per row (NULL = row length)
 };
 
 // L2 eviction-priority policies (createpolicy; PTX ISA "Cache eviction priority hints").
@@ -122,16 +128,33 @@ struct Acc {
         if (MAXMIN) a[j][e] = -1;
       }
   }
+  // Seed vector j from a previous block's result (p.accum). Returns true when
+  // the row already has a first element (max/min: arg != -1).
+  template <typename T, typename VecT>
+  __device__ __forceinline__ bool seed(int j, const T* orow, const int32_t* arow) {
+    typename VecT::R r = *reinterpret_cast<const typename VecT::R*>(orow);
+    VecT::unpack(r, v[j]);
+    bool have = true;
+    if (MAXMIN) {
+#pragma unroll
+      for (int e = 0; e < V; ++e) a[j][e] = arow[e];
+      have = a[j][0] != -1;
+    }
+    return have;
+  }
   // One edge's contribution to vector j. `first`: first edge of the row.
+  // lex: ties go to the smaller COO id (seeded blocks; inside one block ids
+  // ascend, so strict compare alone already keeps the earliest).
   __device__ __forceinline__ void add(int j, const A* vals, bool scaled, A sc, bool first,
-                                      int is_min, int32_t pm) {
+                                      int is_min, int32_t pm, bool lex = false) {
 #pragma unroll
     for (int e = 0; e < V; ++e) {
       const A val = scaled ? mul_rn(vals[e], sc) : vals[e];
       if (!MAXMIN) {
         v[j][e] = add_rn(v[j][e], val);
       } else {
-        const bool better = first || (is_min ? (val < v[j][e]) : (val > v[j][e]));
+        const bool better = first || (is_min ? (val < v[j][e]) : (val > v[j][e])) ||
+                            (lex && val == v[j][e] && static_cast<uint32_t>(pm) < static_cast<uint32_t>(a[j][e]));
         if (better) {
           v[j][e] = val;
           a[j][e] = pm;
@@ -177,6 +200,15 @@ __global__ void __launch_bounds__(256) spmm_light_kernel(const SpmmArgs p) {
     if (ke - kb > p.heavy_thr) continue;  // the heavy kernel owns this row
     Acc<A, NV, V, MAXMIN> acc;
     acc.init();
+    bool seeded = false;
+    if (p.accum) {
+#pragma unroll
+      for (int j = 0; j < NV; ++j)
+        if (valid[j])
+          seeded = acc.template seed<T, VecT>(j, out + static_cast<int64_t>(r) * p.f + slot[j] * V,
+                                             MAXMIN ? p.arg + static_cast<int64_t>(r) * p.f + slot[j] * V : nullptr);
+    }
+    const bool lex = p.accum != 0;
     const int32_t dd = gcn ? p.gdeg_dst[r] : 0;
 
     for (int64_t k = kb; k < ke; k += U) {
@@ -209,7 +241,7 @@ __global__ void __launch_bounds__(256) spmm_light_kernel(const SpmmArgs p) {
         if (k + u < ke) {
 #pragma unroll
           for (int j = 0; j < NV; ++j)
-            if (valid[j]) acc.add(j, buf[u][j].v, scaled, sc[u], k + u == kb, p.is_min, pm[u]);
+            if (valid[j]) acc.add(j, buf[u][j].v, scaled, sc[u], !seeded && k + u == kb, p.is_min, pm[u], lex);
         }
     }
     int64_t cnt = ke - kb;
@@ -223,10 +255,11 @@ __global__ void __launch_bounds__(256) spmm_light_kernel(const SpmmArgs p) {
         if (valid[j]) {
           VecT b;
           b.load_global(xr + slot[j] * V);
-          acc.add(j, b.v, true, sc, cnt == 0, p.is_min, -1);
+          acc.add(j, b.v, true, sc, !seeded && cnt == 0, p.is_min, -1);
         }
       cnt += 1;
     }
+    if (p.mean_deg) cnt = p.mean_deg[r];
     if (!MAXMIN && p.mean && cnt > 0) {
       const A inv = div_rn(A(1), static_cast<A>(cnt));  // message_passing.hpp:81
 #pragma unroll
@@ -273,7 +306,7 @@ __device__ __forceinline__ unsigned short shfl_raw(const unsigned short& v, int 
 // P > 1 (rows of <= 32/P vector slots): one load instruction fetches P edges
 // (lane l loads slot l % (32/P) of edge l / (32/P)); the owning lanes then
 // take each edge's slice by shuffle, in edge order — same accumulation order.
-template <typename T, int VB, int NV, int U, int MODE, bool SCALED, int P = 1>
+template <typename T, int VB, int NV, int U, int MODE, bool SCALED, int P = 1, bool ACC = false>
 __global__ void __launch_bounds__(256, (SCALED || sizeof(T) == 8) ? 3 : 4) spmm_flat_kernel(const SpmmArgs p) {
   static_assert(P == 1 || NV == 1, "lane-split loads need one vector per lane");
   static_assert(U % P == 0, "batch must hold whole load groups");
@@ -322,12 +355,26 @@ __global__ void __launch_bounds__(256, (SCALED || sizeof(T) == 8) ? 3 : 4) spmm_
   int32_t row_end = __shfl_sync(FULL, rend_l, 0);
 
   Acc<A, NV, V, MAXMIN> acc;
-  acc.init();
   bool first = true;
+  constexpr bool lex = MAXMIN && ACC;
+  auto begin_row = [&]() {
+    acc.init();
+    first = true;
+    if constexpr (ACC) {
+      const uint64_t ob = static_cast<uint64_t>(static_cast<uint32_t>(row)) * fu;
+      bool have = false;
+#pragma unroll
+      for (int j = 0; j < NV; ++j)
+        if (valid[j])
+          have = acc.template seed<T, VecT>(j, out + ob + soff[j], MAXMIN ? p.arg + ob + soff[j] : nullptr);
+      first = !have;
+    }
+  };
+  begin_row();
 
   auto flush = [&]() {
     if (MEAN) {
-      const int32_t cnt = row_end - row_start;
+      const int32_t cnt = (ACC && p.mean_deg) ? p.mean_deg[row] : row_end - row_start;
       if (cnt > 0) {
         const A inv = div_rn(A(1), static_cast<A>(cnt));  // message_passing.hpp:81
 #pragma unroll
@@ -347,8 +394,6 @@ __global__ void __launch_bounds__(256, (SCALED || sizeof(T) == 8) ? 3 : 4) spmm_
           for (int e = 0; e < V; ++e) arow[e] = acc.a[j][e];
         }
       }
-    acc.init();
-    first = true;
     ++row;
     row_start = row_end;
     if (row < rb) {
@@ -357,6 +402,7 @@ __global__ void __launch_bounds__(256, (SCALED || sizeof(T) == 8) ? 3 : 4) spmm_
         rend_l = (cbase + lane < rb) ? static_cast<int32_t>(p.rowptr[cbase + 1 + lane]) : kend;
       }
       row_end = __shfl_sync(FULL, rend_l, row - cbase);
+      begin_row();
     }
   };
 
@@ -433,7 +479,7 @@ __global__ void __launch_bounds__(256, (SCALED || sizeof(T) == 8) ? 3 : 4) spmm_
           if (valid[j]) {
             A vals[V];
             VecT::unpack(r, vals);
-            acc.add(j, vals, SCALED, sc, first && u == 0, p.is_min, pm);
+            acc.add(j, vals, SCALED, sc, first && u == 0, p.is_min, pm, lex);
           }
         }
       }
@@ -453,7 +499,7 @@ __global__ void __launch_bounds__(256, (SCALED || sizeof(T) == 8) ? 3 : 4) spmm_
             if (valid[j]) {
               A vals[V];
               VecT::unpack(rs[j], vals);
-              acc.add(j, vals, SCALED, sc, first, p.is_min, pm);
+              acc.add(j, vals, SCALED, sc, first, p.is_min, pm, lex);
             }
           first = false;
         }
@@ -570,6 +616,18 @@ __global__ void __launch_bounds__(kHeavyThreads) spmm_heavy_kernel(const SpmmArg
 
   Acc<A, MH, V, MAXMIN> acc;
   acc.init();
+  bool seeded = false;
+  if (p.accum) {
+    T* orow0 = static_cast<T*>(p.out) + static_cast<int64_t>(r) * p.f;
+#pragma unroll
+    for (int m = 0; m < MH; ++m) {
+      const int s = t + m * kHeavyThreads;
+      if (s < nslots)
+        seeded = acc.template seed<T, VecT>(m, orow0 + (p.slot_base + s) * V,
+                                            MAXMIN ? p.arg + static_cast<int64_t>(r) * p.f + (p.slot_base + s) * V : nullptr);
+    }
+  }
+  const bool lex = MAXMIN && p.accum != 0;
   A sc_next = A(1);
 
   load_meta(0);
@@ -614,7 +672,7 @@ __global__ void __launch_bounds__(kHeavyThreads) spmm_heavy_kernel(const SpmmArg
           for (int e = 0; e < n_e; ++e) {
             VecT v;
             v.load_shared(reinterpret_cast<const T*>(di + static_cast<size_t>(e) * rowb + s * VB));
-            acc.add(m, v.v, scaled, mscale[mi + e], base_e + e == 0, p.is_min, mperm[mi + e]);
+            acc.add(m, v.v, scaled, mscale[mi + e], !seeded && base_e + e == 0, p.is_min, mperm[mi + e], lex);
           }
         }
       }
@@ -622,8 +680,9 @@ __global__ void __launch_bounds__(kHeavyThreads) spmm_heavy_kernel(const SpmmArg
     if (gcn && i + 1 >= 0 && i + 1 < nst && t < se) mscale[((i + 1) % (kRing + 1)) * se + t] = sc_next;
   }
 
-  if (!MAXMIN && p.mean && total > 0) {
-    const A inv = div_rn(A(1), static_cast<A>(total));
+  const int64_t cnt = p.mean_deg ? p.mean_deg[r] : total;
+  if (!MAXMIN && p.mean && cnt > 0) {
+    const A inv = div_rn(A(1), static_cast<A>(cnt));
 #pragma unroll
     for (int m = 0; m < MH; ++m)
 #pragma unroll
@@ -678,10 +737,13 @@ gm_status launch_flat(const SpmmArgs& p0, int64_t ns, cudaStream_t st) {
     const int nv = slots <= 32 ? 1 : slots <= 64 ? 2 : slots <= 128 ? 4 : 8;
     const unsigned grid = static_cast<unsigned>(ceil_div(p.num_light_windows * 32, 256));
     if (grid == 0) continue;
-#define GM_FLAT_M(NV_, U_, M_)                                                       \
-  do {                                                                               \
-    if (scaled) spmm_flat_kernel<T, VB, NV_, U_, M_, true><<<grid, 256, 0, st>>>(p);   \
-    else spmm_flat_kernel<T, VB, NV_, U_, M_, false><<<grid, 256, 0, st>>>(p);         \
+#define GM_FLAT_M(NV_, U_, M_)                                                                   \
+  do {                                                                                           \
+    if (p.accum) {                                                                               \
+      if (scaled) spmm_flat_kernel<T, VB, NV_, U_, M_, true, 1, true><<<grid, 256, 0, st>>>(p);    \
+      else spmm_flat_kernel<T, VB, NV_, U_, M_, false, 1, true><<<grid, 256, 0, st>>>(p);          \
+    } else if (scaled) spmm_flat_kernel<T, VB, NV_, U_, M_, true><<<grid, 256, 0, st>>>(p);        \
+    else spmm_flat_kernel<T, VB, NV_, U_, M_, false><<<grid, 256, 0, st>>>(p);                     \
   } while (0)
 #define GM_FLAT_MP(U_, P_, M_)                                                                 \
   do {                                                                                           \
@@ -700,9 +762,9 @@ gm_status launch_flat(const SpmmArgs& p0, int64_t ns, cudaStream_t st) {
     else if (p.mean) GM_FLAT_M(NV_, U_, 1);            \
     else GM_FLAT_M(NV_, U_, 0);                        \
   } while (0)
-    if (nv == 1 && slots <= 8 && lane_split()) GM_FLAT_P(16, 4);
-    else if (nv == 1 && slots <= 16 && lane_split()) GM_FLAT_P(16, 2);
-    else if (sizeof(T) == 2 && nv == 1 && slots <= 16 && narrow_u16()) {
+    if (nv == 1 && slots <= 8 && lane_split() && !p.accum) GM_FLAT_P(16, 4);
+    else if (nv == 1 && slots <= 16 && lane_split() && !p.accum) GM_FLAT_P(16, 2);
+    else if (sizeof(T) == 2 && nv == 1 && slots <= 16 && narrow_u16() && !p.accum) {
       if constexpr (sizeof(T) == 2) GM_FLAT(1, 16);
     } else if (nv == 1) GM_FLAT(1, 8);
     else if (nv == 2) GM_FLAT(2, 4);

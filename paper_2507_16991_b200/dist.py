@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes as C
 from dataclasses import dataclass
+from typing import Optional
 
 import numpy as np
 import torch
@@ -52,3 +53,132 @@ def allgather_features(x_shard: torch.Tensor, shard: Shard, group=None, out=None
         (shard.shard_rows * shard.world,) + tuple(x_shard.shape[1:]), dtype=x_shard.dtype, device=x_shard.device)
     dist.all_gather_into_tensor(full, x_shard.contiguous(), group=group)
     return full
+
+
+# ---------------------------------------------------------------------------
+# Exchange-overlapped aggregation: the rank's rows are split
+# by source into block 0 (sources in its own X shard: runs at once, while the
+# exchange is in flight) and blocks 1..G (sources delivered by exchange chunk
+# c: the all-gather of shard rows [c*CS, (c+1)*CS) from every rank). Each chunk
+# is its own async all-gather; block c+1 runs as soon as chunk c has landed,
+# continuing the rows' accumulation (gm_spmm_accumulate).
+# ---------------------------------------------------------------------------
+def chunk_layout(num_src_rows: int, world: int, chunks: int):
+    """(shard_rows S, chunk_rows CS): shard q owns sources [q*S, (q+1)*S);
+    exchange chunk c carries shard rows [c*CS, (c+1)*CS) of every rank."""
+    s = -(-num_src_rows // world)
+    return s, -(-s // chunks)
+
+
+def source_blocks(num_src_rows: int, rank: int, world: int, chunks: int, device=None):
+    """Per source id: (block, column inside that block's x).
+    block 0: own shard, column = row inside x_shard;
+    block 1+c: chunk c, column = q*CS + (o - c*CS) inside the chunk's gathered
+    buffer [world*CS, F] (q = owner rank, o = row inside the owner's shard)."""
+    s_rows, cs = chunk_layout(num_src_rows, world, chunks)
+    s = torch.arange(num_src_rows, dtype=torch.int64, device=device)
+    q = s // s_rows
+    o = s - q * s_rows
+    c = o // cs
+    own = q == rank
+    blk = torch.where(own, torch.zeros_like(c), 1 + c).to(torch.int32)
+    col = torch.where(own, o, q * cs + (o - c * cs)).to(torch.int32)
+    return blk, col
+
+
+class _Done:
+    def wait(self):
+        return None
+
+
+class BlockedSpmm:
+    """One rank's exchange-overlapped SpMM over its destination rows.
+
+    rows: this rank's CSC row slice (CsrView, sources are global ids);
+    x_shard passed to __call__: [chunks*CS, F] (this rank's X shard, zero
+    padded). allgather(out, inp) -> work with .wait(): the chunk exchange
+    (default: async NCCL all_gather_into_tensor). Results: MAX/MIN values and
+    argmax equal the single-GPU ones bit-for-bit (NaN-free inputs); SUM/MEAN
+    continue each row's sum across blocks (fp32-tolerance, one re-association
+    per block boundary). For bit-identical sums use exact mode
+    (allgather_features + one gm_spmm)."""
+
+    def __init__(self, rows, num_src_rows: int, rank: int, world: int, chunks: int = 4,
+                 allgather=None, group=None):
+        from .graphmill import CsrView, _p, _stream
+        self.rank, self.world, self.chunks = rank, world, chunks
+        self.s_rows, self.cs = chunk_layout(num_src_rows, world, chunks)
+        self.allgather = allgather or (lambda out, inp: dist.all_gather_into_tensor(
+            out, inp, group=group, async_op=True))
+        dev = rows.rowptr.device
+        lib = L.lib()
+        blk, colmap = source_blocks(num_src_rows, rank, world, chunks, dev)
+        nb = chunks + 1
+        n = rows.num_rows()
+        nnz = rows.num_entries()
+        self.rowptr_b = torch.empty(nb * (n + 1), dtype=torch.int64, device=dev)
+        self.col_b = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+        self.perm_b = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+        wsb = lib.gm_csr_split_blocks_workspace(n, nb)
+        ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+        cs = rows.c_struct()
+        L.check(lib.gm_csr_split_blocks(C.byref(cs), _p(blk), _p(colmap), nb, _p(self.rowptr_b), _p(self.col_b),
+                                        _p(self.perm_b), _p(ws), wsb, _stream()), "gm_csr_split_blocks")
+        rp = self.rowptr_b.view(nb, n + 1)
+        ends = rp[:, n].cpu().tolist()
+        starts = rp[:, 0].cpu().tolist()
+        self.blocks = []
+        for b in range(nb):
+            ncols = chunks * self.cs if b == 0 else world * self.cs
+            self.blocks.append(CsrView(rp[b], self.col_b, self.perm_b, ncols, int(ends[b] - starts[b])))
+        for v in self.blocks:
+            v.plan()
+        rr = rows.rowptr
+        self.mean_deg = (rr[1:] - rr[:-1]).to(torch.int32)
+        self._bufs = {}
+
+    def block_nnz(self):
+        return [v.num_entries() for v in self.blocks]
+
+    def _buffers(self, f, dtype, device):
+        key = (f, dtype)
+        if key not in self._bufs:
+            self._bufs[key] = [torch.empty(self.world * self.cs, f, dtype=dtype, device=device)
+                               for _ in range(self.chunks)]
+        return self._bufs[key]
+
+    def __call__(self, x_shard: torch.Tensor, reduce: str = "sum", out: Optional[torch.Tensor] = None,
+                 arg: Optional[torch.Tensor] = None):
+        from .graphmill import _DT, _KIND, _p, _stream
+        assert x_shard.shape[0] == self.chunks * self.cs, "x_shard must be padded to chunks*CS rows"
+        x_shard = x_shard.contiguous()
+        f = x_shard.shape[1]
+        n = self.blocks[0].num_rows()
+        maxmin = reduce in ("max", "min")
+        if x_shard.dtype == torch.bfloat16 and not maxmin:
+            raise ValueError("BlockedSpmm: bf16 sum/mean rounds between blocks; use exact mode")
+        if out is None:
+            out = torch.empty(n, f, dtype=x_shard.dtype, device=x_shard.device)
+        if maxmin and arg is None:
+            arg = torch.empty(n, f, dtype=torch.int32, device=x_shard.device)
+        bufs = self._buffers(f, x_shard.dtype, x_shard.device)
+        # every chunk's exchange is in flight before the local block starts
+        works = [self.allgather(bufs[c], x_shard[c * self.cs:(c + 1) * self.cs]) or _Done()
+                 for c in range(self.chunks)]
+        lib = L.lib()
+        dt = _DT[x_shard.dtype]
+        first_kind = L.GM_SUM if reduce == "mean" else _KIND[reduce]
+        v = self.blocks[0]
+        cs = v.c_struct()
+        L.check(lib.gm_spmm(C.byref(cs), C.byref(v.plan()), dt, _p(x_shard), f, None, None, first_kind,
+                            _p(out), _p(arg) if maxmin else None, _stream()), "gm_spmm (local block)")
+        for c in range(self.chunks):
+            works[c].wait()
+            v = self.blocks[1 + c]
+            last = c == self.chunks - 1
+            kind = _KIND[reduce] if (last or reduce != "mean") else L.GM_SUM
+            cs = v.c_struct()
+            L.check(lib.gm_spmm_accumulate(C.byref(cs), C.byref(v.plan()), dt, _p(bufs[c]), f, None, kind,
+                                           _p(self.mean_deg) if kind == L.GM_MEAN else None, _p(out),
+                                           _p(arg) if maxmin else None, _stream()), "gm_spmm_accumulate")
+        return (out, arg) if maxmin else out

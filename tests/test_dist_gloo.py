@@ -88,3 +88,49 @@ def test_partitioned_spmm_matches_single_process(world):
     assert got.tobytes() == want.tobytes()
     assert np.concatenate([r[4] for r in results]).tobytes() == wmx.tobytes()
     assert np.array_equal(np.concatenate([r[5] for r in results]), warg)
+
+
+def _chunk_worker(rank, world, port, n, f, chunks, q):
+    """Chunked exchange of BlockedSpmm: every source id's (block, column)
+    must address exactly its feature row — in the own shard (block 0) or in
+    the gathered chunk buffer (block 1+c)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2507_16991_b200.dist import chunk_layout, source_blocks
+        s_rows, cs = chunk_layout(n, world, chunks)
+        x = torch.arange(n * f, dtype=torch.float32).view(n, f)
+        shard = torch.zeros(chunks * cs, f)
+        lo, hi = rank * s_rows, min((rank + 1) * s_rows, n)
+        shard[: max(0, hi - lo)] = x[lo:hi]
+        bufs = [torch.empty(world * cs, f) for _ in range(chunks)]
+        works = [dist.all_gather_into_tensor(bufs[c], shard[c * cs:(c + 1) * cs], async_op=True)
+                 for c in range(chunks)]
+        for w in works:
+            w.wait()
+        blk, col = source_blocks(n, rank, world, chunks)
+        ok = True
+        for s in range(n):
+            b, c = int(blk[s]), int(col[s])
+            row = shard[c] if b == 0 else bufs[b - 1][c]
+            ok &= bool(torch.equal(row, x[s]))
+            ok &= (b == 0) == (lo <= s < hi)
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,chunks", [(2, 3), (3, 2)])
+def test_chunked_exchange_addresses_every_source(world, chunks):
+    n, f = 1001, 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_chunk_worker, args=(r, world, port, n, f, chunks, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok in res)
