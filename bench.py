@@ -38,6 +38,7 @@ sys.path.insert(0, ROOT)
 METRIC = "GEdges/s CSR SpMM aggr (frac of HBM BW) + segment_matmul TFLOP/s @1/2/4/8 B200"
 N_NODES, N_EDGES, F = 2_449_029, 61_859_140, 100
 SEED = 0x67726170686D696C  # derive(..) base seed of SURVEY §8d ("graphmil")
+CHUNKS = 4  # exchange chunks per step at N > 1 (BlockedSpmm)
 
 
 def peaks():
@@ -118,13 +119,20 @@ def make_graph(gm, L, n, e, f, device, stream):
     return g, x
 
 
-def bench_segment_matmul(gm, L, device, f=128, rows=1_939_743):
+def bench_segment_matmul(gm, L, device, f=128, rows=1_939_743, rank=0, world=1, dist=None):
     """Node-type segment_matmul, K = N = f, bf16 in/out. f=128: C3 (OGB-MAG)
-    with the real per-type row counts; larger f: the tensor-bound F-sweep."""
+    with the real per-type row counts; larger f: the tensor-bound F-sweep.
+    world > 1: W replicated, every group's rows split evenly
+    across ranks, no collective; time = max over ranks, TFLOP/s of the whole job."""
     if f == 128 and rows == 1_939_743:
-        ptr = [0, 736_389, 1_871_038, 1_879_778, 1_939_743]
+        gptr = [0, 736_389, 1_871_038, 1_879_778, 1_939_743]
     else:
-        ptr = [0, rows * 38 // 100, rows * 96 // 100, rows * 97 // 100, rows]
+        gptr = [0, rows * 38 // 100, rows * 96 // 100, rows * 97 // 100, rows]
+    total_rows = gptr[-1]
+    ptr = [0]
+    for g in range(4):
+        m = gptr[g + 1] - gptr[g]
+        ptr.append(ptr[-1] + (m * (rank + 1)) // world - (m * rank) // world)
     x = torch.randn(ptr[-1], f, device=device).to(torch.bfloat16)
     w = (torch.randn(4, f, f, device=device) / f ** 0.5).to(torch.bfloat16)
     try:
@@ -141,12 +149,17 @@ def bench_segment_matmul(gm, L, device, f=128, rows=1_939_743):
         ms = ev[0].elapsed_time(ev[1]) / reps
     except Exception as exc:  # reported, never silently substituted
         return {"error": str(exc)[:200]}
-    flops = 2.0 * ptr[-1] * f * f
-    byts = 2.0 * ptr[-1] * f * 2 + 4 * f * f * 2
+    if dist is not None:
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    flops = 2.0 * total_rows * f * f
+    byts = 2.0 * total_rows * f * 2 + world * 4 * f * f * 2
     hbm, bf16_peak, _ = peaks()
     ai = flops / byts
+    hbm, bf16_peak = hbm * world, bf16_peak * world
     ceiling = min(bf16_peak, ai * hbm / 1e3)
-    return {"shape": f"sum_M={ptr[-1]},K=N={f},G=4,bf16", "ms": ms, "tflops": flops / ms / 1e9,
+    return {"shape": f"sum_M={total_rows},K=N={f},G=4,bf16", "n_gpus": world, "ms": ms, "tflops": flops / ms / 1e9,
             "frac_tensor_peak": flops / ms / 1e9 / bf16_peak, "achieved_gbs": byts / ms / 1e6,
             "frac_hbm": byts / ms / 1e6 / hbm, "roofline_ceiling_tflops": ceiling,
             "frac_roofline": flops / ms / 1e9 / ceiling,
@@ -245,7 +258,12 @@ def main():
     torch.cuda.synchronize()
 
     # ---- partition (N > 1): nnz-balanced dst rows, equal-row X shards ----------
-    from paper_2507_16991_b200.dist import allgather_features, make_shard
+    # The timed step at N > 1 is the exchange-overlapped path (BlockedSpmm):
+    # the own-shard block aggregates while the CHUNKS async NCCL all-gathers
+    # of X are in flight, then each chunk's block continues the rows' sums as
+    # it lands. "exact" (one all-gather, then one bit-identical gm_spmm) is
+    # timed beside it as a secondary line.
+    from paper_2507_16991_b200.dist import BlockedSpmm, allgather_features, chunk_layout, make_shard
     rowptr_h = csc.rowptr.cpu().numpy()
     sh = make_shard(rowptr_h, N_NODES, rank, world)
     r0, r1 = sh.row_begin, sh.row_end
@@ -253,20 +271,29 @@ def main():
     local_csr = csc if world == 1 else csc.row_slice(r0, r1, local_edges)
     out = torch.empty(N_NODES, F, dtype=torch.float32, device=device)
     x_full = x
-    if world > 1:
-        x_full = torch.zeros(sh.shard_rows * world, F, dtype=torch.float32, device=device)
-        lo, hi = sh.x_rows()
-        x_shard = torch.zeros(sh.shard_rows, F, dtype=torch.float32, device=device)
-        x_shard[: max(0, min(hi, N_NODES) - lo)].copy_(x[lo:min(hi, N_NODES)])
     plan = local_csr.plan()
     cs = local_csr.c_struct()
+    if world > 1:
+        x_full = torch.zeros(sh.shard_rows * world, F, dtype=torch.float32, device=device)
+        s_rows, c_rows = chunk_layout(N_NODES, world, CHUNKS)
+        lo, hi = rank * s_rows, min((rank + 1) * s_rows, N_NODES)
+        x_shard = torch.zeros(CHUNKS * c_rows, F, dtype=torch.float32, device=device)
+        x_shard[: max(0, hi - lo)].copy_(x[lo:hi])
+        blocked = BlockedSpmm(local_csr, N_NODES, rank, world, CHUNKS)
+        out_local = out[r0:r1]
 
-    def step():
+    def step_exact():
         if world > 1:
-            allgather_features(x_shard, sh, out=x_full)
+            allgather_features(x_shard[: sh.shard_rows], sh, out=x_full)
         L.check(lib.gm_spmm(C.byref(cs), C.byref(plan), L.GM_F32, C.c_void_p(x_full.data_ptr()), F, None,
                             None, L.GM_SUM, C.c_void_p(out[r0:].data_ptr()), None,
                             C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+
+    def step():
+        if world > 1:
+            blocked(x_shard, "sum", out=out_local)
+        else:
+            step_exact()
 
     for _ in range(args.warmup):
         step()
@@ -388,6 +415,27 @@ def main():
                "serial_value": N_EDGES / (sms * 1e-3) / 1e9, "serial_ms_per_step": sms}
 
     secondary = None
+    if world > 1 and not args.no_secondary:
+        # exact mode: one all-gather, then one bit-identical gm_spmm per rank
+        for _ in range(2):
+            step_exact()
+        torch.cuda.synchronize()
+        dist.barrier()
+        a, bev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(5):
+            step_exact()
+        bev.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(bev) / 5], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        secondary = {"exact_mode_spmm": {"ms": float(t.item()), "gedges_s": N_EDGES / float(t.item()) / 1e6,
+                                         "numerics": "bit-identical to 1 GPU"},
+                     "overlap_mode_numerics": "sum continued across 1+CHUNKS source blocks (fp32 tolerance)",
+                     "block_nnz": blocked.block_nnz(),
+                     "segment_matmul_C3": bench_segment_matmul(gm, L, device, rank=rank, world=world, dist=dist),
+                     "segment_matmul_F1024": bench_segment_matmul(gm, L, device, f=1024, rows=500_000, rank=rank,
+                                                                  world=world, dist=dist)}
     if world == 1 and not args.no_secondary:
         secondary = {"segment_matmul_C3": bench_segment_matmul(gm, L, device),
                      "segment_matmul_F1024": bench_segment_matmul(gm, L, device, f=1024, rows=500_000)}
@@ -417,6 +465,8 @@ def main():
             cpu = {"error": str(exc)[:200]}
 
     launches_per_step = 1 + (1 if plan.num_heavy > 0 else 0)
+    if world > 1:
+        launches_per_step = sum(1 + (1 if v.plan().num_heavy > 0 else 0) for v in blocked.blocks)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GEdges/s", "n_gpus": world, "steps": args.steps,
@@ -425,7 +475,9 @@ def main():
             "data": "synthetic",
             "config": {"workload": "ogbn-products-shaped power-law graph (configs[3]), full-graph sum SpMM",
                        "nodes": N_NODES, "edges": N_EDGES, "feats": F, "graph": "Chung-Lu alpha=0.5",
-                       "parallelism": f"dst-row partition x{world}" + (" + NCCL all-gather of X" if world > 1 else ""),
+                       "parallelism": f"dst-row partition x{world}" + (
+                           f" + {CHUNKS} chunked async NCCL all-gathers of X overlapped with source-blocked "
+                           "aggregation" if world > 1 else ""),
                        "l2": "L2 flushed between timed steps (256 MB write); X = 980 MB > L2",
                        "l2_hot_mb": int(plan.l2_hot_bytes >> 20), "heavy_rows": int(plan.num_heavy)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,

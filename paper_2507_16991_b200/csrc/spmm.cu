@@ -35,7 +35,15 @@ namespace gm {
 // Plan: nnz+row balanced windows and the hub list.
 // ---------------------------------------------------------------------------
 constexpr int64_t kWindowCost = 256;    // edges + rows per light window
-constexpr int64_t kHeavyThreshold = 1024;
+constexpr int64_t kHeavyThresholdDefault = 1024;
+// Rows longer than this go to the CTA-per-row hub kernel (GM_HEAVY_THR overrides; tuning only).
+static int64_t heavy_threshold() {
+  static const int64_t thr = [] {
+    const char* e = getenv("GM_HEAVY_THR");
+    return e ? std::max<int64_t>(64, atoll(e)) : kHeavyThresholdDefault;
+  }();
+  return thr;
+}
 
 __global__ void plan_windows_kernel(const int64_t* __restrict__ rowptr, int64_t num_rows,
                                     int64_t num_windows, int32_t* __restrict__ win_row) {
@@ -92,7 +100,7 @@ static int64_t plan_num_windows(int64_t num_rows, int64_t nnz) {
   return std::max<int64_t>(1, ceil_div(nnz + num_rows, kWindowCost));
 }
 static int64_t plan_heavy_cap(int64_t num_rows, int64_t nnz) {
-  return std::min<int64_t>(num_rows, nnz / kHeavyThreshold + 1);
+  return std::min<int64_t>(num_rows, nnz / heavy_threshold() + 1);
 }
 
 
@@ -169,7 +177,7 @@ GM_API gm_status gm_spmm_plan_build(const gm_csr* csr, void* buffer, size_t buff
   GM_TRY_CUDA(cudaMemsetAsync(count, 0, sizeof(unsigned int), st));
   if (csr->num_rows > 0) {
     plan_heavy_kernel<<<static_cast<unsigned>(ceil_div(csr->num_rows, 256)), 256, 0, st>>>(
-        csr->rowptr, csr->num_rows, kHeavyThreshold, cap, keys, count);
+        csr->rowptr, csr->num_rows, heavy_threshold(), cap, keys, count);
     GM_CHECK_LAUNCH("plan_heavy_kernel");
   }
   unsigned int n_heavy = 0;
@@ -219,7 +227,7 @@ GM_API gm_status gm_spmm_plan_build(const gm_csr* csr, void* buffer, size_t buff
   plan->num_windows = g;
   plan->window_edges = kWindowCost;
   plan->num_heavy = nh;
-  plan->heavy_threshold = kHeavyThreshold;
+  plan->heavy_threshold = heavy_threshold();
   plan->win_row = win_row;
   plan->heavy_rows = heavy_rows;
   plan->num_light_windows = static_cast<int64_t>(lw.size() / 2);

@@ -1,0 +1,7 @@
+// spmm_f32_v8.cu — float / 8-byte-vector instantiation of the SpMM kernels
+// (one TU per (dtype, vector width) so the kernel variants build in parallel).
+#include "spmm_kernels.cuh"
+
+namespace gm {
+template gm_status dispatch_vb<float, 8>(const SpmmArgs&, bool, bool, int64_t, int64_t, cudaStream_t);
+}  // namespace gm

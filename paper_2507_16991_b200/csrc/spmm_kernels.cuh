@@ -22,12 +22,13 @@
 //     stream so hubs start before the light sweep; the CTA streams the row's
 //     feature rows into a cp.async shared-memory ring (R stages of `se` edges)
 //     while the owning threads accumulate each column in order.
+#pragma once
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
-#pragma once
 #include "vec.cuh"
 
 namespace gm {
@@ -704,6 +705,226 @@ __global__ void __launch_bounds__(kHeavyThreads) spmm_heavy_kernel(const SpmmArg
 }
 
 // ---------------------------------------------------------------------------
+// Hub path v2: one CTA of two warps per (hub row, 128/256-byte column chunk).
+// Column chunks of a hub row run on different SMs in parallel. Warp 1 (the
+// consumer) owns one 4-byte (f32 / bf16x2) or 8-byte (f64) column slot per
+// lane and accumulates it sequentially in compressed order, so results stay
+// bit-exact. Warp 0 (the producer) streams the chunk's slices of the row's
+// source rows into a kHubRing-deep ring of 32-edge stages with cp.async:
+// per-edge metadata (col, perm, weight) kHubRing stages ahead of the slice
+// copies, each stage published to the consumer by cp.async.mbarrier.arrive on
+// its `full` barrier, slots handed back through `empty`.
+// ---------------------------------------------------------------------------
+constexpr int kHubStage = 32;
+constexpr int kHubRing = 16;
+constexpr int kHubMeta = 2 * kHubRing;
+
+template <typename T>
+struct HubLane {  // per-lane storage unit: 4 bytes (f32, bf16x2) or 8 bytes (f64)
+  static constexpr int LE = sizeof(T) == 2 ? 2 : 1;
+  static constexpr int LB = LE * static_cast<int>(sizeof(T));
+  static constexpr int CB = 32 * LB;  // chunk bytes
+  using R = typename std::conditional<LB == 8, unsigned long long, uint32_t>::type;
+};
+
+template <typename T>
+__host__ __device__ constexpr size_t hub_smem_bytes() {
+  return static_cast<size_t>(kHubRing) * kHubStage * HubLane<T>::CB;
+}
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+// arrives on bar once all of this thread's prior cp.async copies have landed
+__device__ __forceinline__ void mbar_arrive_cp_async(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+template <typename T, int G, bool MAXMIN>
+__global__ void __launch_bounds__(64) spmm_hub_kernel(const SpmmArgs p) {
+  using HL = HubLane<T>;
+  using A = typename AccOf<T>::type;
+  constexpr int LE = HL::LE;
+  constexpr int LB = HL::LB;
+  constexpr int CB = HL::CB;
+  constexpr int GPR = CB / G;  // copy granules per full chunk row
+  extern __shared__ __align__(16) unsigned char hub_data[];  // [kHubRing][kHubStage][CB]
+  __shared__ int32_t mcol[kHubMeta][kHubStage];
+  __shared__ int32_t mperm[kHubMeta][kHubStage];
+  __shared__ int32_t mdeg[kHubMeta][kHubStage];
+  __shared__ A mw[kHubMeta][kHubStage];
+  __shared__ uint64_t full[kHubRing], empty[kHubRing];
+
+  const int lane = threadIdx.x & 31;
+  const bool producer = threadIdx.x < 32;
+  const int64_t row_bytes = p.f * static_cast<int64_t>(sizeof(T));
+  const int nchunks = static_cast<int>((row_bytes + CB - 1) / CB);
+  const int hub = static_cast<int>(blockIdx.x / nchunks);
+  const int r = p.heavy_rows[hub];
+  const int64_t c_off = static_cast<int64_t>(blockIdx.x - static_cast<unsigned>(hub) * nchunks) * CB;
+  const int vbytes = static_cast<int>(row_bytes - c_off < CB ? row_bytes - c_off : CB);
+  const A* __restrict__ w = static_cast<const A*>(p.w);
+  const bool gcn = p.gdeg_src != nullptr;
+  const bool scaled = gcn || w != nullptr;
+  const bool want_arg = MAXMIN && p.arg != nullptr;
+  const int64_t kb = p.rowptr[r];
+  const int64_t deg = p.rowptr[r + 1] - kb;
+  const int64_t total = deg + ((gcn && p.gcn_self) ? 1 : 0);
+  const int nst = static_cast<int>((total + kHubStage - 1) / kHubStage);
+  auto stage_edges = [&](int q) {
+    const int64_t left = total - static_cast<int64_t>(q) * kHubStage;
+    return static_cast<int>(left < kHubStage ? left : kHubStage);
+  };
+
+  if (threadIdx.x < kHubRing) {
+    mbar_init(&full[threadIdx.x], 32);  // every producer lane arrives (cp.async noinc)
+    mbar_init(&empty[threadIdx.x], 1);  // one consumer lane arrives
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+
+  if (producer) {
+    const unsigned char* __restrict__ xb = static_cast<const unsigned char*>(p.x) + c_off;
+    const int vgran = vbytes / G;
+    // metadata of stage q -> meta slot q % kHubMeta (lane e = edge e)
+    auto issue_meta = [&](int q) {
+      if (q >= nst) return;
+      const int ms = q % kHubMeta;
+      const int64_t e = static_cast<int64_t>(q) * kHubStage + lane;
+      if (e < deg) {
+        const int64_t k = kb + e;
+        cp_async(&mcol[ms][lane], p.col + k, 4);
+        if (want_arg) cp_async(&mperm[ms][lane], p.perm + k, 4);
+        if (w) cp_async(&mw[ms][lane], w + k, static_cast<int>(sizeof(A)));
+      } else if (e < total) {  // the fused GCN self loop (r, r), last in the row
+        mcol[ms][lane] = r;
+        mperm[ms][lane] = -1;
+      }
+    };
+    // one commit group per stage's metadata: meta(q) is group q, so after the
+    // R + q commits preceding iteration q's wait, wait_group<R-1> lands it
+#pragma unroll 1
+    for (int q = 0; q < kHubRing; ++q) {
+      issue_meta(q);
+      cp_async_commit();
+    }
+#pragma unroll 1
+    for (int q = 0; q < nst; ++q) {
+      const int slot = q % kHubRing;
+      if (q >= kHubRing) mbar_wait(&empty[slot], static_cast<uint32_t>(((q / kHubRing) - 1) & 1));
+      cp_async_wait<kHubRing - 1>();  // meta(q) = group q landed
+      __syncwarp();
+      const int ms = q % kHubMeta;
+      const int n_e = stage_edges(q);
+      if (gcn && lane < n_e) cp_async(&mdeg[ms][lane], p.gdeg_src + mcol[ms][lane], 4);
+      unsigned char* dq = hub_data + static_cast<size_t>(slot) * kHubStage * CB;
+      for (int g = lane; g < n_e * GPR; g += 32) {
+        const int e2 = g / GPR;
+        const int part = g - e2 * GPR;
+        if (part < vgran)
+          cp_async(dq + e2 * CB + part * G, xb + static_cast<int64_t>(mcol[ms][e2]) * row_bytes + part * G, G);
+      }
+      mbar_arrive_cp_async(&full[slot]);  // fires when this lane's copies (and earlier meta) land
+      issue_meta(q + kHubRing);           // slot of stage q - R: consumed (empty waited above)
+      cp_async_commit();
+    }
+    cp_async_wait<0>();
+    return;
+  }
+
+  // ---- consumer warp ----
+  const int32_t dd = gcn ? p.gdeg_dst[r] : 0;
+  A v[LE];
+  int32_t a[LE];
+  bool first = true;
+  const int64_t e0 = c_off / static_cast<int64_t>(sizeof(T)) + static_cast<int64_t>(lane) * LE;
+  const bool lane_valid = lane * LB < vbytes;
+  T* orow = static_cast<T*>(p.out) + static_cast<int64_t>(r) * p.f;
+#pragma unroll
+  for (int i = 0; i < LE; ++i) {
+    v[i] = A(0);
+    a[i] = -1;
+  }
+  if (p.accum && lane_valid) {
+    T tmp[LE];
+    memcpy(tmp, orow + e0, LB);
+#pragma unroll
+    for (int i = 0; i < LE; ++i) {
+      v[i] = widen(tmp[i]);
+      if (MAXMIN) a[i] = p.arg[static_cast<int64_t>(r) * p.f + e0 + i];
+    }
+    first = MAXMIN ? a[0] == -1 : false;
+  }
+  const bool lex = MAXMIN && p.accum;
+
+#pragma unroll 1
+  for (int i = 0; i < nst; ++i) {
+    const int slot = i % kHubRing;
+    mbar_wait(&full[slot], static_cast<uint32_t>((i / kHubRing) & 1));
+    const int ms = i % kHubMeta;
+    const unsigned char* di = hub_data + static_cast<size_t>(slot) * kHubStage * CB;
+    const int n_e = stage_edges(i);
+    if (lane_valid) {
+#pragma unroll 8
+      for (int e = 0; e < n_e; ++e) {
+        const typename HL::R raw = *reinterpret_cast<const typename HL::R*>(di + e * CB + lane * LB);
+        T tmp[LE];
+        memcpy(tmp, &raw, LB);
+        A sc = A(1);
+        if (w) sc = mw[ms][e];
+        else if (gcn) sc = gcn_scale<A>(mdeg[ms][e], dd);
+        const int32_t pm = want_arg ? mperm[ms][e] : -1;
+#pragma unroll
+        for (int j = 0; j < LE; ++j) {
+          const A val = scaled ? mul_rn(widen(tmp[j]), sc) : widen(tmp[j]);
+          if (!MAXMIN) {
+            v[j] = add_rn(v[j], val);
+          } else {
+            const bool better = first || (p.is_min ? (val < v[j]) : (val > v[j])) ||
+                                (lex && val == v[j] && static_cast<uint32_t>(pm) < static_cast<uint32_t>(a[j]));
+            v[j] = better ? val : v[j];
+            a[j] = better ? pm : a[j];
+          }
+        }
+        first = false;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+  }
+
+  if (!lane_valid) return;
+  const int64_t cnt = p.mean_deg ? p.mean_deg[r] : total;
+  if (!MAXMIN && p.mean && cnt > 0) {
+    const A inv = div_rn(A(1), static_cast<A>(cnt));
+#pragma unroll
+    for (int j = 0; j < LE; ++j) v[j] = mul_rn(v[j], inv);
+  }
+  T tmp[LE];
+#pragma unroll
+  for (int j = 0; j < LE; ++j) tmp[j] = narrow<T, A>(v[j]);
+  memcpy(orow + e0, tmp, LB);
+  if (want_arg) {
+#pragma unroll
+    for (int j = 0; j < LE; ++j) p.arg[static_cast<int64_t>(r) * p.f + e0 + j] = a[j];
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Launch helpers
 // ---------------------------------------------------------------------------
 struct SideStream {
@@ -847,6 +1068,39 @@ gm_status launch_heavy(const SpmmArgs& p0, int64_t num_heavy, int64_t ns, cudaSt
   return GM_OK;
 }
 
+// Hub rows: grid (column chunks, hub rows) of one-warp CTAs, longest row first.
+template <typename T, int VB, bool MAXMIN>
+gm_status launch_hub(const SpmmArgs& p, int64_t num_heavy, cudaStream_t st) {
+  if constexpr (VB < 4) {
+    return fail(GM_ERR_INVALID_ARGUMENT, "hub kernel needs >= 4-byte row alignment");
+  } else {
+    constexpr int CB = HubLane<T>::CB;
+    const int64_t row_bytes = p.f * static_cast<int64_t>(sizeof(T));
+    const unsigned grid = static_cast<unsigned>(ceil_div(row_bytes, CB) * num_heavy);
+    // TMA bulk copies need 16-byte aligned rows (VB == 16: x and the row pitch)
+    auto kern = spmm_hub_kernel<T, (VB > 16 ? 16 : VB), MAXMIN>;
+    gm_status s_ = ensure_smem(kern, hub_smem_bytes<T>());
+    if (s_ != GM_OK) return s_;
+    kern<<<grid, 64, hub_smem_bytes<T>(), st>>>(p);
+    GM_CHECK_LAUNCH("spmm_hub_kernel");
+    return GM_OK;
+  }
+}
+// GM_HUB_V1=1 selects the original CTA-per-row hub kernel (comparison only).
+inline bool hub_v1() {
+  static const bool on = [] { const char* e = getenv("GM_HUB_V1"); return e && atoi(e) != 0; }();
+  return on;
+}
+// Wide rows (>= 1 KB: Reddit-shaped F=602 fp32, where hubs carry a large share
+// of the edges) keep the CTA-per-row kernel: its 256 threads accumulate a
+// whole row's columns at once.
+template <typename T, int VB, bool MAXMIN>
+gm_status launch_hubs(const SpmmArgs& p, int64_t num_heavy, int64_t ns, cudaStream_t st) {
+  if (hub_v1() || p.f * static_cast<int64_t>(sizeof(T)) >= kWideRowBytes)
+    return launch_heavy<T, VB, MAXMIN>(p, num_heavy, ns, st);
+  return launch_hub<T, VB, MAXMIN>(p, num_heavy, st);
+}
+
 template <typename T, int VB>
 gm_status dispatch_vb(const SpmmArgs& p, bool maxmin, bool use_heavy, int64_t num_heavy,
                              int64_t ns, cudaStream_t st) {
@@ -861,13 +1115,17 @@ gm_status dispatch_vb(const SpmmArgs& p, bool maxmin, bool use_heavy, int64_t nu
     return maxmin ? launch_heavy<T, VB, true>(q, p.num_rows, ns, st) : launch_heavy<T, VB, false>(q, p.num_rows, ns, st);
   }
   if (use_heavy) {
+    // profiling only (GM_PROF_SKIP=1: no hub kernel, 2: no light kernel) — results are incomplete
+    static const int prof_skip = [] { const char* e = getenv("GM_PROF_SKIP"); return e ? atoi(e) : 0; }();
+    if (prof_skip == 1) return maxmin ? launch_light<T, VB, true>(p, ns, st) : launch_light<T, VB, false>(p, ns, st);
+    if (prof_skip == 2) return maxmin ? launch_hubs<T, VB, true>(p, num_heavy, ns, st) : launch_hubs<T, VB, false>(p, num_heavy, ns, st);
     SideStream* ss = nullptr;
     gm_status s = side_stream(&ss);
     if (s != GM_OK) return s;
     GM_TRY_CUDA(cudaEventRecord(ss->fork, st));
     GM_TRY_CUDA(cudaStreamWaitEvent(ss->side, ss->fork, 0));
-    s = maxmin ? launch_heavy<T, VB, true>(p, num_heavy, ns, ss->side)
-               : launch_heavy<T, VB, false>(p, num_heavy, ns, ss->side);
+    s = maxmin ? launch_hubs<T, VB, true>(p, num_heavy, ns, ss->side)
+               : launch_hubs<T, VB, false>(p, num_heavy, ns, ss->side);
     if (s != GM_OK) return s;
     GM_TRY_CUDA(cudaEventRecord(ss->join, ss->side));
     s = maxmin ? launch_light<T, VB, true>(p, ns, st) : launch_light<T, VB, false>(p, ns, st);
