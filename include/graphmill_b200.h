@@ -113,6 +113,7 @@ GM_API gm_status gm_permute_edge_values(gm_dtype dtype, const void* in, const in
  * (win_row[num_windows+1]) for the warp-per-row kernel, and rows longer than
  * heavy_threshold go to a CTA-per-row pipelined kernel, longest first
  * (heavy_rows[num_heavy]). Pure scheduling: results do not depend on it. */
+#define GM_PLAN_CLASSES 128
 typedef struct gm_spmm_plan {
   int64_t num_windows;
   int64_t window_edges;
@@ -132,6 +133,11 @@ typedef struct gm_spmm_plan {
    * may change l2_hot_bytes between calls (0 disables the hint). */
   const uint8_t* src_class;
   int64_t l2_hot_bytes;
+  /* hot_edge_frac[c]: share of the entries whose source class is < c. gm_spmm
+   * applies the hint only when the rows that fit l2_hot_bytes serve at least
+   * 15% of the gathers (the per-entry class read and policy select cost more
+   * than they save on flat degree distributions, e.g. papers100M-shaped). */
+  float hot_edge_frac[GM_PLAN_CLASSES];
 } gm_spmm_plan;
 
 GM_API size_t gm_spmm_plan_bytes(int64_t num_rows, int64_t num_cols, int64_t nnz);

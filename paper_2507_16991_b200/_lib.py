@@ -48,6 +48,7 @@ class gm_spmm_plan(C.Structure):
         ("light_windows", C.c_void_p),
         ("src_class", C.c_void_p),
         ("l2_hot_bytes", C.c_int64),
+        ("hot_edge_frac", C.c_float * 128),
     ]
 
 

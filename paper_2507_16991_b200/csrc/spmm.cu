@@ -236,6 +236,7 @@ GM_API gm_status gm_spmm_plan_build(const gm_csr* csr, void* buffer, size_t buff
   // source hotness classes for the L2 residency hint
   plan->src_class = nullptr;
   plan->l2_hot_bytes = 0;
+  for (int c = 0; c < GM_PLAN_CLASSES; ++c) plan->hot_edge_frac[c] = 0.f;
   if (csr->num_cols > 0 && csr->nnz > 0) {
     GM_TRY_CUDA(cudaMemsetAsync(sdeg, 0, csr->num_cols * sizeof(int32_t), st));
     GM_TRY_CUDA(cudaMemsetAsync(dhist, 0, kDegBuckets * sizeof(int32_t), st));
@@ -258,6 +259,19 @@ GM_API gm_status gm_spmm_plan_build(const gm_csr* csr, void* buffer, size_t buff
       const double c = std::floor(4.0 * std::log2(1.0 + static_cast<double>(greater)));
       table[static_cast<size_t>(d)] = static_cast<uint8_t>(std::min(255.0, c));
       greater += hist[static_cast<size_t>(d)];
+    }
+    // share of the entries whose source class is < c (the hint's L2 coverage)
+    std::vector<double> cls_edges(256, 0.0);
+    double all_edges = 0.0;
+    for (int d = 0; d < kDegBuckets; ++d) {
+      const double e = static_cast<double>(d) * hist[static_cast<size_t>(d)];
+      cls_edges[table[static_cast<size_t>(d)]] += e;
+      all_edges += e;
+    }
+    double run = 0.0;
+    for (int c = 0; c < GM_PLAN_CLASSES; ++c) {
+      plan->hot_edge_frac[c] = all_edges > 0 ? static_cast<float>(run / all_edges) : 0.f;
+      run += cls_edges[static_cast<size_t>(c)];
     }
     GM_TRY_CUDA(cudaMemcpyAsync(dtable, table.data(), kDegBuckets, cudaMemcpyHostToDevice, st));
     src_class_kernel<<<grid, 256, 0, st>>>(csr->col + k0, csr->nnz, sdeg, dtable, cls + 0);
@@ -325,11 +339,23 @@ static gm_status spmm_impl(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype
   p.flat_ok = plan->num_heavy == 0 || use_heavy;
   p.src_class = nullptr;
   p.hot_class_limit = 0;
+  // X much larger than L2 streams: every gather carries an eviction policy
+  p.stream_x = static_cast<double>(csr->num_cols) * static_cast<double>(rowbytes) > 64.0 * (1 << 20);
   if (plan->src_class && plan->l2_hot_bytes > 0) {
     // rows that fit the budget: rank < hot_rows  <=>  class < floor(4*log2(1 + hot_rows))
     const double hot_rows = static_cast<double>(plan->l2_hot_bytes) / static_cast<double>(rowbytes);
-    p.src_class = plan->src_class;
-    p.hot_class_limit = static_cast<int>(std::floor(4.0 * std::log2(1.0 + hot_rows)));
+    const int limit = static_cast<int>(std::floor(4.0 * std::log2(1.0 + hot_rows)));
+    // the hint costs a class byte and a policy select per entry: only worth it
+    // when the L2-resident rows serve a large share of the gathers
+    static const double min_cover = [] {
+      const char* e = getenv("GM_L2_MIN_COVER");
+      return e ? atof(e) : 0.15;
+    }();
+    const double cover = plan->hot_edge_frac[std::min(limit, GM_PLAN_CLASSES - 1)];
+    if (cover >= min_cover) {
+      p.src_class = plan->src_class;
+      p.hot_class_limit = limit;
+    }
   }
   cudaStream_t st = as_stream(stream);
 

@@ -65,6 +65,7 @@ struct SpmmArgs {
   // source blocks (multi-GPU exchange overlap, dist.py).
   int accum;
   const int32_t* mean_deg;       // MEAN denominators per row (NULL = row length)
+  int stream_x;                  // X exceeds the L2 budget: gathers carry eviction policies
 };
 
 // L2 eviction-priority policies (createpolicy; PTX ISA "Cache eviction priority hints").
@@ -156,10 +157,8 @@ struct Acc {
       } else {
         const bool better = first || (is_min ? (val < v[j][e]) : (val > v[j][e])) ||
                             (lex && val == v[j][e] && static_cast<uint32_t>(pm) < static_cast<uint32_t>(a[j][e]));
-        if (better) {
-          v[j][e] = val;
-          a[j][e] = pm;
-        }
+        v[j][e] = better ? val : v[j][e];
+        a[j][e] = better ? pm : a[j][e];
       }
     }
   }
@@ -291,28 +290,15 @@ __global__ void __launch_bounds__(256) spmm_light_kernel(const SpmmArgs p) {
 // and broadcast by shuffle; row ends are cached 32 at a time across lanes.
 // Accumulation order per output element is unchanged: ascending CSC position.
 // ---------------------------------------------------------------------------
-// shuffle of a raw vector
-__device__ __forceinline__ uint4 shfl_raw(const uint4& v, int src) {
-  return make_uint4(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src),
-                    __shfl_sync(0xffffffffu, v.z, src), __shfl_sync(0xffffffffu, v.w, src));
-}
-__device__ __forceinline__ uint2 shfl_raw(const uint2& v, int src) {
-  return make_uint2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
-}
-__device__ __forceinline__ uint32_t shfl_raw(const uint32_t& v, int src) { return __shfl_sync(0xffffffffu, v, src); }
-__device__ __forceinline__ unsigned short shfl_raw(const unsigned short& v, int src) {
-  return static_cast<unsigned short>(__shfl_sync(0xffffffffu, static_cast<uint32_t>(v), src));
-}
-
-// P > 1 (rows of <= 32/P vector slots): one load instruction fetches P edges
-// (lane l loads slot l % (32/P) of edge l / (32/P)); the owning lanes then
-// take each edge's slice by shuffle, in edge order — same accumulation order.
-template <typename T, int VB, int NV, int U, int MODE, bool SCALED, int P = 1, bool ACC = false>
+// MODE: 0 sum, 1 mean, 2 max, 3 min. HINT: gathers carry an L2 eviction
+// policy — evict_last for entries whose source class is below
+// p.hot_class_limit (when the plan's classes are in use), evict_first for all
+// others — so streaming rows of an X far larger than L2 do not displace the
+// hot rows. Without HINT (X fits L2) gathers use the default policy.
+template <typename T, int VB, int NV, int U, int MODE, bool SCALED, bool ACC, bool HINT>
 __global__ void __launch_bounds__(256, (SCALED || sizeof(T) == 8) ? 3 : 4) spmm_flat_kernel(const SpmmArgs p) {
-  static_assert(P == 1 || NV == 1, "lane-split loads need one vector per lane");
-  static_assert(U % P == 0, "batch must hold whole load groups");
-  constexpr int SLW = 32 / P;  // lanes per edge in the load phase
-  constexpr bool MAXMIN = MODE == 2;
+  constexpr bool MAXMIN = MODE >= 2;
+  constexpr bool IS_MIN = MODE == 3;
   constexpr bool MEAN = MODE == 1;
   using VecT = Vec<T, VB>;
   using A = typename VecT::A;
@@ -328,19 +314,15 @@ __global__ void __launch_bounds__(256, (SCALED || sizeof(T) == 8) ? 3 : 4) spmm_
   const int32_t* __restrict__ col = p.col;
   const bool want_arg = MAXMIN && p.arg != nullptr;
   const uint32_t fu = static_cast<uint32_t>(p.f);  // row stride (elements)
+  const int nsl = static_cast<int>(p.slot_end - p.slot_base);
 
   uint32_t soff[NV];  // element offset of this lane's vector j inside a row
   bool valid[NV];
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
-    const int64_t sl = p.slot_base + lane + j * 32;
-    valid[j] = sl < p.slot_end;
-    soff[j] = static_cast<uint32_t>(sl * V);
+    valid[j] = lane + j * 32 < nsl;
+    soff[j] = static_cast<uint32_t>((p.slot_base + lane + j * 32) * V);
   }
-  // load-phase slot (P > 1): slot lane % SLW of edge lane / SLW
-  const int64_t lsl = p.slot_base + (lane % SLW);
-  const bool lvalid = lsl < p.slot_end;
-  const uint32_t loff = static_cast<uint32_t>(lsl * V);
 
   // Positions fit int32: gm_build_compressed / plan_build require nnz < 2^31.
   const int ra = p.light_windows[2 * warp];
@@ -407,67 +389,51 @@ __global__ void __launch_bounds__(256, (SCALED || sizeof(T) == 8) ? 3 : 4) spmm_
     }
   };
 
-  const bool hinted = p.src_class != nullptr;
-  const uint64_t pol_hot = policy_evict_last();
-  const uint64_t pol_cold = policy_evict_first();
-  int32_t c_next = 0, p_next = -1, h_next = 0;
+  const uint64_t pol_hot = HINT ? policy_evict_last() : 0;
+  const uint64_t pol_cold = HINT ? policy_evict_first() : 0;
+  int32_t c_next = 0, p_next = -1;
+  bool h_next = false;
   A w_next = A(1);
+  // entries past the window end repeat its last edge: that row is re-read
+  // (an L2 hit) but never accumulated, so the loads need no bounds checks
   auto fetch = [&](int32_t kb) {
-    const int32_t k = kb + lane;
-    if (lane < U && k < kend) {
+    if (lane < U) {
+      const int32_t k = min(kb + lane, kend - 1);
       c_next = col[k];
-      if (hinted) h_next = p.src_class[k] < p.hot_class_limit;
+      if (HINT && p.src_class) h_next = p.src_class[k] < p.hot_class_limit;
       if (SCALED) w_next = static_cast<const A*>(p.w)[k];
       if (MAXMIN) p_next = want_arg ? p.perm[k] : -1;
     }
   };
-  fetch(kbeg);
+  if (kend > kbeg) fetch(kbeg);
 
   for (int32_t k0 = kbeg; k0 < kend; k0 += U) {
     const int32_t c_cur = c_next;
     const int32_t p_cur = p_next;
-    const int32_t h_cur = h_next;
+    const uint32_t hmask = HINT ? __ballot_sync(FULL, h_next) : 0u;
     const A w_cur = w_next;
-    fetch(k0 + U);
+    if (k0 + U < kend) fetch(k0 + U);
     const int nb = min(U, kend - k0);  // edges in this batch
-    R buf[U / P][NV];
-    if constexpr (P == 1) {
+    R buf[U][NV];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint32_t cu = static_cast<uint32_t>(__shfl_sync(FULL, c_cur, u));
-        const int32_t hu = __shfl_sync(FULL, h_cur, u);
-        if (u < nb) {
-          const T* xr = x + static_cast<uint64_t>(cu) * fu;
-          if (hinted) {
-            const uint64_t pol = hu ? pol_hot : pol_cold;
+    for (int u = 0; u < U; ++u) {
+      const T* xr = x + static_cast<uint64_t>(static_cast<uint32_t>(__shfl_sync(FULL, c_cur, u))) * fu;
+      if constexpr (HINT) {
+        if ((hmask >> u) & 1u) {
 #pragma unroll
-            for (int j = 0; j < NV; ++j)
-              if (valid[j]) buf[u][j] = ldg_hint<R>(reinterpret_cast<const R*>(xr + soff[j]), pol);
-          } else {
+          for (int j = 0; j < NV; ++j)
+            if (valid[j]) buf[u][j] = ldg_hint<R>(reinterpret_cast<const R*>(xr + soff[j]), pol_hot);
+        } else {
 #pragma unroll
-            for (int j = 0; j < NV; ++j)
-              if (valid[j]) buf[u][j] = VecT::load_raw(xr + soff[j]);
-          }
+          for (int j = 0; j < NV; ++j)
+            if (valid[j]) buf[u][j] = ldg_hint<R>(reinterpret_cast<const R*>(xr + soff[j]), pol_cold);
         }
-      }
-    } else {
+      } else if (u < nb) {  // (the branch also keeps ptxas from hoisting all U addresses at once)
 #pragma unroll
-      for (int g = 0; g < U / P; ++g) {
-        const int eb = g * P + lane / SLW;  // edge of this lane's load
-        const uint32_t cu = static_cast<uint32_t>(__shfl_sync(FULL, c_cur, eb));
-        const int32_t hu = __shfl_sync(FULL, h_cur, eb);
-        if (eb < nb && lvalid) {
-          const T* xr = x + static_cast<uint64_t>(cu) * fu;
-          if (hinted) buf[g][0] = ldg_hint<R>(reinterpret_cast<const R*>(xr + loff), hu ? pol_hot : pol_cold);
-          else buf[g][0] = VecT::load_raw(xr + loff);
-        }
+        for (int j = 0; j < NV; ++j)
+          if (valid[j]) buf[u][j] = VecT::load_raw(xr + soff[j]);
       }
     }
-    // this lane's slice of edge u (the loads above put it on lane (u%P)*SLW + lane)
-    auto slice = [&](int u, int j) -> R {
-      if constexpr (P == 1) return buf[u][j];
-      else return shfl_raw(buf[u / P][0], (u % P) * SLW + (lane % SLW));
-    };
     if (nb == U && k0 + U <= row_end) {
       // fast path: the whole batch belongs to the current row
 #pragma unroll
@@ -476,11 +442,10 @@ __global__ void __launch_bounds__(256, (SCALED || sizeof(T) == 8) ? 3 : 4) spmm_
         const int32_t pm = MAXMIN ? __shfl_sync(FULL, p_cur, u) : -1;
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
-          const R r = slice(u, j);
           if (valid[j]) {
             A vals[V];
-            VecT::unpack(r, vals);
-            acc.add(j, vals, SCALED, sc, first && u == 0, p.is_min, pm, lex);
+            VecT::unpack(buf[u][j], vals);
+            acc.add(j, vals, SCALED, sc, first && u == 0, IS_MIN, pm, lex);
           }
         }
       }
@@ -490,17 +455,14 @@ __global__ void __launch_bounds__(256, (SCALED || sizeof(T) == 8) ? 3 : 4) spmm_
       for (int u = 0; u < U; ++u) {
         const A sc = SCALED ? __shfl_sync(FULL, w_cur, u) : A(1);
         const int32_t pm = MAXMIN ? __shfl_sync(FULL, p_cur, u) : -1;
-        R rs[NV];
-#pragma unroll
-        for (int j = 0; j < NV; ++j) rs[j] = slice(u, j);
         if (u < nb) {
           while (k0 + u >= row_end) flush();
 #pragma unroll
           for (int j = 0; j < NV; ++j)
             if (valid[j]) {
               A vals[V];
-              VecT::unpack(rs[j], vals);
-              acc.add(j, vals, SCALED, sc, first, p.is_min, pm, lex);
+              VecT::unpack(buf[u][j], vals);
+              acc.add(j, vals, SCALED, sc, first, IS_MIN, pm, lex);
             }
           first = false;
         }
@@ -518,16 +480,6 @@ constexpr int64_t kWideRowBytes = 1024;
 // Experimental: route every wide row through the CTA kernel (GM_WIDE_CTA=1).
 inline bool wide_cta_mode() {
   static const bool on = [] { const char* e = getenv("GM_WIDE_CTA"); return e && atoi(e) == 1; }();
-  return on;
-}
-// Lane-split loads for narrow rows (experimental; GM_LANE_SPLIT=1 enables).
-inline bool lane_split() {
-  static const bool on = [] { const char* e = getenv("GM_LANE_SPLIT"); return e && atoi(e) != 0; }();
-  return on;
-}
-// 16-edge batches for narrow bf16 rows (experimental; GM_NARROW_U16=1 enables).
-inline bool narrow_u16() {
-  static const bool on = [] { const char* e = getenv("GM_NARROW_U16"); return e && atoi(e) != 0; }();
   return on;
 }
 // Max vectors per lane in the flat kernel (GM_FLAT_MAX_NV, default 4: wide
@@ -950,6 +902,8 @@ gm_status launch_flat(const SpmmArgs& p0, int64_t ns, cudaStream_t st) {
   constexpr int kV = VB / static_cast<int>(sizeof(T));
   constexpr int64_t kChunk = 32 * std::min(8, std::max(1, 32 / kV));
   const int64_t chunk = std::min<int64_t>(kChunk, 32 * std::max(1, flat_max_nv()));
+  // policy-carrying gathers unless X is small enough to live in L2
+  const bool hint = p0.stream_x != 0;
   for (int64_t base = 0; base < ns; base += chunk) {
     SpmmArgs p = p0;
     p.slot_base = base;
@@ -958,43 +912,35 @@ gm_status launch_flat(const SpmmArgs& p0, int64_t ns, cudaStream_t st) {
     const int nv = slots <= 32 ? 1 : slots <= 64 ? 2 : slots <= 128 ? 4 : 8;
     const unsigned grid = static_cast<unsigned>(ceil_div(p.num_light_windows * 32, 256));
     if (grid == 0) continue;
-#define GM_FLAT_M(NV_, U_, M_)                                                                   \
+#define GM_FLAT_H(NV_, U_, M_, H_)                                                               \
   do {                                                                                           \
     if (p.accum) {                                                                               \
-      if (scaled) spmm_flat_kernel<T, VB, NV_, U_, M_, true, 1, true><<<grid, 256, 0, st>>>(p);    \
-      else spmm_flat_kernel<T, VB, NV_, U_, M_, false, 1, true><<<grid, 256, 0, st>>>(p);          \
-    } else if (scaled) spmm_flat_kernel<T, VB, NV_, U_, M_, true><<<grid, 256, 0, st>>>(p);        \
-    else spmm_flat_kernel<T, VB, NV_, U_, M_, false><<<grid, 256, 0, st>>>(p);                     \
+      if (scaled) spmm_flat_kernel<T, VB, NV_, U_, M_, true, true, H_><<<grid, 256, 0, st>>>(p);    \
+      else spmm_flat_kernel<T, VB, NV_, U_, M_, false, true, H_><<<grid, 256, 0, st>>>(p);          \
+    } else if (scaled) spmm_flat_kernel<T, VB, NV_, U_, M_, true, false, H_><<<grid, 256, 0, st>>>(p); \
+    else spmm_flat_kernel<T, VB, NV_, U_, M_, false, false, H_><<<grid, 256, 0, st>>>(p);           \
   } while (0)
-#define GM_FLAT_MP(U_, P_, M_)                                                                 \
-  do {                                                                                           \
-    if (scaled) spmm_flat_kernel<T, VB, 1, U_, M_, true, P_><<<grid, 256, 0, st>>>(p);           \
-    else spmm_flat_kernel<T, VB, 1, U_, M_, false, P_><<<grid, 256, 0, st>>>(p);                 \
+#define GM_FLAT_K(NV_, U_, M_)                                                    \
+  do {                                                                            \
+    if (hint) GM_FLAT_H(NV_, U_, M_, true);                                       \
+    else if (!scaled && !p.accum) spmm_flat_kernel<T, VB, NV_, U_, M_, false, false, false><<<grid, 256, 0, st>>>(p); \
+    else GM_FLAT_H(NV_, U_, M_, true);                                            \
   } while (0)
-#define GM_FLAT_P(U_, P_)                              \
-  do {                                                 \
-    if constexpr (MAXMIN) GM_FLAT_MP(U_, P_, 2);       \
-    else if (p.mean) GM_FLAT_MP(U_, P_, 1);            \
-    else GM_FLAT_MP(U_, P_, 0);                        \
+#define GM_FLAT(NV_, U_)                          \
+  do {                                            \
+    if constexpr (MAXMIN) {                       \
+      if (p.is_min) GM_FLAT_K(NV_, U_, 3);        \
+      else GM_FLAT_K(NV_, U_, 2);                 \
+    } else if (p.mean) GM_FLAT_K(NV_, U_, 1);     \
+    else GM_FLAT_K(NV_, U_, 0);                   \
   } while (0)
-#define GM_FLAT(NV_, U_)                               \
-  do {                                                 \
-    if constexpr (MAXMIN) GM_FLAT_M(NV_, U_, 2);       \
-    else if (p.mean) GM_FLAT_M(NV_, U_, 1);            \
-    else GM_FLAT_M(NV_, U_, 0);                        \
-  } while (0)
-    if (nv == 1 && slots <= 8 && lane_split() && !p.accum) GM_FLAT_P(16, 4);
-    else if (nv == 1 && slots <= 16 && lane_split() && !p.accum) GM_FLAT_P(16, 2);
-    else if (sizeof(T) == 2 && nv == 1 && slots <= 16 && narrow_u16() && !p.accum) {
-      if constexpr (sizeof(T) == 2) GM_FLAT(1, 16);
-    } else if (nv == 1) GM_FLAT(1, 8);
+    if (nv == 1) GM_FLAT(1, 8);
     else if (nv == 2) GM_FLAT(2, 4);
     else if (nv == 4 || kChunk <= 128) GM_FLAT(4, 2);
     else if constexpr (kChunk > 128) GM_FLAT(8, 1);
 #undef GM_FLAT
-#undef GM_FLAT_M
-#undef GM_FLAT_P
-#undef GM_FLAT_MP
+#undef GM_FLAT_K
+#undef GM_FLAT_H
     GM_CHECK_LAUNCH("spmm_flat_kernel");
   }
   return GM_OK;
@@ -1003,7 +949,7 @@ gm_status launch_flat(const SpmmArgs& p0, int64_t ns, cudaStream_t st) {
 template <typename T, int VB, bool MAXMIN>
 gm_status launch_light(const SpmmArgs& p0, int64_t ns, cudaStream_t st) {
   // wide rows without the fused GCN term take the flat edge-stream kernel
-  if (p0.gdeg_src == nullptr && (ns > 8 || lane_split()) && p0.flat_ok)
+  if (p0.gdeg_src == nullptr && ns > 8 && p0.flat_ok)
     return launch_flat<T, VB, MAXMIN>(p0, ns, st);
   // chunk columns so a lane holds <= 8 vectors; pick LPR/NV per chunk
   for (int64_t base = 0; base < ns; base += 256) {
