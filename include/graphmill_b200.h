@@ -80,6 +80,16 @@ GM_API gm_status gm_check_index_bounds(const int64_t* ids, int64_t len, int64_t 
 GM_API gm_status gm_first_unsorted(const int64_t* keys, int64_t len, int64_t* pos_host,
                                    void* workspace, gm_stream_t stream);
 
+/* Replaces the is_undirected claim check (edge_index.cpp:98-118): writes the
+ * first COO position i whose pair multiplicity count(src[i], dst[i]) differs
+ * from count(dst[i], src[i]), or -1 if the edge multiset is symmetric, to
+ * *pos_host (radix sort of the pair keys + per-position binary searches).
+ * n = num_src_nodes = num_dst_nodes. Synchronizes. */
+GM_API size_t gm_first_asymmetric_workspace(int64_t len);
+GM_API gm_status gm_first_asymmetric(const int64_t* src, const int64_t* dst, int64_t len, int64_t n,
+                                     int64_t* pos_host, void* workspace, size_t workspace_bytes,
+                                     gm_stream_t stream);
+
 /* Occurrence counts of ids in [0, n) into deg[n] (int32); ids outside are
  * skipped (message_passing.hpp:76-78 spmm-mean degree; 441-443 full-array
  * degrees of gcn_norm). */
@@ -99,7 +109,8 @@ GM_API gm_status gm_build_compressed(const int64_t* keys, const int64_t* values,
 
 /* out[k] = in[perm[k]] for nnz elements of dtype: edge values in COO order ->
  * compressed order (the `w[perm[k]]` lookup of message_passing.hpp:68, done
- * once and cached instead of per edge). */
+ * once and cached instead of per edge). A raw element move: GM_F64 also moves
+ * int64 index arrays (EdgeIndex::sort_by's new src/dst, edge_index.cpp:152-160). */
 GM_API gm_status gm_permute_edge_values(gm_dtype dtype, const void* in, const int32_t* perm,
                                         int64_t nnz, void* out, gm_stream_t stream);
 

@@ -67,6 +67,8 @@ SIGNATURES = {
     "gm_check_index_bounds": (C.c_int, [_P, _I64, _I64, C.c_char_p, _P, _P]),
     "gm_first_unsorted": (C.c_int, [_P, _I64, C.POINTER(C.c_int64), _P, _P]),
     "gm_degree": (C.c_int, [_P, _I64, _I64, _P, _P]),
+    "gm_first_asymmetric_workspace": (C.c_size_t, [_I64]),
+    "gm_first_asymmetric": (C.c_int, [_P, _P, _I64, _I64, C.POINTER(C.c_int64), _P, C.c_size_t, _P]),
     "gm_build_compressed_workspace": (C.c_size_t, [_I64, _I64]),
     "gm_build_compressed": (C.c_int, [_P, _P, _I64, _I64, _P, _P, _P, _P, C.c_size_t, _P]),
     "gm_permute_edge_values": (C.c_int, [C.c_int, _P, _P, _I64, _P, _P]),

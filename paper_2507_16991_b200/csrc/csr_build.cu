@@ -19,6 +19,8 @@
 
 #include "gm_common.cuh"
 
+#include <cub/device/device_radix_sort.cuh>
+
 namespace gm {
 
 // ---------------------------------------------------------------------------
@@ -430,6 +432,54 @@ __global__ void split_rowptr_kernel(const int64_t* __restrict__ off, int64_t row
   }
 }
 
+// ---------------------------------------------------------------------------
+// Undirected-claim check (edge_index.cpp:98-118): count(u,v) == count(v,u)
+// for every COO position; the first position that fails is reported.
+// ---------------------------------------------------------------------------
+__global__ void pair_keys_kernel(const int64_t* __restrict__ src, const int64_t* __restrict__ dst, int64_t len,
+                                 int64_t n, unsigned long long* __restrict__ keys) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < len;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    keys[i] = static_cast<unsigned long long>(src[i]) * static_cast<unsigned long long>(n) +
+              static_cast<unsigned long long>(dst[i]);
+}
+
+__device__ __forceinline__ int64_t key_count(const unsigned long long* __restrict__ sorted, int64_t len,
+                                             unsigned long long k) {
+  int64_t lo = 0, hi = len;  // lower bound
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (sorted[mid] < k) lo = mid + 1;
+    else hi = mid;
+  }
+  int64_t lo2 = lo, hi2 = len;  // upper bound
+  while (lo2 < hi2) {
+    const int64_t mid = (lo2 + hi2) >> 1;
+    if (sorted[mid] <= k) lo2 = mid + 1;
+    else hi2 = mid;
+  }
+  return lo2 - lo;
+}
+
+__global__ void asym_kernel(const int64_t* __restrict__ src, const int64_t* __restrict__ dst, int64_t len, int64_t n,
+                            const unsigned long long* __restrict__ sorted, unsigned long long* __restrict__ first) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < len;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const unsigned long long u = static_cast<unsigned long long>(src[i]);
+    const unsigned long long v = static_cast<unsigned long long>(dst[i]);
+    const unsigned long long nn = static_cast<unsigned long long>(n);
+    if (key_count(sorted, len, u * nn + v) != key_count(sorted, len, v * nn + u))
+      atomicMin(first, static_cast<unsigned long long>(i));
+  }
+}
+
+static size_t asym_cub_bytes(int64_t len) {
+  size_t tmp = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, tmp, static_cast<const unsigned long long*>(nullptr),
+                                 static_cast<unsigned long long*>(nullptr), static_cast<int>(len));
+  return tmp;
+}
+
 struct SplitWs {
   int32_t* cnt;
   int64_t* partial;
@@ -459,6 +509,45 @@ static SplitWs split_layout(void* base, int64_t rows, int64_t nb) {
 using namespace gm;
 
 extern "C" {
+
+GM_API size_t gm_first_asymmetric_workspace(int64_t len) {
+  if (len < 0 || len >= INT32_MAX) return 0;
+  return 2 * align_up(sizeof(unsigned long long) * static_cast<size_t>(std::max<int64_t>(len, 1)), 256) +
+         align_up(asym_cub_bytes(len), 256) + 256;
+}
+
+GM_API gm_status gm_first_asymmetric(const int64_t* src, const int64_t* dst, int64_t len, int64_t n,
+                                     int64_t* pos_host, void* workspace, size_t workspace_bytes,
+                                     gm_stream_t stream) {
+  GM_REQUIRE(pos_host, GM_ERR_INVALID_ARGUMENT, "gm_first_asymmetric: null output");
+  *pos_host = -1;
+  if (len == 0) return GM_OK;
+  GM_REQUIRE(len > 0 && len < INT32_MAX, GM_ERR_INVALID_ARGUMENT, "gm_first_asymmetric: length must be in [0, 2^31)");
+  GM_REQUIRE(n > 0 && n <= (int64_t(1) << 31), GM_ERR_INVALID_ARGUMENT, "gm_first_asymmetric: n must be in (0, 2^31]");
+  GM_REQUIRE(src && dst && workspace && workspace_bytes >= gm_first_asymmetric_workspace(len),
+             GM_ERR_INVALID_ARGUMENT, "gm_first_asymmetric: null pointer or workspace too small");
+  cudaStream_t st = as_stream(stream);
+  unsigned char* b = static_cast<unsigned char*>(workspace);
+  const size_t kb = align_up(sizeof(unsigned long long) * static_cast<size_t>(len), 256);
+  auto* keys = reinterpret_cast<unsigned long long*>(b);
+  auto* sorted = reinterpret_cast<unsigned long long*>(b + kb);
+  void* tmp = b + 2 * kb;
+  size_t tmp_bytes = asym_cub_bytes(len);
+  auto* first = reinterpret_cast<unsigned long long*>(b + 2 * kb + align_up(tmp_bytes, 256));
+  pair_keys_kernel<<<grid_for(len), 256, 0, st>>>(src, dst, len, n, keys);
+  GM_CHECK_LAUNCH("pair_keys_kernel");
+  int bits = 1;
+  while (bits < 64 && (static_cast<unsigned long long>(n) * static_cast<unsigned long long>(n) >> bits) != 0) ++bits;
+  GM_TRY_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, keys, sorted, static_cast<int>(len), 0, bits, st));
+  GM_TRY_CUDA(cudaMemsetAsync(first, 0xff, sizeof(unsigned long long), st));
+  asym_kernel<<<grid_for(len), 256, 0, st>>>(src, dst, len, n, sorted, first);
+  GM_CHECK_LAUNCH("asym_kernel");
+  unsigned long long pos = 0;
+  GM_TRY_CUDA(cudaMemcpyAsync(&pos, first, sizeof(pos), cudaMemcpyDeviceToHost, st));
+  GM_TRY_CUDA(cudaStreamSynchronize(st));
+  if (pos != ~0ull) *pos_host = static_cast<int64_t>(pos);
+  return GM_OK;
+}
 
 GM_API size_t gm_csr_split_blocks_workspace(int64_t num_rows, int32_t num_blocks) {
   if (num_rows < 0 || num_blocks < 1) return 0;

@@ -236,6 +236,41 @@ class EdgeIndex:
     def csc_build_count(self) -> int:
         return self._cache.csc_builds
 
+    def sort_by(self, order: str):
+        """(sorted EdgeIndex, perm) — edge_index.cpp:147-188. The grouped view is
+        a stable device counting sort; the new COO arrays are src[perm] /
+        dst[perm]; the sorted index carries the grouping as its CSR (by_src) or
+        CSC (by_dst) cache with identity perm, as the reference publishes it."""
+        if order not in ("by_src", "by_dst"):
+            raise ValueError("EdgeIndex: sort_by needs by_src or by_dst")
+        by_src = order == "by_src"
+        keys, vals = (self.src(), self.dst()) if by_src else (self.dst(), self.src())
+        n_rows, n_cols = (self._num_src, self._num_dst) if by_src else (self._num_dst, self._num_src)
+        grouped = build_compressed(keys, vals, n_rows, n_cols)
+        e = self._num_edges
+        lib = L.lib()
+        new_src = torch.empty(e, dtype=torch.int64, device=self._src.device)
+        new_dst = torch.empty(e, dtype=torch.int64, device=self._src.device)
+        if e:
+            L.check(lib.gm_permute_edge_values(L.GM_F64, _p(self.src()), _p(grouped.perm), e, _p(new_src), _stream()),
+                    "permute src")
+            L.check(lib.gm_permute_edge_values(L.GM_F64, _p(self.dst()), _p(grouped.perm), e, _p(new_dst), _stream()),
+                    "permute dst")
+        out = EdgeIndex.__new__(EdgeIndex)
+        out._src, out._dst = new_src, new_dst
+        out._num_edges = e
+        out._num_src, out._num_dst = self._num_src, self._num_dst
+        out._sort_order = order
+        out._undirected = self._undirected
+        out._cache = _CacheSlot()
+        carried = CsrView(grouped.rowptr, grouped.col,
+                          torch.arange(e, dtype=torch.int32, device=self._src.device), n_cols)
+        if by_src:
+            out._cache.csr = carried
+        else:
+            out._cache.csc = carried
+        return out, grouped.perm.to(torch.int64)
+
     def prefix_edges(self, count: int, num_src_nodes: int, num_dst_nodes: int) -> "EdgeIndex":
         """Zero-copy view of the first `count` edges (edge_index.cpp:201-216)."""
         if count < 0 or count > self._num_edges:
@@ -268,16 +303,17 @@ class _CacheSlot:
 
 def _first_asymmetric(src: torch.Tensor, dst: torch.Tensor, n: int) -> int:
     """First COO position whose (u,v) multiplicity differs from (v,u)'s
-    (edge_index.cpp:98-118), via sorted pair keys on the device."""
+    (edge_index.cpp:98-118): gm_first_asymmetric (device radix sort of the
+    pair keys + per-position multiplicity lookups)."""
     if src.numel() == 0:
         return -1
-    fwd = src * n + dst
-    rev = dst * n + src
-    sorted_fwd, _ = torch.sort(fwd)
-    cnt_fwd = torch.searchsorted(sorted_fwd, fwd, right=True) - torch.searchsorted(sorted_fwd, fwd)
-    cnt_rev = torch.searchsorted(sorted_fwd, rev, right=True) - torch.searchsorted(sorted_fwd, rev)
-    bad = torch.nonzero(cnt_fwd != cnt_rev)
-    return int(bad[0, 0]) if bad.numel() else -1
+    lib = L.lib()
+    nb = lib.gm_first_asymmetric_workspace(src.numel())
+    ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=src.device)
+    pos = C.c_int64(-1)
+    L.check(lib.gm_first_asymmetric(_p(src), _p(dst), src.numel(), n, C.byref(pos), _p(ws), nb, _stream()),
+            "gm_first_asymmetric")
+    return pos.value
 
 
 # ---------------------------------------------------------------------------
