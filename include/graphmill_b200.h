@@ -37,7 +37,8 @@ typedef enum gm_status {
   GM_ERR_OUT_OF_RANGE = 2,     /* reference: std::out_of_range */
   GM_ERR_CUDA = 3,
   GM_ERR_UNSUPPORTED = 4,
-  GM_ERR_LOGIC = 5             /* reference: std::logic_error */
+  GM_ERR_LOGIC = 5,            /* reference: std::logic_error */
+  GM_ERR_RUNTIME = 6           /* reference: std::runtime_error (dataset IO) */
 } gm_status;
 
 typedef enum gm_dtype { GM_F32 = 0, GM_F64 = 1, GM_BF16 = 2 } gm_dtype;
@@ -285,6 +286,30 @@ GM_API gm_status gm_spmm_accumulate(const gm_csr* csr, const gm_spmm_plan* plan,
                                     const void* x, int64_t f, const void* edge_weight, gm_reduce reduce,
                                     const int32_t* mean_deg, void* out, int32_t* arg_out,
                                     gm_stream_t stream);
+
+/* ------------------------------------------------------------------------ */
+/* Dataset ingestion (L5): dataset_io.hpp:14-20 layout, load_dataset          */
+/* (dataset_io.cpp:295-341) — straight to the device                          */
+/* ------------------------------------------------------------------------ */
+
+/* Reads a whole file (e.g. node_<type>.f32.bin, *.time.i64.bin) into device
+ * memory dst. The file must hold exactly expected_bytes (else
+ * GM_ERR_RUNTIME "dataset: <path> holds X bytes, manifest requires Y", the
+ * reference's MappedFile check, dataset_io.cpp:107-119). staging: PINNED host
+ * buffer, used as two halves so file reads overlap the host->device copies.
+ * Synchronizes `stream` before returning. */
+GM_API gm_status gm_read_file_to_device(const char* path, int64_t expected_bytes, void* dst, void* staging,
+                                        size_t staging_bytes, gm_stream_t stream);
+
+/* Reads edge_<src>__<rel>__<dst>.u64.bin (edge_count interleaved little-endian
+ * (src, dst) u64 pairs) into device int64 src[edge_count], dst[edge_count]
+ * (dataset_io.cpp:317-326; bounds are then checked by EdgeIndex, as in the
+ * reference). workspace: DEVICE bytes >= gm_read_edge_pairs_workspace(staging_bytes).
+ * Synchronizes. */
+GM_API size_t gm_read_edge_pairs_workspace(size_t staging_bytes);
+GM_API gm_status gm_read_edge_pairs_to_device(const char* path, int64_t edge_count, int64_t* src, int64_t* dst,
+                                              void* staging, size_t staging_bytes, void* workspace,
+                                              size_t workspace_bytes, gm_stream_t stream);
 
 /* ------------------------------------------------------------------------ */
 /* Synthetic inputs (bench/test infrastructure; bit-identical host & device) */

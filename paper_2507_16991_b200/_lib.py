@@ -20,6 +20,7 @@ GM_ERR_OUT_OF_RANGE = 2
 GM_ERR_CUDA = 3
 GM_ERR_UNSUPPORTED = 4
 GM_ERR_LOGIC = 5
+GM_ERR_RUNTIME = 6
 
 GM_F32, GM_F64, GM_BF16 = 0, 1, 2
 GM_SUM, GM_MEAN, GM_MAX, GM_MIN = 0, 1, 2, 3
@@ -89,6 +90,9 @@ SIGNATURES = {
                                     _P, C.c_size_t, _P]),
     "gm_partition_rows_by_nnz": (C.c_int, [C.POINTER(C.c_int64), _I64, C.c_int32,
                                            C.POINTER(C.c_int64)]),
+    "gm_read_file_to_device": (C.c_int, [C.c_char_p, _I64, _P, _P, C.c_size_t, _P]),
+    "gm_read_edge_pairs_workspace": (C.c_size_t, [C.c_size_t]),
+    "gm_read_edge_pairs_to_device": (C.c_int, [C.c_char_p, _I64, _P, _P, _P, C.c_size_t, _P, C.c_size_t, _P]),
     "gm_synth_edges": (C.c_int, [C.c_int, _U64, _I64, _I64, _I64, _I64, _P, _P, _P]),
     "gm_synth_edges_host": (None, [C.c_int, _U64, _I64, _I64, _I64, _I64, _P, _P]),
     "gm_synth_features": (C.c_int, [_U64, _I64, _I64, _I64, C.c_int, C.c_int, _P, _P]),
@@ -139,4 +143,6 @@ def check(status: int, what: str = "") -> None:
         raise IndexError(msg)          # std::out_of_range
     if status == GM_ERR_INVALID_ARGUMENT:
         raise ValueError(msg)          # std::invalid_argument
+    if status == GM_ERR_RUNTIME:
+        raise RuntimeError(msg)        # std::runtime_error (dataset IO)
     raise GraphmillError(f"{what}: status {status}: {msg}")

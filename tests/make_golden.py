@@ -2,6 +2,7 @@
 
 Run in the container that has /root/reference:
     make -C oracle ref && python tests/make_golden.py
+    python tests/make_golden.py --dataset      (reference-written dataset dirs)
 
 Every expected output below is produced by the reference's own code
 (build_compressed, spmm, the max path + backward argpos, aggregate, the GCN
@@ -209,5 +210,20 @@ def main():
         print(f"{path}: {len(data)} arrays, {os.path.getsize(path) / 1024:.0f} KiB")
 
 
+def dataset_fixtures() -> None:
+    """tests/golden/dataset_{f32,f64}: written by the reference's OWN
+    save_dataset (oracle/ref_dataset_gen.cpp, `make -C oracle ref-dataset`)."""
+    import shutil
+    import subprocess
+    subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "ref-dataset"], check=True)
+    outs = [os.path.join(OUT, "dataset_f32"), os.path.join(OUT, "dataset_f64")]
+    for o in outs:
+        shutil.rmtree(o, ignore_errors=True)
+    subprocess.run([os.path.join(ROOT, "oracle", "_ref", "ref_dataset_gen"), *outs], check=True)
+
+
 if __name__ == "__main__":
-    main()
+    if "--dataset" in sys.argv:
+        dataset_fixtures()
+    else:
+        main()
