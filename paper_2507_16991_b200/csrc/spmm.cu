@@ -151,6 +151,8 @@ GM_API gm_status gm_spmm_plan_build(const gm_csr* csr, void* buffer, size_t buff
                  std::to_string(need) + ")");
   cudaStream_t st = as_stream(stream);
   const int64_t g = plan_num_windows(csr->num_rows, csr->nnz);
+  // a caller-set threshold (>= the default) selects fewer hub rows
+  const int64_t thr = std::max<int64_t>(heavy_threshold(), plan->heavy_threshold);
   const int64_t cap = plan_heavy_cap(csr->num_rows, csr->nnz);
   unsigned char* b = static_cast<unsigned char*>(buffer);
   int32_t* win_row = reinterpret_cast<int32_t*>(b);
@@ -177,7 +179,7 @@ GM_API gm_status gm_spmm_plan_build(const gm_csr* csr, void* buffer, size_t buff
   GM_TRY_CUDA(cudaMemsetAsync(count, 0, sizeof(unsigned int), st));
   if (csr->num_rows > 0) {
     plan_heavy_kernel<<<static_cast<unsigned>(ceil_div(csr->num_rows, 256)), 256, 0, st>>>(
-        csr->rowptr, csr->num_rows, heavy_threshold(), cap, keys, count);
+        csr->rowptr, csr->num_rows, thr, cap, keys, count);
     GM_CHECK_LAUNCH("plan_heavy_kernel");
   }
   unsigned int n_heavy = 0;
@@ -227,7 +229,7 @@ GM_API gm_status gm_spmm_plan_build(const gm_csr* csr, void* buffer, size_t buff
   plan->num_windows = g;
   plan->window_edges = kWindowCost;
   plan->num_heavy = nh;
-  plan->heavy_threshold = heavy_threshold();
+  plan->heavy_threshold = thr;
   plan->win_row = win_row;
   plan->heavy_rows = heavy_rows;
   plan->num_light_windows = static_cast<int64_t>(lw.size() / 2);
@@ -284,6 +286,12 @@ GM_API gm_status gm_spmm_plan_build(const gm_csr* csr, void* buffer, size_t buff
   return GM_OK;
 }
 
+// GM_NARROW_8B=0 keeps 16-byte vectors for 129..256-byte rows (comparison only).
+static bool narrow_rows_8b() {
+  static const bool on = [] { const char* e = getenv("GM_NARROW_8B"); return !e || atoi(e) != 0; }();
+  return on;
+}
+
 static gm_status spmm_impl(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype dtype,
                            const void* x, int64_t f, const void* edge_weight,
                            const gm_gcn_norm* gcn, gm_reduce reduce, void* out, int32_t* arg_out,
@@ -309,6 +317,9 @@ static gm_status spmm_impl(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype
   while (vb > static_cast<int>(esz) && (rowbytes % vb != 0 || align % vb != 0)) vb >>= 1;
   GM_REQUIRE(rowbytes % vb == 0 && align % vb == 0, GM_ERR_INVALID_ARGUMENT,
              "gm_spmm: x/out must be element-aligned");
+  // 129..256-byte rows (e.g. F=128 bf16, F=64 f32): 8-byte vectors put the row
+  // on all 32 lanes (the flat kernel then keeps 16 edges in flight per batch)
+  if (vb == 16 && rowbytes > 128 && rowbytes <= 256 && narrow_rows_8b()) vb = 8;
   const int64_t ns = static_cast<int64_t>(rowbytes / vb);
 
   SpmmArgs p{};

@@ -934,10 +934,20 @@ gm_status launch_flat(const SpmmArgs& p0, int64_t ns, cudaStream_t st) {
     } else if (p.mean) GM_FLAT_K(NV_, U_, 1);     \
     else GM_FLAT_K(NV_, U_, 0);                   \
   } while (0)
-    if (nv == 1) GM_FLAT(1, 8);
-    else if (nv == 2) GM_FLAT(2, 4);
-    else if (nv == 4 || kChunk <= 128) GM_FLAT(4, 2);
-    else if constexpr (kChunk > 128) GM_FLAT(8, 1);
+    // U x NV raw vectors = 32 registers of gathers in flight per lane
+    // (8-byte single-vector rows keep 16 edges in flight; deeper batches for
+    // multi-vector rows measured slower on Reddit-shaped F=602)
+    if constexpr (VB <= 8) {
+      if (nv == 1) GM_FLAT(1, 16);
+      else if (nv == 2) GM_FLAT(2, 4);
+      else if (nv == 4 || kChunk <= 128) GM_FLAT(4, 2);
+      else if constexpr (kChunk > 128) GM_FLAT(8, 1);
+    } else {
+      if (nv == 1) GM_FLAT(1, 8);
+      else if (nv == 2) GM_FLAT(2, 4);
+      else if (nv == 4 || kChunk <= 128) GM_FLAT(4, 2);
+      else if constexpr (kChunk > 128) GM_FLAT(8, 1);
+    }
 #undef GM_FLAT
 #undef GM_FLAT_K
 #undef GM_FLAT_H
@@ -1042,7 +1052,8 @@ inline bool hub_v1() {
 // whole row's columns at once.
 template <typename T, int VB, bool MAXMIN>
 gm_status launch_hubs(const SpmmArgs& p, int64_t num_heavy, int64_t ns, cudaStream_t st) {
-  if (hub_v1() || p.f * static_cast<int64_t>(sizeof(T)) >= kWideRowBytes)
+  static const bool wide_v1 = [] { const char* e = getenv("GM_HUB_WIDE_V1"); return !e || atoi(e) != 0; }();
+  if (hub_v1() || (wide_v1 && p.f * static_cast<int64_t>(sizeof(T)) >= kWideRowBytes))
     return launch_heavy<T, VB, MAXMIN>(p, num_heavy, ns, st);
   return launch_hub<T, VB, MAXMIN>(p, num_heavy, st);
 }

@@ -131,8 +131,6 @@ class BlockedSpmm:
         for b in range(nb):
             ncols = chunks * self.cs if b == 0 else world * self.cs
             self.blocks.append(CsrView(rp[b], self.col_b, self.perm_b, ncols, int(ends[b] - starts[b])))
-        for v in self.blocks:
-            v.plan()
         rr = rows.rowptr
         self.mean_deg = (rr[1:] - rr[:-1]).to(torch.int32)
         self._bufs = {}
@@ -170,7 +168,8 @@ class BlockedSpmm:
         first_kind = L.GM_SUM if reduce == "mean" else _KIND[reduce]
         v = self.blocks[0]
         cs = v.c_struct()
-        L.check(lib.gm_spmm(C.byref(cs), C.byref(v.plan()), dt, _p(x_shard), f, None, None, first_kind,
+        rb = f * x_shard.element_size()
+        L.check(lib.gm_spmm(C.byref(cs), C.byref(v.plan(rb)), dt, _p(x_shard), f, None, None, first_kind,
                             _p(out), _p(arg) if maxmin else None, _stream()), "gm_spmm (local block)")
         for c in range(self.chunks):
             works[c].wait()
@@ -178,7 +177,7 @@ class BlockedSpmm:
             last = c == self.chunks - 1
             kind = _KIND[reduce] if (last or reduce != "mean") else L.GM_SUM
             cs = v.c_struct()
-            L.check(lib.gm_spmm_accumulate(C.byref(cs), C.byref(v.plan()), dt, _p(bufs[c]), f, None, kind,
+            L.check(lib.gm_spmm_accumulate(C.byref(cs), C.byref(v.plan(rb)), dt, _p(bufs[c]), f, None, kind,
                                            _p(self.mean_deg) if kind == L.GM_MEAN else None, _p(out),
                                            _p(arg) if maxmin else None, _stream()), "gm_spmm_accumulate")
         return (out, arg) if maxmin else out

@@ -56,7 +56,7 @@ class CsrView:
     perm: torch.Tensor
     num_cols: int
     nnz: Optional[int] = None  # edges of these rows (set for row slices of a larger CSR)
-    _plan: Optional[tuple] = field(default=None, repr=False)
+    _plan: Optional[dict] = field(default=None, repr=False)
 
     def num_rows(self) -> int:
         return self.rowptr.numel() - 1
@@ -72,18 +72,24 @@ class CsrView:
         return L.gm_csr(self.num_rows(), self.num_cols, self.num_entries(),
                         self.rowptr.data_ptr(), self.col.data_ptr(), self.perm.data_ptr())
 
-    def plan(self):
-        """Scheduling metadata (gm_spmm_plan), built once and cached."""
+    def plan(self, row_bytes: int = 0):
+        """Scheduling metadata (gm_spmm_plan), built once per hub-threshold
+        class and cached: rows >= 1 KB wide (F=602 fp32) raise the hub
+        threshold to 4096 in-edges, narrower rows keep the default 1024."""
+        thr = 4096 if row_bytes >= 1024 else 0
         if self._plan is None:
+            self._plan = {}
+        if thr not in self._plan:
             lib = L.lib()
             nbytes = lib.gm_spmm_plan_bytes(self.num_rows(), self.num_cols, self.num_entries())
             buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=self.rowptr.device)
             plan = L.gm_spmm_plan()
+            plan.heavy_threshold = thr
             csr = self.c_struct()
             L.check(lib.gm_spmm_plan_build(C.byref(csr), _p(buf), nbytes, C.byref(plan), _stream()),
                     "gm_spmm_plan_build")
-            self._plan = (plan, buf)
-        return self._plan[0]
+            self._plan[thr] = (plan, buf)
+        return self._plan[thr][0]
 
     def to_host(self):
         """(rowptr, col, perm) as int64 CPU tensors, the reference's CsrView layout."""
@@ -330,7 +336,7 @@ def _run_spmm(grouping: CsrView, x: torch.Tensor, kind: str, w_csr: Optional[tor
     out = torch.empty((rows, f) if x.dim() == 2 else (rows,), dtype=x.dtype, device=x.device)
     arg = torch.empty((rows, f), dtype=torch.int32, device=x.device) if want_arg else None
     csr = grouping.c_struct()
-    plan = grouping.plan()
+    plan = grouping.plan(row_bytes=f * x.element_size())
     L.check(L.lib().gm_spmm(C.byref(csr), C.byref(plan), _DT[x.dtype], _p(x), f, _p(w_csr),
                             C.byref(gcn) if gcn is not None else None, _KIND[kind], _p(out), _p(arg),
                             _stream()), "gm_spmm")
