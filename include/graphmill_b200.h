@@ -193,7 +193,7 @@ GM_API gm_status gm_gcn_degrees(const int64_t* full_src, const int64_t* full_dst
  * gcn: NULL or fused GCN norm (exclusive with edge_weight).
  * reduce: SUM, MEAN (sum * (1/deg), deg = row length; message_passing.hpp:76-84),
  *   MAX/MIN (first element initialises, then strict >/<; empty rows 0).
- * arg_out: NULL or int32 [num_rows, f]: COO edge id (perm[k]) of the first
+ * arg_out: NULL or 16-byte aligned int32 [num_rows, f]: COO edge id (perm[k]) of the first
  *   attaining edge, -1 for empty rows (MAX/MIN only; the reference keeps this
  *   only inside its backward closure, aggregate.hpp:295-308). Requires perm.
  * Accumulation is fp32 for F32/BF16 (BF16 in, BF16 out, RNE) and fp64 for F64,

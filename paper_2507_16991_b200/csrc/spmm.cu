@@ -305,6 +305,8 @@ static gm_status spmm_impl(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype
   GM_REQUIRE(!arg_out || maxmin, GM_ERR_INVALID_ARGUMENT, "gm_spmm: arg_out needs max/min");
   GM_REQUIRE(!arg_out || csr->perm || csr->nnz == 0, GM_ERR_INVALID_ARGUMENT,
              "gm_spmm: arg_out needs csr->perm");
+  GM_REQUIRE(reinterpret_cast<uintptr_t>(arg_out) % 16 == 0, GM_ERR_INVALID_ARGUMENT,
+             "gm_spmm: arg_out must be 16-byte aligned");
   GM_REQUIRE(!gcn || (gcn->deg_src && gcn->deg_dst), GM_ERR_INVALID_ARGUMENT,
              "gm_spmm: gcn norm needs both degree arrays");
   if (csr->num_rows == 0 || f == 0) return GM_OK;

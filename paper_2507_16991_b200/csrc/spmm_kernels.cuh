@@ -110,10 +110,74 @@ __device__ __forceinline__ unsigned short ldg_hint<unsigned short>(const unsigne
   return r;
 }
 
+// Both policies as predicated loads (no branch per gather): hot ? evict_last : evict_first.
+template <typename R>
+__device__ __forceinline__ R ldg_hint2(const R* p, bool hot, uint64_t ph, uint64_t pc);
+template <>
+__device__ __forceinline__ uint4 ldg_hint2<uint4>(const uint4* p, bool hot, uint64_t ph, uint64_t pc) {
+  uint4 r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+      "@q ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %6;\n\t"
+      "@!q ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %7;\n\t}"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p), "r"(static_cast<int>(hot)), "l"(ph), "l"(pc));
+  return r;
+}
+template <>
+__device__ __forceinline__ uint2 ldg_hint2<uint2>(const uint2* p, bool hot, uint64_t ph, uint64_t pc) {
+  uint2 r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t"
+      "@q ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %4;\n\t"
+      "@!q ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %5;\n\t}"
+      : "=r"(r.x), "=r"(r.y)
+      : "l"(p), "r"(static_cast<int>(hot)), "l"(ph), "l"(pc));
+  return r;
+}
+template <>
+__device__ __forceinline__ uint32_t ldg_hint2<uint32_t>(const uint32_t* p, bool hot, uint64_t ph, uint64_t pc) {
+  uint32_t r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+      "@q ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %3;\n\t"
+      "@!q ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %4;\n\t}"
+      : "=r"(r)
+      : "l"(p), "r"(static_cast<int>(hot)), "l"(ph), "l"(pc));
+  return r;
+}
+template <>
+__device__ __forceinline__ unsigned short ldg_hint2<unsigned short>(const unsigned short* p, bool hot, uint64_t ph,
+                                                                    uint64_t pc) {
+  unsigned short r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+      "@q ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %3;\n\t"
+      "@!q ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %4;\n\t}"
+      : "=h"(r)
+      : "l"(p), "r"(static_cast<int>(hot)), "l"(ph), "l"(pc));
+  return r;
+}
+
 template <typename A>
 __device__ __forceinline__ A gcn_scale(int32_t ds, int32_t dd) {
   // message_passing.hpp:449-451: S(1) / std::sqrt(S(din[s]) * S(din[d]))
   return div_rn(A(1), sqrt_rn(mul_rn(static_cast<A>(ds), static_cast<A>(dd))));
+}
+
+#ifndef GM_ARG_VEC
+#define GM_ARG_VEC 1
+#endif
+// Argmax ids of one V-element vector: int4/int2 stores (arg_out is 16-byte
+// aligned and V divides F, so every vector's ids are 4V-byte aligned).
+template <int V>
+__device__ __forceinline__ void store_arg(int32_t* p, const int32_t* a) {
+  if constexpr (GM_ARG_VEC && V % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < V / 4; ++i)
+      reinterpret_cast<int4*>(p)[i] = make_int4(a[4 * i], a[4 * i + 1], a[4 * i + 2], a[4 * i + 3]);
+  } else if constexpr (GM_ARG_VEC && V == 2) {
+    *reinterpret_cast<int2*>(p) = make_int2(a[0], a[1]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < V; ++e) p[e] = a[e];
+  }
 }
 
 // Per-thread accumulator for NV vectors of V elements.
@@ -275,7 +339,7 @@ __global__ void __launch_bounds__(256) spmm_light_kernel(const SpmmArgs p) {
         if (want_arg) {
           int32_t* arow = p.arg + static_cast<int64_t>(r) * p.f + slot[j] * V;
 #pragma unroll
-          for (int e = 0; e < V; ++e) arow[e] = acc.a[j][e];
+          store_arg<V>(arow, acc.a[j]);
         }
       }
   }
@@ -374,7 +438,7 @@ __global__ void __launch_bounds__(256, (SCALED || sizeof(T) == 8) ? 3 : 4) spmm_
         if (want_arg) {
           int32_t* arow = p.arg + obase + soff[j];
 #pragma unroll
-          for (int e = 0; e < V; ++e) arow[e] = acc.a[j][e];
+          store_arg<V>(arow, acc.a[j]);
         }
       }
     ++row;
@@ -418,7 +482,15 @@ __global__ void __launch_bounds__(256, (SCALED || sizeof(T) == 8) ? 3 : 4) spmm_
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const T* xr = x + static_cast<uint64_t>(static_cast<uint32_t>(__shfl_sync(FULL, c_cur, u))) * fu;
-      if constexpr (HINT) {
+      if constexpr (HINT && !MAXMIN) {
+        // predicated policy pair: no branch per gather
+        const bool hot = (hmask >> u) & 1u;
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+          if (valid[j]) buf[u][j] = ldg_hint2<R>(reinterpret_cast<const R*>(xr + soff[j]), hot, pol_hot, pol_cold);
+      } else if constexpr (HINT) {
+        // (max/min keep a uniform branch: the predicated pair needs both 64-bit
+        // policies live, which spills at this kernel's 64-register budget)
         if ((hmask >> u) & 1u) {
 #pragma unroll
           for (int j = 0; j < NV; ++j)
@@ -650,7 +722,7 @@ __global__ void __launch_bounds__(kHeavyThreads) spmm_heavy_kernel(const SpmmArg
       if (want_arg) {
         int32_t* arow = p.arg + static_cast<int64_t>(r) * p.f + (p.slot_base + s) * V;
 #pragma unroll
-        for (int e = 0; e < V; ++e) arow[e] = acc.a[m][e];
+        store_arg<V>(arow, acc.a[m]);
       }
     }
   }
@@ -706,8 +778,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-template <typename T, int G, bool MAXMIN>
+template <typename T, int G, int MODE>  // MODE: 0 sum/mean, 2 max, 3 min
 __global__ void __launch_bounds__(64) spmm_hub_kernel(const SpmmArgs p) {
+  constexpr bool MAXMIN = MODE >= 2;
+  constexpr bool IS_MIN = MODE == 3;
   using HL = HubLane<T>;
   using A = typename AccOf<T>::type;
   constexpr int LE = HL::LE;
@@ -821,6 +895,57 @@ __global__ void __launch_bounds__(64) spmm_hub_kernel(const SpmmArgs p) {
     }
     first = MAXMIN ? a[0] == -1 : false;
   }
+  using RawL = typename HL::R;
+  // one edge into the running value(s); LEX: seeded blocks break ties on COO id
+  auto combine = [&](const RawL raw, const A sc, const int32_t pm, const bool is_first, auto lex_c) {
+    constexpr bool LEX = decltype(lex_c)::value;
+    T tmp[LE];
+    memcpy(tmp, &raw, LB);
+#pragma unroll
+    for (int j = 0; j < LE; ++j) {
+      const A val = scaled ? mul_rn(widen(tmp[j]), sc) : widen(tmp[j]);
+      if constexpr (!MAXMIN) {
+        v[j] = add_rn(v[j], val);
+      } else {
+        bool better = is_first || (IS_MIN ? (val < v[j]) : (val > v[j]));
+        if constexpr (LEX) better = better || (val == v[j] && static_cast<uint32_t>(pm) < static_cast<uint32_t>(a[j]));
+        v[j] = better ? val : v[j];
+        a[j] = better ? pm : a[j];
+      }
+    }
+  };
+  auto scale_of = [&](int ms, int e) -> A {
+    if (w) return mw[ms][e];
+    if (gcn) return gcn_scale<A>(mdeg[ms][e], dd);
+    return A(1);
+  };
+  // consume one stage: the row's first edge peeled, then batches of 16 edges
+  // whose shared-memory reads are all issued before the ordered combines
+  auto stage = [&](const unsigned char* dl, int ms, int n_e, auto lex_c) {
+    int e = 0;
+    if (first && n_e > 0) {
+      combine(*reinterpret_cast<const RawL*>(dl), scale_of(ms, 0), want_arg ? mperm[ms][0] : -1, true, lex_c);
+      first = false;
+      e = 1;
+    }
+    constexpr int B = 16;
+    for (; e + B <= n_e; e += B) {
+      RawL raw[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) raw[u] = *reinterpret_cast<const RawL*>(dl + (e + u) * CB);
+      A sc[B];
+      int32_t pm[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        sc[u] = scale_of(ms, e + u);
+        pm[u] = want_arg ? mperm[ms][e + u] : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < B; ++u) combine(raw[u], sc[u], pm[u], false, lex_c);
+    }
+    for (; e < n_e; ++e)
+      combine(*reinterpret_cast<const RawL*>(dl + e * CB), scale_of(ms, e), want_arg ? mperm[ms][e] : -1, false, lex_c);
+  };
   const bool lex = MAXMIN && p.accum;
 
 #pragma unroll 1
@@ -831,29 +956,8 @@ __global__ void __launch_bounds__(64) spmm_hub_kernel(const SpmmArgs p) {
     const unsigned char* di = hub_data + static_cast<size_t>(slot) * kHubStage * CB;
     const int n_e = stage_edges(i);
     if (lane_valid) {
-#pragma unroll 8
-      for (int e = 0; e < n_e; ++e) {
-        const typename HL::R raw = *reinterpret_cast<const typename HL::R*>(di + e * CB + lane * LB);
-        T tmp[LE];
-        memcpy(tmp, &raw, LB);
-        A sc = A(1);
-        if (w) sc = mw[ms][e];
-        else if (gcn) sc = gcn_scale<A>(mdeg[ms][e], dd);
-        const int32_t pm = want_arg ? mperm[ms][e] : -1;
-#pragma unroll
-        for (int j = 0; j < LE; ++j) {
-          const A val = scaled ? mul_rn(widen(tmp[j]), sc) : widen(tmp[j]);
-          if (!MAXMIN) {
-            v[j] = add_rn(v[j], val);
-          } else {
-            const bool better = first || (p.is_min ? (val < v[j]) : (val > v[j])) ||
-                                (lex && val == v[j] && static_cast<uint32_t>(pm) < static_cast<uint32_t>(a[j]));
-            v[j] = better ? val : v[j];
-            a[j] = better ? pm : a[j];
-          }
-        }
-        first = false;
-      }
+      if (lex) stage(di + lane * LB, ms, n_e, std::true_type{});
+      else stage(di + lane * LB, ms, n_e, std::false_type{});
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);
@@ -1034,7 +1138,9 @@ gm_status launch_hub(const SpmmArgs& p, int64_t num_heavy, cudaStream_t st) {
     const int64_t row_bytes = p.f * static_cast<int64_t>(sizeof(T));
     const unsigned grid = static_cast<unsigned>(ceil_div(row_bytes, CB) * num_heavy);
     // TMA bulk copies need 16-byte aligned rows (VB == 16: x and the row pitch)
-    auto kern = spmm_hub_kernel<T, (VB > 16 ? 16 : VB), MAXMIN>;
+    auto kern = !MAXMIN ? spmm_hub_kernel<T, (VB > 16 ? 16 : VB), 0>
+                : p.is_min ? spmm_hub_kernel<T, (VB > 16 ? 16 : VB), 3>
+                           : spmm_hub_kernel<T, (VB > 16 ? 16 : VB), 2>;
     gm_status s_ = ensure_smem(kern, hub_smem_bytes<T>());
     if (s_ != GM_OK) return s_;
     kern<<<grid, 64, hub_smem_bytes<T>(), st>>>(p);
