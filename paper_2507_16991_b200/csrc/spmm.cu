@@ -353,7 +353,9 @@ static gm_status spmm_impl(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype
   p.src_class = nullptr;
   p.hot_class_limit = 0;
   // X much larger than L2 streams: every gather carries an eviction policy
-  p.stream_x = static_cast<double>(csr->num_cols) * static_cast<double>(rowbytes) > 64.0 * (1 << 20);
+  static const int stream_env = [] { const char* e = getenv("GM_STREAM_X"); return e ? atoi(e) : -1; }();
+  p.stream_x = stream_env >= 0 ? stream_env
+                               : static_cast<double>(csr->num_cols) * static_cast<double>(rowbytes) > 64.0 * (1 << 20);
   if (plan->src_class && plan->l2_hot_bytes > 0) {
     // rows that fit the budget: rank < hot_rows  <=>  class < floor(4*log2(1 + hot_rows))
     const double hot_rows = static_cast<double>(plan->l2_hot_bytes) / static_cast<double>(rowbytes);
