@@ -305,6 +305,7 @@ class _CacheSlot:
         self.csr_builds = 0
         self.csc_builds = 0
         self.exact: Optional[CsrView] = None
+        self.gcn_deg: dict = {}
 
 
 def _first_asymmetric(src: torch.Tensor, dst: torch.Tensor, n: int) -> int:
@@ -425,13 +426,20 @@ def neighbor_aggregate(e: EdgeIndex, x: torch.Tensor, kind: str,
 
 
 def gcn_degrees(e: EdgeIndex, square: bool):
-    """Effective degrees of gcn_norm (message_passing.hpp:437-463) from the FULL arrays."""
+    """Effective degrees of gcn_norm (message_passing.hpp:437-463) from the FULL arrays,
+    computed once per index (they depend only on the immutable COO arrays) and
+    cached beside its CSR/CSC, like the reference caches its compressed views."""
+    key = (bool(square), e.num_src_nodes(), e.num_dst_nodes())
+    hit = e._cache.gcn_deg.get(key)
+    if hit is not None:
+        return hit
     dev = e.full_dst().device
     d_dst = torch.empty(e.num_dst_nodes(), dtype=torch.int32, device=dev)
     d_src = d_dst if square else torch.empty(e.num_src_nodes(), dtype=torch.int32, device=dev)
     L.check(L.lib().gm_gcn_degrees(_p(e.full_src()), _p(e.full_dst()), e.full_dst().numel(),
                                    e.num_src_nodes(), e.num_dst_nodes(), int(square), _p(d_src),
                                    _p(d_dst), _stream()), "gcn_degrees")
+    e._cache.gcn_deg[key] = (d_src, d_dst)
     return d_src, d_dst
 
 

@@ -97,8 +97,20 @@ def cora():
         return z @ wh + bh
 
     ms = timed(fwd, reps=50)
-    r = {"config": "C1 cora 2-layer GCN forward", "ms": ms, "nodes": n, "edges": e, "feats": 1433,
-         "note": "launch-bound (2 transforms + 2 fused GCN SpMMs + head); parity config"}
+    # the same forward captured once into a CUDA graph and replayed (launch-bound config)
+    for _ in range(3):
+        fwd()
+    torch.cuda.synchronize()
+    cg = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(cg):
+        static_out = fwd()
+    ref = fwd()
+    cg.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(static_out, ref), "graph replay differs from eager"
+    gms = timed(cg.replay, reps=200)
+    r = {"config": "C1 cora 2-layer GCN forward", "ms": ms, "graph_replay_ms": gms, "nodes": n, "edges": e,
+         "feats": 1433, "note": "launch-bound (2 transforms + 2 fused GCN SpMMs + head); parity config"}
     print(json.dumps(r), flush=True)
 
 
