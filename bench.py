@@ -429,8 +429,28 @@ def main():
         torch.cuda.synchronize()
         t = torch.tensor([a.elapsed_time(bev) / 5], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        secondary = {"exact_mode_spmm": {"ms": float(t.item()), "gedges_s": N_EDGES / float(t.item()) / 1e6,
+        exact_ms = float(t.item())
+        # halo-only exchange: one all_to_all of the referenced remote rows
+        from paper_2507_16991_b200.dist import HaloSpmm, exchange_need_lists, halo_need
+        need = halo_need(local_csr, N_NODES, rank, world)
+        halo = HaloSpmm(local_csr, N_NODES, rank, world, need, exchange_need_lists(need))
+        xs = x_shard[: sh.shard_rows]
+        for _ in range(2):
+            halo(xs, "sum", out=out_local)
+        torch.cuda.synchronize()
+        dist.barrier()
+        a.record()
+        for _ in range(5):
+            halo(xs, "sum", out=out_local)
+        bev.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(bev) / 5, float(halo.halo_rows())], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        secondary = {"exact_mode_spmm": {"ms": exact_ms, "gedges_s": N_EDGES / exact_ms / 1e6,
                                          "numerics": "bit-identical to 1 GPU"},
+                     "halo_mode_spmm": {"ms": float(t[0]), "gedges_s": N_EDGES / float(t[0]) / 1e6,
+                                        "max_halo_rows": int(t[1]), "halo_frac_of_remote_rows":
+                                        float(t[1]) / (N_NODES - sh.shard_rows)},
                      "overlap_mode_numerics": "sum continued across 1+CHUNKS source blocks (fp32 tolerance)",
                      "block_nnz": blocked.block_nnz(),
                      "segment_matmul_C3": bench_segment_matmul(gm, L, device, rank=rank, world=world, dist=dist),

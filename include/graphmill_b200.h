@@ -274,6 +274,13 @@ GM_API gm_status gm_csr_split_blocks(const gm_csr* csr, const int32_t* src_block
                                      int32_t* perm_out, void* workspace, size_t workspace_bytes,
                                      gm_stream_t stream);
 
+/* Halo exchange helpers (SURVEY.md §8e "halo-only variant"): mark[c] = 1 for
+ * every column c referenced by the CSR's rows (num_cols bytes, zeroed first);
+ * out[i] = x[idx[i]] row gather (the per-peer send pack, f elements of dtype). */
+GM_API gm_status gm_mark_columns(const gm_csr* csr, uint8_t* mark, gm_stream_t stream);
+GM_API gm_status gm_gather_rows(gm_dtype dtype, const void* x, int64_t f, const int32_t* idx, int64_t n, void* out,
+                                gm_stream_t stream);
+
 /* Continue an aggregation over another block of the same destination rows
  * (gm_csr_split_blocks): every row starts from the current out (and, for
  * MAX/MIN, arg_out) contents and accumulates this block's entries in

@@ -80,6 +80,8 @@ SIGNATURES = {
                           C.POINTER(gm_gcn_norm), C.c_int, _P, _P, _P]),
     "gm_spmm_accumulate": (C.c_int, [C.POINTER(gm_csr), C.POINTER(gm_spmm_plan), C.c_int, _P, _I64, _P,
                                      C.c_int, _P, _P, _P, _P]),
+    "gm_mark_columns": (C.c_int, [C.POINTER(gm_csr), _P, _P]),
+    "gm_gather_rows": (C.c_int, [C.c_int, _P, _I64, _P, _I64, _P, _P]),
     "gm_csr_split_blocks_workspace": (C.c_size_t, [_I64, C.c_int32]),
     "gm_csr_split_blocks": (C.c_int, [C.POINTER(gm_csr), _P, _P, C.c_int32, _P, _P, _P, _P, C.c_size_t, _P]),
     "gm_scale_rows_div": (C.c_int, [C.c_int, _P, _I64, _I64, _P, _P, _P]),

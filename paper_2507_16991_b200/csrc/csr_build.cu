@@ -480,6 +480,32 @@ static size_t asym_cub_bytes(int64_t len) {
   return tmp;
 }
 
+__global__ void mark_columns_kernel(const int64_t* __restrict__ rowptr, int64_t rows, const int32_t* __restrict__ col,
+                                    uint8_t* __restrict__ mark) {
+  const int64_t k0 = rowptr[0], k1 = rowptr[rows];
+  for (int64_t k = k0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < k1;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    mark[col[k]] = 1;
+}
+
+template <int B>
+__global__ void gather_rows_kernel(const unsigned char* __restrict__ x, int64_t row_bytes, const int32_t* __restrict__ idx,
+                                   int64_t n, unsigned char* __restrict__ out) {
+  // one warp per output row, B-byte vectors
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
+    const unsigned char* src = x + static_cast<int64_t>(idx[i]) * row_bytes;
+    unsigned char* dst = out + i * row_bytes;
+    for (int64_t b = static_cast<int64_t>(lane) * B; b < row_bytes; b += 32 * B) {
+      if constexpr (B == 16) *reinterpret_cast<uint4*>(dst + b) = __ldg(reinterpret_cast<const uint4*>(src + b));
+      else if constexpr (B == 8) *reinterpret_cast<uint2*>(dst + b) = __ldg(reinterpret_cast<const uint2*>(src + b));
+      else if constexpr (B == 4) *reinterpret_cast<uint32_t*>(dst + b) = __ldg(reinterpret_cast<const uint32_t*>(src + b));
+      else *reinterpret_cast<uint16_t*>(dst + b) = __ldg(reinterpret_cast<const uint16_t*>(src + b));
+    }
+  }
+}
+
 struct SplitWs {
   int32_t* cnt;
   int64_t* partial;
@@ -546,6 +572,36 @@ GM_API gm_status gm_first_asymmetric(const int64_t* src, const int64_t* dst, int
   GM_TRY_CUDA(cudaMemcpyAsync(&pos, first, sizeof(pos), cudaMemcpyDeviceToHost, st));
   GM_TRY_CUDA(cudaStreamSynchronize(st));
   if (pos != ~0ull) *pos_host = static_cast<int64_t>(pos);
+  return GM_OK;
+}
+
+GM_API gm_status gm_mark_columns(const gm_csr* csr, uint8_t* mark, gm_stream_t stream) {
+  GM_REQUIRE(csr && mark, GM_ERR_INVALID_ARGUMENT, "gm_mark_columns: null argument");
+  cudaStream_t st = as_stream(stream);
+  GM_TRY_CUDA(cudaMemsetAsync(mark, 0, static_cast<size_t>(csr->num_cols), st));
+  if (csr->num_rows == 0 || csr->nnz == 0) return GM_OK;
+  mark_columns_kernel<<<grid_for(csr->nnz), 256, 0, st>>>(csr->rowptr, csr->num_rows, csr->col, mark);
+  GM_CHECK_LAUNCH("mark_columns_kernel");
+  return GM_OK;
+}
+
+GM_API gm_status gm_gather_rows(gm_dtype dtype, const void* x, int64_t f, const int32_t* idx, int64_t n, void* out,
+                                gm_stream_t stream) {
+  GM_REQUIRE(f >= 0 && n >= 0, GM_ERR_INVALID_ARGUMENT, "gm_gather_rows: negative size");
+  if (n == 0 || f == 0) return GM_OK;
+  GM_REQUIRE(x && idx && out, GM_ERR_INVALID_ARGUMENT, "gm_gather_rows: null pointer");
+  const int64_t esz = dtype == GM_F64 ? 8 : dtype == GM_F32 ? 4 : 2;
+  const int64_t rb = f * esz;
+  const uintptr_t al = reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(out) | static_cast<uintptr_t>(rb);
+  cudaStream_t st = as_stream(stream);
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(ceil_div(n, 8), kNumSMs * 32));
+  const auto* xb = static_cast<const unsigned char*>(x);
+  auto* ob = static_cast<unsigned char*>(out);
+  if (al % 16 == 0) gather_rows_kernel<16><<<grid, 256, 0, st>>>(xb, rb, idx, n, ob);
+  else if (al % 8 == 0) gather_rows_kernel<8><<<grid, 256, 0, st>>>(xb, rb, idx, n, ob);
+  else if (al % 4 == 0) gather_rows_kernel<4><<<grid, 256, 0, st>>>(xb, rb, idx, n, ob);
+  else gather_rows_kernel<2><<<grid, 256, 0, st>>>(xb, rb, idx, n, ob);
+  GM_CHECK_LAUNCH("gather_rows_kernel");
   return GM_OK;
 }
 

@@ -181,3 +181,147 @@ class BlockedSpmm:
                                            _p(self.mean_deg) if kind == L.GM_MEAN else None, _p(out),
                                            _p(arg) if maxmin else None, _stream()), "gm_spmm_accumulate")
         return (out, arg) if maxmin else out
+
+
+# ---------------------------------------------------------------------------
+# Halo-only exchange (SURVEY.md §8e "halo-only variant"): a rank receives only
+# the source rows its destination rows actually reference, per peer, with one
+# all_to_all_single per step instead of all-gathering every shard. The
+# own-shard block aggregates while the exchange is in flight; the halo block
+# (sources remapped into the receive buffer) continues the rows afterwards.
+# ---------------------------------------------------------------------------
+def halo_need(rows, num_src_rows: int, rank: int, world: int):
+    """Per peer q: the ascending rows (indices inside q's X shard) that this
+    rank's destination rows reference (own shard: empty). Device int32."""
+    from .graphmill import _p, _stream
+    s_rows = -(-num_src_rows // world)
+    mark = torch.empty(num_src_rows, dtype=torch.uint8, device=rows.rowptr.device)
+    cs = rows.c_struct()
+    L.check(L.lib().gm_mark_columns(C.byref(cs), _p(mark), _stream()), "gm_mark_columns")
+    ids = torch.nonzero(mark, as_tuple=True)[0]
+    need = []
+    for q in range(world):
+        if q == rank:
+            need.append(torch.empty(0, dtype=torch.int32, device=mark.device))
+            continue
+        sel = ids[(ids >= q * s_rows) & (ids < (q + 1) * s_rows)]
+        need.append((sel - q * s_rows).to(torch.int32))
+    return need
+
+
+def exchange_need_lists(need, group=None):
+    """all_to_all of the need lists: returns send[q] = the rows of MY shard
+    that rank q needs (what I pack for q every step)."""
+    world = len(need)
+    dev = need[0].device
+    counts = torch.tensor([t.numel() for t in need], dtype=torch.int64, device=dev)
+    peer_counts = torch.empty_like(counts)
+    dist.all_to_all_single(peer_counts, counts, group=group)
+    pc = peer_counts.cpu().tolist()
+    out = torch.empty(sum(pc), dtype=torch.int32, device=dev)
+    dist.all_to_all_single(out, torch.cat(need) if need else out, output_split_sizes=pc,
+                           input_split_sizes=[t.numel() for t in need], group=group)
+    return list(torch.split(out, pc))
+
+
+def halo_blocks(need, num_src_rows: int, rank: int, world: int, device=None):
+    """(block, column) per source id for the halo layout: own shard -> block 0
+    at its shard row; a needed row of peer q -> block 1 at its position in the
+    receive buffer (peers in rank order, each peer's rows ascending)."""
+    s_rows = -(-num_src_rows // world)
+    blk = torch.full((num_src_rows,), 1, dtype=torch.int32, device=device)
+    col = torch.zeros(num_src_rows, dtype=torch.int32, device=device)
+    lo, hi = rank * s_rows, min((rank + 1) * s_rows, num_src_rows)
+    blk[lo:hi] = 0
+    col[lo:hi] = torch.arange(hi - lo, dtype=torch.int32, device=device)
+    off = 0
+    for q in range(world):
+        n = need[q].numel()
+        if q != rank and n:
+            col[q * s_rows + need[q].long()] = torch.arange(off, off + n, dtype=torch.int32, device=device)
+        off += n
+    return blk, col
+
+
+class HaloSpmm:
+    """One rank's halo-exchange SpMM: block 0 (own shard) runs while the
+    all_to_all of the packed halo rows is in flight; block 1 (the halo rows)
+    continues every row with gm_spmm_accumulate. Numerics as BlockedSpmm
+    (max/min + argmax exact, sum continued across one block boundary).
+
+    need: halo_need(...) of this rank; send: exchange_need_lists(need) (rows of
+    my shard each peer needs). alltoall(recv, send, recv_splits, send_splits)
+    -> work (default: async NCCL all_to_all_single)."""
+
+    def __init__(self, rows, num_src_rows: int, rank: int, world: int, need, send, alltoall=None, group=None):
+        from .graphmill import CsrView, _p, _stream
+        self.rank, self.world = rank, world
+        self.s_rows = -(-num_src_rows // world)
+        self.recv_splits = [int(t.numel()) for t in need]
+        self.send_splits = [int(t.numel()) for t in send]
+        self.send_idx = torch.cat(send) if send else torch.empty(0, dtype=torch.int32)
+        self.alltoall = alltoall or (lambda r, s, rs, ss: dist.all_to_all_single(
+            r, s, output_split_sizes=rs, input_split_sizes=ss, group=group, async_op=True))
+        dev = rows.rowptr.device
+        blk, colmap = halo_blocks(need, num_src_rows, rank, world, dev)
+        n, nnz = rows.num_rows(), rows.num_entries()
+        lib = L.lib()
+        self.rowptr_b = torch.empty(2 * (n + 1), dtype=torch.int64, device=dev)
+        self.col_b = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+        self.perm_b = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+        wsb = lib.gm_csr_split_blocks_workspace(n, 2)
+        ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+        cs = rows.c_struct()
+        L.check(lib.gm_csr_split_blocks(C.byref(cs), _p(blk), _p(colmap), 2, _p(self.rowptr_b), _p(self.col_b),
+                                        _p(self.perm_b), _p(ws), wsb, _stream()), "gm_csr_split_blocks")
+        rp = self.rowptr_b.view(2, n + 1)
+        ends, starts = rp[:, n].cpu().tolist(), rp[:, 0].cpu().tolist()
+        halo_rows = sum(self.recv_splits)
+        self.blocks = [CsrView(rp[0], self.col_b, self.perm_b, self.s_rows, int(ends[0] - starts[0])),
+                       CsrView(rp[1], self.col_b, self.perm_b, max(halo_rows, 1), int(ends[1] - starts[1]))]
+        rr = rows.rowptr
+        self.mean_deg = (rr[1:] - rr[:-1]).to(torch.int32)
+        self._bufs = {}
+
+    def halo_rows(self) -> int:
+        return sum(self.recv_splits)
+
+    def __call__(self, x_shard: torch.Tensor, reduce: str = "sum", out: Optional[torch.Tensor] = None,
+                 arg: Optional[torch.Tensor] = None):
+        from .graphmill import _DT, _KIND, _p, _stream
+        x_shard = x_shard.contiguous()
+        f = x_shard.shape[1]
+        n = self.blocks[0].num_rows()
+        maxmin = reduce in ("max", "min")
+        if x_shard.dtype == torch.bfloat16 and not maxmin:
+            raise ValueError("HaloSpmm: bf16 sum/mean rounds between blocks; use exact mode")
+        if out is None:
+            out = torch.empty(n, f, dtype=x_shard.dtype, device=x_shard.device)
+        if maxmin and arg is None:
+            arg = torch.empty(n, f, dtype=torch.int32, device=x_shard.device)
+        key = (f, x_shard.dtype)
+        if key not in self._bufs:
+            self._bufs[key] = (torch.empty(max(self.send_idx.numel(), 1), f, dtype=x_shard.dtype, device=x_shard.device),
+                               torch.empty(max(self.halo_rows(), 1), f, dtype=x_shard.dtype, device=x_shard.device))
+        send_buf, recv_buf = self._bufs[key]
+        lib = L.lib()
+        dt = _DT[x_shard.dtype]
+        # pack what every peer needs from my shard, then exchange
+        L.check(lib.gm_gather_rows(dt, _p(x_shard), f, _p(self.send_idx), self.send_idx.numel(), _p(send_buf),
+                                   _stream()), "gm_gather_rows")
+        work = self.alltoall(recv_buf[: self.halo_rows()], send_buf[: self.send_idx.numel()], self.recv_splits,
+                             self.send_splits) or _Done()
+        rb = f * x_shard.element_size()
+        v = self.blocks[0]
+        cs = v.c_struct()
+        first_kind = L.GM_SUM if reduce == "mean" else _KIND[reduce]
+        L.check(lib.gm_spmm(C.byref(cs), C.byref(v.plan(rb)), dt, _p(x_shard), f, None, None, first_kind,
+                            _p(out), _p(arg) if maxmin else None, _stream()), "gm_spmm (own shard)")
+        work.wait()
+        v = self.blocks[1]
+        cs = v.c_struct()
+        kind = _KIND[reduce]
+        L.check(lib.gm_spmm_accumulate(C.byref(cs), C.byref(v.plan(rb)), dt, _p(recv_buf), f, None, kind,
+                                       _p(self.mean_deg) if kind == L.GM_MEAN else None, _p(out),
+                                       _p(arg) if maxmin else None, _stream()), "gm_spmm_accumulate (halo)")
+        return (out, arg) if maxmin else out

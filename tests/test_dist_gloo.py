@@ -134,3 +134,54 @@ def test_chunked_exchange_addresses_every_source(world, chunks):
         p.join(timeout=60)
         assert p.exitcode == 0
     assert all(ok for _, ok in res)
+
+
+def _halo_worker(rank, world, port, n, f, q):
+    """Halo protocol on gloo: need lists exchanged with all_to_all, rows packed
+    per peer (index_select stands in for gm_gather_rows on CPU) and exchanged
+    with all_to_all_single; every referenced remote source must land at the
+    column halo_blocks assigns it."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2507_16991_b200.dist import exchange_need_lists, halo_blocks
+        rng = np.random.default_rng(100 + rank)
+        s_rows = -(-n // world)
+        refd = np.unique(rng.integers(0, n, 700))
+        need = []
+        for p in range(world):
+            sel = refd[(refd >= p * s_rows) & (refd < min((p + 1) * s_rows, n))] - p * s_rows
+            need.append(torch.from_numpy(sel.astype(np.int32)) if p != rank else torch.empty(0, dtype=torch.int32))
+        send = exchange_need_lists(need)
+        x = torch.arange(n * f, dtype=torch.float32).view(n, f)
+        lo, hi = rank * s_rows, min((rank + 1) * s_rows, n)
+        shard = x[lo:hi]
+        packed = torch.cat([shard[s.long()] for s in send]) if sum(s.numel() for s in send) else torch.empty(0, f)
+        recv = torch.empty(sum(t.numel() for t in need), f)
+        dist.all_to_all_single(recv, packed, output_split_sizes=[t.numel() for t in need],
+                               input_split_sizes=[s.numel() for s in send])
+        blk, col = halo_blocks(need, n, rank, world)
+        ok = True
+        for s in refd.tolist():
+            b, c = int(blk[s]), int(col[s])
+            row = shard[c] if b == 0 else recv[c]
+            ok &= bool(torch.equal(row, x[s]))
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_halo_protocol_addresses_every_referenced_source(world):
+    n, f = 3001, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_halo_worker, args=(r, world, port, n, f, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok in res)

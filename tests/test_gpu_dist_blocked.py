@@ -151,3 +151,84 @@ def test_blocked_rejects_bf16_sum():
         ranks[0][2](shards[0], "sum")
     out, arg = ranks[0][2](shards[0], "max")   # max is exact in any dtype
     torch.cuda.synchronize()
+
+
+# ---------------------------------------------------------------------------
+# halo-only exchange (HaloSpmm) over virtual ranks
+# ---------------------------------------------------------------------------
+from paper_2507_16991_b200.dist import HaloSpmm, halo_need  # noqa: E402
+
+
+def _halo_setup(n, e, f, world, dtype=torch.float32):
+    src, dst, x = _graph(n, e, f)
+    g = gm.EdgeIndex(torch.from_numpy(src).cuda(), torch.from_numpy(dst).cuda(), n, n)
+    csc = g.to_csc()
+    rp = csc.rowptr.cpu().numpy()
+    cuts = partition_rows_by_nnz(rp, world)
+    s_rows = -(-n // world)
+    xt = torch.from_numpy(x).cuda().to(dtype)
+    shards = []
+    for q in range(world):
+        sh = torch.zeros(s_rows, f, dtype=dtype, device="cuda")
+        lo, hi = q * s_rows, min((q + 1) * s_rows, n)
+        sh[: hi - lo].copy_(xt[lo:hi])
+        shards.append(sh)
+    views, needs = [], []
+    for r in range(world):
+        r0, r1 = int(cuts[r]), int(cuts[r + 1])
+        v = csc.row_slice(r0, r1, int(rp[r1] - rp[r0]))
+        views.append((r0, r1, v))
+        needs.append(halo_need(v, n, r, world))
+    ranks = []
+    for r in range(world):
+        send = [needs[q][r] for q in range(world)]  # what q needs from me
+
+        def a2a(recv, sendbuf, rs, ss, r=r):
+            # what all_to_all_single delivers: from each peer q its pack for me
+            parts = [shards[q][needs[r][q].long()] for q in range(world)]
+            recv.copy_(torch.cat(parts))
+            return None
+        r0, r1, v = views[r]
+        ranks.append((r0, r1, HaloSpmm(v, n, r, world, needs[r], send, alltoall=a2a)))
+    return src, dst, x, shards, needs, ranks
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("kind", ["max", "sum", "mean"])
+def test_halo_exchange_matches_oracle(world, kind):
+    n, e, f = 20000, 1_200_000, 33
+    src, dst, x, shards, needs, ranks = _halo_setup(n, e, f, world)
+    orc = Oracle()
+    rpo, colo, permo = orc.build_compressed(dst, src, n)
+    if kind == "max":
+        want, warg = orc.spmm_max(rpo, colo, permo, x)
+    else:
+        ref = orc.spmm(rpo, colo, permo, x.astype(np.float64), mean=kind == "mean")
+        scale = orc.spmm(rpo, colo, permo, np.abs(x).astype(np.float64), mean=kind == "mean")
+    for i, (r0, r1, hs) in enumerate(ranks):
+        # the halo is exactly the referenced remote rows
+        s_rows = -(-n // world)
+        refd = np.unique(src[(dst >= r0) & (dst < r1)])
+        remote = refd[(refd < i * s_rows) | (refd >= (i + 1) * s_rows)]
+        assert hs.halo_rows() == remote.size
+        res = hs(shards[i], kind)
+        torch.cuda.synchronize()
+        if kind == "max":
+            out, arg = res
+            assert out.cpu().numpy().tobytes() == want[r0:r1].tobytes()
+            assert np.array_equal(arg.cpu().numpy().astype(np.int64), warg[r0:r1])
+        else:
+            err = np.abs(res.cpu().numpy().astype(np.float64) - ref[r0:r1])
+            assert np.all(err <= 1e-5 * scale[r0:r1] + 1e-6), float(err.max())
+
+
+def test_gather_rows_pack():
+    lib = L.lib()
+    for dtype, code, f in ((torch.float32, L.GM_F32, 33), (torch.bfloat16, L.GM_BF16, 128), (torch.float64, L.GM_F64, 5)):
+        x = torch.randn(5000, f, device="cuda").to(dtype)
+        idx = torch.randint(0, 5000, (3001,), device="cuda", dtype=torch.int32)
+        out = torch.empty(3001, f, dtype=dtype, device="cuda")
+        L.check(lib.gm_gather_rows(code, x.data_ptr(), f, idx.data_ptr(), 3001, out.data_ptr(),
+                                   torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        assert torch.equal(out, x[idx.long()])
