@@ -415,7 +415,8 @@ def main():
                "serial_value": N_EDGES / (sms * 1e-3) / 1e9, "serial_ms_per_step": sms}
 
     secondary = None
-    if world > 1 and not args.no_secondary:
+
+    def multi_gpu_secondary():
         # exact mode: one all-gather, then one bit-identical gm_spmm per rank
         for _ in range(2):
             step_exact()
@@ -446,7 +447,7 @@ def main():
         torch.cuda.synchronize()
         t = torch.tensor([a.elapsed_time(bev) / 5, float(halo.halo_rows())], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        secondary = {"exact_mode_spmm": {"ms": exact_ms, "gedges_s": N_EDGES / exact_ms / 1e6,
+        return {"exact_mode_spmm": {"ms": exact_ms, "gedges_s": N_EDGES / exact_ms / 1e6,
                                          "numerics": "bit-identical to 1 GPU"},
                      "halo_mode_spmm": {"ms": float(t[0]), "gedges_s": N_EDGES / float(t[0]) / 1e6,
                                         "max_halo_rows": int(t[1]), "halo_frac_of_remote_rows":
@@ -456,6 +457,11 @@ def main():
                      "segment_matmul_C3": bench_segment_matmul(gm, L, device, rank=rank, world=world, dist=dist),
                      "segment_matmul_F1024": bench_segment_matmul(gm, L, device, f=1024, rows=500_000, rank=rank,
                                                                   world=world, dist=dist)}
+    if world > 1 and not args.no_secondary:
+        try:  # reported, never substituted for the headline
+            secondary = multi_gpu_secondary()
+        except Exception as exc:  # noqa: BLE001
+            secondary = {"error": str(exc)[:300]}
     if world == 1 and not args.no_secondary:
         secondary = {"segment_matmul_C3": bench_segment_matmul(gm, L, device),
                      "segment_matmul_F1024": bench_segment_matmul(gm, L, device, f=1024, rows=500_000)}
