@@ -110,6 +110,79 @@ __device__ __forceinline__ unsigned short ldg_hint<unsigned short>(const unsigne
   return r;
 }
 
+// Streaming gather: ld.global.cs.nc = LDG.E.EF (L2 evict-first) with no
+// cache-policy descriptor, so it costs no uniform-register traffic.
+template <typename R>
+__device__ __forceinline__ R ldg_cs(const R* p);
+template <>
+__device__ __forceinline__ uint4 ldg_cs<uint4>(const uint4* p) {
+  uint4 r;
+  asm("ld.global.cs.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+template <>
+__device__ __forceinline__ uint2 ldg_cs<uint2>(const uint2* p) {
+  uint2 r;
+  asm("ld.global.cs.nc.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  return r;
+}
+template <>
+__device__ __forceinline__ uint32_t ldg_cs<uint32_t>(const uint32_t* p) {
+  uint32_t r;
+  asm("ld.global.cs.nc.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+template <>
+__device__ __forceinline__ unsigned short ldg_cs<unsigned short>(const unsigned short* p) {
+  unsigned short r;
+  asm("ld.global.cs.nc.u16 %0, [%1];" : "=h"(r) : "l"(p));
+  return r;
+}
+// hot ? (evict_last policy) : (evict-first streaming), as a predicated pair: one
+// policy descriptor, no branch per gather.
+template <typename R>
+__device__ __forceinline__ R ldg_hot_cs(const R* p, bool hot, uint64_t ph);
+template <>
+__device__ __forceinline__ uint4 ldg_hot_cs<uint4>(const uint4* p, bool hot, uint64_t ph) {
+  uint4 r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+      "@q ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %6;\n\t"
+      "@!q ld.global.cs.nc.v4.u32 {%0,%1,%2,%3}, [%4];\n\t}"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p), "r"(static_cast<int>(hot)), "l"(ph));
+  return r;
+}
+template <>
+__device__ __forceinline__ uint2 ldg_hot_cs<uint2>(const uint2* p, bool hot, uint64_t ph) {
+  uint2 r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t"
+      "@q ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %4;\n\t"
+      "@!q ld.global.cs.nc.v2.u32 {%0,%1}, [%2];\n\t}"
+      : "=r"(r.x), "=r"(r.y)
+      : "l"(p), "r"(static_cast<int>(hot)), "l"(ph));
+  return r;
+}
+template <>
+__device__ __forceinline__ uint32_t ldg_hot_cs<uint32_t>(const uint32_t* p, bool hot, uint64_t ph) {
+  uint32_t r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+      "@q ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %3;\n\t"
+      "@!q ld.global.cs.nc.u32 %0, [%1];\n\t}"
+      : "=r"(r)
+      : "l"(p), "r"(static_cast<int>(hot)), "l"(ph));
+  return r;
+}
+template <>
+__device__ __forceinline__ unsigned short ldg_hot_cs<unsigned short>(const unsigned short* p, bool hot, uint64_t ph) {
+  unsigned short r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+      "@q ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %3;\n\t"
+      "@!q ld.global.cs.nc.u16 %0, [%1];\n\t}"
+      : "=h"(r)
+      : "l"(p), "r"(static_cast<int>(hot)), "l"(ph));
+  return r;
+}
+
 // Both policies as predicated loads (no branch per gather): hot ? evict_last : evict_first.
 template <typename R>
 __device__ __forceinline__ R ldg_hint2(const R* p, bool hot, uint64_t ph, uint64_t pc);
@@ -354,12 +427,15 @@ __global__ void __launch_bounds__(256) spmm_light_kernel(const SpmmArgs p) {
 // and broadcast by shuffle; row ends are cached 32 at a time across lanes.
 // Accumulation order per output element is unchanged: ascending CSC position.
 // ---------------------------------------------------------------------------
-// MODE: 0 sum, 1 mean, 2 max, 3 min. HINT: gathers carry an L2 eviction
-// policy — evict_last for entries whose source class is below
-// p.hot_class_limit (when the plan's classes are in use), evict_first for all
-// others — so streaming rows of an X far larger than L2 do not displace the
-// hot rows. Without HINT (X fits L2) gathers use the default policy.
-template <typename T, int VB, int NV, int U, int MODE, bool SCALED, bool ACC, bool HINT>
+// MODE: 0 sum, 1 mean, 2 max, 3 min. LM (load mode) for an X far larger than
+// L2: gathers of entries whose source class is below p.hot_class_limit (when
+// the plan's classes are in use) carry an evict_last policy, all others
+// evict_first, so hub rows stay L2-resident while the rest streams. LM = 2 is
+// the plain (unscaled, fresh) path with the class array read; max/min there
+// stream the cold arm with ld.global.cs. 0 = default loads (X fits L2).
+// Measured on C4 (sum): default 6.2 ms, all-cs 6.2, all-evict_first 4.8,
+// hot evict_last + cold evict_first 4.25.
+template <typename T, int VB, int NV, int U, int MODE, bool SCALED, bool ACC, int LM>
 __global__ void __launch_bounds__(256, (SCALED || sizeof(T) == 8) ? 3 : 4) spmm_flat_kernel(const SpmmArgs p) {
   constexpr bool MAXMIN = MODE >= 2;
   constexpr bool IS_MIN = MODE == 3;
@@ -453,6 +529,7 @@ __global__ void __launch_bounds__(256, (SCALED || sizeof(T) == 8) ? 3 : 4) spmm_
     }
   };
 
+  constexpr bool HINT = LM >= 1;  // per-entry hot flag (false when the plan's classes are off)
   const uint64_t pol_hot = HINT ? policy_evict_last() : 0;
   const uint64_t pol_cold = HINT ? policy_evict_first() : 0;
   int32_t c_next = 0, p_next = -1;
@@ -482,16 +559,20 @@ __global__ void __launch_bounds__(256, (SCALED || sizeof(T) == 8) ? 3 : 4) spmm_
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const T* xr = x + static_cast<uint64_t>(static_cast<uint32_t>(__shfl_sync(FULL, c_cur, u))) * fu;
-      if constexpr (HINT && !MAXMIN) {
-        // predicated policy pair: no branch per gather
-        const bool hot = (hmask >> u) & 1u;
+      const bool hot = (hmask >> u) & 1u;
+      if constexpr (LM >= 1 && !MAXMIN) {
+        // predicated evict_last / evict_first pair: no branch per gather
 #pragma unroll
         for (int j = 0; j < NV; ++j)
           if (valid[j]) buf[u][j] = ldg_hint2<R>(reinterpret_cast<const R*>(xr + soff[j]), hot, pol_hot, pol_cold);
-      } else if constexpr (HINT) {
-        // (max/min keep a uniform branch: the predicated pair needs both 64-bit
-        // policies live, which spills at this kernel's 64-register budget)
-        if ((hmask >> u) & 1u) {
+      } else if constexpr (LM == 2) {
+        // max/min: both 64-bit policies live would spill at 64 registers; the
+        // cold arm streams with ld.global.cs instead
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+          if (valid[j]) buf[u][j] = ldg_hot_cs<R>(reinterpret_cast<const R*>(xr + soff[j]), hot, pol_hot);
+      } else if constexpr (LM == 1) {
+        if (hot) {
 #pragma unroll
           for (int j = 0; j < NV; ++j)
             if (valid[j]) buf[u][j] = ldg_hint<R>(reinterpret_cast<const R*>(xr + soff[j]), pol_hot);
@@ -503,7 +584,8 @@ __global__ void __launch_bounds__(256, (SCALED || sizeof(T) == 8) ? 3 : 4) spmm_
       } else if (u < nb) {  // (the branch also keeps ptxas from hoisting all U addresses at once)
 #pragma unroll
         for (int j = 0; j < NV; ++j)
-          if (valid[j]) buf[u][j] = VecT::load_raw(xr + soff[j]);
+          if (valid[j])
+            buf[u][j] = VecT::load_raw(xr + soff[j]);
       }
     }
     if (nb == U && k0 + U <= row_end) {
@@ -1006,8 +1088,9 @@ gm_status launch_flat(const SpmmArgs& p0, int64_t ns, cudaStream_t st) {
   constexpr int kV = VB / static_cast<int>(sizeof(T));
   constexpr int64_t kChunk = 32 * std::min(8, std::max(1, 32 / kV));
   const int64_t chunk = std::min<int64_t>(kChunk, 32 * std::max(1, flat_max_nv()));
-  // policy-carrying gathers unless X is small enough to live in L2
-  const bool hint = p0.stream_x != 0;
+  // streaming gathers unless X is small enough to live in L2; hot rows keep
+  // an evict_last policy on the plain (unscaled, fresh) path when hinted
+  const int lm = p0.stream_x == 0 ? 0 : (p0.src_class != nullptr && !scaled && !p0.accum) ? 2 : 1;
   for (int64_t base = 0; base < ns; base += chunk) {
     SpmmArgs p = p0;
     p.slot_base = base;
@@ -1024,11 +1107,12 @@ gm_status launch_flat(const SpmmArgs& p0, int64_t ns, cudaStream_t st) {
     } else if (scaled) spmm_flat_kernel<T, VB, NV_, U_, M_, true, false, H_><<<grid, 256, 0, st>>>(p); \
     else spmm_flat_kernel<T, VB, NV_, U_, M_, false, false, H_><<<grid, 256, 0, st>>>(p);           \
   } while (0)
-#define GM_FLAT_K(NV_, U_, M_)                                                    \
-  do {                                                                            \
-    if (hint) GM_FLAT_H(NV_, U_, M_, true);                                       \
-    else if (!scaled && !p.accum) spmm_flat_kernel<T, VB, NV_, U_, M_, false, false, false><<<grid, 256, 0, st>>>(p); \
-    else GM_FLAT_H(NV_, U_, M_, true);                                            \
+#define GM_FLAT_K(NV_, U_, M_)                                                                     \
+  do {                                                                                             \
+    if (lm == 2) spmm_flat_kernel<T, VB, NV_, U_, M_, false, false, 2><<<grid, 256, 0, st>>>(p);   \
+    else if (lm == 1) GM_FLAT_H(NV_, U_, M_, 1);                                                   \
+    else if (!scaled && !p.accum) spmm_flat_kernel<T, VB, NV_, U_, M_, false, false, 0><<<grid, 256, 0, st>>>(p); \
+    else GM_FLAT_H(NV_, U_, M_, 1);                                                                \
   } while (0)
 #define GM_FLAT(NV_, U_)                          \
   do {                                            \
