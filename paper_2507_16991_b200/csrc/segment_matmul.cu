@@ -498,6 +498,57 @@ extern "C" {
 
 static int64_t pad_to(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
+// fp32 operands as three bf16 pieces: hi = bf16(v), mid = bf16(v - hi),
+// lo = bf16(v - hi - mid), |v - hi - mid - lo| <= 2^-27 |v|. Along K the
+// operands are laid out so that ONE bf16 tcgen05 GEMM over K' = 6K with fp32
+// TMEM accumulation forms the six products down to 2^-18 scale:
+//   x' = [hi | hi | mid | hi | lo | mid],  W' = [hi; mid; hi; lo; hi; mid]
+//   sum = hi*hi + hi*mid + mid*hi + hi*lo + lo*hi + mid*mid = x W + O(2^-26)|x||W|.
+constexpr int kSplit = 6;
+__device__ __forceinline__ void split_bf16(float v, __nv_bfloat16& hi, __nv_bfloat16& mid, __nv_bfloat16& lo) {
+  hi = __float2bfloat16_rn(v);
+  const float r1 = __fsub_rn(v, __bfloat162float(hi));  // exact (Sterbenz-range subtraction)
+  mid = __float2bfloat16_rn(r1);
+  lo = __float2bfloat16_rn(__fsub_rn(r1, __bfloat162float(mid)));
+}
+
+__global__ void split_x_kernel(const float* __restrict__ x, int64_t rows, int k, __nv_bfloat16* __restrict__ xs) {
+  const int64_t total = rows * k;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / k;
+    const int c = static_cast<int>(i - r * k);
+    __nv_bfloat16 hi, mid, lo;
+    split_bf16(x[i], hi, mid, lo);
+    __nv_bfloat16* o = xs + r * kSplit * k + c;
+    o[0] = hi;
+    o[k] = hi;
+    o[2 * k] = mid;
+    o[3 * k] = hi;
+    o[4 * k] = lo;
+    o[5 * k] = mid;
+  }
+}
+
+__global__ void split_w_kernel(const float* __restrict__ w, int groups, int k, int n, __nv_bfloat16* __restrict__ ws) {
+  const int64_t total = static_cast<int64_t>(groups) * k * n;
+  const int64_t kn = static_cast<int64_t>(k) * n;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t g = i / kn;
+    const int64_t rem = i - g * kn;  // kk * n + nn
+    __nv_bfloat16 hi, mid, lo;
+    split_bf16(w[i], hi, mid, lo);
+    __nv_bfloat16* o = ws + g * kSplit * kn + rem;
+    o[0] = hi;
+    o[kn] = mid;
+    o[2 * kn] = hi;
+    o[3 * kn] = lo;
+    o[4 * kn] = hi;
+    o[5 * kn] = mid;
+  }
+}
+
 GM_API size_t gm_segment_matmul_workspace(int64_t rows, int64_t groups, int64_t k, int64_t n) {
   if (rows < 0 || groups < 0 || k < 0 || n < 0) return 0;
   const int64_t kp = pad_to(std::max<int64_t>(k, 1), 64), np = pad_to(std::max<int64_t>(n, 1), 16);
@@ -618,6 +669,39 @@ GM_API gm_status gm_segment_matmul(const void* x, const int64_t* ptr_host, int64
     GM_CHECK_LAUNCH("unpad_cols_kernel");
   }
   return GM_OK;
+}
+
+GM_API size_t gm_segment_matmul_f32_workspace(int64_t rows, int64_t groups, int64_t k, int64_t n) {
+  if (rows < 0 || groups < 0 || k < 0 || n < 0) return 0;
+  return align_up(static_cast<size_t>(rows * kSplit * k) * 2, 256) +
+         align_up(static_cast<size_t>(groups * kSplit * k * n) * 2, 256) +
+         gm_segment_matmul_workspace(rows, groups, kSplit * k, n);
+}
+
+GM_API gm_status gm_segment_matmul_f32(const float* x, const int64_t* ptr_host, int64_t groups, int64_t k,
+                                       int64_t n, const float* w, float* out, void* workspace, size_t workspace_bytes,
+                                       gm_stream_t stream) {
+  GM_REQUIRE(ptr_host && groups >= 1, GM_ERR_INVALID_ARGUMENT, "segment_matmul: bad groups");
+  GM_REQUIRE(k > 0 && n > 0, GM_ERR_INVALID_ARGUMENT, "segment_matmul: K and N must be positive");
+  const int64_t rows = ptr_host[groups];
+  if (rows == 0) return GM_OK;
+  GM_REQUIRE(x && w && out, GM_ERR_INVALID_ARGUMENT, "segment_matmul: null pointer");
+  const size_t need = gm_segment_matmul_f32_workspace(rows, groups, k, n);
+  GM_REQUIRE(workspace && workspace_bytes >= need, GM_ERR_INVALID_ARGUMENT, "segment_matmul: workspace too small");
+  cudaStream_t st = as_stream(stream);
+  unsigned char* b = static_cast<unsigned char*>(workspace);
+  auto* xs = reinterpret_cast<__nv_bfloat16*>(b);
+  b += align_up(static_cast<size_t>(rows * kSplit * k) * 2, 256);
+  auto* ws = reinterpret_cast<__nv_bfloat16*>(b);
+  b += align_up(static_cast<size_t>(groups * kSplit * k * n) * 2, 256);
+  split_x_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(rows * k, 256), kNumSMs * 32)), 256, 0, st>>>(
+      x, rows, static_cast<int>(k), xs);
+  GM_CHECK_LAUNCH("split_x_kernel");
+  split_w_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(groups * k * n, 256), kNumSMs * 32)), 256, 0, st>>>(
+      w, static_cast<int>(groups), static_cast<int>(k), static_cast<int>(n), ws);
+  GM_CHECK_LAUNCH("split_w_kernel");
+  return gm_segment_matmul(xs, ptr_host, groups, kSplit * k, n, ws, GM_F32, out, b,
+                           workspace_bytes - static_cast<size_t>(b - static_cast<unsigned char*>(workspace)), stream);
 }
 
 }  // extern "C"

@@ -489,9 +489,12 @@ def aggregate(values: torch.Tensor, index: torch.Tensor, num_groups: int, kind: 
 # ---------------------------------------------------------------------------
 
 def segment_matmul(x: torch.Tensor, ptr: Sequence[int], weights: torch.Tensor,
-                   out_dtype: torch.dtype = torch.bfloat16) -> torch.Tensor:
-    """out[ptr[g]:ptr[g+1]] = x[ptr[g]:ptr[g+1]] @ weights[g] (hetero.hpp:134-157),
-    bf16 tensor cores (tcgen05), fp32 accumulation."""
+                   out_dtype: Optional[torch.dtype] = None) -> torch.Tensor:
+    """out[ptr[g]:ptr[g+1]] = x[ptr[g]:ptr[g+1]] @ weights[g] (hetero.hpp:134-157)
+    on tcgen05 tensor cores with fp32 accumulation. bf16 operands: one bf16
+    GEMM (bf16 output by default). fp32 operands (the reference's
+    grouped_matmul<float>): fp32-accurate split-bf16 GEMM (gm_segment_matmul_f32),
+    fp32 output."""
     if weights.dim() != 3:
         raise ValueError("grouped_matmul: weights must be [groups, F, F']")
     groups, k, n = weights.shape
@@ -499,9 +502,20 @@ def segment_matmul(x: torch.Tensor, ptr: Sequence[int], weights: torch.Tensor,
         raise ValueError(f"grouped_matmul: group count mismatch ({len(ptr) - 1} inputs, {groups} weight slabs)")
     if x.dim() != 2 or x.shape[1] != k:
         raise ValueError("grouped_matmul: inner dimension mismatch")
+    rows = int(ptr[-1])
+    if x.dtype == torch.float32 and weights.dtype == torch.float32 and out_dtype in (None, torch.float32):
+        xf, wf = x.contiguous(), weights.contiguous()
+        out = torch.empty((rows, n), dtype=torch.float32, device=x.device)
+        ptr_h = (C.c_int64 * (groups + 1))(*[int(p) for p in ptr])
+        lib = L.lib()
+        ws_bytes = lib.gm_segment_matmul_f32_workspace(rows, groups, k, n)
+        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=x.device)
+        L.check(lib.gm_segment_matmul_f32(_p(xf), ptr_h, groups, k, n, _p(wf), _p(out), _p(ws), ws_bytes, _stream()),
+                "gm_segment_matmul_f32")
+        return out
+    out_dtype = out_dtype or torch.bfloat16
     x = x.to(torch.bfloat16).contiguous()
     w = weights.to(torch.bfloat16).contiguous()
-    rows = int(ptr[-1])
     out = torch.empty((rows, n), dtype=out_dtype, device=x.device)
     ptr_h = (C.c_int64 * (groups + 1))(*[int(p) for p in ptr])
     lib = L.lib()
@@ -513,7 +527,7 @@ def segment_matmul(x: torch.Tensor, ptr: Sequence[int], weights: torch.Tensor,
 
 
 def grouped_matmul(inputs: Sequence[torch.Tensor], weights: torch.Tensor,
-                   out_dtype: torch.dtype = torch.bfloat16):
+                   out_dtype: Optional[torch.dtype] = None):
     """List form of hetero.hpp:134-157 (validates like the reference)."""
     if weights.dim() != 3:
         raise ValueError("grouped_matmul: weights must be [groups, F, F']")

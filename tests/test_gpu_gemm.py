@@ -113,3 +113,35 @@ def test_odd_shapes_pad_internally():
         x = torch.randn(ptr[-1], k, device="cuda").to(torch.bfloat16)
         w = torch.randn(3, k, n, device="cuda").to(torch.bfloat16)
         check(gm.segment_matmul(x, ptr, w, out_dtype=torch.float32), x, ptr, w, np.arange(ptr[-1]), False)
+
+
+# ---------------------------------------------------------------------------
+# fp32 operands: split-bf16 GEMM on the same tcgen05 kernel (gm_segment_matmul_f32)
+# bar (north_star, fp32 GEMM): |gpu - ref64| <= 1e-5 * sum_k |x_ik||W_kj| + 1e-7
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("k,n", [(3, 5), (64, 16), (100, 7), (128, 128), (130, 33), (256, 64), (512, 256)])
+def test_fp32_operands_meet_fp32_bound(k, n):
+    torch.manual_seed(k * 7 + n)
+    ptr = [0, 5, 5, 133, 400, 401, 1031]
+    x = torch.randn(ptr[-1], k, device="cuda") * 3.0
+    w = torch.randn(len(ptr) - 1, k, n, device="cuda") / k ** 0.5
+    out = gm.segment_matmul(x, ptr, w)
+    assert out.dtype == torch.float32
+    ref = Oracle().segment_matmul(x.double().cpu().numpy(), np.array(ptr), w.double().cpu().numpy())
+    scale = Oracle().segment_matmul(np.abs(x.double().cpu().numpy()), np.array(ptr), np.abs(w.double().cpu().numpy()))
+    err = np.abs(out.double().cpu().numpy() - ref)
+    assert np.all(err <= 1e-5 * scale + 1e-7), f"max err {err.max():.3e}, max rel-to-scale {(err / scale).max():.3e}"
+
+
+def test_fp32_reference_golden_cases():
+    # test_hetero.cpp:61-106 shapes (K=3 -> N=5/4/2), the reference's f64 outputs
+    d = np.load(os.path.join(GOLD, "gemm.npz"))
+    for xk, wk, ptr, ok in (("gm_x", "gm_w", [0, 2, 6], "gm_out"), ("gm_empty_x", "gm_empty_w", [0, 0, 2], "gm_empty_out")):
+        x = torch.from_numpy(d[xk]).cuda().float()
+        w = torch.from_numpy(d[wk]).cuda().float()
+        got = gm.segment_matmul(x, ptr, w).double().cpu().numpy()
+        scale = Oracle().segment_matmul(np.abs(d[xk].astype(np.float64)), np.array(ptr), np.abs(d[wk].astype(np.float64)))
+        assert np.all(np.abs(got - d[ok]) <= 1e-5 * scale + 1e-7)
+    outs = gm.grouped_matmul([torch.from_numpy(d["gm_x"][:2]).cuda().float(), torch.from_numpy(d["gm_x"][2:]).cuda().float()],
+                             torch.from_numpy(d["gm_w"]).cuda().float())
+    assert outs[0].dtype == torch.float32 and outs[1].shape[0] == 4
