@@ -127,6 +127,53 @@ def mag_gemm():
     print(json.dumps(r), flush=True)
 
 
+def products_backward():
+    """C4 backward of a weighted sum SpMM: dx (transposed product over the
+    CSR-by-source cache) and dw (per-edge dot), message_passing.hpp:119-166."""
+    n, e, f = 2_449_029, 61_859_140, 100
+    g = graph(1, n, e)
+    x = feats(n, f, torch.float32)
+    w = torch.rand(e, device="cuda") + 0.5
+    gout = feats(n, f, torch.float32)
+    g.to_csr().plan(row_bytes=f * 4)
+    dx_ms = timed(lambda: gm.spmm_backward(g, x, None, "sum", gout), reps=5)
+    wfwd_ms = timed(lambda: gm.spmm(g, x, w, "sum"), reps=5)
+    src, dst = g.src(), g.dst()
+    dw = torch.empty(e, device="cuda")
+    dot_ms = timed(lambda: L.check(L.lib().gm_edge_dot(L.GM_F32, src.data_ptr(), dst.data_ptr(), e, gout.data_ptr(),
+                                                       x.data_ptr(), f, dw.data_ptr(),
+                                                       torch.cuda.current_stream().cuda_stream)), reps=5)
+    full_ms = timed(lambda: gm.spmm_backward(g, x, w, "sum", gout), reps=5)
+    r = {"config": "C4 backward (sum)", "dx_ms": dx_ms, "dx_gedges_s": e / dx_ms / 1e6, "dx_and_dw_ms": full_ms,
+         "weighted_fwd_ms": wfwd_ms, "edge_dot_ms": dot_ms}
+    print(json.dumps(r), flush=True)
+
+
+def mag_layer():
+    """C3 end-to-end RGCN-shaped hetero SAGE layer (bf16 weights -> bf16 GEMMs)."""
+    from paper_2507_16991_b200.hetero import hetero_sage_layer
+    counts = {"paper": 736_389, "author": 1_134_649, "institution": 8_740, "field_of_study": 59_965}
+    rels = [("author", "writes", "paper", 7_145_660), ("author", "affiliated_with", "institution", 1_043_998),
+            ("paper", "cites", "paper", 5_416_271), ("paper", "has_topic", "field_of_study", 7_505_078)]
+    torch.manual_seed(0)
+    h = {t: torch.randn(c, 128, device="cuda") for t, c in counts.items()}
+    edges, wn = {}, {}
+    for i, (s_t, r, d_t, m) in enumerate(rels):
+        src = torch.empty(m, dtype=torch.int64, device="cuda")
+        dst = torch.empty(m, dtype=torch.int64, device="cuda")
+        L.check(L.lib().gm_synth_edges(0, SEED + i, 0, m, counts[s_t], counts[d_t], src.data_ptr(), dst.data_ptr(),
+                                       torch.cuda.current_stream().cuda_stream))
+        edges[(s_t, r, d_t)] = gm.EdgeIndex(src, dst, counts[s_t], counts[d_t])
+        wn[(s_t, r, d_t)] = (torch.randn(128, 128, device="cuda") / 11).to(torch.bfloat16)
+    ws = {t: (torch.randn(128, 128, device="cuda") / 11).to(torch.bfloat16) for t in counts}
+    b = {t: torch.zeros(128, device="cuda") for t in counts}
+    ms = timed(lambda: hetero_sage_layer(edges, h, wn, ws, b), reps=10)
+    e_tot = sum(m for *_, m in rels)
+    r = {"config": "C3 hetero SAGE layer (4 relations mean SpMM + 2 grouped GEMMs + combine, bf16 W)", "ms": ms,
+         "edges": e_tot, "nodes": sum(counts.values())}
+    print(json.dumps(r), flush=True)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["C1", "C2", "C3", "C4", "C5"]
     if "C1" in which:
@@ -140,5 +187,9 @@ if __name__ == "__main__":
         spmm_line("C4 ogbn-products", 1, 2_449_029, 61_859_140, 100, torch.float32, "max")
     if "C2" in which:
         spmm_line("C2 reddit", 1, 232_965, 114_615_892, 602, torch.float32, "mean")
+    if "C4B" in which:
+        products_backward()
+    if "C3L" in which:
+        mag_layer()
     if "C5" in which:
         spmm_line("C5 ogbn-papers100M (1 GPU)", 1, 111_059_956, 1_615_685_872, 128, torch.bfloat16, "sum")
