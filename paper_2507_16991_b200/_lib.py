@@ -12,7 +12,8 @@ import os
 import subprocess
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgraphmill_b200.so")
+# GM_LIB_PATH selects an alternative in-tree build (A/B kernel experiments only)
+LIB_PATH = os.environ.get("GM_LIB_PATH") or os.path.join(_HERE, "libgraphmill_b200.so")
 
 GM_OK = 0
 GM_ERR_INVALID_ARGUMENT = 1
