@@ -194,6 +194,41 @@ struct CombineArgs {
   int64_t f;
   float* out;
 };
+// float4 rows, one warp per row (f % 4 == 0, 16-byte aligned arrays)
+__global__ void hetero_combine_vec_kernel(const CombineArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t f4 = a.f / 4;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < a.rows; r += nw) {
+    for (int64_t c = lane; c < f4; c += 32) {
+      const int64_t i = r * f4 + c;
+      float4 acc = a.n_parts > 0 ? __ldcs(reinterpret_cast<const float4*>(a.parts[0]) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int p = 1; p < a.n_parts; ++p) {
+        const float4 v = __ldcs(reinterpret_cast<const float4*>(a.parts[p]) + i);
+        acc.x = __fadd_rn(acc.x, v.x);
+        acc.y = __fadd_rn(acc.y, v.y);
+        acc.z = __fadd_rn(acc.z, v.z);
+        acc.w = __fadd_rn(acc.w, v.w);
+      }
+      if (a.self) {
+        const float4 v = __ldcs(reinterpret_cast<const float4*>(a.self) + i);
+        acc.x = __fadd_rn(acc.x, v.x);
+        acc.y = __fadd_rn(acc.y, v.y);
+        acc.z = __fadd_rn(acc.z, v.z);
+        acc.w = __fadd_rn(acc.w, v.w);
+      }
+      if (a.bias) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(a.bias) + c);
+        acc.x = __fadd_rn(acc.x, v.x);
+        acc.y = __fadd_rn(acc.y, v.y);
+        acc.z = __fadd_rn(acc.z, v.z);
+        acc.w = __fadd_rn(acc.w, v.w);
+      }
+      __stcs(reinterpret_cast<float4*>(a.out) + i, acc);
+    }
+  }
+}
+
 __global__ void hetero_combine_kernel(const CombineArgs a) {
   const int64_t total = a.rows * a.f;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
@@ -221,7 +256,15 @@ extern "C" GM_API gm_status gm_hetero_combine(const float* const* parts, int32_t
   a.rows = rows;
   a.f = f;
   a.out = out;
-  hetero_combine_kernel<<<grid_of(rows * f), 256, 0, as_stream(stream)>>>(a);
+  uintptr_t al = reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(self_term) |
+                 reinterpret_cast<uintptr_t>(bias) | static_cast<uintptr_t>(f * 4);
+  for (int p = 0; p < n_parts; ++p) al |= reinterpret_cast<uintptr_t>(parts[p]);
+  if (al % 16 == 0) {
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(ceil_div(rows, 8), kNumSMs * 16));
+    hetero_combine_vec_kernel<<<grid, 256, 0, as_stream(stream)>>>(a);
+  } else {
+    hetero_combine_kernel<<<grid_of(rows * f), 256, 0, as_stream(stream)>>>(a);
+  }
   GM_CHECK_LAUNCH("hetero_combine_kernel");
   return GM_OK;
 }

@@ -328,13 +328,17 @@ def _first_asymmetric(src: torch.Tensor, dst: torch.Tensor, n: int) -> int:
 # ---------------------------------------------------------------------------
 
 def _run_spmm(grouping: CsrView, x: torch.Tensor, kind: str, w_csr: Optional[torch.Tensor] = None,
-              gcn: Optional[L.gm_gcn_norm] = None, want_arg: bool = False, num_rows: Optional[int] = None):
+              gcn: Optional[L.gm_gcn_norm] = None, want_arg: bool = False, num_rows: Optional[int] = None,
+              out: Optional[torch.Tensor] = None):
     if x.dtype not in _DT:
         raise ValueError(f"spmm: unsupported dtype {x.dtype}")
     x = x.contiguous()
     f = x.shape[1] if x.dim() == 2 else 1
     rows = grouping.num_rows() if num_rows is None else num_rows
-    out = torch.empty((rows, f) if x.dim() == 2 else (rows,), dtype=x.dtype, device=x.device)
+    if out is None:
+        out = torch.empty((rows, f) if x.dim() == 2 else (rows,), dtype=x.dtype, device=x.device)
+    elif out.shape[0] != rows or not out.is_contiguous() or out.dtype != x.dtype:
+        raise ValueError("spmm: out must be a contiguous [num_dst_nodes, F] tensor of x's dtype")
     arg = torch.empty((rows, f), dtype=torch.int32, device=x.device) if want_arg else None
     csr = grouping.c_struct()
     plan = grouping.plan(row_bytes=f * x.element_size())
@@ -351,8 +355,11 @@ def _permute(values: torch.Tensor, perm: torch.Tensor) -> torch.Tensor:
     return out
 
 
-def spmm(e: EdgeIndex, x: torch.Tensor, edge_weight: Optional[torch.Tensor], reduce: str) -> torch.Tensor:
-    """message_passing.hpp:92-169 forward: out[v] = sum_{(w,v)} weight * x[w] (or mean)."""
+def spmm(e: EdgeIndex, x: torch.Tensor, edge_weight: Optional[torch.Tensor], reduce: str,
+         out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """message_passing.hpp:92-169 forward: out[v] = sum_{(w,v)} weight * x[w] (or mean).
+    `out` (optional): a contiguous [num_dst_nodes, F] destination, e.g. a slice of
+    a concatenated buffer, so callers avoid a copy."""
     if reduce not in ("sum", "mean"):
         raise ValueError("spmm: reduce must be sum or mean")
     if x.shape[0] != e.num_src_nodes():
@@ -367,7 +374,7 @@ def spmm(e: EdgeIndex, x: torch.Tensor, edge_weight: Optional[torch.Tensor], red
         w_csr = _permute(edge_weight.to(_acc_dtype(x.dtype)).contiguous(), grouping.perm)
     else:
         grouping = e.transpose_view()
-    return _run_spmm(grouping, x, reduce, w_csr=w_csr, num_rows=e.num_dst_nodes())
+    return _run_spmm(grouping, x, reduce, w_csr=w_csr, num_rows=e.num_dst_nodes(), out=out)
 
 
 def spmm_backward(e: EdgeIndex, x: torch.Tensor, edge_weight: Optional[torch.Tensor], reduce: str,

@@ -50,15 +50,19 @@ def hetero_sage_layer(edges: Dict[EdgeKey, EdgeIndex], h: Dict[str, torch.Tensor
     f_out = next(iter(w_self.values())).shape[1]
     dev = next(iter(h.values())).device
 
-    # 1. per-edge-type mean aggregation (exact)
-    aggs = [spmm(edges[et], h[et[0]], None, "mean") for et in edge_types]
+    # 1. per-edge-type mean aggregation (exact), written straight into the
+    #    segments of the grouped GEMM's input (no concatenation copy)
+    ptr = [0]
+    for et in edge_types:
+        ptr.append(ptr[-1] + edges[et].num_dst_nodes())
+    f_in = next(iter(h.values())).shape[1]
+    agg_all = torch.empty(ptr[-1], f_in, dtype=next(iter(h.values())).dtype, device=dev)
+    for i, et in enumerate(edge_types):
+        spmm(edges[et], h[et[0]], None, "mean", out=agg_all[ptr[i]:ptr[i + 1]])
     # 2. one grouped GEMM over edge types (tcgen05)
     parts_by_dst: Dict[str, list] = {nt: [] for nt in node_types}
     if edge_types:
-        ptr = [0]
-        for a in aggs:
-            ptr.append(ptr[-1] + a.shape[0])
-        proj = segment_matmul(torch.cat(aggs, 0), ptr, torch.stack([w_neigh[et] for et in edge_types]),
+        proj = segment_matmul(agg_all, ptr, torch.stack([w_neigh[et] for et in edge_types]),
                               out_dtype=torch.float32)
         for i, et in enumerate(edge_types):
             parts_by_dst[et[2]].append(proj[ptr[i]:ptr[i + 1]])
