@@ -110,34 +110,6 @@ __device__ __forceinline__ unsigned short ldg_hint<unsigned short>(const unsigne
   return r;
 }
 
-// Streaming gather: ld.global.cs.nc = LDG.E.EF (L2 evict-first) with no
-// cache-policy descriptor, so it costs no uniform-register traffic.
-template <typename R>
-__device__ __forceinline__ R ldg_cs(const R* p);
-template <>
-__device__ __forceinline__ uint4 ldg_cs<uint4>(const uint4* p) {
-  uint4 r;
-  asm("ld.global.cs.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-  return r;
-}
-template <>
-__device__ __forceinline__ uint2 ldg_cs<uint2>(const uint2* p) {
-  uint2 r;
-  asm("ld.global.cs.nc.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
-  return r;
-}
-template <>
-__device__ __forceinline__ uint32_t ldg_cs<uint32_t>(const uint32_t* p) {
-  uint32_t r;
-  asm("ld.global.cs.nc.u32 %0, [%1];" : "=r"(r) : "l"(p));
-  return r;
-}
-template <>
-__device__ __forceinline__ unsigned short ldg_cs<unsigned short>(const unsigned short* p) {
-  unsigned short r;
-  asm("ld.global.cs.nc.u16 %0, [%1];" : "=h"(r) : "l"(p));
-  return r;
-}
 // hot ? (evict_last policy) : (evict-first streaming), as a predicated pair: one
 // policy descriptor, no branch per gather.
 template <typename R>
@@ -234,21 +206,15 @@ __device__ __forceinline__ A gcn_scale(int32_t ds, int32_t dd) {
   return div_rn(A(1), sqrt_rn(mul_rn(static_cast<A>(ds), static_cast<A>(dd))));
 }
 
-#ifndef GM_SLOW_PASSES
-#define GM_SLOW_PASSES 1
-#endif
-#ifndef GM_ARG_VEC
-#define GM_ARG_VEC 1
-#endif
 // Argmax ids of one V-element vector: int4/int2 stores (arg_out is 16-byte
 // aligned and V divides F, so every vector's ids are 4V-byte aligned).
 template <int V>
 __device__ __forceinline__ void store_arg(int32_t* p, const int32_t* a) {
-  if constexpr (GM_ARG_VEC && V % 4 == 0) {
+  if constexpr (V % 4 == 0) {
 #pragma unroll
     for (int i = 0; i < V / 4; ++i)
       reinterpret_cast<int4*>(p)[i] = make_int4(a[4 * i], a[4 * i + 1], a[4 * i + 2], a[4 * i + 3]);
-  } else if constexpr (GM_ARG_VEC && V == 2) {
+  } else if constexpr (V == 2) {
     *reinterpret_cast<int2*>(p) = make_int2(a[0], a[1]);
   } else {
 #pragma unroll
@@ -608,7 +574,7 @@ __global__ void __launch_bounds__(256, (SCALED || sizeof(T) == 8) ? 3 : 4) spmm_
       }
       first = false;
     } else {
-      if constexpr (GM_SLOW_PASSES && U <= 8) {
+      if constexpr (U <= 8) {
       // rows end inside the batch: consume it in passes — each pass adds the
       // current row's edges [u0, m) (one predicated copy of the add block),
       // then the row is flushed; empty rows take passes with no adds.
@@ -664,11 +630,6 @@ __global__ void __launch_bounds__(256, (SCALED || sizeof(T) == 8) ? 3 : 4) spmm_
 // ---------------------------------------------------------------------------
 constexpr int kHeavyThreads = 256;
 constexpr int64_t kWideRowBytes = 1024;
-// Experimental: route every wide row through the CTA kernel (GM_WIDE_CTA=1).
-inline bool wide_cta_mode() {
-  static const bool on = [] { const char* e = getenv("GM_WIDE_CTA"); return e && atoi(e) == 1; }();
-  return on;
-}
 // Max vectors per lane in the flat kernel (GM_FLAT_MAX_NV, default 4: wide
 // rows take more column passes with more edges in flight per batch).
 inline int flat_max_nv() {
@@ -1285,15 +1246,6 @@ template <typename T, int VB>
 gm_status dispatch_vb(const SpmmArgs& p, bool maxmin, bool use_heavy, int64_t num_heavy,
                              int64_t ns, cudaStream_t st) {
   if constexpr (VB >= 4) {
-  // Wide rows (>= 1 KB): every row takes the CTA-per-row cp.async pipeline,
-  // whose in-flight bytes do not cost registers (Reddit-shaped F=602).
-  if (wide_cta_mode() && static_cast<int64_t>(p.f) * static_cast<int64_t>(sizeof(T)) >= kWideRowBytes &&
-      p.num_rows > 0) {
-    SpmmArgs q = p;
-    q.heavy_rows = nullptr;
-    q.heavy_thr = -1;
-    return maxmin ? launch_heavy<T, VB, true>(q, p.num_rows, ns, st) : launch_heavy<T, VB, false>(q, p.num_rows, ns, st);
-  }
   if (use_heavy) {
     // profiling only (GM_PROF_SKIP=1: no hub kernel, 2: no light kernel) — results are incomplete
     static const int prof_skip = [] { const char* e = getenv("GM_PROF_SKIP"); return e ? atoi(e) : 0; }();
