@@ -216,6 +216,16 @@ GM_API gm_status gm_edge_dot(gm_dtype dtype, const int64_t* src, const int64_t* 
                              const void* a_by_dst, const void* b_by_src, int64_t f, void* out,
                              gm_stream_t stream);
 
+/* dw in destination-grouped order (same result as gm_edge_dot, bit-identical):
+ * entry k of the CSC view pairs a_by_dst[entry_rows[k]] with b_by_src[col[k]]
+ * and writes out[perm[k]] (COO order). Consecutive entries share the
+ * destination row, so its gradient row is fetched once per row run instead of
+ * once per edge. entry_rows: gm_csr_entry_rows of the same view (int32 per
+ * entry, indexed from the view's first entry); cache it beside the view. */
+GM_API gm_status gm_csr_entry_rows(const gm_csr* csr, int32_t* rows_out, gm_stream_t stream);
+GM_API gm_status gm_edge_dot_csc(gm_dtype dtype, const gm_csr* csc, const int32_t* entry_rows, const void* a_by_dst,
+                                 const void* b_by_src, int64_t f, void* out, gm_stream_t stream);
+
 /* Heterogeneous combine (hetero.hpp:338-343 InterCombine::sum, then
  * layer_update hetero.hpp:362 / message_passing.hpp:579-580 for SAGE):
  *   out = ((((parts[0] + parts[1]) + ...) + self_term) + bias)   fp32, in this

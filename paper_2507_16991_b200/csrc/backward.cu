@@ -118,6 +118,64 @@ __global__ void __launch_bounds__(kDotWarps * 32) edge_dot_warp_kernel(const int
   }
 }
 
+// CSC-ordered variant: entry k of a destination-grouped view (rows[k] = its
+// destination, col[k] = its source, perm[k] = its COO position). Consecutive
+// entries share the destination row, so the a-row chunks of a warp's 32
+// entries are mostly the same lines (L1 hits) and DRAM traffic drops to about
+// one b-row per edge; the result lands at out[perm[k]].
+template <typename S>
+__global__ void __launch_bounds__(kDotWarps * 32) edge_dot_csc_kernel(const int32_t* __restrict__ rows,
+                                                                      const int32_t* __restrict__ col,
+                                                                      const int32_t* __restrict__ perm, int64_t k0,
+                                                                      int64_t e, const S* __restrict__ a,
+                                                                      const S* __restrict__ b, int64_t f,
+                                                                      S* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char dot_smem[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  S* buf = reinterpret_cast<S*>(dot_smem) + static_cast<size_t>(wib) * 2 * 32 * 33;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * kDotWarps;
+  for (int64_t base = (static_cast<int64_t>(blockIdx.x) * kDotWarps + wib) * 32; base < e; base += nw * 32) {
+    const int64_t my = base + lane;
+    const int64_t ra = my < e ? rows[k0 + my] : 0;
+    const int64_t rb = my < e ? col[k0 + my] : 0;
+    const int ne = static_cast<int>(e - base < 32 ? e - base : 32);
+    S acc = S(0);
+    for (int64_t c0 = 0; c0 < f; c0 += 32) {
+      const int cw = static_cast<int>(f - c0 < 32 ? f - c0 : 32);
+      S* sa = buf;
+      S* sb = buf + 32 * 33;
+#pragma unroll 8
+      for (int t = 0; t < 32; ++t) {
+        const int64_t rat = __shfl_sync(0xffffffffu, ra, t);
+        const int64_t rbt = __shfl_sync(0xffffffffu, rb, t);
+        if (t < ne && lane < cw) {
+          cp_async_elem<S>(sa + t * 33 + lane, a + rat * f + c0 + lane);
+          cp_async_elem<S>(sb + t * 33 + lane, b + rbt * f + c0 + lane);
+        }
+      }
+      asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+      __syncwarp();
+      if (lane < ne) {
+        const S* pa = sa + lane * 33;
+        const S* pb = sb + lane * 33;
+        for (int j = 0; j < cw; ++j) acc = add_rn(acc, mul_rn(pa[j], pb[j]));
+      }
+      __syncwarp();
+    }
+    if (my < e) out[perm[k0 + my]] = acc;
+  }
+}
+
+__global__ void entry_rows_kernel(const int64_t* __restrict__ rowptr, int64_t rows, int32_t* __restrict__ out) {
+  // one warp per row: the row id for each of its entries (positions relative to rowptr[0])
+  const int lane = threadIdx.x & 31;
+  const int64_t k0 = rowptr[0];
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < rows; r += nw)
+    for (int64_t k = rowptr[r] + lane; k < rowptr[r + 1]; k += 32) out[k - k0] = static_cast<int32_t>(r);
+}
+
 static unsigned grid_of(int64_t n) {
   return static_cast<unsigned>(std::min<int64_t>(std::max<int64_t>(ceil_div(n, 256), 1), kNumSMs * 32));
 }
@@ -141,6 +199,54 @@ GM_API gm_status gm_scale_rows_div(gm_dtype dtype, const void* in, int64_t rows,
     scale_rows_div_kernel<double><<<grid_of(rows * f), 256, 0, st>>>(static_cast<const double*>(in), rows, f, deg,
                                                                      static_cast<double*>(out));
   GM_CHECK_LAUNCH("scale_rows_div_kernel");
+  return GM_OK;
+}
+
+GM_API gm_status gm_csr_entry_rows(const gm_csr* csr, int32_t* rows_out, gm_stream_t stream) {
+  GM_REQUIRE(csr && rows_out, GM_ERR_INVALID_ARGUMENT, "gm_csr_entry_rows: null argument");
+  if (csr->num_rows == 0 || csr->nnz == 0) return GM_OK;
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(ceil_div(csr->num_rows, 8), kNumSMs * 32));
+  entry_rows_kernel<<<grid, 256, 0, as_stream(stream)>>>(csr->rowptr, csr->num_rows, rows_out);
+  GM_CHECK_LAUNCH("entry_rows_kernel");
+  return GM_OK;
+}
+
+GM_API gm_status gm_edge_dot_csc(gm_dtype dtype, const gm_csr* csc, const int32_t* entry_rows, const void* a_by_dst,
+                                 const void* b_by_src, int64_t f, void* out, gm_stream_t stream) {
+  GM_REQUIRE(csc && entry_rows, GM_ERR_INVALID_ARGUMENT, "gm_edge_dot_csc: null argument");
+  GM_REQUIRE(dtype == GM_F32 || dtype == GM_F64, GM_ERR_INVALID_ARGUMENT, "gm_edge_dot_csc: f32/f64 only");
+  GM_REQUIRE(csc->nnz == 0 || csc->perm, GM_ERR_INVALID_ARGUMENT, "gm_edge_dot_csc: csc->perm required");
+  if (csc->nnz == 0 || csc->num_rows == 0) return GM_OK;
+  int64_t k0 = 0;
+  cudaStream_t st = as_stream(stream);
+  GM_TRY_CUDA(cudaMemcpyAsync(&k0, csc->rowptr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GM_TRY_CUDA(cudaStreamSynchronize(st));
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(csc->nnz, 32 * kDotWarps), kNumSMs * 64));
+  // entry_rows is indexed from the view's first entry: pass it pre-offset by -k0
+  if (dtype == GM_F32) {
+    const size_t smem = sizeof(float) * 2 * 32 * 33 * kDotWarps;
+    static bool attr_f = [] {
+      cudaFuncSetAttribute(edge_dot_csc_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(sizeof(float) * 2 * 32 * 33 * kDotWarps));
+      return true;
+    }();
+    (void)attr_f;
+    edge_dot_csc_kernel<float><<<blocks, kDotWarps * 32, smem, st>>>(
+        entry_rows - k0, csc->col, csc->perm, k0, csc->nnz, static_cast<const float*>(a_by_dst),
+        static_cast<const float*>(b_by_src), f, static_cast<float*>(out));
+  } else {
+    const size_t smem = sizeof(double) * 2 * 32 * 33 * kDotWarps;
+    static bool attr_d = [] {
+      cudaFuncSetAttribute(edge_dot_csc_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(sizeof(double) * 2 * 32 * 33 * kDotWarps));
+      return true;
+    }();
+    (void)attr_d;
+    edge_dot_csc_kernel<double><<<blocks, kDotWarps * 32, smem, st>>>(
+        entry_rows - k0, csc->col, csc->perm, k0, csc->nnz, static_cast<const double*>(a_by_dst),
+        static_cast<const double*>(b_by_src), f, static_cast<double*>(out));
+  }
+  GM_CHECK_LAUNCH("edge_dot_csc_kernel");
   return GM_OK;
 }
 

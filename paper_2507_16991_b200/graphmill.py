@@ -91,6 +91,16 @@ class CsrView:
             self._plan[thr] = (plan, buf)
         return self._plan[thr][0]
 
+    def entry_rows(self) -> torch.Tensor:
+        """Per-entry row id (int32, from the view's first entry), cached beside the view."""
+        er = getattr(self, "_entry_rows", None)
+        if er is None:
+            er = torch.empty(max(self.num_entries(), 1), dtype=torch.int32, device=self.rowptr.device)
+            cs = self.c_struct()
+            L.check(L.lib().gm_csr_entry_rows(C.byref(cs), _p(er), _stream()), "gm_csr_entry_rows")
+            self._entry_rows = er
+        return er
+
     def to_host(self):
         """(rowptr, col, perm) as int64 CPU tensors, the reference's CsrView layout."""
         return self.rowptr.cpu(), self.col.cpu().long(), self.perm.cpu().long()
@@ -404,9 +414,13 @@ def spmm_backward(e: EdgeIndex, x: torch.Tensor, edge_weight: Optional[torch.Ten
     dx = _run_spmm(csr, gs, "sum", w_csr=w_csr, num_rows=e.num_src_nodes())
     dw = None
     if edge_weight is not None:
+        # destination-grouped order (the CSC cache): each gradient row is read
+        # once per row run; results land at their COO positions
         dw = torch.empty(e.num_edges(), dtype=x.dtype, device=x.device)
-        L.check(lib.gm_edge_dot(_DT[x.dtype], _p(e.src()), _p(e.dst()), e.num_edges(), _p(gs), _p(x.contiguous()),
-                                f, _p(dw), _stream()), "edge_dot")
+        csc = e.to_csc()
+        cs = csc.c_struct()
+        L.check(lib.gm_edge_dot_csc(_DT[x.dtype], C.byref(cs), _p(csc.entry_rows()), _p(gs), _p(x.contiguous()),
+                                    f, _p(dw), _stream()), "edge_dot_csc")
     return dx, dw
 
 

@@ -144,7 +144,14 @@ def products_backward():
                                                        x.data_ptr(), f, dw.data_ptr(),
                                                        torch.cuda.current_stream().cuda_stream)), reps=5)
     full_ms = timed(lambda: gm.spmm_backward(g, x, w, "sum", gout), reps=5)
-    r = {"config": "C4 backward (sum)", "dx_ms": dx_ms, "dx_gedges_s": e / dx_ms / 1e6, "dx_and_dw_ms": full_ms,
+    csc = g.to_csc()
+    cs = csc.c_struct()
+    er = csc.entry_rows()
+    import ctypes as _C
+    dot_csc_ms = timed(lambda: L.check(L.lib().gm_edge_dot_csc(L.GM_F32, _C.byref(cs), er.data_ptr(), gout.data_ptr(),
+                                                               x.data_ptr(), f, dw.data_ptr(),
+                                                               torch.cuda.current_stream().cuda_stream)), reps=5)
+    r = {"config": "C4 backward (sum)", "edge_dot_csc_ms": dot_csc_ms, "dx_ms": dx_ms, "dx_gedges_s": e / dx_ms / 1e6, "dx_and_dw_ms": full_ms,
          "weighted_fwd_ms": wfwd_ms, "edge_dot_ms": dot_ms}
     print(json.dumps(r), flush=True)
 
