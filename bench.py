@@ -243,13 +243,17 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=device)
+        backend = os.environ.get("GM_BENCH_BACKEND", "nccl")  # "gloo": N>1 logic check on one GPU (not a bench)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(backend)
     stream = torch.cuda.current_stream().cuda_stream
     lib = L.lib()
 
@@ -431,6 +435,14 @@ def main():
         t = torch.tensor([a.elapsed_time(bev) / 5], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         exact_ms = float(t.item())
+        # numerics check at N > 1: overlap-mode rows vs the exact (1-GPU-identical) rows
+        blk_out = torch.empty_like(out_local)
+        blocked(x_shard, "sum", out=blk_out)
+        torch.cuda.synchronize()
+        diff = (blk_out - out_local).abs().max()
+        ref_mag = out_local.abs().max()
+        chk = torch.stack([diff, ref_mag])
+        dist.all_reduce(chk, op=dist.ReduceOp.MAX)
         # halo-only exchange: one all_to_all of the referenced remote rows
         from paper_2507_16991_b200.dist import HaloSpmm, exchange_need_lists, halo_need
         need = halo_need(local_csr, N_NODES, rank, world)
@@ -453,6 +465,7 @@ def main():
                                         "max_halo_rows": int(t[1]), "halo_frac_of_remote_rows":
                                         float(t[1]) / (N_NODES - sh.shard_rows)},
                      "overlap_mode_numerics": "sum continued across 1+CHUNKS source blocks (fp32 tolerance)",
+                "overlap_vs_exact_max_abs_diff": float(chk[0]), "exact_max_abs": float(chk[1]),
                      "block_nnz": blocked.block_nnz(),
                      "segment_matmul_C3": bench_segment_matmul(gm, L, device, rank=rank, world=world, dist=dist),
                      "segment_matmul_F1024": bench_segment_matmul(gm, L, device, f=1024, rows=500_000, rank=rank,
