@@ -257,6 +257,17 @@ GM_API gm_status gm_segment_matmul(const void* x, const int64_t* ptr_host, int64
                                    void* out, void* workspace, size_t workspace_bytes,
                                    gm_stream_t stream);
 
+/* Pre-packed weights (serving: pack once, reuse every call): the K-major,
+ * zero-padded W^T that gm_segment_matmul otherwise rebuilds per call.
+ * packed: gm_segment_matmul_packed_w_bytes(groups, k, n) device bytes. */
+GM_API size_t gm_segment_matmul_packed_w_bytes(int64_t groups, int64_t k, int64_t n);
+GM_API gm_status gm_segment_matmul_pack_w(const void* w, int64_t groups, int64_t k, int64_t n, void* packed,
+                                          gm_stream_t stream);
+GM_API size_t gm_segment_matmul_packed_workspace(int64_t rows, int64_t groups, int64_t k, int64_t n);
+GM_API gm_status gm_segment_matmul_packed(const void* x, const int64_t* ptr_host, int64_t groups, int64_t k,
+                                          int64_t n, const void* packed_w, gm_dtype out_dtype, void* out,
+                                          void* workspace, size_t workspace_bytes, gm_stream_t stream);
+
 /* fp32 grouped_matmul (hetero.hpp:134-157 with S = float) at fp32 accuracy on
  * the same tcgen05 kernel: each fp32 operand is split into three bf16 pieces
  * (hi, mid, lo; residual <= 2^-27 |v|) laid out along K so that ONE bf16 GEMM

@@ -558,9 +558,9 @@ GM_API size_t gm_segment_matmul_workspace(int64_t rows, int64_t groups, int64_t 
   return b;
 }
 
-GM_API gm_status gm_segment_matmul(const void* x, const int64_t* ptr_host, int64_t groups, int64_t k_in,
-                                   int64_t n_in, const void* w, gm_dtype out_dtype, void* out, void* workspace,
-                                   size_t workspace_bytes, gm_stream_t stream) {
+static gm_status segment_matmul_impl(const void* x, const int64_t* ptr_host, int64_t groups, int64_t k_in,
+                                     int64_t n_in, const void* w, const void* w_packed, gm_dtype out_dtype, void* out,
+                                     void* workspace, size_t workspace_bytes, gm_stream_t stream) {
   using namespace gm::gmm;
   GM_REQUIRE(ptr_host && groups >= 1 && groups <= kMaxGroups, GM_ERR_INVALID_ARGUMENT,
              "segment_matmul: groups must be in [1, " + std::to_string(kMaxGroups) + "]");
@@ -575,13 +575,17 @@ GM_API gm_status gm_segment_matmul(const void* x, const int64_t* ptr_host, int64
   const int64_t rows = ptr_host[groups];
   GM_REQUIRE(rows < INT32_MAX, GM_ERR_INVALID_ARGUMENT, "segment_matmul: too many rows");
   if (rows == 0) return GM_OK;
-  GM_REQUIRE(x && w && out, GM_ERR_INVALID_ARGUMENT, "segment_matmul: null pointer");
-  const size_t need = gm_segment_matmul_workspace(rows, groups, k_in, n_in);
-  GM_REQUIRE(workspace && workspace_bytes >= need, GM_ERR_INVALID_ARGUMENT, "segment_matmul: workspace too small");
+  GM_REQUIRE(x && (w || w_packed) && out, GM_ERR_INVALID_ARGUMENT, "segment_matmul: null pointer");
+  const size_t wt_bytes = w_packed ? 0 : align_up(static_cast<size_t>(groups * k * n) * 2, 256);
+  const size_t need = gm_segment_matmul_workspace(rows, groups, k_in, n_in) -
+                      align_up(static_cast<size_t>(groups * k * n) * 2, 256) + wt_bytes;
+  GM_REQUIRE(need == 0 || (workspace && workspace_bytes >= need), GM_ERR_INVALID_ARGUMENT,
+             "segment_matmul: workspace too small");
   cudaStream_t st = as_stream(stream);
   unsigned char* wsp = static_cast<unsigned char*>(workspace);
-  __nv_bfloat16* wt = reinterpret_cast<__nv_bfloat16*>(wsp);
-  wsp += align_up(static_cast<size_t>(groups * k * n) * 2, 256);
+  __nv_bfloat16* wt = w_packed ? static_cast<__nv_bfloat16*>(const_cast<void*>(w_packed))
+                               : reinterpret_cast<__nv_bfloat16*>(wsp);
+  wsp += wt_bytes;
   const void* xk = x;
   if (k != k_in) {
     __nv_bfloat16* xp = reinterpret_cast<__nv_bfloat16*>(wsp);
@@ -636,10 +640,13 @@ GM_API gm_status gm_segment_matmul(const void* x, const int64_t* ptr_host, int64
                       (P.b_resident ? b_full_bytes : static_cast<size_t>(stages) * b_stage_bytes) + kCStageBytes + 256;
 
   // K-major copy of the weights: W^T as a zero-padded [G*N, K] bf16 matrix
-  transpose_w_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(groups * k * n, 256), 4096)), 256, 0, st>>>(
-      static_cast<const __nv_bfloat16*>(w), static_cast<int>(groups), static_cast<int>(k_in), static_cast<int>(n_in),
-      static_cast<int>(k), static_cast<int>(n), wt);
-  GM_CHECK_LAUNCH("transpose_w_kernel");
+  // (skipped when the caller pre-packed it with gm_segment_matmul_pack_w)
+  if (!w_packed) {
+    transpose_w_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(groups * k * n, 256), 4096)), 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(w), static_cast<int>(groups), static_cast<int>(k_in), static_cast<int>(n_in),
+        static_cast<int>(k), static_cast<int>(n), wt);
+    GM_CHECK_LAUNCH("transpose_w_kernel");
+  }
 
   CUtensorMap map_a, map_b;
   gm_status s = make_map(&map_a, xk, static_cast<uint64_t>(k), static_cast<uint64_t>(rows), BK, BM);
@@ -669,6 +676,44 @@ GM_API gm_status gm_segment_matmul(const void* x, const int64_t* ptr_host, int64
     GM_CHECK_LAUNCH("unpad_cols_kernel");
   }
   return GM_OK;
+}
+
+GM_API gm_status gm_segment_matmul(const void* x, const int64_t* ptr_host, int64_t groups, int64_t k_in,
+                                   int64_t n_in, const void* w, gm_dtype out_dtype, void* out, void* workspace,
+                                   size_t workspace_bytes, gm_stream_t stream) {
+  return segment_matmul_impl(x, ptr_host, groups, k_in, n_in, w, nullptr, out_dtype, out, workspace, workspace_bytes,
+                             stream);
+}
+
+GM_API size_t gm_segment_matmul_packed_w_bytes(int64_t groups, int64_t k, int64_t n) {
+  if (groups < 0 || k < 0 || n < 0) return 0;
+  return static_cast<size_t>(groups * pad_to(std::max<int64_t>(k, 1), 64) * pad_to(std::max<int64_t>(n, 1), 16)) * 2;
+}
+
+GM_API gm_status gm_segment_matmul_pack_w(const void* w, int64_t groups, int64_t k, int64_t n, void* packed,
+                                          gm_stream_t stream) {
+  GM_REQUIRE(w && packed && groups >= 1 && k > 0 && n > 0, GM_ERR_INVALID_ARGUMENT, "segment_matmul_pack_w: bad args");
+  const int64_t kp = pad_to(k, 64), np = pad_to(n, 16);
+  cudaStream_t st = as_stream(stream);
+  gm::gmm::transpose_w_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(groups * kp * np, 256), 4096)), 256, 0,
+                                st>>>(static_cast<const __nv_bfloat16*>(w), static_cast<int>(groups), static_cast<int>(k),
+                                      static_cast<int>(n), static_cast<int>(kp), static_cast<int>(np),
+                                      static_cast<__nv_bfloat16*>(packed));
+  GM_CHECK_LAUNCH("transpose_w_kernel");
+  return GM_OK;
+}
+
+GM_API size_t gm_segment_matmul_packed_workspace(int64_t rows, int64_t groups, int64_t k, int64_t n) {
+  return gm_segment_matmul_workspace(rows, groups, k, n) -
+         align_up(gm_segment_matmul_packed_w_bytes(groups, k, n), 256);
+}
+
+GM_API gm_status gm_segment_matmul_packed(const void* x, const int64_t* ptr_host, int64_t groups, int64_t k,
+                                          int64_t n, const void* packed_w, gm_dtype out_dtype, void* out,
+                                          void* workspace, size_t workspace_bytes, gm_stream_t stream) {
+  GM_REQUIRE(packed_w, GM_ERR_INVALID_ARGUMENT, "segment_matmul: null packed weights");
+  return segment_matmul_impl(x, ptr_host, groups, k, n, nullptr, packed_w, out_dtype, out, workspace, workspace_bytes,
+                             stream);
 }
 
 GM_API size_t gm_segment_matmul_f32_workspace(int64_t rows, int64_t groups, int64_t k, int64_t n) {

@@ -537,14 +537,29 @@ def segment_matmul(x: torch.Tensor, ptr: Sequence[int], weights: torch.Tensor,
     out_dtype = out_dtype or torch.bfloat16
     x = x.to(torch.bfloat16).contiguous()
     w = weights.to(torch.bfloat16).contiguous()
+    packed = _packed_weights(w, groups, k, n)
     out = torch.empty((rows, n), dtype=out_dtype, device=x.device)
     ptr_h = (C.c_int64 * (groups + 1))(*[int(p) for p in ptr])
     lib = L.lib()
-    ws_bytes = lib.gm_segment_matmul_workspace(rows, groups, k, n)
+    ws_bytes = lib.gm_segment_matmul_packed_workspace(rows, groups, k, n)
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=x.device)
-    L.check(lib.gm_segment_matmul(_p(x), ptr_h, groups, k, n, _p(w), _DT[out_dtype], _p(out), _p(ws),
-                                  ws_bytes, _stream()), "gm_segment_matmul")
+    L.check(lib.gm_segment_matmul_packed(_p(x), ptr_h, groups, k, n, _p(packed), _DT[out_dtype], _p(out), _p(ws),
+                                         ws_bytes, _stream()), "gm_segment_matmul_packed")
     return out
+
+
+def _packed_weights(w: torch.Tensor, groups: int, k: int, n: int) -> torch.Tensor:
+    """K-major padded W^T for the tcgen05 kernel, packed once per weight tensor
+    version and kept on the tensor (re-packed after any in-place update)."""
+    hit = getattr(w, "_gm_packed", None)
+    if hit is not None and hit[0] == w._version and hit[1] == (groups, k, n):
+        return hit[2]
+    lib = L.lib()
+    packed = torch.empty(max(lib.gm_segment_matmul_packed_w_bytes(groups, k, n), 1), dtype=torch.uint8,
+                         device=w.device)
+    L.check(lib.gm_segment_matmul_pack_w(_p(w), groups, k, n, _p(packed), _stream()), "gm_segment_matmul_pack_w")
+    w._gm_packed = (w._version, (groups, k, n), packed)
+    return packed
 
 
 def grouped_matmul(inputs: Sequence[torch.Tensor], weights: torch.Tensor,

@@ -145,3 +145,18 @@ def test_fp32_reference_golden_cases():
     outs = gm.grouped_matmul([torch.from_numpy(d["gm_x"][:2]).cuda().float(), torch.from_numpy(d["gm_x"][2:]).cuda().float()],
                              torch.from_numpy(d["gm_w"]).cuda().float())
     assert outs[0].dtype == torch.float32 and outs[1].shape[0] == 4
+
+
+def test_packed_weights_cached_and_invalidated_by_inplace_update():
+    torch.manual_seed(5)
+    ptr = [0, 300, 300, 1000]
+    x = torch.randn(ptr[-1], 128, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(3, 128, 64, device="cuda") / 11).to(torch.bfloat16)
+    a = gm.segment_matmul(x, ptr, w, out_dtype=torch.float32)
+    packed = w._gm_packed[2]
+    b = gm.segment_matmul(x, ptr, w, out_dtype=torch.float32)
+    assert w._gm_packed[2] is packed and torch.equal(a, b)  # reused, same result
+    w.mul_(2)  # in-place update -> version bump -> re-pack
+    c = gm.segment_matmul(x, ptr, w, out_dtype=torch.float32)
+    assert w._gm_packed[2] is not packed
+    check(c, x, ptr, w, np.arange(ptr[-1]), False)
