@@ -111,10 +111,22 @@ struct Vec {
     return ldg_na<R>(reinterpret_cast<const R*>(p));
   }
   __device__ static __forceinline__ void unpack(const R& r, A* out) {
-    T tmp[V];
-    memcpy(tmp, &r, VB);
+    if constexpr (sizeof(T) == 2 && VB >= 4) {
+      // bf16 -> fp32 is exact: the low half shifts up 16 bits, the high half
+      // keeps its upper 16 bits (2 integer ops per packed word)
+      uint32_t words[VB / 4];
+      memcpy(words, &r, VB);
 #pragma unroll
-    for (int i = 0; i < V; ++i) out[i] = widen(tmp[i]);
+      for (int i = 0; i < VB / 4; ++i) {
+        out[2 * i] = __uint_as_float(words[i] << 16);
+        out[2 * i + 1] = __uint_as_float(words[i] & 0xffff0000u);
+      }
+    } else {
+      T tmp[V];
+      memcpy(tmp, &r, VB);
+#pragma unroll
+      for (int i = 0; i < V; ++i) out[i] = widen(tmp[i]);
+    }
   }
   __device__ static __forceinline__ void store_global(T* p, const A* vals) {
     T tmp[V];
