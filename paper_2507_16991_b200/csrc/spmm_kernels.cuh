@@ -200,6 +200,58 @@ __device__ __forceinline__ unsigned short ldg_hint2<unsigned short>(const unsign
   return r;
 }
 
+// ldg_hint2 with the lane's column-validity folded into the predicates: no
+// branch at all per gather (invalid lanes issue nothing, their register is
+// never read).
+template <typename R>
+__device__ __forceinline__ R ldg_hint2v(const R* p, bool valid, bool hot, uint64_t ph, uint64_t pc);
+template <>
+__device__ __forceinline__ uint4 ldg_hint2v<uint4>(const uint4* p, bool valid, bool hot, uint64_t ph, uint64_t pc) {
+  uint4 r;
+  asm("{\n\t.reg .pred v, h, a, b;\n\tsetp.ne.b32 v, %5, 0;\n\tsetp.ne.b32 h, %6, 0;\n\t"
+      "and.pred a, v, h;\n\tand.pred b, v, !h;\n\t"
+      "@a ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %7;\n\t"
+      "@b ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %8;\n\t}"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p), "r"(static_cast<int>(valid)), "r"(static_cast<int>(hot)), "l"(ph), "l"(pc));
+  return r;
+}
+template <>
+__device__ __forceinline__ uint2 ldg_hint2v<uint2>(const uint2* p, bool valid, bool hot, uint64_t ph, uint64_t pc) {
+  uint2 r;
+  asm("{\n\t.reg .pred v, h, a, b;\n\tsetp.ne.b32 v, %3, 0;\n\tsetp.ne.b32 h, %4, 0;\n\t"
+      "and.pred a, v, h;\n\tand.pred b, v, !h;\n\t"
+      "@a ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %5;\n\t"
+      "@b ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %6;\n\t}"
+      : "=r"(r.x), "=r"(r.y)
+      : "l"(p), "r"(static_cast<int>(valid)), "r"(static_cast<int>(hot)), "l"(ph), "l"(pc));
+  return r;
+}
+template <>
+__device__ __forceinline__ uint32_t ldg_hint2v<uint32_t>(const uint32_t* p, bool valid, bool hot, uint64_t ph,
+                                                         uint64_t pc) {
+  uint32_t r;
+  asm("{\n\t.reg .pred v, h, a, b;\n\tsetp.ne.b32 v, %2, 0;\n\tsetp.ne.b32 h, %3, 0;\n\t"
+      "and.pred a, v, h;\n\tand.pred b, v, !h;\n\t"
+      "@a ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %4;\n\t"
+      "@b ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %5;\n\t}"
+      : "=r"(r)
+      : "l"(p), "r"(static_cast<int>(valid)), "r"(static_cast<int>(hot)), "l"(ph), "l"(pc));
+  return r;
+}
+template <>
+__device__ __forceinline__ unsigned short ldg_hint2v<unsigned short>(const unsigned short* p, bool valid, bool hot,
+                                                                     uint64_t ph, uint64_t pc) {
+  unsigned short r;
+  asm("{\n\t.reg .pred v, h, a, b;\n\tsetp.ne.b32 v, %2, 0;\n\tsetp.ne.b32 h, %3, 0;\n\t"
+      "and.pred a, v, h;\n\tand.pred b, v, !h;\n\t"
+      "@a ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %4;\n\t"
+      "@b ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %5;\n\t}"
+      : "=h"(r)
+      : "l"(p), "r"(static_cast<int>(valid)), "r"(static_cast<int>(hot)), "l"(ph), "l"(pc));
+  return r;
+}
+
 template <typename A>
 __device__ __forceinline__ A gcn_scale(int32_t ds, int32_t dd) {
   // message_passing.hpp:449-451: S(1) / std::sqrt(S(din[s]) * S(din[d]))
@@ -432,6 +484,9 @@ __global__ void __launch_bounds__(256, (SCALED || sizeof(T) == 8) ? 3 : 4) spmm_
     valid[j] = lane + j * 32 < nsl;
     soff[j] = static_cast<uint32_t>((p.slot_base + lane + j * 32) * V);
   }
+  // gather address = this lane's slice base + source * row bytes: one IMAD.WIDE
+  const unsigned char* xlane = reinterpret_cast<const unsigned char*>(x) + static_cast<size_t>(soff[0]) * sizeof(T);
+  const uint32_t rowb = fu * static_cast<uint32_t>(sizeof(T));
 
   // Positions fit int32: gm_build_compressed / plan_build require nnz < 2^31.
   const int ra = p.light_windows[2 * warp];
@@ -529,7 +584,16 @@ __global__ void __launch_bounds__(256, (SCALED || sizeof(T) == 8) ? 3 : 4) spmm_
     for (int u = 0; u < U; ++u) {
       const T* xr = x + static_cast<uint64_t>(static_cast<uint32_t>(__shfl_sync(FULL, c_cur, u))) * fu;
       const bool hot = (hmask >> u) & 1u;
-      if constexpr (LM >= 1 && !MAXMIN) {
+      if constexpr (LM >= 1 && !MAXMIN && VB <= 8) {
+        // predicated evict_last / evict_first pair with the column validity
+        // folded in and a precomputed lane base: no branch, one IMAD.WIDE per
+        // gather (8-byte vectors: C5 87 -> 79 ms, C2 55 -> 51 ms in A/B runs;
+        // the 16-byte C4 path measured slower this way and keeps the form below)
+        const unsigned char* xs = xlane + static_cast<uint64_t>(static_cast<uint32_t>(__shfl_sync(FULL, c_cur, u))) * rowb;
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+          buf[u][j] = ldg_hint2v<R>(reinterpret_cast<const R*>(xs + j * 32 * VB), valid[j], hot, pol_hot, pol_cold);
+      } else if constexpr (LM >= 1 && !MAXMIN) {
         // predicated evict_last / evict_first pair: no branch per gather
 #pragma unroll
         for (int j = 0; j < NV; ++j)
