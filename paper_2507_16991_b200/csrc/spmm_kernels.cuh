@@ -501,12 +501,12 @@ __global__ void __launch_bounds__(256) spmm_light_kernel(const SpmmArgs p) {
 // L2: gathers of entries whose source class is below p.hot_class_limit (when
 // the plan's classes are in use) carry an evict_last policy, all others
 // evict_first, so hub rows stay L2-resident while the rest streams. LM = 2 is
-// the plain (unscaled, fresh) path with the class array read; max/min there
+// the fresh (non-seeded) path with the class array read; max/min there
 // stream the cold arm with ld.global.cs. 0 = default loads (X fits L2).
 // Measured on C4 (sum): default 6.2 ms, all-cs 6.2, all-evict_first 4.8,
 // hot evict_last + cold evict_first 4.25.
 template <typename T, int VB, int NV, int U, int MODE, bool SCALED, bool ACC, int LM>
-__global__ void __launch_bounds__(256, (SCALED || sizeof(T) == 8) ? 3 : 4) spmm_flat_kernel(const SpmmArgs p) {
+__global__ void __launch_bounds__(256, (sizeof(T) == 8 || (SCALED && (MODE >= 2 || NV > 1 || VB <= 8))) ? 3 : 4) spmm_flat_kernel(const SpmmArgs p) {
   constexpr bool MAXMIN = MODE >= 2;
   constexpr bool IS_MIN = MODE == 3;
   constexpr bool MEAN = MODE == 1;
@@ -1205,7 +1205,7 @@ gm_status launch_flat(const SpmmArgs& p0, int64_t ns, cudaStream_t st) {
   const int64_t chunk = std::min<int64_t>(kChunk, 32 * std::max(1, flat_max_nv()));
   // streaming gathers unless X is small enough to live in L2; hot rows keep
   // an evict_last policy on the plain (unscaled, fresh) path when hinted
-  const int lm = p0.stream_x == 0 ? 0 : (p0.src_class != nullptr && !scaled && !p0.accum) ? 2 : 1;
+  const int lm = p0.stream_x == 0 ? 0 : (p0.src_class != nullptr && !p0.accum) ? 2 : 1;
   for (int64_t base = 0; base < ns; base += chunk) {
     SpmmArgs p = p0;
     p.slot_base = base;
@@ -1224,7 +1224,10 @@ gm_status launch_flat(const SpmmArgs& p0, int64_t ns, cudaStream_t st) {
   } while (0)
 #define GM_FLAT_K(NV_, U_, M_)                                                                     \
   do {                                                                                             \
-    if (lm == 2) spmm_flat_kernel<T, VB, NV_, U_, M_, false, false, 2><<<grid, 256, 0, st>>>(p);   \
+    if (lm == 2) {                                                                                 \
+      if (scaled) spmm_flat_kernel<T, VB, NV_, U_, M_, true, false, 2><<<grid, 256, 0, st>>>(p);     \
+      else spmm_flat_kernel<T, VB, NV_, U_, M_, false, false, 2><<<grid, 256, 0, st>>>(p);           \
+    }                                                                                              \
     else if (lm == 1) GM_FLAT_H(NV_, U_, M_, 1);                                                   \
     else if (!scaled && !p.accum) spmm_flat_kernel<T, VB, NV_, U_, M_, false, false, 0><<<grid, 256, 0, st>>>(p); \
     else GM_FLAT_H(NV_, U_, M_, 1);                                                                \
