@@ -225,23 +225,15 @@ GM_API gm_status gm_edge_dot_csc(gm_dtype dtype, const gm_csr* csc, const int32_
   // entry_rows is indexed from the view's first entry: pass it pre-offset by -k0
   if (dtype == GM_F32) {
     const size_t smem = sizeof(float) * 2 * 32 * 33 * kDotWarps;
-    static bool attr_f = [] {
-      cudaFuncSetAttribute(edge_dot_csc_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(sizeof(float) * 2 * 32 * 33 * kDotWarps));
-      return true;
-    }();
-    (void)attr_f;
+    GM_TRY_CUDA(cudaFuncSetAttribute(edge_dot_csc_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(sizeof(float) * 2 * 32 * 33 * kDotWarps)));  // per device, so per call
     edge_dot_csc_kernel<float><<<blocks, kDotWarps * 32, smem, st>>>(
         entry_rows - k0, csc->col, csc->perm, k0, csc->nnz, static_cast<const float*>(a_by_dst),
         static_cast<const float*>(b_by_src), f, static_cast<float*>(out));
   } else {
     const size_t smem = sizeof(double) * 2 * 32 * 33 * kDotWarps;
-    static bool attr_d = [] {
-      cudaFuncSetAttribute(edge_dot_csc_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(sizeof(double) * 2 * 32 * 33 * kDotWarps));
-      return true;
-    }();
-    (void)attr_d;
+    GM_TRY_CUDA(cudaFuncSetAttribute(edge_dot_csc_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(sizeof(double) * 2 * 32 * 33 * kDotWarps)));  // per device, so per call
     edge_dot_csc_kernel<double><<<blocks, kDotWarps * 32, smem, st>>>(
         entry_rows - k0, csc->col, csc->perm, k0, csc->nnz, static_cast<const double*>(a_by_dst),
         static_cast<const double*>(b_by_src), f, static_cast<double*>(out));
@@ -259,23 +251,15 @@ GM_API gm_status gm_edge_dot(gm_dtype dtype, const int64_t* src, const int64_t* 
   const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(num_edges, 32 * kDotWarps), kNumSMs * 64));
   if (dtype == GM_F32) {
     const size_t smem = sizeof(float) * 2 * 32 * 33 * kDotWarps;
-    static bool attr_f = [] {
-      cudaFuncSetAttribute(edge_dot_warp_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(sizeof(float) * 2 * 32 * 33 * kDotWarps));
-      return true;
-    }();
-    (void)attr_f;
+    GM_TRY_CUDA(cudaFuncSetAttribute(edge_dot_warp_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(sizeof(float) * 2 * 32 * 33 * kDotWarps)));  // per device, so per call
     edge_dot_warp_kernel<float><<<blocks, kDotWarps * 32, smem, st>>>(
         src, dst, num_edges, static_cast<const float*>(a_by_dst), static_cast<const float*>(b_by_src), f,
         static_cast<float*>(out));
   } else {
     const size_t smem = sizeof(double) * 2 * 32 * 33 * kDotWarps;
-    static bool attr = [] {
-      cudaFuncSetAttribute(edge_dot_warp_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(sizeof(double) * 2 * 32 * 33 * kDotWarps));
-      return true;
-    }();
-    (void)attr;
+    GM_TRY_CUDA(cudaFuncSetAttribute(edge_dot_warp_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(sizeof(double) * 2 * 32 * 33 * kDotWarps)));  // per device, so per call
     edge_dot_warp_kernel<double><<<blocks, kDotWarps * 32, smem, st>>>(
         src, dst, num_edges, static_cast<const double*>(a_by_dst), static_cast<const double*>(b_by_src), f,
         static_cast<double*>(out));

@@ -660,12 +660,8 @@ static gm_status segment_matmul_impl(const void* x, const int64_t* ptr_host, int
                static_cast<uint64_t>(esz));
   if (s != GM_OK) return s;
 
-  static std::once_flag attr_once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(attr_once, [] {
-    attr_err = cudaFuncSetAttribute(segment_matmul_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  });
-  GM_TRY_CUDA(attr_err);
+  // per call: the attribute is per device, and a process may drive several
+  GM_TRY_CUDA(cudaFuncSetAttribute(segment_matmul_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   const unsigned grid = static_cast<unsigned>(std::min<int32_t>(tiles, kNumSMs));
   segment_matmul_kernel<<<grid, kThreads, smem, st>>>(P, map_a, map_b, map_c);
   GM_CHECK_LAUNCH("segment_matmul_kernel");
