@@ -130,6 +130,20 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
   d |= static_cast<uint64_t>(2) << 61;
   return d;
 }
+// K-major, SWIZZLE_64B: 8-row x 64-byte atoms, 512 B apart (SBO), layout 4.
+__device__ __forceinline__ uint64_t sdesc_sw64(uint32_t saddr) {
+  uint64_t d = static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(1) << 16;
+  d |= static_cast<uint64_t>(512 >> 4) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(4) << 61;
+  return d;
+}
+template <int KBLK>
+__device__ __forceinline__ uint64_t sdesc_k(uint32_t saddr) {
+  if constexpr (KBLK == 64) return sdesc_sw128(saddr);
+  else return sdesc_sw64(saddr);
+}
 // Instruction descriptor: bf16 x bf16 -> f32, both K-major, M=128, N=bn.
 __device__ __forceinline__ uint32_t idesc_bf16(int bn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(bn >> 3) << 17) |
@@ -176,6 +190,10 @@ __device__ __forceinline__ uint32_t pack_bf16(uint32_t lo_f32, uint32_t hi_f32) 
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 
+// KBLK: k elements per pipeline stage — 64 (128-byte rows, SWIZZLE_128B) or 32
+// (64-byte rows, SWIZZLE_64B: twice the stages for the same bytes in flight,
+// each released after half the MMAs).
+template <int KBLK>
 __global__ void __launch_bounds__(kThreads, 1)
 segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ CUtensorMap map_a,
                       const __grid_constant__ CUtensorMap map_b, const __grid_constant__ CUtensorMap map_c) {
@@ -183,9 +201,10 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
   // 1024-B alignment for the SWIZZLE_128B atoms
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int S = P.stages;
-  const uint32_t b_kblock_bytes = static_cast<uint32_t>(P.bn) * BK * 2;
+  const uint32_t b_kblock_bytes = static_cast<uint32_t>(P.bn) * KBLK * 2;
+  constexpr uint32_t kAStage = BM * KBLK * 2;
   unsigned char* a_ring = smem;
-  unsigned char* b_buf = smem + static_cast<size_t>(S) * kAStageBytes;
+  unsigned char* b_buf = smem + static_cast<size_t>(S) * kAStage;
   const size_t b_bytes = P.b_resident ? static_cast<size_t>(P.k_blocks) * b_kblock_bytes
                                       : static_cast<size_t>(S) * b_kblock_bytes;
   // output staging: per epilogue warp two 32-row x 128-byte SWIZZLE_128B boxes
@@ -244,19 +263,19 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
           if (nbload > 0) mbar_wait(bempty, (nbload - 1) & 1);
           mbar_expect_tx(bfull, static_cast<uint32_t>(P.k_blocks) * b_kblock_bytes);
           for (int kb = 0; kb < P.k_blocks; ++kb)
-            tma_load_2d(b_buf + static_cast<size_t>(kb) * b_kblock_bytes, &map_b, bfull, kb * BK, brow0);
+            tma_load_2d(b_buf + static_cast<size_t>(kb) * b_kblock_bytes, &map_b, bfull, kb * KBLK, brow0);
           cur_g = g;
           ++nbload;
         }
         for (int kb = 0; kb < P.k_blocks; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           if (P.b_resident) {
-            mbar_expect_tx(&full[s], kAStageBytes);
+            mbar_expect_tx(&full[s], kAStage);
           } else {
-            mbar_expect_tx(&full[s], kAStageBytes + b_kblock_bytes);
-            tma_load_2d(b_buf + static_cast<size_t>(s) * b_kblock_bytes, &map_b, &full[s], kb * BK, brow0);
+            mbar_expect_tx(&full[s], kAStage + b_kblock_bytes);
+            tma_load_2d(b_buf + static_cast<size_t>(s) * b_kblock_bytes, &map_b, &full[s], kb * KBLK, brow0);
           }
-          tma_load_2d(a_ring + static_cast<size_t>(s) * kAStageBytes, &map_a, &full[s], kb * BK, row0);
+          tma_load_2d(a_ring + static_cast<size_t>(s) * kAStage, &map_a, &full[s], kb * KBLK, row0);
           if (++s == S) {
             s = 0;
             ph ^= 1;
@@ -288,13 +307,13 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
         mbar_wait(&full[s], ph);
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t a_addr = smem_u32(a_ring + static_cast<size_t>(s) * kAStageBytes);
+          const uint32_t a_addr = smem_u32(a_ring + static_cast<size_t>(s) * kAStage);
           const uint32_t b_addr = P.b_resident ? smem_u32(b_buf + static_cast<size_t>(kb) * b_kblock_bytes)
                                                : smem_u32(b_buf + static_cast<size_t>(s) * b_kblock_bytes);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            // advancing 16 bf16 = 32 B inside the 128-B swizzle atom
-            tc_mma(tmem_d, sdesc_sw128(a_addr + k * 32), sdesc_sw128(b_addr + k * 32), idesc,
+          for (int k = 0; k < KBLK / 16; ++k) {
+            // advancing 16 bf16 = 32 B inside the swizzle atom
+            tc_mma(tmem_d, sdesc_k<KBLK>(a_addr + k * 32), sdesc_k<KBLK>(b_addr + k * 32), idesc,
                    (kb > 0 || k > 0) ? 1u : 0u);
           }
           tc_commit(&empty[s]);  // smem stage free once these MMAs retire
@@ -475,7 +494,7 @@ static EncodeTiledFn encode_fn() {
 
 static gm_status make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
                           uint32_t box_outer, CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
-                          uint64_t esz = 2) {
+                          uint64_t esz = 2, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeTiledFn fn = encode_fn();
   GM_REQUIRE(fn, GM_ERR_CUDA, "segment_matmul: cuTensorMapEncodeTiled unavailable");
   const cuuint64_t dims[2] = {inner, outer};
@@ -483,7 +502,7 @@ static gm_status make_map(CUtensorMap* map, const void* base, uint64_t inner, ui
   const cuuint32_t box[2] = {box_inner, box_outer};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = fn(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   GM_REQUIRE(r == CUDA_SUCCESS, GM_ERR_CUDA, "segment_matmul: cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
   return GM_OK;
@@ -609,7 +628,12 @@ static gm_status segment_matmul_impl(const void* x, const int64_t* ptr_host, int
   P.bn = static_cast<int32_t>(std::min<int64_t>(n, 256));
   while (n % P.bn != 0) P.bn -= 16;
   P.n_tiles = static_cast<int32_t>(n / P.bn);
-  P.k_blocks = static_cast<int32_t>(k / BK);
+  // 64-deep k-blocks (SWIZZLE_128B). 32-deep blocks (SWIZZLE_64B, twice the
+  // stages) measured slower at F=2048 (1.41 vs 1.11 PFLOP/s); GM_GEMM_KBLK=32
+  // selects them for experiments.
+  static const int kblk_env = [] { const char* e = getenv("GM_GEMM_KBLK"); return e ? atoi(e) : 0; }();
+  const int kblk = kblk_env == 32 ? 32 : 64;
+  P.k_blocks = static_cast<int32_t>(k / kblk);
   P.n = static_cast<int32_t>(n);
   P.out_f32 = out_dtype == GM_F32;
   P.out = outk;
@@ -627,17 +651,18 @@ static gm_status segment_matmul_impl(const void* x, const int64_t* ptr_host, int
   while (cols < static_cast<uint32_t>(2 * P.bn)) cols <<= 1;
   P.tmem_cols = cols;
 
-  const size_t b_full_bytes = static_cast<size_t>(P.k_blocks) * P.bn * BK * 2;
-  const size_t b_stage_bytes = static_cast<size_t>(P.bn) * BK * 2;
+  const size_t b_full_bytes = static_cast<size_t>(P.k_blocks) * P.bn * kblk * 2;
+  const size_t b_stage_bytes = static_cast<size_t>(P.bn) * kblk * 2;
+  const size_t a_stage_bytes = static_cast<size_t>(BM) * kblk * 2;
   P.b_resident = (P.n_tiles == 1 && b_full_bytes <= 64 * 1024) ? 1 : 0;
-  const size_t budget = 227 * 1024 - 1024 - 256 - kCStageBytes;  // alignment slack, barriers, out staging
+  const size_t budget = 227 * 1024 - 1024 - 512 - kCStageBytes;  // alignment slack, barriers, out staging
   int stages;
-  if (P.b_resident) stages = static_cast<int>((budget - b_full_bytes) / kAStageBytes);
-  else stages = static_cast<int>(budget / (kAStageBytes + b_stage_bytes));
-  stages = std::max(2, std::min(stages, 8));
+  if (P.b_resident) stages = static_cast<int>((budget - b_full_bytes) / a_stage_bytes);
+  else stages = static_cast<int>(budget / (a_stage_bytes + b_stage_bytes));
+  stages = std::max(2, std::min(stages, kblk == 32 ? 16 : 8));
   P.stages = stages;
-  const size_t smem = 1024 + static_cast<size_t>(stages) * kAStageBytes +
-                      (P.b_resident ? b_full_bytes : static_cast<size_t>(stages) * b_stage_bytes) + kCStageBytes + 256;
+  const size_t smem = 1024 + static_cast<size_t>(stages) * a_stage_bytes +
+                      (P.b_resident ? b_full_bytes : static_cast<size_t>(stages) * b_stage_bytes) + kCStageBytes + 512;
 
   // K-major copy of the weights: W^T as a zero-padded [G*N, K] bf16 matrix
   // (skipped when the caller pre-packed it with gm_segment_matmul_pack_w)
@@ -649,9 +674,12 @@ static gm_status segment_matmul_impl(const void* x, const int64_t* ptr_host, int
   }
 
   CUtensorMap map_a, map_b;
-  gm_status s = make_map(&map_a, xk, static_cast<uint64_t>(k), static_cast<uint64_t>(rows), BK, BM);
+  const CUtensorMapSwizzle swz = kblk == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  gm_status s = make_map(&map_a, xk, static_cast<uint64_t>(k), static_cast<uint64_t>(rows), kblk, BM,
+                         CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, swz);
   if (s != GM_OK) return s;
-  s = make_map(&map_b, wt, static_cast<uint64_t>(k), static_cast<uint64_t>(groups * n), BK, static_cast<uint32_t>(P.bn));
+  s = make_map(&map_b, wt, static_cast<uint64_t>(k), static_cast<uint64_t>(groups * n), kblk,
+               static_cast<uint32_t>(P.bn), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, swz);
   if (s != GM_OK) return s;
   // output map: [rows, n] of the output dtype, 128-byte x 32-row SWIZZLE_128B boxes
   CUtensorMap map_c;
@@ -661,9 +689,10 @@ static gm_status segment_matmul_impl(const void* x, const int64_t* ptr_host, int
   if (s != GM_OK) return s;
 
   // per call: the attribute is per device, and a process may drive several
-  GM_TRY_CUDA(cudaFuncSetAttribute(segment_matmul_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  auto kern = kblk == 64 ? segment_matmul_kernel<64> : segment_matmul_kernel<32>;
+  GM_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   const unsigned grid = static_cast<unsigned>(std::min<int32_t>(tiles, kNumSMs));
-  segment_matmul_kernel<<<grid, kThreads, smem, st>>>(P, map_a, map_b, map_c);
+  kern<<<grid, kThreads, smem, st>>>(P, map_a, map_b, map_c);
   GM_CHECK_LAUNCH("segment_matmul_kernel");
   if (n != n_in) {
     unpad_cols_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(rows * n_in, 256), 8192)), 256, 0, st>>>(
