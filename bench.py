@@ -477,7 +477,8 @@ def main():
             secondary = {"error": str(exc)[:300]}
     if world == 1 and not args.no_secondary:
         secondary = {"segment_matmul_C3": bench_segment_matmul(gm, L, device),
-                     "segment_matmul_F1024": bench_segment_matmul(gm, L, device, f=1024, rows=500_000)}
+                     "segment_matmul_F1024": bench_segment_matmul(gm, L, device, f=1024, rows=500_000),
+                     "segment_matmul_F2048": bench_segment_matmul(gm, L, device, f=2048, rows=262_144)}
         # max + argmax SpMM on the same graph
         mo = torch.empty(N_NODES, F, dtype=torch.float32, device=device)
         ma = torch.empty(N_NODES, F, dtype=torch.int32, device=device)
