@@ -34,10 +34,11 @@ namespace gmm {
 constexpr int kMaxGroups = 128;
 constexpr int BM = 128;          // UMMA M (cta_group::1)
 constexpr int BK = 64;           // k elements per stage (128 B rows, SWIZZLE_128B)
-constexpr int kThreads = 192;    // 6 warps
+constexpr int kEpiWarps = 8;     // two per TMEM lane quarter, each half the tile's columns
+constexpr int kThreads = 64 + 32 * kEpiWarps;  // producer + MMA warps + epilogue
 constexpr uint32_t kAStageBytes = BM * BK * 2;  // 16 KB
 constexpr uint32_t kCBoxBytes = 32 * 128;       // 32 rows x 128 B
-constexpr uint32_t kCStageBytes = 4 * 2 * kCBoxBytes;  // 4 warps x double buffer = 32 KB
+constexpr uint32_t kCStageBytes = kEpiWarps * kCBoxBytes;  // one 4 KB staging box per epilogue warp = 32 KB
 
 struct Params {
   int64_t ptr[kMaxGroups + 1];        // group row offsets
@@ -228,7 +229,7 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+      mbar_init(&tempty[a], kEpiWarps);  // one arrive per epilogue warp
     }
     mbar_init(bfull, 1);
     mbar_init(bempty, 1);
@@ -344,7 +345,13 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int esz = P.out_f32 ? 4 : 2;
     const int chunk_cols = 128 / esz;  // columns per 128-byte TMA box
-    unsigned char* my_stage = c_stage + static_cast<size_t>(warp - 2) * 2 * kCBoxBytes;
+    unsigned char* my_stage = c_stage + static_cast<size_t>(warp - 2) * kCBoxBytes;
+    // the two warps of a quarter split the columns; a tile too narrow to split
+    // (half not a multiple of the TMA box / 16-column loads) stays on half 0
+    const int half = (warp - 2) >> 2;
+    const bool split = (P.bn / 2) % chunk_cols == 0 && (P.bn / 2) % 16 == 0;
+    const int c_lo = split ? half * (P.bn / 2) : 0;
+    const int c_hi = split ? c_lo + P.bn / 2 : (half == 0 ? P.bn : 0);
     int acc = 0;
     uint32_t aph = 0;
     int nstore = 0;
@@ -359,7 +366,7 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
       tc_fence_after();
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * P.bn);
       if (full_tile) {
-        for (int c = 0; c < P.bn; c += chunk_cols) {
+        for (int c = c_lo; c < c_hi; c += chunk_cols) {
           // 128 bytes of this lane's row: 32 fp32 or 64 bf16 values
           uint32_t packed[32];
           if (P.out_f32) {
@@ -376,8 +383,8 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
 #pragma unroll
             for (int i = 0; i < 16; ++i) packed[16 + i] = pack_bf16(v[2 * i], v[2 * i + 1]);
           }
-          const int b = nstore & 1;
-          if (lane == 0 && nstore >= 2) bulk_wait_read<1>();  // buffer b's previous store has read smem
+          const int b = 0;
+          if (lane == 0 && nstore >= 1) bulk_wait_read<0>();  // the previous store has read the box
           __syncwarp();
           const uint32_t sbase = smem_u32(my_stage + b * kCBoxBytes) + lane * 128;
 #pragma unroll
@@ -394,9 +401,9 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
         }
       } else {
         const bool live = row < grow_end;
-        for (int c = 0; c < P.bn; c += 32) {
+        for (int c = c_lo; c < c_hi; c += 32) {
           uint32_t v[32];
-          const int width = min(32, P.bn - c);
+          const int width = min(32, c_hi - c);
           if (width == 32) tmem_ld32<32>(tbase + c, v);
           else tmem_ld32<16>(tbase + c, v);
           tmem_wait_ld();
