@@ -313,10 +313,10 @@ template <int V>
 __device__ __forceinline__ void store_arg(int32_t* p, const int32_t* a) {
   if constexpr (V % 4 == 0) {
 #pragma unroll
-    for (int i = 0; i < V / 4; ++i)
-      reinterpret_cast<int4*>(p)[i] = make_int4(a[4 * i], a[4 * i + 1], a[4 * i + 2], a[4 * i + 3]);
+    for (int i = 0; i < V / 4; ++i)  // streaming stores: ids are written once, keep L2 for hot rows
+      __stcs(reinterpret_cast<int4*>(p) + i, make_int4(a[4 * i], a[4 * i + 1], a[4 * i + 2], a[4 * i + 3]));
   } else if constexpr (V == 2) {
-    *reinterpret_cast<int2*>(p) = make_int2(a[0], a[1]);
+    __stcs(reinterpret_cast<int2*>(p), make_int2(a[0], a[1]));
   } else {
 #pragma unroll
     for (int e = 0; e < V; ++e) p[e] = a[e];
