@@ -54,6 +54,11 @@ struct Params {
   int32_t b_resident;
   int32_t tma_store;                  // full tiles leave through TMA bulk stores
   uint32_t tmem_cols;
+  // A operand as segments of a narrower matrix (fp32 split path): K' k-block
+  // coordinate kc reads column (seg_map[kc / a_seg_k]) * a_seg_k + kc % a_seg_k
+  // of x; 2 bits per segment. a_seg_k == 0: identity.
+  int32_t a_seg_k;
+  uint32_t a_seg_map;
   void* out;
 };
 
@@ -276,7 +281,12 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
             mbar_expect_tx(&full[s], kAStage + b_kblock_bytes);
             tma_load_2d(b_buf + static_cast<size_t>(s) * b_kblock_bytes, &map_b, &full[s], kb * KBLK, brow0);
           }
-          tma_load_2d(a_ring + static_cast<size_t>(s) * kAStage, &map_a, &full[s], kb * KBLK, row0);
+          int ac = kb * KBLK;
+          if (P.a_seg_k > 0) {
+            const int seg = ac / P.a_seg_k;
+            ac += (static_cast<int>((P.a_seg_map >> (2 * seg)) & 3u) - seg) * P.a_seg_k;
+          }
+          tma_load_2d(a_ring + static_cast<size_t>(s) * kAStage, &map_a, &full[s], ac, row0);
           if (++s == S) {
             s = 0;
             ph ^= 1;
@@ -526,11 +536,16 @@ static int64_t pad_to(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
 // fp32 operands as three bf16 pieces: hi = bf16(v), mid = bf16(v - hi),
 // lo = bf16(v - hi - mid), |v - hi - mid - lo| <= 2^-27 |v|. Along K the
-// operands are laid out so that ONE bf16 tcgen05 GEMM over K' = 6K with fp32
+// operands are arranged so that ONE bf16 tcgen05 GEMM over K' = 6K with fp32
 // TMEM accumulation forms the six products down to 2^-18 scale:
 //   x' = [hi | hi | mid | hi | lo | mid],  W' = [hi; mid; hi; lo; hi; mid]
 //   sum = hi*hi + hi*mid + mid*hi + hi*lo + lo*hi + mid*mid = x W + O(2^-26)|x||W|.
+// x' is never materialised: x is split once into [hi | mid | lo] (3K wide,
+// each piece zero-padded to a whole number of 64-deep k-blocks) and the
+// producer's TMA coordinates walk the six segments over it (Params::a_seg_*),
+// so the repeated pieces are re-read from L2 within a tile, not from HBM.
 constexpr int kSplit = 6;
+constexpr uint32_t kSplitSegMap = 0u | (0u << 2) | (1u << 4) | (0u << 6) | (2u << 8) | (1u << 10);
 __device__ __forceinline__ void split_bf16(float v, __nv_bfloat16& hi, __nv_bfloat16& mid, __nv_bfloat16& lo) {
   hi = __float2bfloat16_rn(v);
   const float r1 = __fsub_rn(v, __bfloat162float(hi));  // exact (Sterbenz-range subtraction)
@@ -538,40 +553,48 @@ __device__ __forceinline__ void split_bf16(float v, __nv_bfloat16& hi, __nv_bflo
   lo = __float2bfloat16_rn(__fsub_rn(r1, __bfloat162float(mid)));
 }
 
-__global__ void split_x_kernel(const float* __restrict__ x, int64_t rows, int k, __nv_bfloat16* __restrict__ xs) {
-  const int64_t total = rows * k;
+// x [rows, k] fp32 -> pieces [rows, 3*kp] bf16, four columns per thread
+// (8-byte stores per piece); columns k..kp-1 of every piece are zero.
+__global__ void split_x_kernel(const float* __restrict__ x, int64_t rows, int k, int kp,
+                               __nv_bfloat16* __restrict__ xs) {
+  const int q = kp / 4;
+  const int64_t total = rows * q;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t r = i / k;
-    const int c = static_cast<int>(i - r * k);
-    __nv_bfloat16 hi, mid, lo;
-    split_bf16(x[i], hi, mid, lo);
-    __nv_bfloat16* o = xs + r * kSplit * k + c;
-    o[0] = hi;
-    o[k] = hi;
-    o[2 * k] = mid;
-    o[3 * k] = hi;
-    o[4 * k] = lo;
-    o[5 * k] = mid;
+    const int64_t r = i / q;
+    const int c = static_cast<int>(i - r * q) * 4;
+    __align__(8) __nv_bfloat16 hi[4], mid[4], lo[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float v = c + j < k ? __ldcs(x + r * k + c + j) : 0.f;
+      split_bf16(v, hi[j], mid[j], lo[j]);
+    }
+    __nv_bfloat16* o = xs + r * 3 * kp + c;
+    *reinterpret_cast<uint2*>(o) = *reinterpret_cast<const uint2*>(hi);
+    *reinterpret_cast<uint2*>(o + kp) = *reinterpret_cast<const uint2*>(mid);
+    *reinterpret_cast<uint2*>(o + 2 * kp) = *reinterpret_cast<const uint2*>(lo);
   }
 }
 
-__global__ void split_w_kernel(const float* __restrict__ w, int groups, int k, int n, __nv_bfloat16* __restrict__ ws) {
-  const int64_t total = static_cast<int64_t>(groups) * k * n;
-  const int64_t kn = static_cast<int64_t>(k) * n;
+// w [G, k, n] fp32 -> W' [G, 6*kp, n] bf16 (rows k..kp-1 of each segment zero).
+__global__ void split_w_kernel(const float* __restrict__ w, int groups, int k, int kp, int n,
+                               __nv_bfloat16* __restrict__ ws) {
+  const int64_t total = static_cast<int64_t>(groups) * kp * n;
+  const int64_t kpn = static_cast<int64_t>(kp) * n;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t g = i / kn;
-    const int64_t rem = i - g * kn;  // kk * n + nn
+    const int64_t g = i / kpn;
+    const int64_t rem = i - g * kpn;  // kk * n + nn
+    const int kk = static_cast<int>(rem / n);
     __nv_bfloat16 hi, mid, lo;
-    split_bf16(w[i], hi, mid, lo);
-    __nv_bfloat16* o = ws + g * kSplit * kn + rem;
+    split_bf16(kk < k ? w[g * k * n + rem] : 0.f, hi, mid, lo);
+    __nv_bfloat16* o = ws + g * kSplit * kpn + rem;
     o[0] = hi;
-    o[kn] = mid;
-    o[2 * kn] = hi;
-    o[3 * kn] = lo;
-    o[4 * kn] = hi;
-    o[5 * kn] = mid;
+    o[kpn] = mid;
+    o[2 * kpn] = hi;
+    o[3 * kpn] = lo;
+    o[4 * kpn] = hi;
+    o[5 * kpn] = mid;
   }
 }
 
@@ -586,7 +609,8 @@ GM_API size_t gm_segment_matmul_workspace(int64_t rows, int64_t groups, int64_t 
 
 static gm_status segment_matmul_impl(const void* x, const int64_t* ptr_host, int64_t groups, int64_t k_in,
                                      int64_t n_in, const void* w, const void* w_packed, gm_dtype out_dtype, void* out,
-                                     void* workspace, size_t workspace_bytes, gm_stream_t stream) {
+                                     void* workspace, size_t workspace_bytes, gm_stream_t stream,
+                                     int64_t a_seg_k = 0, uint32_t a_seg_map = 0, int64_t a_cols = 0) {
   using namespace gm::gmm;
   GM_REQUIRE(ptr_host && groups >= 1 && groups <= kMaxGroups, GM_ERR_INVALID_ARGUMENT,
              "segment_matmul: groups must be in [1, " + std::to_string(kMaxGroups) + "]");
@@ -645,6 +669,8 @@ static gm_status segment_matmul_impl(const void* x, const int64_t* ptr_host, int
   P.out_f32 = out_dtype == GM_F32;
   P.out = outk;
   P.tma_store = (P.bn % (128 / static_cast<int>(out_dtype == GM_F32 ? 4 : 2))) == 0 ? 1 : 0;
+  P.a_seg_k = static_cast<int32_t>(a_seg_k);
+  P.a_seg_map = a_seg_map;
   int32_t tiles = 0;
   for (int64_t g = 0; g < groups; ++g) {
     P.ptr[g] = ptr_host[g];
@@ -682,7 +708,7 @@ static gm_status segment_matmul_impl(const void* x, const int64_t* ptr_host, int
 
   CUtensorMap map_a, map_b;
   const CUtensorMapSwizzle swz = kblk == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
-  gm_status s = make_map(&map_a, xk, static_cast<uint64_t>(k), static_cast<uint64_t>(rows), kblk, BM,
+  gm_status s = make_map(&map_a, xk, static_cast<uint64_t>(a_seg_k > 0 ? a_cols : k), static_cast<uint64_t>(rows), kblk, BM,
                          CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, swz);
   if (s != GM_OK) return s;
   s = make_map(&map_b, wt, static_cast<uint64_t>(k), static_cast<uint64_t>(groups * n), kblk,
@@ -750,9 +776,10 @@ GM_API gm_status gm_segment_matmul_packed(const void* x, const int64_t* ptr_host
 
 GM_API size_t gm_segment_matmul_f32_workspace(int64_t rows, int64_t groups, int64_t k, int64_t n) {
   if (rows < 0 || groups < 0 || k < 0 || n < 0) return 0;
-  return align_up(static_cast<size_t>(rows * kSplit * k) * 2, 256) +
-         align_up(static_cast<size_t>(groups * kSplit * k * n) * 2, 256) +
-         gm_segment_matmul_workspace(rows, groups, kSplit * k, n);
+  const int64_t kp = pad_to(std::max<int64_t>(k, 1), 64);
+  return align_up(static_cast<size_t>(rows * 3 * kp) * 2, 256) +
+         align_up(static_cast<size_t>(groups * kSplit * kp * n) * 2, 256) +
+         gm_segment_matmul_workspace(rows, groups, kSplit * kp, n);
 }
 
 GM_API gm_status gm_segment_matmul_f32(const float* x, const int64_t* ptr_host, int64_t groups, int64_t k,
@@ -765,20 +792,24 @@ GM_API gm_status gm_segment_matmul_f32(const float* x, const int64_t* ptr_host, 
   GM_REQUIRE(x && w && out, GM_ERR_INVALID_ARGUMENT, "segment_matmul: null pointer");
   const size_t need = gm_segment_matmul_f32_workspace(rows, groups, k, n);
   GM_REQUIRE(workspace && workspace_bytes >= need, GM_ERR_INVALID_ARGUMENT, "segment_matmul: workspace too small");
+  const int64_t kp = pad_to(k, 64);
+  GM_REQUIRE(rows * 3 * kp < (int64_t{1} << 40) && 3 * kp < (int64_t{1} << 31), GM_ERR_INVALID_ARGUMENT,
+             "segment_matmul: operand too large");
   cudaStream_t st = as_stream(stream);
   unsigned char* b = static_cast<unsigned char*>(workspace);
   auto* xs = reinterpret_cast<__nv_bfloat16*>(b);
-  b += align_up(static_cast<size_t>(rows * kSplit * k) * 2, 256);
+  b += align_up(static_cast<size_t>(rows * 3 * kp) * 2, 256);
   auto* ws = reinterpret_cast<__nv_bfloat16*>(b);
-  b += align_up(static_cast<size_t>(groups * kSplit * k * n) * 2, 256);
-  split_x_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(rows * k, 256), kNumSMs * 32)), 256, 0, st>>>(
-      x, rows, static_cast<int>(k), xs);
+  b += align_up(static_cast<size_t>(groups * kSplit * kp * n) * 2, 256);
+  split_x_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(rows * kp / 4, 256), kNumSMs * 32)), 256, 0, st>>>(
+      x, rows, static_cast<int>(k), static_cast<int>(kp), xs);
   GM_CHECK_LAUNCH("split_x_kernel");
-  split_w_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(groups * k * n, 256), kNumSMs * 32)), 256, 0, st>>>(
-      w, static_cast<int>(groups), static_cast<int>(k), static_cast<int>(n), ws);
+  split_w_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(groups * kp * n, 256), kNumSMs * 32)), 256, 0,
+                   st>>>(w, static_cast<int>(groups), static_cast<int>(k), static_cast<int>(kp), static_cast<int>(n), ws);
   GM_CHECK_LAUNCH("split_w_kernel");
-  return gm_segment_matmul(xs, ptr_host, groups, kSplit * k, n, ws, GM_F32, out, b,
-                           workspace_bytes - static_cast<size_t>(b - static_cast<unsigned char*>(workspace)), stream);
+  return segment_matmul_impl(xs, ptr_host, groups, kSplit * kp, n, ws, nullptr, GM_F32, out, b,
+                             workspace_bytes - static_cast<size_t>(b - static_cast<unsigned char*>(workspace)), stream,
+                             kp, kSplitSegMap, 3 * kp);
 }
 
 }  // extern "C"
