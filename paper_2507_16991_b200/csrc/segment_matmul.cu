@@ -39,6 +39,7 @@ constexpr int kThreads = 64 + 32 * kEpiWarps;  // producer + MMA warps + epilogu
 constexpr uint32_t kAStageBytes = BM * BK * 2;  // 16 KB
 constexpr uint32_t kCBoxBytes = 32 * 128;       // 32 rows x 128 B
 constexpr uint32_t kCStageBytes = kEpiWarps * kCBoxBytes;  // one 4 KB staging box per epilogue warp = 32 KB
+constexpr int kCvtWarps = 4;     // fp32 split path: warps converting x tiles into bf16 pieces in smem
 
 struct Params {
   int64_t ptr[kMaxGroups + 1];        // group row offsets
@@ -59,6 +60,11 @@ struct Params {
   // of x; 2 bits per segment. a_seg_k == 0: identity.
   int32_t a_seg_k;
   uint32_t a_seg_map;
+  // fused fp32 split (SPLIT kernels): x [rows, a_ld] fp32 read by the
+  // converter warps; a_seg_k = padded K (piece stride of the W pieces)
+  const float* a_f32;
+  int32_t a_ld;
+  int32_t x_stages;                   // SPLIT: fp32 x staging ring depth
   void* out;
 };
 
@@ -199,20 +205,38 @@ __device__ __forceinline__ uint32_t pack_bf16(uint32_t lo_f32, uint32_t hi_f32) 
 // KBLK: k elements per pipeline stage — 64 (128-byte rows, SWIZZLE_128B) or 32
 // (64-byte rows, SWIZZLE_64B: twice the stages for the same bytes in flight,
 // each released after half the MMAs).
-template <int KBLK>
-__global__ void __launch_bounds__(kThreads, 1)
+// fp32 -> three bf16 pieces (see kSplit below): hi = bf16(v), mid = bf16(v - hi),
+// lo = bf16(v - hi - mid); the subtractions are exact.
+__device__ __forceinline__ void split3(float v, float& hi, float& mid, float& lo) {
+  hi = __bfloat162float(__float2bfloat16_rn(v));
+  const float r1 = __fsub_rn(v, hi);
+  mid = __bfloat162float(__float2bfloat16_rn(r1));
+  lo = __fsub_rn(r1, mid);
+}
+
+// SPLIT: fp32 operands at fp32 accuracy with the split fused into the kernel.
+// The producer TMA-loads each fp32 x tile ONCE into a staging ring; kCvtWarps
+// converter warps turn it into hi/mid/lo bf16 pieces in three swizzled smem
+// buffers of the MMA stage, and the MMA issuer forms the six products hi*hi + hi*mid + mid*hi +
+// hi*lo + lo*hi + mid*mid against the matching W pieces (K-major [G*N, 3*Kp]).
+template <int KBLK, bool SPLIT>
+__global__ void __launch_bounds__(SPLIT ? kThreads + 32 * kCvtWarps : kThreads, 1)
 segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ CUtensorMap map_a,
                       const __grid_constant__ CUtensorMap map_b, const __grid_constant__ CUtensorMap map_c) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-B alignment for the SWIZZLE_128B atoms
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int S = P.stages;
+  constexpr int kPieces = SPLIT ? 3 : 1;
   const uint32_t b_kblock_bytes = static_cast<uint32_t>(P.bn) * KBLK * 2;
-  constexpr uint32_t kAStage = BM * KBLK * 2;
+  constexpr uint32_t kAStage = BM * KBLK * 2;  // one piece
+  constexpr uint32_t kXStage = BM * KBLK * 4;  // SPLIT: one fp32 x tile
+  const int SX = SPLIT ? P.x_stages : 0;
   unsigned char* a_ring = smem;
-  unsigned char* b_buf = smem + static_cast<size_t>(S) * kAStage;
-  const size_t b_bytes = P.b_resident ? static_cast<size_t>(P.k_blocks) * b_kblock_bytes
-                                      : static_cast<size_t>(S) * b_kblock_bytes;
+  unsigned char* x_ring = smem + static_cast<size_t>(S) * kPieces * kAStage;
+  unsigned char* b_buf = x_ring + static_cast<size_t>(SX) * kXStage;
+  const size_t b_bytes = P.b_resident ? static_cast<size_t>(kPieces) * P.k_blocks * b_kblock_bytes
+                                      : static_cast<size_t>(S) * kPieces * b_kblock_bytes;
   // output staging: per epilogue warp two 32-row x 128-byte SWIZZLE_128B boxes
   unsigned char* c_stage = b_buf + b_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(c_stage + kCStageBytes);
@@ -222,15 +246,22 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
   uint64_t* tempty = bars + 2 * S + 2;// [2]
   uint64_t* bfull = bars + 2 * S + 4;
   uint64_t* bempty = bars + 2 * S + 5;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 6);
+  uint64_t* xfull = bars + 2 * S + 6;       // [SX]
+  uint64_t* xempty = bars + 2 * S + 6 + SX; // [SX]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 6 + 2 * SX);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
+      // SPLIT: each converter warp (+ the producer's W bytes when W streams)
+      mbar_init(&full[s], SPLIT ? kCvtWarps + (P.b_resident ? 0 : 1) : 1);
       mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < SX; ++s) {
+      mbar_init(&xfull[s], 1);
+      mbar_init(&xempty[s], kCvtWarps);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -260,6 +291,8 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
       uint32_t ph = 0;
       int cur_g = -1;
       uint32_t nbload = 0;
+      int sx = 0;
+      uint32_t xph = 0;
       for (int t = blockIdx.x; t < P.num_tiles; t += gridDim.x) {
         int g, mt, nt;
         decode_tile(P, t, g, mt, nt);
@@ -267,13 +300,39 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
         const int brow0 = g * P.n + nt * P.bn;
         if (P.b_resident && g != cur_g) {
           if (nbload > 0) mbar_wait(bempty, (nbload - 1) & 1);
-          mbar_expect_tx(bfull, static_cast<uint32_t>(P.k_blocks) * b_kblock_bytes);
-          for (int kb = 0; kb < P.k_blocks; ++kb)
-            tma_load_2d(b_buf + static_cast<size_t>(kb) * b_kblock_bytes, &map_b, bfull, kb * KBLK, brow0);
+          mbar_expect_tx(bfull, static_cast<uint32_t>(kPieces * P.k_blocks) * b_kblock_bytes);
+          for (int pc = 0; pc < kPieces; ++pc)
+            for (int kb = 0; kb < P.k_blocks; ++kb)
+              tma_load_2d(b_buf + static_cast<size_t>(pc * P.k_blocks + kb) * b_kblock_bytes, &map_b, bfull,
+                          pc * P.a_seg_k + kb * KBLK, brow0);
           cur_g = g;
           ++nbload;
         }
         for (int kb = 0; kb < P.k_blocks; ++kb) {
+          if constexpr (SPLIT) {
+            // fp32 x tile -> staging ring (rows / columns past the end read as zero)
+            mbar_wait(&xempty[sx], xph ^ 1);
+            mbar_expect_tx(&xfull[sx], kXStage);
+            tma_load_2d(x_ring + static_cast<size_t>(sx) * kXStage, &map_a, &xfull[sx], kb * KBLK, row0);
+            if (++sx == SX) {
+              sx = 0;
+              xph ^= 1;
+            }
+            if (P.b_resident) continue;
+            // streamed W pieces for this k-block
+            mbar_wait(&empty[s], ph ^ 1);
+            {
+              mbar_expect_tx(&full[s], kPieces * b_kblock_bytes);
+              for (int pc = 0; pc < kPieces; ++pc)
+                tma_load_2d(b_buf + static_cast<size_t>(s * kPieces + pc) * b_kblock_bytes, &map_b, &full[s],
+                            pc * P.a_seg_k + kb * KBLK, brow0);
+            }
+            if (++s == S) {
+              s = 0;
+              ph ^= 1;
+            }
+            continue;
+          }
           mbar_wait(&empty[s], ph ^ 1);
           if (P.b_resident) {
             mbar_expect_tx(&full[s], kAStage);
@@ -317,7 +376,25 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
       for (int kb = 0; kb < P.k_blocks; ++kb) {
         mbar_wait(&full[s], ph);
         tc_fence_after();
-        if (lane == 0) {
+        if (SPLIT && lane == 0) {
+          const uint32_t a_addr = smem_u32(a_ring + static_cast<size_t>(s) * kPieces * kAStage);
+          uint32_t b_addr[3];
+#pragma unroll
+          for (int pc = 0; pc < 3; ++pc)
+            b_addr[pc] = P.b_resident
+                             ? smem_u32(b_buf + static_cast<size_t>(pc * P.k_blocks + kb) * b_kblock_bytes)
+                             : smem_u32(b_buf + static_cast<size_t>(s * kPieces + pc) * b_kblock_bytes);
+          // (x piece, W piece): hi*hi, hi*mid, mid*hi, hi*lo, lo*hi, mid*mid
+          constexpr int kPa[6] = {0, 0, 1, 0, 2, 1};
+          constexpr int kPb[6] = {0, 1, 0, 2, 0, 1};
+#pragma unroll
+          for (int pr = 0; pr < 6; ++pr)
+#pragma unroll
+            for (int k = 0; k < KBLK / 16; ++k)
+              tc_mma(tmem_d, sdesc_k<KBLK>(a_addr + kPa[pr] * kAStage + k * 32),
+                     sdesc_k<KBLK>(b_addr[kPb[pr]] + k * 32), idesc, (kb > 0 || pr > 0 || k > 0) ? 1u : 0u);
+          tc_commit(&empty[s]);
+        } else if (!SPLIT && lane == 0) {
           const uint32_t a_addr = smem_u32(a_ring + static_cast<size_t>(s) * kAStage);
           const uint32_t b_addr = P.b_resident ? smem_u32(b_buf + static_cast<size_t>(kb) * b_kblock_bytes)
                                                : smem_u32(b_buf + static_cast<size_t>(s) * b_kblock_bytes);
@@ -350,10 +427,11 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
         aph ^= 1;
       }
     }
-  } else {
+  } else if (warp < 2 + kEpiWarps) {
     // ------------------------------------------------------------ epilogue
+    const bool out_f32 = SPLIT || P.out_f32 != 0;  // SPLIT writes fp32
     const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const int esz = P.out_f32 ? 4 : 2;
+    const int esz = out_f32 ? 4 : 2;
     const int chunk_cols = 128 / esz;  // columns per 128-byte TMA box
     unsigned char* my_stage = c_stage + static_cast<size_t>(warp - 2) * kCBoxBytes;
     // the two warps of a quarter split the columns; a tile too narrow to split
@@ -379,7 +457,7 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
         for (int c = c_lo; c < c_hi; c += chunk_cols) {
           // 128 bytes of this lane's row: 32 fp32 or 64 bf16 values
           uint32_t packed[32];
-          if (P.out_f32) {
+          if (out_f32) {
             tmem_ld32<32>(tbase + c, packed);
             tmem_wait_ld();
           } else {
@@ -419,7 +497,7 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
           tmem_wait_ld();
           if (live) {
             const int64_t col0 = static_cast<int64_t>(nt) * P.bn + c;
-            if (P.out_f32) {
+            if (out_f32) {
               float* o = static_cast<float*>(P.out) + row * P.n + col0;
               for (int i = 0; i < width; i += 4) st_na_v4(o + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
             } else {
@@ -441,6 +519,67 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
     }
     if (lane == 0) bulk_wait_all();  // stores complete before the CTA exits
     __syncwarp();
+  } else if constexpr (SPLIT) {
+    // ------------------------------------------------------------ converters
+    // chunk j of a stage = 8 consecutive k of one row: 32 B of fp32 read from
+    // the staging tile, one 16-B bf16 chunk written per piece at its swizzled
+    // position (consecutive lanes -> consecutive chunks: conflict-free)
+    constexpr int kChunks = KBLK / 8;
+    constexpr int kPer = BM * kChunks / (32 * kCvtWarps);
+    const int ct = (warp - 2 - kEpiWarps) * 32 + lane;
+    int s = 0, sx = 0;
+    uint32_t ph = 0, xph = 0;
+    for (int t = blockIdx.x; t < P.num_tiles; t += gridDim.x) {
+      for (int kb = 0; kb < P.k_blocks; ++kb) {
+        mbar_wait(&xfull[sx], xph);
+        const uint32_t xbase = smem_u32(x_ring + static_cast<size_t>(sx) * kXStage);
+        float4 v[kPer][2];
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+          const uint32_t a = xbase + static_cast<uint32_t>(ct + i * 32 * kCvtWarps) * 32;
+          asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                       : "=f"(v[i][0].x), "=f"(v[i][0].y), "=f"(v[i][0].z), "=f"(v[i][0].w) : "r"(a));
+          asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                       : "=f"(v[i][1].x), "=f"(v[i][1].y), "=f"(v[i][1].z), "=f"(v[i][1].w) : "r"(a + 16));
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&xempty[sx]);  // staging tile consumed
+        if (++sx == SX) {
+          sx = 0;
+          xph ^= 1;
+        }
+        mbar_wait(&empty[s], ph ^ 1);
+        const uint32_t base = smem_u32(a_ring + static_cast<size_t>(s) * kPieces * kAStage);
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+          const int j = ct + i * 32 * kCvtWarps;
+          const int r = j / kChunks, ch = j % kChunks;
+          const int sw = KBLK == 64 ? (r & 7) : ((r >> 1) & 3);  // SWIZZLE_128B / SWIZZLE_64B
+          const uint32_t off = static_cast<uint32_t>(r * KBLK * 2 + ((ch ^ sw) << 4));
+          const float f[8] = {v[i][0].x, v[i][0].y, v[i][0].z, v[i][0].w, v[i][1].x, v[i][1].y, v[i][1].z, v[i][1].w};
+          uint32_t hw[4], mw[4], lw[4];
+#pragma unroll
+          for (int e = 0; e < 8; e += 2) {
+            float h0, m0, l0, h1, m1, l1;
+            split3(f[e], h0, m0, l0);
+            split3(f[e + 1], h1, m1, l1);
+            hw[e / 2] = pack_bf16(__float_as_uint(h0), __float_as_uint(h1));
+            mw[e / 2] = pack_bf16(__float_as_uint(m0), __float_as_uint(m1));
+            lw[e / 2] = pack_bf16(__float_as_uint(l0), __float_as_uint(l1));
+          }
+          st_shared_v4(base + off, hw[0], hw[1], hw[2], hw[3]);
+          st_shared_v4(base + kAStage + off, mw[0], mw[1], mw[2], mw[3]);
+          st_shared_v4(base + 2 * kAStage + off, lw[0], lw[1], lw[2], lw[3]);
+        }
+        fence_async_smem();  // generic-proxy smem writes visible to tcgen05.mma
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[s]);
+        if (++s == S) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
   }
 
   tc_fence_before();
@@ -598,6 +737,26 @@ __global__ void split_w_kernel(const float* __restrict__ w, int groups, int k, i
   }
 }
 
+// w [G, k, n] fp32 -> K-major pieces [G*np, 3*kp] bf16 (hi | mid | lo along K),
+// zero-padded: the B operand of the fused-split kernel.
+__global__ void split_wt_kernel(const float* __restrict__ w, int groups, int k, int n, int kp, int np,
+                                __nv_bfloat16* __restrict__ wt) {
+  const int64_t total = static_cast<int64_t>(groups) * np * kp;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t g = i / (static_cast<int64_t>(np) * kp);
+    const int64_t rem = i - g * np * kp;
+    const int64_t nn = rem / kp;
+    const int64_t kk = rem - nn * kp;
+    __nv_bfloat16 hi, mid, lo;
+    split_bf16((nn < n && kk < k) ? w[(g * k + kk) * n + nn] : 0.f, hi, mid, lo);
+    __nv_bfloat16* o = wt + (g * np + nn) * 3 * kp + kk;
+    o[0] = hi;
+    o[kp] = mid;
+    o[2 * kp] = lo;
+  }
+}
+
 GM_API size_t gm_segment_matmul_workspace(int64_t rows, int64_t groups, int64_t k, int64_t n) {
   if (rows < 0 || groups < 0 || k < 0 || n < 0) return 0;
   const int64_t kp = pad_to(std::max<int64_t>(k, 1), 64), np = pad_to(std::max<int64_t>(n, 1), 16);
@@ -610,7 +769,8 @@ GM_API size_t gm_segment_matmul_workspace(int64_t rows, int64_t groups, int64_t 
 static gm_status segment_matmul_impl(const void* x, const int64_t* ptr_host, int64_t groups, int64_t k_in,
                                      int64_t n_in, const void* w, const void* w_packed, gm_dtype out_dtype, void* out,
                                      void* workspace, size_t workspace_bytes, gm_stream_t stream,
-                                     int64_t a_seg_k = 0, uint32_t a_seg_map = 0, int64_t a_cols = 0) {
+                                     int64_t a_seg_k = 0, uint32_t a_seg_map = 0, int64_t a_cols = 0,
+                                     const float* a_f32 = nullptr, int64_t a_ld = 0) {
   using namespace gm::gmm;
   GM_REQUIRE(ptr_host && groups >= 1 && groups <= kMaxGroups, GM_ERR_INVALID_ARGUMENT,
              "segment_matmul: groups must be in [1, " + std::to_string(kMaxGroups) + "]");
@@ -663,14 +823,19 @@ static gm_status segment_matmul_impl(const void* x, const int64_t* ptr_host, int
   // stages) measured slower at F=2048 (1.41 vs 1.11 PFLOP/s); GM_GEMM_KBLK=32
   // selects them for experiments.
   static const int kblk_env = [] { const char* e = getenv("GM_GEMM_KBLK"); return e ? atoi(e) : 0; }();
-  const int kblk = kblk_env == 32 ? 32 : 64;
+  // the fused fp32 split path runs 32-deep blocks: three bf16 pieces + an fp32
+  // staging tile per stage leave room for 3-4 stages only at that depth
+  const int kblk = (kblk_env == 32 || (a_f32 && kblk_env != 64)) ? 32 : 64;
   P.k_blocks = static_cast<int32_t>(k / kblk);
   P.n = static_cast<int32_t>(n);
   P.out_f32 = out_dtype == GM_F32;
   P.out = outk;
   P.tma_store = (P.bn % (128 / static_cast<int>(out_dtype == GM_F32 ? 4 : 2))) == 0 ? 1 : 0;
-  P.a_seg_k = static_cast<int32_t>(a_seg_k);
+  P.a_seg_k = static_cast<int32_t>(a_f32 ? k : a_seg_k);
   P.a_seg_map = a_seg_map;
+  P.a_f32 = a_f32;
+  P.a_ld = static_cast<int32_t>(a_ld);
+  const int pieces = a_f32 ? 3 : 1;
   int32_t tiles = 0;
   for (int64_t g = 0; g < groups; ++g) {
     P.ptr[g] = ptr_host[g];
@@ -684,18 +849,30 @@ static gm_status segment_matmul_impl(const void* x, const int64_t* ptr_host, int
   while (cols < static_cast<uint32_t>(2 * P.bn)) cols <<= 1;
   P.tmem_cols = cols;
 
-  const size_t b_full_bytes = static_cast<size_t>(P.k_blocks) * P.bn * kblk * 2;
-  const size_t b_stage_bytes = static_cast<size_t>(P.bn) * kblk * 2;
-  const size_t a_stage_bytes = static_cast<size_t>(BM) * kblk * 2;
-  P.b_resident = (P.n_tiles == 1 && b_full_bytes <= 64 * 1024) ? 1 : 0;
+  const size_t b_full_bytes = static_cast<size_t>(pieces) * P.k_blocks * P.bn * kblk * 2;
+  const size_t b_stage_bytes = static_cast<size_t>(pieces) * P.bn * kblk * 2;
+  const size_t a_stage_bytes = static_cast<size_t>(pieces) * BM * kblk * 2;
   const size_t budget = 227 * 1024 - 1024 - 512 - kCStageBytes;  // alignment slack, barriers, out staging
+  // SPLIT: an fp32 staging tile rides along with every MMA stage
+  const size_t x_stage_bytes = a_f32 ? static_cast<size_t>(BM) * kblk * 4 : 0;
   int stages;
-  if (P.b_resident) stages = static_cast<int>((budget - b_full_bytes) / a_stage_bytes);
-  else stages = static_cast<int>(budget / (a_stage_bytes + b_stage_bytes));
-  stages = std::max(2, std::min(stages, kblk == 32 ? 16 : 8));
+  if (a_f32) {
+    const int res = P.n_tiles == 1 && b_full_bytes < budget
+                        ? static_cast<int>((budget - b_full_bytes) / (a_stage_bytes + x_stage_bytes)) : 0;
+    P.b_resident = res >= 3 ? 1 : 0;
+    stages = P.b_resident ? res : static_cast<int>(budget / (a_stage_bytes + b_stage_bytes + x_stage_bytes));
+    stages = std::max(2, std::min(stages, 8));
+  } else {
+    P.b_resident = (P.n_tiles == 1 && b_full_bytes <= 64 * 1024) ? 1 : 0;
+    if (P.b_resident) stages = static_cast<int>((budget - b_full_bytes) / a_stage_bytes);
+    else stages = static_cast<int>(budget / (a_stage_bytes + b_stage_bytes));
+    stages = std::max(2, std::min(stages, kblk == 32 ? 16 : 8));
+  }
   P.stages = stages;
-  const size_t smem = 1024 + static_cast<size_t>(stages) * a_stage_bytes +
+  P.x_stages = a_f32 ? stages : 0;
+  const size_t smem = 1024 + static_cast<size_t>(stages) * (a_stage_bytes + x_stage_bytes) +
                       (P.b_resident ? b_full_bytes : static_cast<size_t>(stages) * b_stage_bytes) + kCStageBytes + 512;
+  GM_REQUIRE(smem <= 227 * 1024, GM_ERR_INVALID_ARGUMENT, "segment_matmul: tile does not fit shared memory");
 
   // K-major copy of the weights: W^T as a zero-padded [G*N, K] bf16 matrix
   // (skipped when the caller pre-packed it with gm_segment_matmul_pack_w)
@@ -708,12 +885,19 @@ static gm_status segment_matmul_impl(const void* x, const int64_t* ptr_host, int
 
   CUtensorMap map_a, map_b;
   const CUtensorMapSwizzle swz = kblk == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
-  gm_status s = make_map(&map_a, xk, static_cast<uint64_t>(a_seg_k > 0 ? a_cols : k), static_cast<uint64_t>(rows), kblk, BM,
-                         CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, swz);
+  gm_status s = make_map(&map_b, wt, static_cast<uint64_t>(pieces * k), static_cast<uint64_t>(groups * n), kblk,
+                         static_cast<uint32_t>(P.bn), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, swz);
   if (s != GM_OK) return s;
-  s = make_map(&map_b, wt, static_cast<uint64_t>(k), static_cast<uint64_t>(groups * n), kblk,
-               static_cast<uint32_t>(P.bn), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, swz);
-  if (s != GM_OK) return s;
+  if (a_f32) {
+    // fp32 x tiles for the staging ring: KBLK columns x BM rows, zero-filled past the edges
+    s = make_map(&map_a, a_f32, static_cast<uint64_t>(a_ld), static_cast<uint64_t>(rows), kblk, BM,
+                 CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (s != GM_OK) return s;
+  } else {
+    s = make_map(&map_a, xk, static_cast<uint64_t>(a_seg_k > 0 ? a_cols : k), static_cast<uint64_t>(rows), kblk, BM,
+                 CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, swz);
+    if (s != GM_OK) return s;
+  }
   // output map: [rows, n] of the output dtype, 128-byte x 32-row SWIZZLE_128B boxes
   CUtensorMap map_c;
   s = make_map(&map_c, outk, static_cast<uint64_t>(n), static_cast<uint64_t>(rows), 128 / static_cast<uint32_t>(esz),
@@ -722,10 +906,11 @@ static gm_status segment_matmul_impl(const void* x, const int64_t* ptr_host, int
   if (s != GM_OK) return s;
 
   // per call: the attribute is per device, and a process may drive several
-  auto kern = kblk == 64 ? segment_matmul_kernel<64> : segment_matmul_kernel<32>;
+  auto kern = a_f32 ? (kblk == 64 ? segment_matmul_kernel<64, true> : segment_matmul_kernel<32, true>)
+                    : (kblk == 64 ? segment_matmul_kernel<64, false> : segment_matmul_kernel<32, false>);
   GM_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   const unsigned grid = static_cast<unsigned>(std::min<int32_t>(tiles, kNumSMs));
-  kern<<<grid, kThreads, smem, st>>>(P, map_a, map_b, map_c);
+  kern<<<grid, a_f32 ? kThreads + 32 * kCvtWarps : kThreads, smem, st>>>(P, map_a, map_b, map_c);
   GM_CHECK_LAUNCH("segment_matmul_kernel");
   if (n != n_in) {
     unpad_cols_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(rows * n_in, 256), 8192)), 256, 0, st>>>(
@@ -796,6 +981,21 @@ GM_API gm_status gm_segment_matmul_f32(const float* x, const int64_t* ptr_host, 
   GM_REQUIRE(rows * 3 * kp < (int64_t{1} << 40) && 3 * kp < (int64_t{1} << 31), GM_ERR_INVALID_ARGUMENT,
              "segment_matmul: operand too large");
   cudaStream_t st = as_stream(stream);
+  // fused split (x read once by TMA, pieces formed in shared memory) when x
+  // rows meet TMA's 16-byte stride rule; GM_GEMM_FUSED_SPLIT=0 selects the staged path below
+  static const bool fused_env = [] { const char* e = getenv("GM_GEMM_FUSED_SPLIT"); return !(e && e[0] == '0'); }();
+  if (fused_env && k % 4 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0) {
+    const int64_t np = pad_to(n, 16);
+    auto* wt = static_cast<__nv_bfloat16*>(workspace);
+    const size_t wt_bytes = align_up(static_cast<size_t>(groups * np * 3 * kp) * 2, 256);
+    split_wt_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(groups * np * kp, 256), kNumSMs * 32)), 256, 0,
+                      st>>>(w, static_cast<int>(groups), static_cast<int>(k), static_cast<int>(n), static_cast<int>(kp),
+                            static_cast<int>(np), wt);
+    GM_CHECK_LAUNCH("split_wt_kernel");
+    return segment_matmul_impl(x, ptr_host, groups, kp, n, nullptr, wt, GM_F32, out,
+                               static_cast<unsigned char*>(workspace) + wt_bytes, workspace_bytes - wt_bytes, stream,
+                               0, 0, 0, x, k);
+  }
   unsigned char* b = static_cast<unsigned char*>(workspace);
   auto* xs = reinterpret_cast<__nv_bfloat16*>(b);
   b += align_up(static_cast<size_t>(rows * 3 * kp) * 2, 256);

@@ -119,10 +119,12 @@ def test_odd_shapes_pad_internally():
 # fp32 operands: split-bf16 GEMM on the same tcgen05 kernel (gm_segment_matmul_f32)
 # bar (north_star, fp32 GEMM): |gpu - ref64| <= 1e-5 * sum_k |x_ik||W_kj| + 1e-7
 # ---------------------------------------------------------------------------
-@pytest.mark.parametrize("k,n", [(3, 5), (64, 16), (100, 7), (128, 128), (130, 33), (256, 64), (512, 256)])
-def test_fp32_operands_meet_fp32_bound(k, n):
+# k % 4 == 0: fused split (TMA fp32 tiles -> pieces in smem); otherwise the staged pieces path
+@pytest.mark.parametrize("k,n", [(3, 5), (36, 40), (64, 16), (100, 7), (128, 128), (128, 512), (130, 33), (256, 64),
+                                 (512, 256), (1024, 64)])
+@pytest.mark.parametrize("ptr", [[0, 5, 5, 133, 400, 401, 1031], [0, 9000, 9001, 23000]])
+def test_fp32_operands_meet_fp32_bound(k, n, ptr):
     torch.manual_seed(k * 7 + n)
-    ptr = [0, 5, 5, 133, 400, 401, 1031]
     x = torch.randn(ptr[-1], k, device="cuda") * 3.0
     w = torch.randn(len(ptr) - 1, k, n, device="cuda") / k ** 0.5
     out = gm.segment_matmul(x, ptr, w)
