@@ -39,7 +39,10 @@ constexpr int kThreads = 64 + 32 * kEpiWarps;  // producer + MMA warps + epilogu
 constexpr uint32_t kAStageBytes = BM * BK * 2;  // 16 KB
 constexpr uint32_t kCBoxBytes = 32 * 128;       // 32 rows x 128 B
 constexpr uint32_t kCStageBytes = kEpiWarps * kCBoxBytes;  // one 4 KB staging box per epilogue warp = 32 KB
-constexpr int kCvtWarps = 4;     // fp32 split path: warps converting x tiles into bf16 pieces in smem
+#ifndef GM_CVT_WARPS
+#define GM_CVT_WARPS 8
+#endif
+constexpr int kCvtWarps = GM_CVT_WARPS;     // fp32 split path: warps converting x tiles into bf16 pieces in smem
 
 struct Params {
   int64_t ptr[kMaxGroups + 1];        // group row offsets
@@ -205,13 +208,15 @@ __device__ __forceinline__ uint32_t pack_bf16(uint32_t lo_f32, uint32_t hi_f32) 
 // KBLK: k elements per pipeline stage — 64 (128-byte rows, SWIZZLE_128B) or 32
 // (64-byte rows, SWIZZLE_64B: twice the stages for the same bytes in flight,
 // each released after half the MMAs).
-// fp32 -> three bf16 pieces (see kSplit below): hi = bf16(v), mid = bf16(v - hi),
-// lo = bf16(v - hi - mid); the subtractions are exact.
-__device__ __forceinline__ void split3(float v, float& hi, float& mid, float& lo) {
-  hi = __bfloat162float(__float2bfloat16_rn(v));
-  const float r1 = __fsub_rn(v, hi);
-  mid = __bfloat162float(__float2bfloat16_rn(r1));
-  lo = __fsub_rn(r1, mid);
+// fp32 -> three bf16 pieces (see kSplit below) for two values at once:
+// hi = bf16(v), mid = bf16(v - hi), lo = bf16(v - hi - mid), the subtractions
+// exact; one bf16x2 cvt per piece pair, halves widened back by shift / mask.
+__device__ __forceinline__ void split3x2(float a, float b, uint32_t& hw, uint32_t& mw, uint32_t& lw) {
+  hw = pack_bf16(__float_as_uint(a), __float_as_uint(b));
+  const float ra = __fsub_rn(a, __uint_as_float(hw << 16)), rb = __fsub_rn(b, __uint_as_float(hw & 0xffff0000u));
+  mw = pack_bf16(__float_as_uint(ra), __float_as_uint(rb));
+  lw = pack_bf16(__float_as_uint(__fsub_rn(ra, __uint_as_float(mw << 16))),
+                 __float_as_uint(__fsub_rn(rb, __uint_as_float(mw & 0xffff0000u))));
 }
 
 // SPLIT: fp32 operands at fp32 accuracy with the split fused into the kernel.
@@ -559,14 +564,7 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
           const float f[8] = {v[i][0].x, v[i][0].y, v[i][0].z, v[i][0].w, v[i][1].x, v[i][1].y, v[i][1].z, v[i][1].w};
           uint32_t hw[4], mw[4], lw[4];
 #pragma unroll
-          for (int e = 0; e < 8; e += 2) {
-            float h0, m0, l0, h1, m1, l1;
-            split3(f[e], h0, m0, l0);
-            split3(f[e + 1], h1, m1, l1);
-            hw[e / 2] = pack_bf16(__float_as_uint(h0), __float_as_uint(h1));
-            mw[e / 2] = pack_bf16(__float_as_uint(m0), __float_as_uint(m1));
-            lw[e / 2] = pack_bf16(__float_as_uint(l0), __float_as_uint(l1));
-          }
+          for (int e = 0; e < 8; e += 2) split3x2(f[e], f[e + 1], hw[e / 2], mw[e / 2], lw[e / 2]);
           st_shared_v4(base + off, hw[0], hw[1], hw[2], hw[3]);
           st_shared_v4(base + kAStage + off, mw[0], mw[1], mw[2], mw[3]);
           st_shared_v4(base + 2 * kAStage + off, lw[0], lw[1], lw[2], lw[3]);
