@@ -526,11 +526,11 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
     __syncwarp();
   } else if constexpr (SPLIT) {
     // ------------------------------------------------------------ converters
-    // chunk j of a stage = 8 consecutive k of one row: 32 B of fp32 read from
-    // the staging tile, one 16-B bf16 chunk written per piece at its swizzled
-    // position (consecutive lanes -> consecutive chunks: conflict-free)
-    constexpr int kChunks = KBLK / 8;
-    constexpr int kPer = BM * kChunks / (32 * kCvtWarps);
+    // unit u of a stage = 4 consecutive k of one row: 16 B of fp32 read from the
+    // staging tile, 8 B of bf16 written per piece at its swizzled position;
+    // consecutive lanes take consecutive units, so both sides are conflict-free
+    constexpr int kUnits = KBLK / 4;  // per row
+    constexpr int kPer = BM * kUnits / (32 * kCvtWarps);
     const int ct = (warp - 2 - kEpiWarps) * 32 + lane;
     int s = 0, sx = 0;
     uint32_t ph = 0, xph = 0;
@@ -538,14 +538,12 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
       for (int kb = 0; kb < P.k_blocks; ++kb) {
         mbar_wait(&xfull[sx], xph);
         const uint32_t xbase = smem_u32(x_ring + static_cast<size_t>(sx) * kXStage);
-        float4 v[kPer][2];
+        float4 v[kPer];
 #pragma unroll
         for (int i = 0; i < kPer; ++i) {
-          const uint32_t a = xbase + static_cast<uint32_t>(ct + i * 32 * kCvtWarps) * 32;
+          const uint32_t a = xbase + static_cast<uint32_t>(ct + i * 32 * kCvtWarps) * 16;
           asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-                       : "=f"(v[i][0].x), "=f"(v[i][0].y), "=f"(v[i][0].z), "=f"(v[i][0].w) : "r"(a));
-          asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-                       : "=f"(v[i][1].x), "=f"(v[i][1].y), "=f"(v[i][1].z), "=f"(v[i][1].w) : "r"(a + 16));
+                       : "=f"(v[i].x), "=f"(v[i].y), "=f"(v[i].z), "=f"(v[i].w) : "r"(a));
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&xempty[sx]);  // staging tile consumed
@@ -557,17 +555,17 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
         const uint32_t base = smem_u32(a_ring + static_cast<size_t>(s) * kPieces * kAStage);
 #pragma unroll
         for (int i = 0; i < kPer; ++i) {
-          const int j = ct + i * 32 * kCvtWarps;
-          const int r = j / kChunks, ch = j % kChunks;
+          const int u = ct + i * 32 * kCvtWarps;
+          const int r = u / kUnits, q = u % kUnits;
           const int sw = KBLK == 64 ? (r & 7) : ((r >> 1) & 3);  // SWIZZLE_128B / SWIZZLE_64B
-          const uint32_t off = static_cast<uint32_t>(r * KBLK * 2 + ((ch ^ sw) << 4));
-          const float f[8] = {v[i][0].x, v[i][0].y, v[i][0].z, v[i][0].w, v[i][1].x, v[i][1].y, v[i][1].z, v[i][1].w};
-          uint32_t hw[4], mw[4], lw[4];
-#pragma unroll
-          for (int e = 0; e < 8; e += 2) split3x2(f[e], f[e + 1], hw[e / 2], mw[e / 2], lw[e / 2]);
-          st_shared_v4(base + off, hw[0], hw[1], hw[2], hw[3]);
-          st_shared_v4(base + kAStage + off, mw[0], mw[1], mw[2], mw[3]);
-          st_shared_v4(base + 2 * kAStage + off, lw[0], lw[1], lw[2], lw[3]);
+          const uint32_t off = static_cast<uint32_t>(r * KBLK * 2 + (((q >> 1) ^ sw) << 4) + (q & 1) * 8);
+          uint32_t h0, m0, l0, h1, m1, l1;
+          split3x2(v[i].x, v[i].y, h0, m0, l0);
+          split3x2(v[i].z, v[i].w, h1, m1, l1);
+          asm volatile("st.shared.v2.b32 [%0], {%1,%2};" ::"r"(base + off), "r"(h0), "r"(h1) : "memory");
+          asm volatile("st.shared.v2.b32 [%0], {%1,%2};" ::"r"(base + kAStage + off), "r"(m0), "r"(m1) : "memory");
+          asm volatile("st.shared.v2.b32 [%0], {%1,%2};" ::"r"(base + 2 * kAStage + off), "r"(l0), "r"(l1)
+                       : "memory");
         }
         fence_async_smem();  // generic-proxy smem writes visible to tcgen05.mma
         __syncwarp();
@@ -854,12 +852,17 @@ static gm_status segment_matmul_impl(const void* x, const int64_t* ptr_host, int
   // SPLIT: an fp32 staging tile rides along with every MMA stage
   const size_t x_stage_bytes = a_f32 ? static_cast<size_t>(BM) * kblk * 4 : 0;
   int stages;
+  int xstages = 0;
   if (a_f32) {
+    static const int res_min = [] { const char* e = getenv("GM_GEMM_SPLIT_RES"); return e ? atoi(e) : 2; }();
     const int res = P.n_tiles == 1 && b_full_bytes < budget
                         ? static_cast<int>((budget - b_full_bytes) / (a_stage_bytes + x_stage_bytes)) : 0;
-    P.b_resident = res >= 3 ? 1 : 0;
+    P.b_resident = res >= res_min ? 1 : 0;
     stages = P.b_resident ? res : static_cast<int>(budget / (a_stage_bytes + b_stage_bytes + x_stage_bytes));
     stages = std::max(2, std::min(stages, 8));
+    xstages = stages;
+    if (P.b_resident)  // spare bytes deepen the fp32 staging ring
+      xstages = std::min<int>(8, static_cast<int>((budget - b_full_bytes - stages * a_stage_bytes) / x_stage_bytes));
   } else {
     P.b_resident = (P.n_tiles == 1 && b_full_bytes <= 64 * 1024) ? 1 : 0;
     if (P.b_resident) stages = static_cast<int>((budget - b_full_bytes) / a_stage_bytes);
@@ -867,8 +870,8 @@ static gm_status segment_matmul_impl(const void* x, const int64_t* ptr_host, int
     stages = std::max(2, std::min(stages, kblk == 32 ? 16 : 8));
   }
   P.stages = stages;
-  P.x_stages = a_f32 ? stages : 0;
-  const size_t smem = 1024 + static_cast<size_t>(stages) * (a_stage_bytes + x_stage_bytes) +
+  P.x_stages = xstages;
+  const size_t smem = 1024 + static_cast<size_t>(stages) * a_stage_bytes + static_cast<size_t>(xstages) * x_stage_bytes +
                       (P.b_resident ? b_full_bytes : static_cast<size_t>(stages) * b_stage_bytes) + kCStageBytes + 512;
   GM_REQUIRE(smem <= 227 * 1024, GM_ERR_INVALID_ARGUMENT, "segment_matmul: tile does not fit shared memory");
 

@@ -186,6 +186,13 @@ def mag_layer():
     r = {"config": "C3 hetero SAGE layer (4 relations mean SpMM + 2 grouped GEMMs + combine, bf16 W)", "ms": ms,
          "edges": e_tot, "nodes": sum(counts.values())}
     print(json.dumps(r), flush=True)
+    # the reference's dtype throughout: fp32 weights -> fp32-accurate fused-split GEMMs
+    wn32 = {k: v.float() for k, v in wn.items()}
+    ws32 = {k: v.float() for k, v in ws.items()}
+    ms = timed(lambda: hetero_sage_layer(edges, h, wn32, ws32, b), reps=10)
+    r = {"config": "C3 hetero SAGE layer, fp32 W (fp32-accurate GEMMs)", "ms": ms,
+         "edges": e_tot, "nodes": sum(counts.values())}
+    print(json.dumps(r), flush=True)
 
 
 if __name__ == "__main__":
