@@ -119,9 +119,11 @@ def make_graph(gm, L, n, e, f, device, stream):
     return g, x
 
 
-def bench_segment_matmul(gm, L, device, f=128, rows=1_939_743, rank=0, world=1, dist=None):
+def bench_segment_matmul(gm, L, device, f=128, rows=1_939_743, rank=0, world=1, dist=None, fp32=False):
     """Node-type segment_matmul, K = N = f, bf16 in/out. f=128: C3 (OGB-MAG)
     with the real per-type row counts; larger f: the tensor-bound F-sweep.
+    fp32=True: the reference's dtype, fp32 in/out through the fused 3-piece
+    split (six bf16 products per MAC: tensor ceiling = bf16 peak / 6).
     world > 1: W replicated, every group's rows split evenly
     across ranks, no collective; time = max over ranks, TFLOP/s of the whole job."""
     if f == 128 and rows == 1_939_743:
@@ -135,6 +137,9 @@ def bench_segment_matmul(gm, L, device, f=128, rows=1_939_743, rank=0, world=1, 
         ptr.append(ptr[-1] + (m * (rank + 1)) // world - (m * rank) // world)
     x = torch.randn(ptr[-1], f, device=device).to(torch.bfloat16)
     w = (torch.randn(4, f, f, device=device) / f ** 0.5).to(torch.bfloat16)
+    if fp32:
+        x, w = x.float(), w.float()
+    esz, tscale = (4, 6) if fp32 else (2, 1)
     try:
         for _ in range(3):
             gm.segment_matmul(x, ptr, w)
@@ -154,12 +159,12 @@ def bench_segment_matmul(gm, L, device, f=128, rows=1_939_743, rank=0, world=1, 
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     flops = 2.0 * total_rows * f * f
-    byts = 2.0 * total_rows * f * 2 + world * 4 * f * f * 2
+    byts = 2.0 * total_rows * f * esz + world * 4 * f * f * esz
     hbm, bf16_peak, _ = peaks()
     ai = flops / byts
-    hbm, bf16_peak = hbm * world, bf16_peak * world
+    hbm, bf16_peak = hbm * world, bf16_peak * world / tscale
     ceiling = min(bf16_peak, ai * hbm / 1e3)
-    return {"shape": f"sum_M={total_rows},K=N={f},G=4,bf16", "n_gpus": world, "ms": ms, "tflops": flops / ms / 1e9,
+    return {"shape": f"sum_M={total_rows},K=N={f},G=4,{'fp32' if fp32 else 'bf16'}", "n_gpus": world, "ms": ms, "tflops": flops / ms / 1e9,
             "frac_tensor_peak": flops / ms / 1e9 / bf16_peak, "achieved_gbs": byts / ms / 1e6,
             "frac_hbm": byts / ms / 1e6 / hbm, "roofline_ceiling_tflops": ceiling,
             "frac_roofline": flops / ms / 1e9 / ceiling,
@@ -477,6 +482,7 @@ def main():
             secondary = {"error": str(exc)[:300]}
     if world == 1 and not args.no_secondary:
         secondary = {"segment_matmul_C3": bench_segment_matmul(gm, L, device),
+                     "segment_matmul_C3_fp32": bench_segment_matmul(gm, L, device, fp32=True),
                      "segment_matmul_F1024": bench_segment_matmul(gm, L, device, f=1024, rows=500_000),
                      "segment_matmul_F2048": bench_segment_matmul(gm, L, device, f=2048, rows=262_144)}
         # max + argmax SpMM on the same graph
