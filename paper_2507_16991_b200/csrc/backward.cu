@@ -167,6 +167,96 @@ __global__ void __launch_bounds__(kDotWarps * 32) edge_dot_csc_kernel(const int3
   }
 }
 
+// fp32 rows of 16-byte multiples: the 32 source rows of a warp's batch are
+// gathered into shared memory with 16-byte cp.async (the (row, piece) pairs
+// spread over all lanes), double-buffered so batch n+1 streams in while the
+// lanes run batch n's dot chains; each lane's destination row (mostly shared
+// by consecutive CSC entries) is read straight from L1 with float4 loads. Rows
+// wider than kDotChunk floats go through in column chunks. The per-edge chain
+// is the same sequential mul/add as above: bit-identical results.
+constexpr int kDotChunk = 128;  // floats of a row staged per unit
+constexpr int kDotV4Warps = 4;
+// stage unit u = (batch u / nc, column chunk u % nc) of this warp into buffer u & 1
+__device__ __forceinline__ void dot_v4_issue(int64_t u, int64_t gw, int64_t nw, int nc, int64_t e, int64_t k0,
+                                             int64_t f, int stride, const int32_t* __restrict__ col,
+                                             const float* __restrict__ b, float* buf, int lane, int32_t& rb_iss) {
+  const int64_t base = (gw + (u / nc) * nw) * 32;
+  const int ci = static_cast<int>(u % nc);
+  if (ci == 0) rb_iss = base + lane < e ? col[k0 + base + lane] : 0;
+  const int ne = static_cast<int>(e - base < 32 ? e - base : 32);
+  const int64_t c0 = static_cast<int64_t>(ci) * kDotChunk;
+  const int n16 = static_cast<int>((f - c0 < kDotChunk ? f - c0 : kDotChunk) / 4);  // 16-B pieces per row
+  float* stage = buf + (u & 1) * 32 * stride;
+  for (int idx = lane; idx < 32 * n16; idx += 32) {
+    const int t = idx / n16, pc = idx - t * n16;
+    const int32_t rbt = __shfl_sync(0xffffffffu, rb_iss, t);  // every lane reaches the shuffle
+    if (t < ne) {
+      const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(stage + t * stride + pc * 4));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(b + static_cast<int64_t>(rbt) * f + c0 + pc * 4)
+                   : "memory");
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__global__ void __launch_bounds__(kDotV4Warps * 32) edge_dot_csc_v4_kernel(
+    const int32_t* __restrict__ rows, const int32_t* __restrict__ col, const int32_t* __restrict__ perm, int64_t k0,
+    int64_t e, const float* __restrict__ a, const float* __restrict__ b, int64_t f, int stride,
+    float* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char dot_smem[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  float* buf = reinterpret_cast<float*>(dot_smem) + static_cast<size_t>(wib) * 2 * 32 * stride;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * kDotV4Warps;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * kDotV4Warps + wib;
+  const int64_t nb_all = (e + 31) / 32;
+  if (gw >= nb_all) return;
+  const int nc = static_cast<int>((f + kDotChunk - 1) / kDotChunk);
+  const int64_t units = ((nb_all - gw + nw - 1) / nw) * nc;
+
+  int32_t rb_iss = 0;
+  float acc = 0.f;
+  int32_t ra = 0;
+  dot_v4_issue(0, gw, nw, nc, e, k0, f, stride, col, b, buf, lane, rb_iss);
+  for (int64_t u = 0; u < units; ++u) {
+    if (u + 1 < units) dot_v4_issue(u + 1, gw, nw, nc, e, k0, f, stride, col, b, buf, lane, rb_iss);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    const int64_t base = (gw + (u / nc) * nw) * 32;
+    const int ci = static_cast<int>(u % nc);
+    const int64_t my = base + lane;
+    if (ci == 0) {
+      acc = 0.f;
+      ra = my < e ? rows[k0 + my] : 0;
+    }
+    const int64_t c0 = static_cast<int64_t>(ci) * kDotChunk;
+    const int n4 = static_cast<int>((f - c0 < kDotChunk ? f - c0 : kDotChunk) / 4);
+    // the destination row's chunk goes to registers first: all its loads are in
+    // flight together (they mostly hit L1/L2: consecutive entries share it)
+    float4 av[kDotChunk / 4];
+    const float4* pa = reinterpret_cast<const float4*>(a + static_cast<int64_t>(ra) * f + c0);
+#pragma unroll
+    for (int j = 0; j < kDotChunk / 4; ++j)
+      if (j < n4) av[j] = __ldg(pa + j);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncwarp();
+    if (my < e) {
+      const float* pb = buf + (u & 1) * 32 * stride + lane * stride;
+#pragma unroll
+      for (int j = 0; j < kDotChunk / 4; ++j) {
+        if (j < n4) {
+          const float4 bv = *reinterpret_cast<const float4*>(pb + 4 * j);
+          acc = __fadd_rn(acc, __fmul_rn(av[j].x, bv.x));
+          acc = __fadd_rn(acc, __fmul_rn(av[j].y, bv.y));
+          acc = __fadd_rn(acc, __fmul_rn(av[j].z, bv.z));
+          acc = __fadd_rn(acc, __fmul_rn(av[j].w, bv.w));
+        }
+      }
+      if (ci == nc - 1) out[perm[k0 + my]] = acc;
+    }
+    __syncwarp();  // stage (u & 1) is refilled by the issue of unit u + 2
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
 __global__ void entry_rows_kernel(const int64_t* __restrict__ rowptr, int64_t rows, int32_t* __restrict__ out) {
   // one warp per row: the row id for each of its entries (positions relative to rowptr[0])
   const int lane = threadIdx.x & 31;
@@ -221,8 +311,27 @@ GM_API gm_status gm_edge_dot_csc(gm_dtype dtype, const gm_csr* csc, const int32_
   cudaStream_t st = as_stream(stream);
   GM_TRY_CUDA(cudaMemcpyAsync(&k0, csc->rowptr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GM_TRY_CUDA(cudaStreamSynchronize(st));
-  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(csc->nnz, 32 * kDotWarps), kNumSMs * 64));
   // entry_rows is indexed from the view's first entry: pass it pre-offset by -k0
+  static const bool v4_env = [] { const char* ev = getenv("GM_EDGE_DOT_V4"); return !(ev && ev[0] == '0'); }();
+  if (dtype == GM_F32 && v4_env && f % 4 == 0 &&
+      ((reinterpret_cast<uintptr_t>(a_by_dst) | reinterpret_cast<uintptr_t>(b_by_src)) & 15) == 0) {
+    // row stride in smem: 16-B aligned, odd in 16-B units (conflict-free float4 reads)
+    int stride = static_cast<int>(std::min<int64_t>(f, kDotChunk));
+    if ((stride / 4) % 2 == 0) stride += 4;
+    const size_t smem = sizeof(float) * 2 * 32 * stride * kDotV4Warps;
+    GM_TRY_CUDA(cudaFuncSetAttribute(edge_dot_csc_v4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+    int per_sm = 0;
+    GM_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, edge_dot_csc_v4_kernel, kDotV4Warps * 32, smem));
+    const unsigned blocks = static_cast<unsigned>(
+        std::min<int64_t>(ceil_div(csc->nnz, 32 * kDotV4Warps), static_cast<int64_t>(kNumSMs) * std::max(per_sm, 1)));
+    edge_dot_csc_v4_kernel<<<blocks, kDotV4Warps * 32, smem, st>>>(
+        entry_rows - k0, csc->col, csc->perm, k0, csc->nnz, static_cast<const float*>(a_by_dst),
+        static_cast<const float*>(b_by_src), f, stride, static_cast<float*>(out));
+    GM_CHECK_LAUNCH("edge_dot_csc_v4_kernel");
+    return GM_OK;
+  }
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(csc->nnz, 32 * kDotWarps), kNumSMs * 64));
   if (dtype == GM_F32) {
     const size_t smem = sizeof(float) * 2 * 32 * 33 * kDotWarps;
     GM_TRY_CUDA(cudaFuncSetAttribute(edge_dot_csc_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -19,3 +19,13 @@ for _ in range(2):
     L.check(L.lib().gm_edge_dot(L.GM_F32, g.src().data_ptr(), g.dst().data_ptr(), e, gout.data_ptr(), x.data_ptr(), f,
                                 dw.data_ptr(), torch.cuda.current_stream().cuda_stream))
 torch.cuda.synchronize()
+
+# the CSC-order kernel spmm_backward uses (gm_edge_dot_csc)
+import ctypes as C  # noqa: E402
+csc = g.to_csc()
+cs = csc.c_struct()
+rows = csc.entry_rows()
+for _ in range(2):
+    L.check(L.lib().gm_edge_dot_csc(L.GM_F32, C.byref(cs), rows.data_ptr(), gout.data_ptr(), x.data_ptr(), f,
+                                    dw.data_ptr(), torch.cuda.current_stream().cuda_stream))
+torch.cuda.synchronize()
