@@ -174,9 +174,9 @@ __global__ void __launch_bounds__(kDotWarps * 32) edge_dot_csc_kernel(const int3
 // by consecutive CSC entries) is read straight from L1 with float4 loads. Rows
 // wider than kDotChunk floats go through in column chunks. The per-edge chain
 // is the same sequential mul/add as above: bit-identical results.
-constexpr int kDotChunk = 128;  // floats of a row staged per unit
 constexpr int kDotV4Warps = 4;
 // stage unit u = (batch u / nc, column chunk u % nc) of this warp into buffer u & 1
+template <int kDotChunk>
 __device__ __forceinline__ void dot_v4_issue(int64_t u, int64_t gw, int64_t nw, int nc, int64_t e, int64_t k0,
                                              int64_t f, int stride, const int32_t* __restrict__ col,
                                              const float* __restrict__ b, float* buf, int lane, int32_t& rb_iss) {
@@ -198,6 +198,7 @@ __device__ __forceinline__ void dot_v4_issue(int64_t u, int64_t gw, int64_t nw, 
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
+template <int kDotChunk>  // floats of a row staged per unit
 __global__ void __launch_bounds__(kDotV4Warps * 32) edge_dot_csc_v4_kernel(
     const int32_t* __restrict__ rows, const int32_t* __restrict__ col, const int32_t* __restrict__ perm, int64_t k0,
     int64_t e, const float* __restrict__ a, const float* __restrict__ b, int64_t f, int stride,
@@ -216,9 +217,9 @@ __global__ void __launch_bounds__(kDotV4Warps * 32) edge_dot_csc_v4_kernel(
   int32_t rb_iss = 0;
   float acc = 0.f;
   int32_t ra = 0;
-  dot_v4_issue(0, gw, nw, nc, e, k0, f, stride, col, b, buf, lane, rb_iss);
+  dot_v4_issue<kDotChunk>(0, gw, nw, nc, e, k0, f, stride, col, b, buf, lane, rb_iss);
   for (int64_t u = 0; u < units; ++u) {
-    if (u + 1 < units) dot_v4_issue(u + 1, gw, nw, nc, e, k0, f, stride, col, b, buf, lane, rb_iss);
+    if (u + 1 < units) dot_v4_issue<kDotChunk>(u + 1, gw, nw, nc, e, k0, f, stride, col, b, buf, lane, rb_iss);
     else asm volatile("cp.async.commit_group;" ::: "memory");
     const int64_t base = (gw + (u / nc) * nw) * 32;
     const int ci = static_cast<int>(u % nc);
@@ -315,17 +316,22 @@ GM_API gm_status gm_edge_dot_csc(gm_dtype dtype, const gm_csr* csc, const int32_
   static const bool v4_env = [] { const char* ev = getenv("GM_EDGE_DOT_V4"); return !(ev && ev[0] == '0'); }();
   if (dtype == GM_F32 && v4_env && f % 4 == 0 &&
       ((reinterpret_cast<uintptr_t>(a_by_dst) | reinterpret_cast<uintptr_t>(b_by_src)) & 15) == 0) {
+    // column chunk per staged unit (GM_EDGE_DOT_CHUNK: 16 / 32 / 64 / 128 floats)
+    static const int chunk_env = [] { const char* ev = getenv("GM_EDGE_DOT_CHUNK"); return ev ? atoi(ev) : 32; }();
+    const int chunk = chunk_env == 128 ? 128 : chunk_env == 64 ? 64 : chunk_env == 16 ? 16 : 32;
     // row stride in smem: 16-B aligned, odd in 16-B units (conflict-free float4 reads)
-    int stride = static_cast<int>(std::min<int64_t>(f, kDotChunk));
+    int stride = static_cast<int>(std::min<int64_t>(f, chunk));
     if ((stride / 4) % 2 == 0) stride += 4;
     const size_t smem = sizeof(float) * 2 * 32 * stride * kDotV4Warps;
-    GM_TRY_CUDA(cudaFuncSetAttribute(edge_dot_csc_v4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem)));
+    auto kern = chunk == 128 ? edge_dot_csc_v4_kernel<128>
+                : chunk == 64 ? edge_dot_csc_v4_kernel<64>
+                : chunk == 16 ? edge_dot_csc_v4_kernel<16> : edge_dot_csc_v4_kernel<32>;
+    GM_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int per_sm = 0;
-    GM_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, edge_dot_csc_v4_kernel, kDotV4Warps * 32, smem));
+    GM_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDotV4Warps * 32, smem));
     const unsigned blocks = static_cast<unsigned>(
         std::min<int64_t>(ceil_div(csc->nnz, 32 * kDotV4Warps), static_cast<int64_t>(kNumSMs) * std::max(per_sm, 1)));
-    edge_dot_csc_v4_kernel<<<blocks, kDotV4Warps * 32, smem, st>>>(
+    kern<<<blocks, kDotV4Warps * 32, smem, st>>>(
         entry_rows - k0, csc->col, csc->perm, k0, csc->nnz, static_cast<const float*>(a_by_dst),
         static_cast<const float*>(b_by_src), f, stride, static_cast<float*>(out));
     GM_CHECK_LAUNCH("edge_dot_csc_v4_kernel");
