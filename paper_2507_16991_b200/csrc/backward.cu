@@ -175,7 +175,11 @@ __global__ void __launch_bounds__(kDotWarps * 32) edge_dot_csc_kernel(const int3
 // wider than kDotChunk floats go through in column chunks. The per-edge chain
 // is the same sequential mul/add as above: bit-identical results.
 constexpr int kDotV4Warps = 4;
-// stage unit u = (batch u / nc, column chunk u % nc) of this warp into buffer u & 1
+#ifndef GM_DOT_BUFS
+#define GM_DOT_BUFS 2
+#endif
+constexpr int kDotBufs = GM_DOT_BUFS;  // staged units per warp (3 and 4 measured slower: fewer resident warps)
+// stage unit u = (batch u / nc, column chunk u % nc) of this warp into buffer u % kDotBufs
 template <int kDotChunk>
 __device__ __forceinline__ void dot_v4_issue(int64_t u, int64_t gw, int64_t nw, int nc, int64_t e, int64_t k0,
                                              int64_t f, int stride, const int32_t* __restrict__ col,
@@ -186,7 +190,7 @@ __device__ __forceinline__ void dot_v4_issue(int64_t u, int64_t gw, int64_t nw, 
   const int ne = static_cast<int>(e - base < 32 ? e - base : 32);
   const int64_t c0 = static_cast<int64_t>(ci) * kDotChunk;
   const int n16 = static_cast<int>((f - c0 < kDotChunk ? f - c0 : kDotChunk) / 4);  // 16-B pieces per row
-  float* stage = buf + (u & 1) * 32 * stride;
+  float* stage = buf + (u % kDotBufs) * 32 * stride;
   for (int idx = lane; idx < 32 * n16; idx += 32) {
     const int t = idx / n16, pc = idx - t * n16;
     const int32_t rbt = __shfl_sync(0xffffffffu, rb_iss, t);  // every lane reaches the shuffle
@@ -206,7 +210,7 @@ __global__ void __launch_bounds__(kDotV4Warps * 32) edge_dot_csc_v4_kernel(
   extern __shared__ __align__(16) unsigned char dot_smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  float* buf = reinterpret_cast<float*>(dot_smem) + static_cast<size_t>(wib) * 2 * 32 * stride;
+  float* buf = reinterpret_cast<float*>(dot_smem) + static_cast<size_t>(wib) * kDotBufs * 32 * stride;
   const int64_t nw = static_cast<int64_t>(gridDim.x) * kDotV4Warps;
   const int64_t gw = static_cast<int64_t>(blockIdx.x) * kDotV4Warps + wib;
   const int64_t nb_all = (e + 31) / 32;
@@ -217,9 +221,13 @@ __global__ void __launch_bounds__(kDotV4Warps * 32) edge_dot_csc_v4_kernel(
   int32_t rb_iss = 0;
   float acc = 0.f;
   int32_t ra = 0;
-  dot_v4_issue<kDotChunk>(0, gw, nw, nc, e, k0, f, stride, col, b, buf, lane, rb_iss);
+  for (int64_t u = 0; u < kDotBufs - 1; ++u) {
+    if (u < units) dot_v4_issue<kDotChunk>(u, gw, nw, nc, e, k0, f, stride, col, b, buf, lane, rb_iss);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   for (int64_t u = 0; u < units; ++u) {
-    if (u + 1 < units) dot_v4_issue<kDotChunk>(u + 1, gw, nw, nc, e, k0, f, stride, col, b, buf, lane, rb_iss);
+    if (u + kDotBufs - 1 < units)
+      dot_v4_issue<kDotChunk>(u + kDotBufs - 1, gw, nw, nc, e, k0, f, stride, col, b, buf, lane, rb_iss);
     else asm volatile("cp.async.commit_group;" ::: "memory");
     const int64_t base = (gw + (u / nc) * nw) * 32;
     const int ci = static_cast<int>(u % nc);
@@ -237,10 +245,10 @@ __global__ void __launch_bounds__(kDotV4Warps * 32) edge_dot_csc_v4_kernel(
 #pragma unroll
     for (int j = 0; j < kDotChunk / 4; ++j)
       if (j < n4) av[j] = __ldg(pa + j);
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    asm volatile("cp.async.wait_group %0;" ::"n"(kDotBufs - 1) : "memory");
     __syncwarp();
     if (my < e) {
-      const float* pb = buf + (u & 1) * 32 * stride + lane * stride;
+      const float* pb = buf + (u % kDotBufs) * 32 * stride + lane * stride;
 #pragma unroll
       for (int j = 0; j < kDotChunk / 4; ++j) {
         if (j < n4) {
@@ -253,7 +261,7 @@ __global__ void __launch_bounds__(kDotV4Warps * 32) edge_dot_csc_v4_kernel(
       }
       if (ci == nc - 1) out[perm[k0 + my]] = acc;
     }
-    __syncwarp();  // stage (u & 1) is refilled by the issue of unit u + 2
+    __syncwarp();  // this stage is refilled by the issue of unit u + kDotBufs
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
@@ -322,7 +330,7 @@ GM_API gm_status gm_edge_dot_csc(gm_dtype dtype, const gm_csr* csc, const int32_
     // row stride in smem: 16-B aligned, odd in 16-B units (conflict-free float4 reads)
     int stride = static_cast<int>(std::min<int64_t>(f, chunk));
     if ((stride / 4) % 2 == 0) stride += 4;
-    const size_t smem = sizeof(float) * 2 * 32 * stride * kDotV4Warps;
+    const size_t smem = sizeof(float) * kDotBufs * 32 * stride * kDotV4Warps;
     auto kern = chunk == 128 ? edge_dot_csc_v4_kernel<128>
                 : chunk == 64 ? edge_dot_csc_v4_kernel<64>
                 : chunk == 16 ? edge_dot_csc_v4_kernel<16> : edge_dot_csc_v4_kernel<32>;
