@@ -269,11 +269,14 @@ GM_API gm_status gm_segment_matmul_packed(const void* x, const int64_t* ptr_host
                                           void* workspace, size_t workspace_bytes, gm_stream_t stream);
 
 /* fp32 grouped_matmul (hetero.hpp:134-157 with S = float) at fp32 accuracy on
- * the same tcgen05 kernel: each fp32 operand is split into three bf16 pieces
- * (hi, mid, lo; residual <= 2^-27 |v|) laid out along K so that ONE bf16 GEMM
- * over K' = 6K with fp32 TMEM accumulation forms the six products down to
- * 2^-18 scale: |out - x W| <= 1e-5 * sum_k |x_ik||W_kj| (the north_star fp32
- * GEMM bar). x [rows, k], w [groups, k, n], out [rows, n], all f32 row-major. */
+ * the tcgen05 tensor pipe: each fp32 operand is split into three bf16 pieces
+ * (hi, mid, lo; residual <= 2^-27 |v|) and fp32 TMEM accumulators collect the
+ * six products hi*hi + hi*mid + mid*hi + hi*lo + lo*hi + mid*mid down to 2^-18
+ * scale: |out - x W| <= 1e-5 * sum_k |x_ik||W_kj| (the north_star fp32 GEMM
+ * bar). When k % 4 == 0 and x is 16-byte aligned the split of x happens inside
+ * the GEMM kernel (x read once); otherwise x is split into a staged piece
+ * matrix first. x [rows, k], w [groups, k, n], out [rows, n], all f32
+ * row-major; the workspace size covers either route. */
 GM_API size_t gm_segment_matmul_f32_workspace(int64_t rows, int64_t groups, int64_t k, int64_t n);
 GM_API gm_status gm_segment_matmul_f32(const float* x, const int64_t* ptr_host, int64_t groups, int64_t k,
                                        int64_t n, const float* w, float* out, void* workspace, size_t workspace_bytes,
