@@ -267,6 +267,14 @@ GM_API size_t gm_segment_matmul_packed_workspace(int64_t rows, int64_t groups, i
 GM_API gm_status gm_segment_matmul_packed(const void* x, const int64_t* ptr_host, int64_t groups, int64_t k,
                                           int64_t n, const void* packed_w, gm_dtype out_dtype, void* out,
                                           void* workspace, size_t workspace_bytes, gm_stream_t stream);
+/* fp32 activations x bf16 pre-packed weights, fp32 out: x is read once as fp32
+ * by the GEMM kernel and rounded to bf16 (RNE) in shared memory — the same
+ * operands as casting x to bf16 first, without the separate cast pass.
+ * Requires k % 4 == 0 and x 16-byte aligned; workspace as
+ * gm_segment_matmul_packed_workspace. */
+GM_API gm_status gm_segment_matmul_packed_xf32(const float* x, const int64_t* ptr_host, int64_t groups, int64_t k,
+                                               int64_t n, const void* packed_w, float* out, void* workspace,
+                                               size_t workspace_bytes, gm_stream_t stream);
 
 /* fp32 grouped_matmul (hetero.hpp:134-157 with S = float) at fp32 accuracy on
  * the tcgen05 tensor pipe: each fp32 operand is split into three bf16 pieces

@@ -98,6 +98,8 @@ SIGNATURES = {
     "gm_segment_matmul_packed_workspace": (C.c_size_t, [_I64, _I64, _I64, _I64]),
     "gm_segment_matmul_packed": (C.c_int, [_P, C.POINTER(C.c_int64), _I64, _I64, _I64, _P, C.c_int, _P, _P,
                                            C.c_size_t, _P]),
+    "gm_segment_matmul_packed_xf32": (C.c_int, [_P, C.POINTER(C.c_int64), _I64, _I64, _I64, _P, _P, _P, C.c_size_t,
+                                                _P]),
     "gm_segment_matmul_f32_workspace": (C.c_size_t, [_I64, _I64, _I64, _I64]),
     "gm_segment_matmul_f32": (C.c_int, [_P, C.POINTER(C.c_int64), _I64, _I64, _I64, _P, _P, _P, C.c_size_t, _P]),
     "gm_partition_rows_by_nnz": (C.c_int, [C.POINTER(C.c_int64), _I64, C.c_int32,

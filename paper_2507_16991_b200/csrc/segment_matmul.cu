@@ -224,15 +224,18 @@ __device__ __forceinline__ void split3x2(float a, float b, uint32_t& hw, uint32_
 // converter warps turn it into hi/mid/lo bf16 pieces in three swizzled smem
 // buffers of the MMA stage, and the MMA issuer forms the six products hi*hi + hi*mid + mid*hi +
 // hi*lo + lo*hi + mid*mid against the matching W pieces (K-major [G*N, 3*Kp]).
-template <int KBLK, bool SPLIT>
-__global__ void __launch_bounds__(SPLIT ? kThreads + 32 * kCvtWarps : kThreads, 1)
+// CVT = 1: the same converter path with a single piece (fp32 x rounded to bf16
+// in the kernel, bf16 W): x is read once as fp32 instead of a separate cast pass.
+template <int KBLK, int CVT>
+__global__ void __launch_bounds__(CVT > 0 ? kThreads + 32 * kCvtWarps : kThreads, 1)
 segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ CUtensorMap map_a,
                       const __grid_constant__ CUtensorMap map_b, const __grid_constant__ CUtensorMap map_c) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-B alignment for the SWIZZLE_128B atoms
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int S = P.stages;
-  constexpr int kPieces = SPLIT ? 3 : 1;
+  constexpr bool SPLIT = CVT > 0;           // x arrives as fp32 through the converter warps
+  constexpr int kPieces = CVT == 3 ? 3 : 1;  // bf16 pieces per operand
   const uint32_t b_kblock_bytes = static_cast<uint32_t>(P.bn) * KBLK * 2;
   constexpr uint32_t kAStage = BM * KBLK * 2;  // one piece
   constexpr uint32_t kXStage = BM * KBLK * 4;  // SPLIT: one fp32 x tile
@@ -383,17 +386,18 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
         tc_fence_after();
         if (SPLIT && lane == 0) {
           const uint32_t a_addr = smem_u32(a_ring + static_cast<size_t>(s) * kPieces * kAStage);
-          uint32_t b_addr[3];
+          uint32_t b_addr[3] = {0u, 0u, 0u};
 #pragma unroll
-          for (int pc = 0; pc < 3; ++pc)
+          for (int pc = 0; pc < kPieces; ++pc)
             b_addr[pc] = P.b_resident
                              ? smem_u32(b_buf + static_cast<size_t>(pc * P.k_blocks + kb) * b_kblock_bytes)
                              : smem_u32(b_buf + static_cast<size_t>(s * kPieces + pc) * b_kblock_bytes);
           // (x piece, W piece): hi*hi, hi*mid, mid*hi, hi*lo, lo*hi, mid*mid
           constexpr int kPa[6] = {0, 0, 1, 0, 2, 1};
           constexpr int kPb[6] = {0, 1, 0, 2, 0, 1};
+          constexpr int kPairs = CVT == 3 ? 6 : 1;
 #pragma unroll
-          for (int pr = 0; pr < 6; ++pr)
+          for (int pr = 0; pr < kPairs; ++pr)
 #pragma unroll
             for (int k = 0; k < KBLK / 16; ++k)
               tc_mma(tmem_d, sdesc_k<KBLK>(a_addr + kPa[pr] * kAStage + k * 32),
@@ -559,13 +563,19 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
           const int r = u / kUnits, q = u % kUnits;
           const int sw = KBLK == 64 ? (r & 7) : ((r >> 1) & 3);  // SWIZZLE_128B / SWIZZLE_64B
           const uint32_t off = static_cast<uint32_t>(r * KBLK * 2 + (((q >> 1) ^ sw) << 4) + (q & 1) * 8);
-          uint32_t h0, m0, l0, h1, m1, l1;
-          split3x2(v[i].x, v[i].y, h0, m0, l0);
-          split3x2(v[i].z, v[i].w, h1, m1, l1);
-          asm volatile("st.shared.v2.b32 [%0], {%1,%2};" ::"r"(base + off), "r"(h0), "r"(h1) : "memory");
-          asm volatile("st.shared.v2.b32 [%0], {%1,%2};" ::"r"(base + kAStage + off), "r"(m0), "r"(m1) : "memory");
-          asm volatile("st.shared.v2.b32 [%0], {%1,%2};" ::"r"(base + 2 * kAStage + off), "r"(l0), "r"(l1)
-                       : "memory");
+          if constexpr (CVT == 3) {
+            uint32_t h0, m0, l0, h1, m1, l1;
+            split3x2(v[i].x, v[i].y, h0, m0, l0);
+            split3x2(v[i].z, v[i].w, h1, m1, l1);
+            asm volatile("st.shared.v2.b32 [%0], {%1,%2};" ::"r"(base + off), "r"(h0), "r"(h1) : "memory");
+            asm volatile("st.shared.v2.b32 [%0], {%1,%2};" ::"r"(base + kAStage + off), "r"(m0), "r"(m1) : "memory");
+            asm volatile("st.shared.v2.b32 [%0], {%1,%2};" ::"r"(base + 2 * kAStage + off), "r"(l0), "r"(l1)
+                         : "memory");
+          } else {
+            const uint32_t h0 = pack_bf16(__float_as_uint(v[i].x), __float_as_uint(v[i].y));
+            const uint32_t h1 = pack_bf16(__float_as_uint(v[i].z), __float_as_uint(v[i].w));
+            asm volatile("st.shared.v2.b32 [%0], {%1,%2};" ::"r"(base + off), "r"(h0), "r"(h1) : "memory");
+          }
         }
         fence_async_smem();  // generic-proxy smem writes visible to tcgen05.mma
         __syncwarp();
@@ -766,7 +776,7 @@ static gm_status segment_matmul_impl(const void* x, const int64_t* ptr_host, int
                                      int64_t n_in, const void* w, const void* w_packed, gm_dtype out_dtype, void* out,
                                      void* workspace, size_t workspace_bytes, gm_stream_t stream,
                                      int64_t a_seg_k = 0, uint32_t a_seg_map = 0, int64_t a_cols = 0,
-                                     const float* a_f32 = nullptr, int64_t a_ld = 0) {
+                                     const float* a_f32 = nullptr, int64_t a_ld = 0, int a_pieces = 3) {
   using namespace gm::gmm;
   GM_REQUIRE(ptr_host && groups >= 1 && groups <= kMaxGroups, GM_ERR_INVALID_ARGUMENT,
              "segment_matmul: groups must be in [1, " + std::to_string(kMaxGroups) + "]");
@@ -831,7 +841,7 @@ static gm_status segment_matmul_impl(const void* x, const int64_t* ptr_host, int
   P.a_seg_map = a_seg_map;
   P.a_f32 = a_f32;
   P.a_ld = static_cast<int32_t>(a_ld);
-  const int pieces = a_f32 ? 3 : 1;
+  const int pieces = a_f32 ? a_pieces : 1;
   int32_t tiles = 0;
   for (int64_t g = 0; g < groups; ++g) {
     P.ptr[g] = ptr_host[g];
@@ -907,8 +917,9 @@ static gm_status segment_matmul_impl(const void* x, const int64_t* ptr_host, int
   if (s != GM_OK) return s;
 
   // per call: the attribute is per device, and a process may drive several
-  auto kern = a_f32 ? (kblk == 64 ? segment_matmul_kernel<64, true> : segment_matmul_kernel<32, true>)
-                    : (kblk == 64 ? segment_matmul_kernel<64, false> : segment_matmul_kernel<32, false>);
+  auto kern = a_f32 ? (a_pieces == 3 ? (kblk == 64 ? segment_matmul_kernel<64, 3> : segment_matmul_kernel<32, 3>)
+                                      : (kblk == 64 ? segment_matmul_kernel<64, 1> : segment_matmul_kernel<32, 1>))
+                    : (kblk == 64 ? segment_matmul_kernel<64, 0> : segment_matmul_kernel<32, 0>);
   GM_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   const unsigned grid = static_cast<unsigned>(std::min<int32_t>(tiles, kNumSMs));
   kern<<<grid, a_f32 ? kThreads + 32 * kCvtWarps : kThreads, smem, st>>>(P, map_a, map_b, map_c);
@@ -958,6 +969,17 @@ GM_API gm_status gm_segment_matmul_packed(const void* x, const int64_t* ptr_host
   GM_REQUIRE(packed_w, GM_ERR_INVALID_ARGUMENT, "segment_matmul: null packed weights");
   return segment_matmul_impl(x, ptr_host, groups, k, n, nullptr, packed_w, out_dtype, out, workspace, workspace_bytes,
                              stream);
+}
+
+GM_API gm_status gm_segment_matmul_packed_xf32(const float* x, const int64_t* ptr_host, int64_t groups, int64_t k,
+                                               int64_t n, const void* packed_w, float* out, void* workspace,
+                                               size_t workspace_bytes, gm_stream_t stream) {
+  GM_REQUIRE(packed_w, GM_ERR_INVALID_ARGUMENT, "segment_matmul: null packed weights");
+  GM_REQUIRE(k % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0, GM_ERR_INVALID_ARGUMENT,
+             "segment_matmul: fp32 x needs k % 4 == 0 and 16-byte alignment");
+  const int64_t kp = pad_to(std::max<int64_t>(k, 1), 64);
+  return segment_matmul_impl(x, ptr_host, groups, kp, n, nullptr, packed_w, GM_F32, out, workspace, workspace_bytes,
+                             stream, 0, 0, 0, x, k, 1);
 }
 
 GM_API size_t gm_segment_matmul_f32_workspace(int64_t rows, int64_t groups, int64_t k, int64_t n) {

@@ -535,9 +535,21 @@ def segment_matmul(x: torch.Tensor, ptr: Sequence[int], weights: torch.Tensor,
                 "gm_segment_matmul_f32")
         return out
     out_dtype = out_dtype or torch.bfloat16
-    x = x.to(torch.bfloat16).contiguous()
     w = weights.to(torch.bfloat16).contiguous()
     packed = _packed_weights(w, groups, k, n)
+    if x.dtype == torch.float32 and out_dtype == torch.float32 and k % 4 == 0:
+        # fp32 activations: rounded to bf16 inside the GEMM kernel (x read once)
+        xf = x.contiguous()
+        if xf.data_ptr() % 16 == 0:
+            out = torch.empty((rows, n), dtype=torch.float32, device=x.device)
+            ptr_h = (C.c_int64 * (groups + 1))(*[int(p) for p in ptr])
+            lib = L.lib()
+            ws_bytes = lib.gm_segment_matmul_packed_workspace(rows, groups, k, n)
+            ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=x.device)
+            L.check(lib.gm_segment_matmul_packed_xf32(_p(xf), ptr_h, groups, k, n, _p(packed), _p(out), _p(ws),
+                                                      ws_bytes, _stream()), "gm_segment_matmul_packed_xf32")
+            return out
+    x = x.to(torch.bfloat16).contiguous()
     out = torch.empty((rows, n), dtype=out_dtype, device=x.device)
     ptr_h = (C.c_int64 * (groups + 1))(*[int(p) for p in ptr])
     lib = L.lib()

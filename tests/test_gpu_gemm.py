@@ -162,3 +162,20 @@ def test_packed_weights_cached_and_invalidated_by_inplace_update():
     c = gm.segment_matmul(x, ptr, w, out_dtype=torch.float32)
     assert w._gm_packed[2] is not packed
     check(c, x, ptr, w, np.arange(ptr[-1]), False)
+
+
+# fp32 activations x bf16 weights (the hetero layer's bf16-W route): x is read
+# as fp32 and rounded to bf16 inside the GEMM kernel (gm_segment_matmul_packed_xf32);
+# the operands are exactly those of casting x first, so the result must match
+# the cast-then-GEMM route bit for bit.
+@pytest.mark.parametrize("k,n", [(128, 128), (36, 40), (100, 7), (256, 512)])
+def test_fp32_activations_bf16_weights_match_cast_route(k, n):
+    torch.manual_seed(k + n)
+    ptr = [0, 5, 5, 133, 400, 401, 9031]
+    x = torch.randn(ptr[-1], k, device="cuda") * 2.0
+    w = (torch.randn(len(ptr) - 1, k, n, device="cuda") / k ** 0.5).to(torch.bfloat16)
+    got = gm.segment_matmul(x, ptr, w, out_dtype=torch.float32)
+    want = gm.segment_matmul(x.to(torch.bfloat16), ptr, w, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    assert got.dtype == torch.float32
+    assert torch.equal(got, want), float((got - want).abs().max())
