@@ -52,6 +52,21 @@ def test_version_and_error_plumbing():
         L.check(st)
 
 
+def test_segment_matmul_argument_validation_without_cuda():
+    # argument checks run before any device work: safe on a CPU-only host
+    import ctypes as C
+    lib = L.lib()
+    ptr = (C.c_int64 * 2)(0, 8)
+    fake = C.c_void_p(16)  # never dereferenced: validation fails first
+    st = lib.gm_segment_matmul_packed_xf32(fake, ptr, 1, 6, 8, fake, fake, None, 0, None)
+    assert st == L.GM_ERR_INVALID_ARGUMENT
+    assert b"k % 4" in lib.gm_last_error()
+    st = lib.gm_segment_matmul_packed_xf32(fake, ptr, 1, 8, 8, None, fake, None, 0, None)
+    assert st == L.GM_ERR_INVALID_ARGUMENT and b"null packed weights" in lib.gm_last_error()
+    st = lib.gm_segment_matmul_f32(fake, ptr, 1, 0, 8, fake, fake, None, 0, None)
+    assert st == L.GM_ERR_INVALID_ARGUMENT and b"K and N must be positive" in lib.gm_last_error()
+
+
 def test_host_uniform_generator_matches_reference_rng():
     # edge i draws next_below from Stream(derive(seed, "src"/"dst", i)) (random.hpp)
     lib = L.lib()
