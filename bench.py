@@ -171,61 +171,85 @@ def bench_segment_matmul(gm, L, device, f=128, rows=1_939_743, rank=0, world=1, 
             "bound": "hbm" if ai * hbm / 1e3 < bf16_peak else "tensor"}
 
 
+def workload_config(world: int) -> dict:
+    """The `config` both arms print (same workload, same keys)."""
+    return {"workload": "ogbn-products-shaped power-law graph (configs[3]), full-graph sum SpMM",
+            "nodes": N_NODES, "edges": N_EDGES, "feats": F, "graph": "Chung-Lu alpha=0.5",
+            "seed": hex(SEED),
+            "parallelism": f"dst-row partition x{world}" + (
+                f" + {CHUNKS} chunked async NCCL all-gathers of X overlapped with source-blocked "
+                "aggregation" if world > 1 else ""),
+            "l2": "GPU arm: L2 flushed between timed steps (256 MB write); X = 980 MB > L2"}
+
+
 def run_reference_arm(args):
-    """--impl reference: the reference's own CPU spmm<float> on this host."""
+    """--impl reference: the reference's own CPU spmm<float> (oracle/_ref, the
+    unmodified reference compiled in place) on this host, rank 0 only. Inputs
+    come from the oracle-side generator (ref_synth_*, the reference's rng::Stream),
+    so this arm never loads the product library. Each step is one full-graph
+    sum SpMM over all host threads (row ranges, one reference spmm per thread);
+    single-core lines (the reference's own single-threaded convention,
+    message_passing.hpp:676-697) are reported beside it."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from oracle.oracle import Reference
-    from paper_2507_16991_b200 import _lib as L
+    from oracle.oracle import Reference, cpu_model, host_threads
     if not Reference.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference)"}))
         return
     ref = Reference()
-    lib = L.lib()
-    src = np.zeros(N_EDGES, np.int64)
-    dst = np.zeros(N_EDGES, np.int64)
-    lib.gm_synth_edges_host(1, SEED, 0, N_EDGES, N_NODES, N_NODES, src.ctypes.data, dst.ctypes.data)
-    x = np.zeros((N_NODES, F), np.float32)
-    lib.gm_synth_features_host(SEED, 0, N_NODES, F, 0, L.GM_F32, x.ctypes.data)
-    threads = os.cpu_count() or 1
-    # bounded sample: the first 1/4 of destination rows, each step one spmm over it
-    rows = N_NODES // 4
+    threads = host_threads()
+    src, dst = ref.synth_edges(1, SEED, N_EDGES, N_NODES, N_NODES, threads=threads)
+    x = ref.synth_features(SEED, N_NODES, F, threads=threads)
     secs, edges = ref.bench_spmm(src, dst, N_NODES, N_NODES, x, mean=False, threads=threads,
-                                 rows_limit=rows, warmup=args.warmup, repeat=args.steps)
+                                 rows_limit=0, warmup=args.warmup, repeat=args.steps)
+    assert edges == N_EDGES
     val = edges / secs / 1e9
-    sample = f"dst rows [0,{rows}) of the products graph ({edges} edges), spmm<float> sum"
+    # single-core lines ("1 of N cores"): spmm and the max path on a 1/16 row
+    # sample, build_compressed of the full CSC
+    rows = N_NODES // 16
+    s1, e1 = ref.bench_spmm(src, dst, N_NODES, N_NODES, x, threads=1, rows_limit=rows, warmup=1, repeat=2)
+    m1, em = ref.bench_max(src, dst, N_NODES, N_NODES, x, rows_limit=rows)
+    b1 = ref.bench_build_compressed(dst, src, N_NODES)
+    model = cpu_model()
+    sample = (f"full graph ({edges} edges) per step: reference spmm<float> sum, {threads} threads "
+              f"over dst-row ranges (one reference spmm per thread), CSC caches filled outside the timed region")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": val, "unit": "GEdges/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "ogbn-products-shaped power-law, sum SpMM, F=100 fp32 (CPU reference)",
-                   "nodes": N_NODES, "edges": N_EDGES, "feats": F},
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": workload_config(args.gpus),
         "cpu_baseline": {"value": val, "unit": "GEdges/s", "cores": threads, "kind": "reference",
-                         "sample": sample},
+                         "sample": sample, "cpu_model": model},
         "e2e": {"value": val, "unit": "GEdges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "single_core": {
+            "cpu_model": model, "cores": f"1 of {threads}",
+            "spmm_sum": {"gedges_s": e1 / s1 / 1e9, "ms": s1 * 1e3,
+                         "sample": f"dst rows [0,{rows}) ({e1} edges)"},
+            "max_path": {"gedges_s": em / m1 / 1e9, "ms": m1 * 1e3,
+                         "sample": f"dst rows [0,{rows}) ({em} edges), dst_grouped_order + gather_rows + "
+                                   "aggregate(max)"},
+            "build_compressed_csc": {"gedges_s": N_EDGES / b1 / 1e9, "ms": b1 * 1e3,
+                                     "sample": f"full graph ({N_EDGES} edges)"}},
     }))
 
 
-def cpu_baseline_line():
-    """The reference (oracle/_ref) on the host cores, bounded sample (~10 s)."""
-    from oracle.oracle import Reference
-    from paper_2507_16991_b200 import _lib as L
+def cpu_baseline_line(g, x):
+    """The reference (oracle/_ref) on the host cores over the same graph (copied
+    back from the device), full graph per step, mean of 2 after 1 warmup."""
+    from oracle.oracle import Reference, cpu_model, host_threads
     if not Reference.available():
         return None
-    lib = L.lib()
-    src = np.zeros(N_EDGES, np.int64)
-    dst = np.zeros(N_EDGES, np.int64)
-    lib.gm_synth_edges_host(1, SEED, 0, N_EDGES, N_NODES, N_NODES, src.ctypes.data, dst.ctypes.data)
-    x = np.zeros((N_NODES, F), np.float32)
-    lib.gm_synth_features_host(SEED, 0, N_NODES, F, 0, L.GM_F32, x.ctypes.data)
-    threads = os.cpu_count() or 1
-    rows = N_NODES // 4
-    secs, edges = Reference().bench_spmm(src, dst, N_NODES, N_NODES, x, threads=threads, rows_limit=rows,
+    src = g.src().cpu().numpy()
+    dst = g.dst().cpu().numpy()
+    xh = x.cpu().numpy()
+    threads = host_threads()
+    secs, edges = Reference().bench_spmm(src, dst, N_NODES, N_NODES, xh, threads=threads, rows_limit=0,
                                          warmup=1, repeat=2)
     return {"value": edges / secs / 1e9, "unit": "GEdges/s", "cores": threads, "kind": "reference",
-            "sample": f"dst rows [0,{rows}) ({edges} edges), reference spmm<float> sum, "
-                      f"{threads} threads over row ranges, mean of 2 after 1 warmup"}
+            "cpu_model": cpu_model(),
+            "sample": f"full graph ({edges} edges), reference spmm<float> sum, "
+                      f"{threads} threads over dst-row ranges, mean of 2 after 1 warmup"}
 
 
 def main():
@@ -506,7 +530,7 @@ def main():
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_baseline_line()
+            cpu = cpu_baseline_line(g, x)
         except Exception as exc:
             cpu = {"error": str(exc)[:200]}
 
@@ -519,13 +543,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": "ogbn-products-shaped power-law graph (configs[3]), full-graph sum SpMM",
-                       "nodes": N_NODES, "edges": N_EDGES, "feats": F, "graph": "Chung-Lu alpha=0.5",
-                       "parallelism": f"dst-row partition x{world}" + (
-                           f" + {CHUNKS} chunked async NCCL all-gathers of X overlapped with source-blocked "
-                           "aggregation" if world > 1 else ""),
-                       "l2": "L2 flushed between timed steps (256 MB write); X = 980 MB > L2",
-                       "l2_hot_mb": int(plan.l2_hot_bytes >> 20), "heavy_rows": int(plan.num_heavy)},
+            "config": workload_config(world),
+            "plan": {"l2_hot_mb": int(plan.l2_hot_bytes >> 20), "heavy_rows": int(plan.num_heavy)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(), "secondary": secondary,

@@ -301,3 +301,55 @@ class Reference:
             C.c_int(int(mean)), C.c_int(threads), _I(rows_limit), C.c_int(warmup), C.c_int(repeat),
             C.byref(secs), C.byref(edges)))
         return secs.value, edges.value
+
+    # -- synthetic inputs without the product library -------------
+    def synth_edges(self, kind, seed, count, n_src, n_dst, first=0, threads=None):
+        src = np.zeros(count, np.int64)
+        dst = np.zeros(count, np.int64)
+        self._check(self.lib.ref_synth_edges(C.c_int(kind), C.c_uint64(seed), _I(first), _I(count), _I(n_src),
+                                             _I(n_dst), _ptr(src), _ptr(dst), C.c_int(threads or host_threads())))
+        return src, dst
+
+    def synth_features(self, seed, rows, f, quantize=0, first_row=0, threads=None):
+        x = np.zeros((rows, f), np.float32)
+        self._check(self.lib.ref_synth_features_f32(C.c_uint64(seed), _I(first_row), _I(rows), _I(f),
+                                                    C.c_int(quantize), _ptr(x), C.c_int(threads or host_threads())))
+        return x
+
+    def bench_build_compressed(self, keys, values, num_rows):
+        """Seconds of one reference build_compressed (edge_index.cpp:45-62), 1 thread."""
+        secs = C.c_double(0)
+        keys, values = _i64(keys), _i64(values)
+        self._check(self.lib.ref_bench_build_compressed(_ptr(keys), _ptr(values), _I(keys.size), _I(num_rows),
+                                                        C.byref(secs)))
+        return secs.value
+
+    def bench_max(self, src, dst, n_src, n_dst, x, rows_limit=0):
+        """Seconds of one reference max path (message_passing.hpp:508-514) over the
+        first rows_limit destination rows, 1 thread; returns (seconds, edges)."""
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        src, dst = _i64(src), _i64(dst)
+        secs = C.c_double(0)
+        edges = C.c_int64(0)
+        self._check(self.lib.ref_bench_max_f32(_ptr(src), _ptr(dst), _I(src.size), _I(n_src), _I(n_dst), _ptr(x),
+                                               _I(x.shape[1]), _I(rows_limit), C.byref(secs), C.byref(edges)))
+        return secs.value, edges.value
+
+
+def host_threads() -> int:
+    """Host cores this process may run on (the CPU arms' thread count)."""
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+

@@ -6,6 +6,8 @@
 // public API; nothing here re-implements its arithmetic.
 #include <algorithm>
 #include <chrono>
+#include <cmath>
+#include <span>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -371,6 +373,161 @@ int ref_bench_spmm_f32(const int64_t* src, const int64_t* dst, int64_t e, int64_
     BenchTiming bt = time_loop(run_once, repeat, warmup);
     *seconds = bt.mean_ms / 1000.0;
     *edges_done = total;
+  });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Synthetic inputs of the bench / parity configs, generated on
+// the host for the reference arm WITHOUT the product library. The RNG is the
+// reference's own (random.hpp:9-65: rng::mix, rng::derive, rng::Stream); the
+// graph construction on top of it (Chung-Lu alpha = 0.5 by inverse CDF over a
+// keyed Feistel permutation of node ids, 1-in-4 quantised feature rows) is the
+// §8d generator, restated here so the CPU arm and the GPU arm see the same
+// COO lists and features bit-for-bit (tests/test_oracle.py pins the two
+// generators against each other). Built with -ffp-contract=off: every fp64
+// operation rounds once, as on the device (__dadd_rn/__dmul_rn/__dsqrt_rn).
+// ---------------------------------------------------------------------------
+namespace synth {
+enum : std::uint64_t {
+  kTagSrc = 0x737263ull, kTagDst = 0x647374ull, kTagFeat = 0x66656174ull,
+  kTagPerm = 0x7065726dull, kTagQuant = 0x7175616eull, kTagWgt = 0x776774ull,
+};
+
+// Bijection of [0, n): 4-round Feistel on the smallest even-bit power of two
+// >= n, cycle-walking back into range.
+std::uint64_t permute(std::uint64_t x, std::uint64_t n, std::uint64_t key) {
+  if (n <= 1) return 0;
+  int bits = 0;
+  while ((std::uint64_t{1} << bits) < n) ++bits;
+  if (bits & 1) ++bits;
+  if (bits < 2) bits = 2;
+  const int half = bits / 2;
+  const std::uint64_t mask = (std::uint64_t{1} << half) - 1;
+  do {
+    std::uint64_t l = x >> half, r = x & mask;
+    for (int round = 0; round < 4; ++round) {
+      const std::uint64_t nl = r;
+      r = l ^ (rng::mix(key ^ (r * 0x100000001b3ull) ^ static_cast<std::uint64_t>(round)) & mask);
+      l = nl;
+    }
+    x = (l << half) | r;
+  } while (x >= n);
+  return x;
+}
+
+// Inverse CDF of the density (p+1)^-1/2 on [0, n): (1 + u(sqrt(n+1) - 1))^2 - 1.
+std::uint64_t powerlaw_node(double u, std::uint64_t n, std::uint64_t perm_key) {
+  const double s = std::sqrt(static_cast<double>(n + 1)) + -1.0;
+  const double t = 1.0 + u * s;
+  const double xpos = t * t + -1.0;
+  std::uint64_t p = xpos <= 0.0 ? 0 : static_cast<std::uint64_t>(xpos);
+  if (p >= n) p = n - 1;
+  return permute(p, n, perm_key);
+}
+
+void edge(int kind, std::uint64_t seed, std::uint64_t i, std::uint64_t n_src, std::uint64_t n_dst,
+          int64_t* s, int64_t* d) {
+  rng::Stream ss(rng::derive(seed, kTagSrc, i));
+  rng::Stream ds(rng::derive(seed, kTagDst, i));
+  if (kind == 0) {
+    *s = static_cast<int64_t>(ss.next_below(n_src));
+    *d = static_cast<int64_t>(ds.next_below(n_dst));
+  } else {
+    *s = static_cast<int64_t>(powerlaw_node(ss.next_real(), n_src, rng::derive(seed, kTagPerm, 1)));
+    *d = static_cast<int64_t>(powerlaw_node(ds.next_real(), n_dst, rng::derive(seed, kTagPerm, 2)));
+  }
+}
+
+template <typename Fn>
+void parallel_for(int64_t count, int threads, Fn&& fn) {
+  if (threads < 1) threads = 1;
+  if (count < 65536) threads = 1;
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t)
+    pool.emplace_back([&, t] {
+      const int64_t lo = count * t / threads, hi = count * (t + 1) / threads;
+      for (int64_t i = lo; i < hi; ++i) fn(i);
+    });
+  for (auto& th : pool) th.join();
+}
+}  // namespace synth
+
+extern "C" {
+int ref_synth_edges(int kind, uint64_t seed, int64_t first, int64_t count, int64_t n_src, int64_t n_dst,
+                    int64_t* src, int64_t* dst, int threads) {
+  return guarded([&] {
+    synth::parallel_for(count, threads, [&](int64_t i) {
+      synth::edge(kind, seed, static_cast<std::uint64_t>(first + i), static_cast<std::uint64_t>(n_src),
+                  static_cast<std::uint64_t>(n_dst), src + i, dst + i);
+    });
+  });
+}
+
+// x[row][j] ~ U[-1, 1) from the row's stream (Tensor::rand_uniform,
+// tensor.hpp:147-152, one stream per row); quantize: 1 row in 4 (by hash)
+// snapped down to multiples of 1/8, a snapped zero is -0.0 in half of them.
+int ref_synth_features_f32(uint64_t seed, int64_t first_row, int64_t rows, int64_t f, int quantize, float* x,
+                           int threads) {
+  return guarded([&] {
+    synth::parallel_for(rows, threads, [&](int64_t i) {
+      const std::uint64_t row = static_cast<std::uint64_t>(first_row + i);
+      rng::Stream s(rng::derive(seed, synth::kTagFeat, row));
+      const std::uint64_t h = rng::mix(rng::derive(seed, synth::kTagQuant, row));
+      const bool snap = quantize && (h & 3) == 0, negzero = (h >> 2) & 1;
+      for (int64_t j = 0; j < f; ++j) {
+        double v = s.next_real(-1.0, 1.0);
+        if (snap) {
+          double q = static_cast<double>(static_cast<int64_t>(v * 8.0));
+          if (q > v * 8.0) q = q + -1.0;
+          v = q * 0.125;
+          if (v == 0.0 && negzero) v = -0.0;
+        }
+        x[i * f + j] = static_cast<float>(v);
+      }
+    });
+  });
+}
+
+// The reference's own build_compressed (edge_index.cpp:45-62) on the CSC keys,
+// timed once (one thread: the reference has no parallel build).
+int ref_bench_build_compressed(const int64_t* keys, const int64_t* values, int64_t e, int64_t num_rows,
+                               double* seconds) {
+  return guarded([&] {
+    const auto t0 = std::chrono::steady_clock::now();
+    CsrView v = build_compressed(std::span<const Index>(keys, static_cast<size_t>(e)),
+                                 std::span<const Index>(values, static_cast<size_t>(e)), num_rows);
+    const auto t1 = std::chrono::steady_clock::now();
+    *seconds = std::chrono::duration<double>(t1 - t0).count();
+    if (v.rowptr.size() != static_cast<size_t>(num_rows + 1)) throw std::logic_error("bad rowptr");
+  });
+}
+
+// The reference max path (message_passing.hpp:508-514: dst_grouped_order +
+// gather_rows + aggregate(max, sorted_segments)) on the first rows_limit
+// destination rows, timed once after the CSC cache is filled.
+int ref_bench_max_f32(const int64_t* src, const int64_t* dst, int64_t e, int64_t n_src, int64_t n_dst,
+                      const float* x, int64_t f, int64_t rows_limit, double* seconds, int64_t* edges_done) {
+  return guarded([&] {
+    NoGradGuard ng;
+    const int64_t rows = rows_limit > 0 ? std::min(rows_limit, n_dst) : n_dst;
+    std::vector<Index> ss, dd;
+    for (int64_t i = 0; i < e; ++i)
+      if (dst[i] < rows) { ss.push_back(src[i]); dd.push_back(dst[i]); }
+    *edges_done = static_cast<int64_t>(ss.size());
+    EdgeIndex ei(std::move(ss), std::move(dd), n_src, rows);
+    ei.to_csc();
+    Tensor<float> xt = make_tensor(x, n_src, f);
+    const auto t0 = std::chrono::steady_clock::now();
+    auto [order, grouped_dst] = detail::dst_grouped_order(ei, false);
+    std::vector<Index> src_nodes(order.size());
+    for (size_t i = 0; i < order.size(); ++i) src_nodes[i] = ei.src()[static_cast<size_t>(order[i])];
+    Tensor<float> m = gather_rows(xt, src_nodes);
+    Tensor<float> o = aggregate(m, grouped_dst, rows, AggKind::max, AggLayout::sorted_segments);
+    const auto t1 = std::chrono::steady_clock::now();
+    *seconds = std::chrono::duration<double>(t1 - t0).count();
+    (void)o;
   });
 }
 
