@@ -252,6 +252,93 @@ def cpu_baseline_line(g, x):
                       f"{threads} threads over dst-row ranges, mean of 2 after 1 warmup"}
 
 
+def timed_steps(fn, steps, flush_buf, stream=None):
+    """Per-step CUDA-event times (ms) of fn(), L2 flushed by a write larger
+    than L2 outside the events before every step, like the headline."""
+    fn()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for a, b in evs:
+        flush_buf.zero_()
+        a.record(stream)
+        fn()
+        b.record(stream)
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in evs]
+
+
+def traffic_of(name):
+    """Measured DRAM bytes per call from a committed ncu capture (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", name)
+    if not os.path.exists(p):
+        return None
+    try:
+        return json.load(open(p)).get("dram_bytes_per_call")
+    except Exception:
+        return None
+
+
+def single_gpu_secondary(gm, L, lib, g, x, cs, plan, flush_buf, steps, hbm):
+    """Secondary lines at N = 1, each timed like the headline (per-step events,
+    L2 flushed between steps): max + argmax SpMM and CSR build on the same
+    graph first, then the segment_matmul lines (tensor-heavy, so they run last
+    and cannot leave the SpMM lines at power-capped clocks)."""
+    stream = torch.cuda.current_stream()
+    sec = {}
+    # max + argmax SpMM (the reference's max path, fused; int32 COO-id argmax)
+    mo = torch.empty(N_NODES, F, dtype=torch.float32, device=x.device)
+    ma = torch.empty(N_NODES, F, dtype=torch.int32, device=x.device)
+
+    def max_step():
+        L.check(lib.gm_spmm(C.byref(cs), C.byref(plan), L.GM_F32, C.c_void_p(x.data_ptr()), F, None, None,
+                            L.GM_MAX, C.c_void_p(mo.data_ptr()), C.c_void_p(ma.data_ptr()),
+                            C.c_void_p(stream.cuda_stream)))
+    for _ in range(3):
+        max_step()
+    per = timed_steps(max_step, steps, flush_buf)
+    mms = statistics.mean(per)
+    mb = spmm_bytes(N_NODES, N_EDGES, F) + N_NODES * F * 4
+    sec["max_argmax_spmm"] = {
+        "ms": mms, "gedges_s": N_EDGES / mms / 1e6, "per_step_ms": {"min": min(per), "median": statistics.median(per)},
+        "roofline": {"bound": "hbm", "achieved": mb / mms / 1e6, "peak": hbm, "unit": "GB/s",
+                     "frac": mb / mms / 1e6 / hbm, "traffic": traffic_of("spmm_max_traffic.json"),
+                     "algorithmic_bytes_per_call": mb,
+                     "bytes_model": "gather model + 4 B int32 argmax per output element"}}
+    del mo, ma
+    # CSR build (build_compressed of the CSC: keys = dst, values = src), a fresh
+    # build per step (the reference rebuilds it per EdgeIndex, edge_index.cpp:121-136)
+    dst, src = g.dst(), g.src()
+    ws_bytes = lib.gm_build_compressed_workspace(N_EDGES, N_NODES)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=x.device)
+    rp = torch.empty(N_NODES + 1, dtype=torch.int64, device=x.device)
+    col = torch.empty(N_EDGES, dtype=torch.int32, device=x.device)
+    perm = torch.empty(N_EDGES, dtype=torch.int32, device=x.device)
+
+    def build_step():
+        L.check(lib.gm_build_compressed(C.c_void_p(dst.data_ptr()), C.c_void_p(src.data_ptr()), N_EDGES, N_NODES,
+                                        C.c_void_p(rp.data_ptr()), C.c_void_p(col.data_ptr()),
+                                        C.c_void_p(perm.data_ptr()), C.c_void_p(ws.data_ptr()), ws_bytes,
+                                        C.c_void_p(stream.cuda_stream)))
+    per = timed_steps(build_step, max(3, steps // 3), flush_buf)
+    bms = statistics.mean(per)
+    bb = 32 * N_EDGES + 8 * (N_NODES + 1)
+    csc = g.to_csc()
+    same = bool(torch.equal(rp, csc.rowptr) and torch.equal(col, csc.col) and torch.equal(perm, csc.perm))
+    sec["csr_build"] = {
+        "ms": bms, "gedges_s": N_EDGES / bms / 1e6, "identical_to_cached_csc": same,
+        "roofline": {"bound": "hbm", "achieved": bb / bms / 1e6, "peak": hbm, "unit": "GB/s",
+                     "frac": bb / bms / 1e6 / hbm, "traffic": traffic_of("csr_build_traffic.json"),
+                     "algorithmic_bytes_per_call": bb,
+                     "bytes_model": "two-pass stable counting sort: read dst (8E), read dst+src (16E), "
+                                    "write col+perm int32 (8E), write rowptr (8(N+1))"}}
+    del ws, col, perm
+    sec["segment_matmul_C3"] = bench_segment_matmul(gm, L, x.device)
+    sec["segment_matmul_C3_fp32"] = bench_segment_matmul(gm, L, x.device, fp32=True)
+    sec["segment_matmul_F1024"] = bench_segment_matmul(gm, L, x.device, f=1024, rows=500_000)
+    sec["segment_matmul_F2048"] = bench_segment_matmul(gm, L, x.device, f=2048, rows=262_144)
+    return sec
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -505,27 +592,7 @@ def main():
         except Exception as exc:  # noqa: BLE001
             secondary = {"error": str(exc)[:300]}
     if world == 1 and not args.no_secondary:
-        secondary = {"segment_matmul_C3": bench_segment_matmul(gm, L, device),
-                     "segment_matmul_C3_fp32": bench_segment_matmul(gm, L, device, fp32=True),
-                     "segment_matmul_F1024": bench_segment_matmul(gm, L, device, f=1024, rows=500_000),
-                     "segment_matmul_F2048": bench_segment_matmul(gm, L, device, f=2048, rows=262_144)}
-        # max + argmax SpMM on the same graph
-        mo = torch.empty(N_NODES, F, dtype=torch.float32, device=device)
-        ma = torch.empty(N_NODES, F, dtype=torch.int32, device=device)
-        for _ in range(2):
-            L.check(lib.gm_spmm(C.byref(cs), C.byref(plan), L.GM_F32, C.c_void_p(x.data_ptr()), F, None, None,
-                                L.GM_MAX, C.c_void_p(mo.data_ptr()), C.c_void_p(ma.data_ptr()), stream))
-        a, bev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for _ in range(5):
-            L.check(lib.gm_spmm(C.byref(cs), C.byref(plan), L.GM_F32, C.c_void_p(x.data_ptr()), F, None, None,
-                                L.GM_MAX, C.c_void_p(mo.data_ptr()), C.c_void_p(ma.data_ptr()), stream))
-        bev.record()
-        torch.cuda.synchronize()
-        mms = a.elapsed_time(bev) / 5
-        mb = spmm_bytes(N_NODES, N_EDGES, F) + N_NODES * F * 4
-        secondary["max_argmax_spmm"] = {"ms": mms, "gedges_s": N_EDGES / mms / 1e6,
-                                        "frac_hbm": mb / mms / 1e6 / hbm}
+        secondary = single_gpu_secondary(gm, L, lib, g, x, cs, plan, flush_buf, args.steps, hbm)
 
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline:

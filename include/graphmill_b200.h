@@ -167,11 +167,19 @@ GM_API gm_status gm_spmm_plan_build(const gm_csr* csr, void* buffer, size_t buff
  * which with_self_loops appends after all edges (edge_index.cpp:218-231) and
  * therefore comes last in CSC order. deg arrays are the effective degrees
  * (square: din+1 from the FULL dst array; bipartite: dout/din clamped >= 1),
- * see gm_gcn_degrees. */
+ * see gm_gcn_degrees.
+ * Layer epilogue, fused into the same store (no separate elementwise kernel):
+ * bias (NULL or [f] of the accumulation type: float for F32/BF16, double for
+ * F64) is added after the row's last term — layer_update's add(agg, bias),
+ * message_passing.hpp:578 — and relu != 0 then applies the model's
+ * inter-layer relu (message_passing.hpp:637, tensor.hpp:393-396:
+ * v > 0 ? v : 0), both in the accumulation type before the final narrowing. */
 typedef struct gm_gcn_norm {
   const int32_t* deg_src;
   const int32_t* deg_dst;
   int self_loops;
+  const void* bias;
+  int relu;
 } gm_gcn_norm;
 
 /* Effective GCN degrees (message_passing.hpp:441-460): square != 0 ->

@@ -264,6 +264,21 @@ class Reference:
                                                _I(h.shape[1]), _ptr(w), _ptr(b), _I(w.shape[1]), _ptr(out)))
         return out
 
+    def gcn_model(self, src, dst, n, h, layers, dtype=np.float32):
+        """Model<S>::forward of a GCN stack (message_passing.hpp:631-641):
+        layers = [(W [f_in, f_out], b [f_out]), ...], relu between layers."""
+        h = np.ascontiguousarray(h, dtype=dtype)
+        dims = np.array([h.shape[1]] + [w.shape[1] for w, _ in layers], np.int64)
+        ws = np.ascontiguousarray(np.concatenate([np.asarray(w, dtype).ravel() for w, _ in layers]))
+        bs = np.ascontiguousarray(np.concatenate([np.asarray(b, dtype).ravel() for _, b in layers]))
+        src, dst = _i64(src), _i64(dst)
+        out = np.zeros((n, dims[-1]), dtype)
+        suf = "f64" if dtype == np.float64 else "f32"
+        self._check(getattr(self.lib, "ref_gcn_model_" + suf)(
+            _ptr(src), _ptr(dst), _I(src.size), _I(n), _ptr(h), C.c_int32(len(layers)), _ptr(dims), _ptr(ws),
+            _ptr(bs), _ptr(out)))
+        return out
+
     def grouped_matmul(self, x, ptr, w):
         x = np.ascontiguousarray(x)
         w = np.ascontiguousarray(w, dtype=x.dtype)

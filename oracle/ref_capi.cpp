@@ -295,8 +295,50 @@ int ref_gcn_layer_f32(const int64_t* src, const int64_t* dst, int64_t e, int64_t
   });
 }
 
-// hetero.hpp:134-157 over segments of a concatenated x.
 }  // extern "C"
+
+// Model<S>::forward (message_passing.hpp:631-641) of a GCN stack: layer_forward
+// per layer with relu in between, segment_fused path. layer l maps dims[l] ->
+// dims[l+1]; weights/biases are concatenated in layer order.
+template <typename S>
+static int gcn_model_impl(const int64_t* src, const int64_t* dst, int64_t e, int64_t n, const S* h,
+                          int32_t n_layers, const int64_t* dims, const S* weights, const S* biases, S* out) {
+  return guarded([&] {
+    NoGradGuard ng;
+    EdgeIndex ei = make_index(src, dst, e, n, n, 0);
+    Model<S> m;
+    const S* w = weights;
+    const S* b = biases;
+    for (int32_t l = 0; l < n_layers; ++l) {
+      LayerParams<S> p;
+      p.kind = LayerKind::gcn;
+      p.in_dim = dims[l];
+      p.out_dim = dims[l + 1];
+      p.weights["weight"] = make_tensor(w, dims[l], dims[l + 1]);
+      p.weights["bias"] = Tensor<S>::from_data({dims[l + 1]}, std::vector<S>(b, b + dims[l + 1]));
+      w += dims[l] * dims[l + 1];
+      b += dims[l + 1];
+      m.layers.push_back(std::move(p));
+    }
+    Tensor<S> o = m.forward(ei, make_tensor(h, n, dims[0]), ExecPath::segment_fused);
+    std::memcpy(out, o.data().data(), sizeof(S) * static_cast<size_t>(n * dims[n_layers]));
+  });
+}
+
+extern "C" {
+int ref_gcn_model_f32(const int64_t* src, const int64_t* dst, int64_t e, int64_t n, const float* h,
+                      int32_t n_layers, const int64_t* dims, const float* weights, const float* biases,
+                      float* out) {
+  return gcn_model_impl<float>(src, dst, e, n, h, n_layers, dims, weights, biases, out);
+}
+int ref_gcn_model_f64(const int64_t* src, const int64_t* dst, int64_t e, int64_t n, const double* h,
+                      int32_t n_layers, const int64_t* dims, const double* weights, const double* biases,
+                      double* out) {
+  return gcn_model_impl<double>(src, dst, e, n, h, n_layers, dims, weights, biases, out);
+}
+}  // extern "C"
+
+// hetero.hpp:134-157 over segments of a concatenated x.
 template <typename S>
 static int gmm_impl(const S* x, const int64_t* ptr, int64_t groups, int64_t k, int64_t n,
                     const S* w, S* out) {

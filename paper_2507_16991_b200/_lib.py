@@ -55,7 +55,8 @@ class gm_spmm_plan(C.Structure):
 
 
 class gm_gcn_norm(C.Structure):
-    _fields_ = [("deg_src", C.c_void_p), ("deg_dst", C.c_void_p), ("self_loops", C.c_int)]
+    _fields_ = [("deg_src", C.c_void_p), ("deg_dst", C.c_void_p), ("self_loops", C.c_int),
+                ("bias", C.c_void_p), ("relu", C.c_int)]
 
 
 # name -> (restype, argtypes); mirrors include/graphmill_b200.h one to one.

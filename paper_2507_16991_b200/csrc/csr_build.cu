@@ -355,6 +355,16 @@ static BuildWs build_layout(void* base, int64_t e, int64_t n) {
   return w;
 }
 
+}  // namespace gm
+#include "csr_bucket.cuh"
+namespace gm {
+
+// GM_CSR_BUCKET=0 keeps the scatter + per-row sort build (A/B comparison only).
+static bool use_bucket_build(int64_t e, int64_t rows) {
+  static const bool on = [] { const char* v = getenv("GM_CSR_BUCKET"); return !(v && v[0] == '0'); }();
+  return on && cb::bucket_path_ok(e, rows);
+}
+
 // ---------------------------------------------------------------------------
 // Stable split of a CSR's entries into source blocks (multi-GPU overlap):
 // entry k of row r goes to block src_block[col[k]] with column src_col[col[k]];
@@ -743,7 +753,9 @@ GM_API gm_status gm_gcn_degrees(const int64_t* full_src, const int64_t* full_dst
 
 GM_API size_t gm_build_compressed_workspace(int64_t num_edges, int64_t num_rows) {
   if (num_edges < 0 || num_rows < 0) return 0;
-  return build_layout(nullptr, num_edges, num_rows).bytes;
+  size_t b = build_layout(nullptr, num_edges, num_rows).bytes;
+  if (cb::bucket_path_ok(num_edges, num_rows)) b += cb::bucket_layout(nullptr, num_edges, num_rows).bytes;
+  return b;
 }
 
 GM_API gm_status gm_build_compressed(const int64_t* keys, const int64_t* values,
@@ -755,10 +767,10 @@ GM_API gm_status gm_build_compressed(const int64_t* keys, const int64_t* values,
   GM_REQUIRE(num_edges < INT32_MAX && num_rows < INT32_MAX, GM_ERR_INVALID_ARGUMENT,
              "build_compressed: num_edges and num_rows must be < 2^31 (int32 col/perm)");
   GM_REQUIRE(rowptr, GM_ERR_INVALID_ARGUMENT, "build_compressed: null rowptr");
-  const BuildWs need = build_layout(nullptr, num_edges, num_rows);
-  GM_REQUIRE(workspace_bytes >= need.bytes && workspace, GM_ERR_INVALID_ARGUMENT,
+  const size_t need = gm_build_compressed_workspace(num_edges, num_rows);
+  GM_REQUIRE(workspace_bytes >= need && workspace, GM_ERR_INVALID_ARGUMENT,
              "build_compressed: workspace too small (" + std::to_string(workspace_bytes) + " < " +
-                 std::to_string(need.bytes) + ")");
+                 std::to_string(need) + ")");
   cudaStream_t st = as_stream(stream);
   if (num_rows == 0) {  // rowptr = {0}
     GM_TRY_CUDA(cudaMemsetAsync(rowptr, 0, sizeof(int64_t), st));
@@ -779,6 +791,10 @@ GM_API gm_status gm_build_compressed(const int64_t* keys, const int64_t* values,
   scan_down_kernel<<<static_cast<unsigned>(nb), kScanThreads, 0, st>>>(w.cnt, num_rows, w.partial, rowptr);
   GM_CHECK_LAUNCH("scan_down_kernel");
   if (num_edges == 0) return GM_OK;
+  if (use_bucket_build(num_edges, num_rows)) {
+    const cb::BucketWs bw = cb::bucket_layout(static_cast<unsigned char*>(workspace) + w.bytes, num_edges, num_rows);
+    return cb::bucket_build(keys, values, num_edges, num_rows, rowptr, col, perm, bw, st);
+  }
   scatter_kernel<<<grid_for(num_edges), 256, 0, st>>>(keys, num_edges, rowptr, w.cnt, perm);
   GM_CHECK_LAUNCH("scatter_kernel");
   sort_small_kernel<<<grid_for(num_rows * 32), 256, 0, st>>>(rowptr, num_rows, values, perm, col,

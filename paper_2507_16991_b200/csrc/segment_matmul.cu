@@ -675,9 +675,10 @@ static gm_status make_map(CUtensorMap* map, const void* base, uint64_t inner, ui
 
 using namespace gm;
 
-extern "C" {
-
 static int64_t pad_to(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+namespace gm {
+namespace gmm {
 
 // fp32 operands as three bf16 pieces: hi = bf16(v), mid = bf16(v - hi),
 // lo = bf16(v - hi - mid), |v - hi - mid - lo| <= 2^-27 |v|. Along K the
@@ -762,6 +763,12 @@ __global__ void split_wt_kernel(const float* __restrict__ w, int groups, int k, 
     o[2 * kp] = lo;
   }
 }
+
+}  // namespace gmm
+}  // namespace gm
+using namespace gm::gmm;
+
+extern "C" {
 
 GM_API size_t gm_segment_matmul_workspace(int64_t rows, int64_t groups, int64_t k, int64_t n) {
   if (rows < 0 || groups < 0 || k < 0 || n < 0) return 0;

@@ -309,6 +309,8 @@ static gm_status spmm_impl(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype
              "gm_spmm: arg_out must be 16-byte aligned");
   GM_REQUIRE(!gcn || (gcn->deg_src && gcn->deg_dst), GM_ERR_INVALID_ARGUMENT,
              "gm_spmm: gcn norm needs both degree arrays");
+  GM_REQUIRE(!gcn || !(gcn->bias || gcn->relu) || reduce == GM_SUM || reduce == GM_MEAN, GM_ERR_INVALID_ARGUMENT,
+             "gm_spmm: the bias/relu epilogue applies to sum/mean");
   if (csr->num_rows == 0 || f == 0) return GM_OK;
   GM_REQUIRE(x && out, GM_ERR_INVALID_ARGUMENT, "gm_spmm: null x/out");
 
@@ -335,6 +337,8 @@ static gm_status spmm_impl(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype
   p.gdeg_src = gcn ? gcn->deg_src : nullptr;
   p.gdeg_dst = gcn ? gcn->deg_dst : nullptr;
   p.gcn_self = gcn ? gcn->self_loops : 0;
+  p.bias = gcn ? gcn->bias : nullptr;
+  p.relu = gcn ? gcn->relu : 0;
   p.mean = reduce == GM_MEAN;
   p.is_min = reduce == GM_MIN;
   p.accum = accum;

@@ -345,10 +345,12 @@ def _run_spmm(grouping: CsrView, x: torch.Tensor, kind: str, w_csr: Optional[tor
     x = x.contiguous()
     f = x.shape[1] if x.dim() == 2 else 1
     rows = grouping.num_rows() if num_rows is None else num_rows
+    shape = (rows, f) if x.dim() == 2 else (rows,)
     if out is None:
-        out = torch.empty((rows, f) if x.dim() == 2 else (rows,), dtype=x.dtype, device=x.device)
-    elif out.shape[0] != rows or not out.is_contiguous() or out.dtype != x.dtype:
-        raise ValueError("spmm: out must be a contiguous [num_dst_nodes, F] tensor of x's dtype")
+        out = torch.empty(shape, dtype=x.dtype, device=x.device)
+    elif (tuple(out.shape) != shape or not out.is_contiguous() or out.dtype != x.dtype
+          or out.device != x.device):
+        raise ValueError("spmm: out must be a contiguous [num_dst_nodes, F] tensor of x's dtype and device")
     arg = torch.empty((rows, f), dtype=torch.int32, device=x.device) if want_arg else None
     csr = grouping.c_struct()
     plan = grouping.plan(row_bytes=f * x.element_size())
@@ -397,6 +399,12 @@ def spmm_backward(e: EdgeIndex, x: torch.Tensor, edge_weight: Optional[torch.Ten
         raise ValueError("spmm: reduce must be sum or mean")
     if x.dtype not in (torch.float32, torch.float64):
         raise ValueError("spmm_backward: f32/f64 only")
+    if x.dim() != 2 or x.shape[0] != e.num_src_nodes():
+        raise ValueError("spmm: feature rows != num_src_nodes")
+    if grad_out.dim() != 2 or tuple(grad_out.shape) != (e.num_dst_nodes(), x.shape[1]):
+        raise ValueError("spmm_backward: grad_out must be [num_dst_nodes, F]")
+    if edge_weight is not None and edge_weight.numel() != e.num_edges():
+        raise ValueError("spmm: edge weight length != num_edges")
     lib = L.lib()
     g = grad_out.to(x.dtype).contiguous()
     f = g.shape[1]
@@ -464,26 +472,54 @@ def gcn_degrees(e: EdgeIndex, square: bool):
     return d_src, d_dst
 
 
-def gcn_aggregate(e: EdgeIndex, xw: torch.Tensor) -> torch.Tensor:
+def gcn_aggregate(e: EdgeIndex, xw: torch.Tensor, bias: Optional[torch.Tensor] = None,
+                  relu: bool = False) -> torch.Tensor:
     """GCN neighbour side after the transform (message_passing.hpp:490-495):
-    with_self_loops + gcn_norm + spmm(sum), fused into one pass over e's CSC."""
+    with_self_loops + gcn_norm + spmm(sum), fused into one pass over e's CSC.
+    bias / relu: layer_update's add(agg, bias) (:578) and the model's
+    inter-layer relu (:637), applied in the same kernel's store epilogue."""
+    if xw.shape[0] != e.num_src_nodes():
+        raise ValueError("spmm: feature rows != num_src_nodes")
     square = e.num_src_nodes() == e.num_dst_nodes()
     d_src, d_dst = gcn_degrees(e, square)
-    gcn = L.gm_gcn_norm(d_src.data_ptr(), d_dst.data_ptr(), int(square))
+    b = None
+    if bias is not None:
+        f = xw.shape[1] if xw.dim() == 2 else 1
+        b = bias.to(device=xw.device, dtype=_acc_dtype(xw.dtype)).contiguous()
+        if b.numel() != f:
+            raise ValueError("layer_update: bias length != feature width")
+    gcn = L.gm_gcn_norm(d_src.data_ptr(), d_dst.data_ptr(), int(square),
+                        None if b is None else b.data_ptr(), int(bool(relu)))
     # with_self_loops builds a claim-less index, so its transpose_view is the CSC
     return _run_spmm(e.to_csc(), xw, "sum", gcn=gcn, num_rows=e.num_dst_nodes())
 
 
-def gcn_layer(e: EdgeIndex, h: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor) -> torch.Tensor:
-    """layer_forward for LayerKind::gcn (message_passing.hpp:490-499, 578): the dense
-    transform is a plain library GEMM (fp32, TF32 off), then the fused aggregate."""
-    prev = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = False
-    try:
-        xw = h @ weight
-    finally:
-        torch.backends.cuda.matmul.allow_tf32 = prev
-    return gcn_aggregate(e, xw) + bias
+def gcn_layer(e: EdgeIndex, h: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor,
+              relu: bool = False) -> torch.Tensor:
+    """layer_forward for LayerKind::gcn (message_passing.hpp:490-499, 578), two
+    launches of this library: the transform h @ W on the tcgen05 grouped GEMM
+    (one group; fp32 operands take the fp32-accurate split route, the
+    reference's matmul<float>), then the fused aggregate whose epilogue adds
+    the bias (and the optional inter-layer relu)."""
+    if h.dim() != 2 or h.shape[0] != e.num_src_nodes() or e.num_src_nodes() != e.num_dst_nodes():
+        raise ValueError("layer_forward: square index matching h required")
+    if weight.dim() != 2 or weight.shape[0] != h.shape[1]:
+        raise ValueError("matmul: inner dimension mismatch")
+    if h.dtype not in (torch.float32, torch.bfloat16):
+        raise ValueError("gcn_layer: f32 or bf16 features")
+    w = weight.to(h.dtype).unsqueeze(0)
+    xw = segment_matmul(h, [0, h.shape[0]], w, out_dtype=h.dtype)
+    return gcn_aggregate(e, xw, bias=bias, relu=relu)
+
+
+def gcn_forward(e: EdgeIndex, x: torch.Tensor, layers: Sequence[tuple]) -> torch.Tensor:
+    """Model::forward for a GCN stack (message_passing.hpp:631-641, no head):
+    relu between layers, fused into each aggregate's epilogue.
+    layers: [(weight, bias), ...]."""
+    h = x
+    for i, (w, b) in enumerate(layers):
+        h = gcn_layer(e, h, w, b, relu=i + 1 < len(layers))
+    return h
 
 
 def aggregate(values: torch.Tensor, index: torch.Tensor, num_groups: int, kind: str) -> torch.Tensor:
@@ -523,7 +559,12 @@ def segment_matmul(x: torch.Tensor, ptr: Sequence[int], weights: torch.Tensor,
         raise ValueError(f"grouped_matmul: group count mismatch ({len(ptr) - 1} inputs, {groups} weight slabs)")
     if x.dim() != 2 or x.shape[1] != k:
         raise ValueError("grouped_matmul: inner dimension mismatch")
-    rows = int(ptr[-1])
+    ptr = [int(p) for p in (ptr.tolist() if isinstance(ptr, torch.Tensor) else ptr)]
+    if ptr[0] != 0 or any(b < a for a, b in zip(ptr, ptr[1:])):
+        raise ValueError("grouped_matmul: segment offsets must start at 0 and be non-decreasing")
+    rows = ptr[-1]
+    if rows != x.shape[0]:
+        raise ValueError(f"grouped_matmul: segment offsets cover {rows} rows, x has {x.shape[0]}")
     if x.dtype == torch.float32 and weights.dtype == torch.float32 and out_dtype in (None, torch.float32):
         xf, wf = x.contiguous(), weights.contiguous()
         out = torch.empty((rows, n), dtype=torch.float32, device=x.device)
