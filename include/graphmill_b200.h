@@ -234,6 +234,25 @@ GM_API gm_status gm_csr_entry_rows(const gm_csr* csr, int32_t* rows_out, gm_stre
 GM_API gm_status gm_edge_dot_csc(gm_dtype dtype, const gm_csr* csc, const int32_t* entry_rows, const void* a_by_dst,
                                  const void* b_by_src, int64_t f, void* out, gm_stream_t stream);
 
+/* Backward of the max/min aggregation path (message_passing.hpp:508-514):
+ * the argpos scatter of aggregate's closure (aggregate.hpp:295-308) followed by
+ * the gather_rows adjoint (tensor.hpp:510-524), fused and without atomics.
+ * gm_source_view builds, once per graph, the "source view" of a CSC: per
+ * source node its entries in ascending CSC position (rowptr[n_src+1], col =
+ * destination node, eid = COO edge id) — a stable counting sort of the CSC
+ * sequence by source. Then
+ *   dx[s][j] = sum over the view's row s, in order, of g[v][j] where
+ *              arg[v][j] == eid  (arg: gm_spmm's MAX/MIN arg_out)
+ * accumulated sequentially from +0 — bit-identical to the reference tape
+ * (the non-winning positions it adds are exact zeros). plan: gm_spmm_plan_build
+ * of the source view (hub sources take a column-parallel kernel). f32/f64;
+ * dx [n_src, f] is fully written. */
+GM_API size_t gm_source_view_workspace(int64_t nnz, int64_t n_src);
+GM_API gm_status gm_source_view(const gm_csr* csc, int64_t n_src, int64_t* rowptr, int32_t* col, int32_t* eid,
+                                void* workspace, size_t workspace_bytes, gm_stream_t stream);
+GM_API gm_status gm_spmm_max_backward(const gm_csr* source_view, const gm_spmm_plan* plan, gm_dtype dtype,
+                                      const int32_t* arg, const void* g, int64_t f, void* dx, gm_stream_t stream);
+
 /* Heterogeneous combine (hetero.hpp:338-343 InterCombine::sum, then
  * layer_update hetero.hpp:362 / message_passing.hpp:579-580 for SAGE):
  *   out = ((((parts[0] + parts[1]) + ...) + self_term) + bias)   fp32, in this

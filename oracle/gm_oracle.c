@@ -112,6 +112,28 @@ DEFINE_SPMM_COO(f64, double)
 DEFINE_MAX(f32, float)
 DEFINE_MAX(f64, double)
 
+/* Backward of the max/min path (aggregate.hpp:295-308 then the gather_rows
+ * adjoint tensor.hpp:510-524): the gradient of output (v, j) lands on the
+ * grouped position whose COO edge id is arg[v][j], and gather_rows' adjoint
+ * adds every grouped position's row into dx[src] in ascending grouped (CSC)
+ * order, starting from +0. Positions that did not win add exact zeros, which
+ * never change a sum that starts at +0 under round-to-nearest, so only the
+ * winners are added here. rowptr/col/perm: the CSC (destination grouping). */
+#define DEFINE_MAX_BWD(SUF, S)                                                                 \
+  void or_spmm_max_backward_##SUF(const int64_t* rowptr, const int64_t* col, const int64_t* perm,   \
+                                  int64_t n_rows, const int64_t* arg, const S* g, int64_t f,        \
+                                  int64_t n_src, S* dx) {                                           \
+    for (int64_t i = 0; i < n_src * f; ++i) dx[i] = (S)0;                                        \
+    for (int64_t v = 0; v < n_rows; ++v)                                                         \
+      for (int64_t k = rowptr[v]; k < rowptr[v + 1]; ++k) {                                      \
+        S* d = dx + col[k] * f;                                                                  \
+        for (int64_t j = 0; j < f; ++j)                                                          \
+          if (arg[v * f + j] == perm[k]) d[j] = d[j] + g[v * f + j];                             \
+      }                                                                                          \
+  }
+DEFINE_MAX_BWD(f32, float)
+DEFINE_MAX_BWD(f64, double)
+
 /* message_passing.hpp:437-463 */
 #define DEFINE_GCN_NORM(SUF, S, SQRT)                                                         \
   void or_gcn_norm_##SUF(const int64_t* base_src, const int64_t* base_dst, int64_t base_len,  \

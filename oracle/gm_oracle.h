@@ -62,6 +62,12 @@ void or_spmm_max_f64(const int64_t* rowptr, const int64_t* col, const int64_t* p
 /* message_passing.hpp:437-463 gcn_norm. base_full_{src,dst}: the base index's
  * FULL arrays (lengths base_len). g_{src,dst}: the (self-loop augmented) graph
  * the norm is for. square != 0: din+1 both ends; else dout/din clamped >= 1. */
+/* Backward of the max/min path (aggregate.hpp:295-308 + gather_rows adjoint
+ * tensor.hpp:510-524): dx[n_src, f] from the CSC, the COO-id argmax and g. */
+void or_spmm_max_backward_f32(const int64_t* rowptr, const int64_t* col, const int64_t* perm, int64_t n_rows,
+                              const int64_t* arg, const float* g, int64_t f, int64_t n_src, float* dx);
+void or_spmm_max_backward_f64(const int64_t* rowptr, const int64_t* col, const int64_t* perm, int64_t n_rows,
+                              const int64_t* arg, const double* g, int64_t f, int64_t n_src, double* dx);
 void or_gcn_norm_f32(const int64_t* base_full_src, const int64_t* base_full_dst, int64_t base_len,
                      int64_t n_src, int64_t n_dst, const int64_t* g_src, const int64_t* g_dst,
                      int64_t g_len, int square, float* norm);

@@ -53,7 +53,8 @@ class Oracle:
         for name in ("or_build_compressed", "or_spmm_f32", "or_spmm_f64", "or_spmm_coo_f32",
                      "or_spmm_coo_f64", "or_spmm_max_f32", "or_spmm_max_f64", "or_gcn_norm_f32",
                      "or_gcn_norm_f64", "or_degree", "or_segment_matmul_f64", "or_segment_matmul_f32",
-                     "or_spmm_backward_f32", "or_spmm_backward_f64"):
+                     "or_spmm_backward_f32", "or_spmm_backward_f64", "or_spmm_max_backward_f32",
+                     "or_spmm_max_backward_f64"):
             getattr(self.lib, name).restype = None
 
     def build_compressed(self, keys, values, num_rows):
@@ -90,6 +91,17 @@ class Oracle:
         getattr(self.lib, "or_spmm_coo_" + suf)(_ptr(_i64(src)), _ptr(_i64(dst)), _I(len(src)), _I(n_dst),
                                                 _ptr(x), _I(f), _ptr(w), C.c_int(int(mean)), _ptr(out))
         return out
+
+    def spmm_max_backward(self, rowptr, col, perm, arg, g, n_src):
+        """dx of the max/min path from the CSC, the COO-id argmax and the output gradient."""
+        g = np.ascontiguousarray(g)
+        suf = "f64" if g.dtype == np.float64 else "f32"
+        f = g.shape[1]
+        dx = np.zeros((n_src, f), g.dtype)
+        getattr(self.lib, "or_spmm_max_backward_" + suf)(_ptr(_i64(rowptr)), _ptr(_i64(col)), _ptr(_i64(perm)),
+                                                         _I(rowptr.size - 1), _ptr(_i64(arg)), _ptr(g), _I(f),
+                                                         _I(n_src), _ptr(dx))
+        return dx
 
     def spmm_max(self, rowptr, col, perm, x, w_coo=None, is_min=False, rows=None):
         x = np.ascontiguousarray(x)
@@ -234,6 +246,19 @@ class Reference:
             _ptr(src), _ptr(dst), _I(src.size), _I(n_src), _I(n_dst), _ptr(x), _I(f), C.c_int(int(is_min)),
             _ptr(out), _ptr(arg)))
         return out, arg
+
+    def max_backward(self, src, dst, n_src, n_dst, x, g, is_min=False):
+        """dx of the layer max/min path through the reference's own tape."""
+        x = np.ascontiguousarray(x)
+        g = np.ascontiguousarray(g, dtype=x.dtype)
+        suf = "f64" if x.dtype == np.float64 else "f32"
+        src, dst = _i64(src), _i64(dst)
+        f = x.shape[1]
+        dx = np.zeros((n_src, f), x.dtype)
+        self._check(getattr(self.lib, "ref_max_backward_" + suf)(
+            _ptr(src), _ptr(dst), _I(src.size), _I(n_src), _I(n_dst), _ptr(x), _I(f), C.c_int(int(is_min)),
+            _ptr(g), _ptr(dx)))
+        return dx
 
     def aggregate(self, values, index, n, kind):
         values = np.ascontiguousarray(values, dtype=np.float32)

@@ -103,6 +103,34 @@ int max_impl(const int64_t* src, const int64_t* dst, int64_t e, int64_t n_src, i
   });
 }
 
+// Backward of the layer max/min path (message_passing.hpp:508-514) through the
+// reference's own tape: x -> gather_rows(x, src in grouped order) (tracked) ->
+// aggregate(max|min, sorted_segments) -> loss = sum(mul(out, G)); dx = x.grad()
+// (aggregate.hpp:295-308 argpos scatter, then the gather_rows adjoint
+// tensor.hpp:510-524).
+template <typename S>
+int max_bwd_impl(const int64_t* src, const int64_t* dst, int64_t e, int64_t n_src, int64_t n_dst, const S* x,
+                 int64_t f, int is_min, const S* G, S* dx) {
+  return guarded([&] {
+    EdgeIndex ei = make_index(src, dst, e, n_src, n_dst, 0);
+    auto [order, grouped_dst] = detail::dst_grouped_order(ei, false);
+    std::vector<Index> src_nodes(order.size());
+    for (size_t i = 0; i < order.size(); ++i) src_nodes[i] = ei.src()[static_cast<size_t>(order[i])];
+    Tensor<S> xt = make_tensor(x, n_src, f);
+    xt.set_requires_grad(true);
+    Tensor<S> m = gather_rows(xt, src_nodes);
+    Tensor<S> o = aggregate(m, grouped_dst, n_dst, is_min ? AggKind::min : AggKind::max,
+                            AggLayout::sorted_segments);
+    backward(sum(mul(o, make_tensor(G, n_dst, f))));
+    if (xt.has_grad()) {
+      Tensor<S> gx = xt.grad();
+      std::memcpy(dx, gx.data().data(), sizeof(S) * static_cast<size_t>(n_src * f));
+    } else {
+      std::fill(dx, dx + n_src * f, S(0));
+    }
+  });
+}
+
 // spmm backward through the reference's own tape: loss = sum(mul(spmm(e, x, w), G)),
 // so the gradient entering spmm's closure is exactly G (test_message_passing.cpp:92-105).
 template <typename S>
@@ -248,6 +276,14 @@ int ref_max_f32(const int64_t* src, const int64_t* dst, int64_t e, int64_t n_src
 int ref_max_f64(const int64_t* src, const int64_t* dst, int64_t e, int64_t n_src, int64_t n_dst,
                 const double* x, int64_t f, int is_min, double* out, int64_t* arg) {
   return max_impl<double>(src, dst, e, n_src, n_dst, x, f, is_min, out, arg);
+}
+int ref_max_backward_f32(const int64_t* src, const int64_t* dst, int64_t e, int64_t n_src, int64_t n_dst,
+                         const float* x, int64_t f, int is_min, const float* G, float* dx) {
+  return max_bwd_impl<float>(src, dst, e, n_src, n_dst, x, f, is_min, G, dx);
+}
+int ref_max_backward_f64(const int64_t* src, const int64_t* dst, int64_t e, int64_t n_src, int64_t n_dst,
+                         const double* x, int64_t f, int is_min, const double* G, double* dx) {
+  return max_bwd_impl<double>(src, dst, e, n_src, n_dst, x, f, is_min, G, dx);
 }
 
 // aggregate.hpp:155-215 on edge-level values (a6): kind 0 sum, 1 mean, 2 max, 3 min.

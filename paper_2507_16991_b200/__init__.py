@@ -6,7 +6,7 @@ The compute lives in libgraphmill_b200.so (C-ABI, include/graphmill_b200.h);
 from . import _lib  # noqa: F401
 from .graphmill import (  # noqa: F401
     CsrView, EdgeIndex, aggregate, build_compressed, gcn_aggregate, gcn_forward, gcn_layer, grouped_matmul,
-    neighbor_aggregate, segment_matmul, spmm, spmm_backward)
+    neighbor_aggregate, neighbor_aggregate_backward, segment_matmul, spmm, spmm_backward)
 
 __all__ = ["CsrView", "EdgeIndex", "aggregate", "build_compressed", "gcn_aggregate", "gcn_forward", "gcn_layer",
-           "grouped_matmul", "neighbor_aggregate", "segment_matmul", "spmm", "spmm_backward"]
+           "grouped_matmul", "neighbor_aggregate", "neighbor_aggregate_backward", "segment_matmul", "spmm", "spmm_backward"]

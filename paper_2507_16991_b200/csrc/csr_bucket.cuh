@@ -97,19 +97,34 @@ __global__ void __launch_bounds__(kTileThreads) tile_hist_kernel(const int64_t* 
   for (int d = threadIdx.x; d < nb_max; d += kTileThreads) table[static_cast<int64_t>(d) * tiles + t] = hist[d];
 }
 
+// Lanes of the warp holding the same BITS-bit key as this lane: one ballot
+// per key bit (warp multisplit; cheaper than __match_any_sync). Invalid lanes
+// pass valid = false and are never anyone's peer.
+template <int BITS>
+__device__ __forceinline__ unsigned peers_of(uint32_t key, bool valid) {
+  unsigned m = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+  for (int b = 0; b < BITS; ++b) {
+    const unsigned bb = __ballot_sync(0xffffffffu, (key >> b) & 1u);
+    m &= ((key >> b) & 1u) ? bb : ~bb;
+  }
+  return m;
+}
+
 // 3. stable scatter of each tile's entries into their buckets' runs. The
-// codes of a warp's 512 positions are loaded up front (independent loads), the
-// 16 ranking rounds then only touch registers and shared memory.
+// codes of a warp's 512 positions are loaded up front (independent loads); the
+// 16 ranking rounds then only touch registers and shared memory. Staged as
+// (local row u16) and (COO position, value) int2.
 __global__ void __launch_bounds__(kTileThreads) tile_scatter_kernel(
     const uint32_t* __restrict__ code, const int64_t* __restrict__ values, int64_t e, int32_t nb_max, int64_t tiles,
-    const int32_t* __restrict__ table_off, uint16_t* __restrict__ st_row, int32_t* __restrict__ st_pos,
-    int32_t* __restrict__ st_val) {
-  extern __shared__ uint16_t whist[];  // [kTileWarps][nb_max]
+    const int32_t* __restrict__ table_off, uint16_t* __restrict__ st_row, int2* __restrict__ st_pv) {
+  extern __shared__ int32_t tile_off[];  // [nb_max] this tile's first slot per bucket, then whist
+  uint16_t* whist = reinterpret_cast<uint16_t*>(tile_off + nb_max);  // [kTileWarps][nb_max]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t t = blockIdx.x;
   for (int i = threadIdx.x; i < kTileWarps * nb_max; i += kTileThreads) whist[i] = 0;
   const int64_t wbase = t * kTileItems + static_cast<int64_t>(w) * (32 * kRounds);
-  uint32_t c[kRounds];  // bucket << 16 | local row, then | rank << 22 after ranking
+  uint32_t c[kRounds];  // bucket << 16 | local row, then rank << 22 | bucket << 10 | local row
 #pragma unroll
   for (int j = 0; j < kRounds; ++j) {
     const int64_t i = wbase + j * 32 + lane;
@@ -121,22 +136,20 @@ __global__ void __launch_bounds__(kTileThreads) tile_scatter_kernel(
 #pragma unroll
   for (int j = 0; j < kRounds; ++j) {
     const bool valid = c[j] != 0xffffffffu;
-    // invalid lanes get a digit no other lane has
-    const int32_t d = valid ? static_cast<int32_t>(c[j] >> 16) : static_cast<int32_t>(0x40000000 | lane);
-    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t d = valid ? (c[j] >> 16) : 0u;
+    const unsigned peers = peers_of<12>(d, valid);
     uint16_t old = 0;
     if (valid) old = my[d];
     __syncwarp();
     if (valid && (peers & lt) == 0) my[d] = static_cast<uint16_t>(old + __popc(peers));
     __syncwarp();
-    // rank inside the warp's 512 positions (< 512): bits 22..31 over the
-    // local row (bits 0..9, kBucketRows = 1024); the bucket stays readable
-    // from the saved d
-    if (valid) c[j] = (static_cast<uint32_t>(old + __popc(peers & lt)) << 22) | (c[j] & 0x3ffu) |
-                      (static_cast<uint32_t>(d) << 10);
+    // rank inside the warp's 512 positions (< 512) in bits 22..31, bucket in
+    // bits 10..21, local row (kBucketRows = 1024) in bits 0..9
+    if (valid) c[j] = (static_cast<uint32_t>(old + __popc(peers & lt)) << 22) | (d << 10) | (c[j] & 0x3ffu);
   }
   __syncthreads();
   // per bucket: exclusive prefix over the warps (tile totals <= 8192 fit u16)
+  // and this tile's first output slot
   for (int d = threadIdx.x; d < nb_max; d += kTileThreads) {
     uint16_t run = 0;
 #pragma unroll
@@ -145,6 +158,7 @@ __global__ void __launch_bounds__(kTileThreads) tile_scatter_kernel(
       whist[ww * nb_max + d] = run;
       run = static_cast<uint16_t>(run + cnt);
     }
+    tile_off[d] = run ? table_off[static_cast<int64_t>(d) * tiles + t] : 0;
   }
   __syncthreads();
 #pragma unroll
@@ -152,10 +166,9 @@ __global__ void __launch_bounds__(kTileThreads) tile_scatter_kernel(
     const int64_t i = wbase + j * 32 + lane;
     if (i < e) {
       const int32_t d = static_cast<int32_t>((c[j] >> 10) & 0xfffu);
-      const int64_t out = static_cast<int64_t>(table_off[static_cast<int64_t>(d) * tiles + t]) + my[d] + (c[j] >> 22);
+      const int64_t out = static_cast<int64_t>(tile_off[d]) + my[d] + (c[j] >> 22);
       st_row[out] = static_cast<uint16_t>(c[j] & 0x3ffu);
-      st_pos[out] = static_cast<int32_t>(i);
-      st_val[out] = static_cast<int32_t>(values[i]);
+      st_pv[out] = make_int2(static_cast<int32_t>(i), static_cast<int32_t>(values[i]));
     }
   }
 }
@@ -163,8 +176,8 @@ __global__ void __launch_bounds__(kTileThreads) tile_scatter_kernel(
 // 4. per bucket: rank by row (stable), write perm / col at the final slots.
 __global__ void __launch_bounds__(32 * kFinWarps) bucket_finalize_kernel(
     const int64_t* __restrict__ rowptr, const int32_t* __restrict__ first_row, const int32_t* __restrict__ num,
-    const uint16_t* __restrict__ st_row, const int32_t* __restrict__ st_pos, const int32_t* __restrict__ st_val,
-    int32_t* __restrict__ perm, int32_t* __restrict__ col) {
+    const uint16_t* __restrict__ st_row, const int2* __restrict__ st_pv, int32_t* __restrict__ perm,
+    int32_t* __restrict__ col) {
   extern __shared__ int32_t fin_smem[];  // [kFinWarps][kBucketRows] row counters
   int32_t(*cnt)[kBucketRows] = reinterpret_cast<int32_t(*)[kBucketRows]>(fin_smem);
   const int b = blockIdx.x;
@@ -174,8 +187,9 @@ __global__ void __launch_bounds__(32 * kFinWarps) bucket_finalize_kernel(
   if (e == s) return;
   if (r1 - r0 == 1) {  // one row (a hub): already in COO order
     for (int64_t k = s + threadIdx.x; k < e; k += blockDim.x) {
-      perm[k] = st_pos[k];
-      col[k] = st_val[k];
+      const int2 pv = st_pv[k];
+      perm[k] = pv.x;
+      col[k] = pv.y;
     }
     return;
   }
@@ -201,8 +215,9 @@ __global__ void __launch_bounds__(32 * kFinWarps) bucket_finalize_kernel(
   for (int64_t k0 = ws; k0 < we; k0 += 32) {
     const int64_t k = k0 + lane;
     const bool valid = k < we;
-    const int32_t r = valid ? static_cast<int32_t>(st_row[k]) : (0x40000000 | lane);
-    const unsigned peers = __match_any_sync(0xffffffffu, r);
+    const uint32_t r = valid ? static_cast<uint32_t>(st_row[k]) : 0u;
+    const int2 pv = valid ? st_pv[k] : make_int2(0, 0);
+    const unsigned peers = peers_of<10>(r, valid);
     int32_t old = 0;
     if (valid) old = cnt[w][r];
     __syncwarp();
@@ -210,8 +225,8 @@ __global__ void __launch_bounds__(32 * kFinWarps) bucket_finalize_kernel(
     __syncwarp();
     if (valid) {
       const int64_t dst = s + old + __popc(peers & lt);
-      perm[dst] = st_pos[k];
-      col[dst] = st_val[k];
+      perm[dst] = pv.x;
+      col[dst] = pv.y;
     }
   }
 }
@@ -318,8 +333,7 @@ struct BucketWs {
   int32_t* partial;    // scan32 block sums
   uint32_t* code;      // [e] bucket << 16 | local row
   uint16_t* st_row;    // [e]
-  int32_t* st_pos;     // [e]
-  int32_t* st_val;     // [e]
+  int2* st_pv;         // [e] (COO position, value)
   size_t bytes;
 };
 
@@ -342,8 +356,7 @@ inline BucketWs bucket_layout(void* base, int64_t e, int64_t rows) {
       take(sizeof(int32_t) * static_cast<size_t>(scan32_blocks(std::max(nb * tiles, rows)))));
   w.code = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * static_cast<size_t>(e)));
   w.st_row = reinterpret_cast<uint16_t*>(take(sizeof(uint16_t) * static_cast<size_t>(e)));
-  w.st_pos = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(e)));
-  w.st_val = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(e)));
+  w.st_pv = reinterpret_cast<int2*>(take(sizeof(int2) * static_cast<size_t>(e)));
   w.bytes = off;
   return w;
 }
@@ -372,12 +385,12 @@ inline gm_status bucket_build(const int64_t* keys, const int64_t* values, int64_
   GM_CHECK_LAUNCH("tile_hist_kernel");
   s = scan32_exclusive(w.table, nb * tiles, w.partial, st);
   if (s != GM_OK) return s;
-  const size_t smem = sizeof(uint16_t) * kTileWarps * static_cast<size_t>(nb);
+  const size_t smem = (sizeof(int32_t) + sizeof(uint16_t) * kTileWarps) * static_cast<size_t>(nb);
   if (smem > 48 * 1024)
     GM_TRY_CUDA(cudaFuncSetAttribute(tile_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
   tile_scatter_kernel<<<static_cast<unsigned>(tiles), kTileThreads, smem, st>>>(
-      w.code, values, e, static_cast<int32_t>(nb), tiles, w.table, w.st_row, w.st_pos, w.st_val);
+      w.code, values, e, static_cast<int32_t>(nb), tiles, w.table, w.st_row, w.st_pv);
   GM_CHECK_LAUNCH("tile_scatter_kernel");
   // GM_CSR_FIN_SMEM (bytes, tuning only) can reserve more shared memory to
   // cap the finalize CTAs per SM (fewer open output regions in L2)
@@ -386,7 +399,7 @@ inline gm_status bucket_build(const int64_t* keys, const int64_t* values, int64_
   GM_TRY_CUDA(cudaFuncSetAttribute(bucket_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(fin_smem)));
   bucket_finalize_kernel<<<static_cast<unsigned>(nb), 32 * kFinWarps, fin_smem, st>>>(rowptr, w.first_row, w.num, w.st_row,
-                                                                             w.st_pos, w.st_val, perm, col);
+                                                                             w.st_pv, perm, col);
   GM_CHECK_LAUNCH("bucket_finalize_kernel");
   return GM_OK;
 }

@@ -68,6 +68,13 @@ struct Params {
   const float* a_f32;
   int32_t a_ld;
   int32_t x_stages;                   // SPLIT: fp32 x staging ring depth
+  // fp32-accurate split (CVT = 3): acc_sets > 0 keeps the hi*hi product and
+  // the five correction products in separate TMEM accumulators and spreads
+  // the k-blocks round-robin over acc_sets such pairs, summed in the
+  // epilogue: each fp32 accumulator sees ~1/(6 acc_sets) of the MMA steps, so
+  // the tensor pipe's per-step accumulation error grows that much slower.
+  int32_t acc_sets;
+  int32_t acc_cols;                   // TMEM columns per double-buffer slot
   void* out;
 };
 
@@ -380,7 +387,7 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
       }
       mbar_wait(&tempty[acc], aph ^ 1);
       tc_fence_after();
-      const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * P.bn);
+      const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * P.acc_cols);
       for (int kb = 0; kb < P.k_blocks; ++kb) {
         mbar_wait(&full[s], ph);
         tc_fence_after();
@@ -396,12 +403,27 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
           constexpr int kPa[6] = {0, 0, 1, 0, 2, 1};
           constexpr int kPb[6] = {0, 1, 0, 2, 0, 1};
           constexpr int kPairs = CVT == 3 ? 6 : 1;
+          if (CVT == 3 && P.acc_sets > 0) {
+            // set kb % R: columns [2 set, 2 set + 1) * bn hold (hi*hi, corrections)
+            const int set = kb % P.acc_sets;
+            const bool first_use = kb < P.acc_sets;
+            const uint32_t d_main = tmem_d + static_cast<uint32_t>(2 * set * P.bn);
+            const uint32_t d_corr = d_main + static_cast<uint32_t>(P.bn);
 #pragma unroll
-          for (int pr = 0; pr < kPairs; ++pr)
+            for (int pr = 0; pr < kPairs; ++pr)
 #pragma unroll
-            for (int k = 0; k < KBLK / 16; ++k)
-              tc_mma(tmem_d, sdesc_k<KBLK>(a_addr + kPa[pr] * kAStage + k * 32),
-                     sdesc_k<KBLK>(b_addr[kPb[pr]] + k * 32), idesc, (kb > 0 || pr > 0 || k > 0) ? 1u : 0u);
+              for (int k = 0; k < KBLK / 16; ++k)
+                tc_mma(pr == 0 ? d_main : d_corr, sdesc_k<KBLK>(a_addr + kPa[pr] * kAStage + k * 32),
+                       sdesc_k<KBLK>(b_addr[kPb[pr]] + k * 32), idesc,
+                       (!first_use || k > 0 || pr > 1) ? 1u : 0u);
+          } else {
+#pragma unroll
+            for (int pr = 0; pr < kPairs; ++pr)
+#pragma unroll
+              for (int k = 0; k < KBLK / 16; ++k)
+                tc_mma(tmem_d, sdesc_k<KBLK>(a_addr + kPa[pr] * kAStage + k * 32),
+                       sdesc_k<KBLK>(b_addr[kPb[pr]] + k * 32), idesc, (kb > 0 || pr > 0 || k > 0) ? 1u : 0u);
+          }
           tc_commit(&empty[s]);
         } else if (!SPLIT && lane == 0) {
           const uint32_t a_addr = smem_u32(a_ring + static_cast<size_t>(s) * kAStage);
@@ -461,14 +483,69 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
       const bool full_tile = P.tma_store && row0 + BM <= grow_end;  // else: masked direct stores
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
-      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * P.bn);
+      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * P.acc_cols);
+      // split accumulators: (sum of the hi*hi sets) + (sum of the correction sets), fp32 RN
+      auto load_cols = [&](uint32_t col, uint32_t* v, auto width_c) {
+        constexpr int W = decltype(width_c)::value;
+        if (!(CVT == 3 && P.acc_sets > 0)) {
+          tmem_ld32<W>(tbase + col, v);
+          tmem_wait_ld();
+          return;
+        }
+        // 16 columns at a time keeps the partial sums in registers
+#pragma unroll
+        for (int h = 0; h < W; h += 16) {
+          uint32_t* vh = v + h;
+          uint32_t t[16];
+          float corr[16];
+          tmem_ld32<16>(tbase + col + h, vh);
+          tmem_ld32<16>(tbase + static_cast<uint32_t>(P.bn) + col + h, t);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) corr[i] = __uint_as_float(t[i]);
+          for (int set = 1; set < P.acc_sets; ++set) {
+            tmem_ld32<16>(tbase + static_cast<uint32_t>(2 * set * P.bn) + col + h, t);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) vh[i] = __float_as_uint(__fadd_rn(__uint_as_float(vh[i]), __uint_as_float(t[i])));
+            tmem_ld32<16>(tbase + static_cast<uint32_t>((2 * set + 1) * P.bn) + col + h, t);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) corr[i] = __fadd_rn(corr[i], __uint_as_float(t[i]));
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) vh[i] = __float_as_uint(__fadd_rn(__uint_as_float(vh[i]), corr[i]));
+        }
+      };
       if (full_tile) {
         for (int c = c_lo; c < c_hi; c += chunk_cols) {
+          if (CVT == 3 && P.acc_sets > 0) {
+            // split accumulators: summed and staged 16 columns at a time
+            if (lane == 0 && nstore >= 1) bulk_wait_read<0>();  // the previous store has read the box
+            __syncwarp();
+            const uint32_t sb = smem_u32(my_stage) + lane * 128;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              uint32_t part[16];
+              load_cols(static_cast<uint32_t>(c + 16 * h), part, std::integral_constant<int, 16>{});
+#pragma unroll
+              for (int ch = 0; ch < 4; ++ch)
+                st_shared_v4(sb + (((4 * h + ch) ^ (lane & 7)) << 4), part[4 * ch], part[4 * ch + 1],
+                             part[4 * ch + 2], part[4 * ch + 3]);
+            }
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&map_c, my_stage, nt * P.bn + c, static_cast<int32_t>(row0 + q * 32));
+              bulk_commit();
+            }
+            ++nstore;
+            continue;
+          }
           // 128 bytes of this lane's row: 32 fp32 or 64 bf16 values
           uint32_t packed[32];
           if (out_f32) {
-            tmem_ld32<32>(tbase + c, packed);
-            tmem_wait_ld();
+            load_cols(static_cast<uint32_t>(c), packed, std::integral_constant<int, 32>{});
           } else {
             uint32_t v[32];
             tmem_ld32<32>(tbase + c, v);
@@ -498,20 +575,19 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
         }
       } else {
         const bool live = row < grow_end;
-        for (int c = c_lo; c < c_hi; c += 32) {
-          uint32_t v[32];
-          const int width = min(32, c_hi - c);
-          if (width == 32) tmem_ld32<32>(tbase + c, v);
-          else tmem_ld32<16>(tbase + c, v);
-          tmem_wait_ld();
+        for (int c = c_lo; c < c_hi; c += 16) {  // bn is a multiple of 16
+          uint32_t v[16];
+          load_cols(static_cast<uint32_t>(c), v, std::integral_constant<int, 16>{});
           if (live) {
             const int64_t col0 = static_cast<int64_t>(nt) * P.bn + c;
             if (out_f32) {
               float* o = static_cast<float*>(P.out) + row * P.n + col0;
-              for (int i = 0; i < width; i += 4) st_na_v4(o + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
+#pragma unroll
+              for (int i = 0; i < 16; i += 4) st_na_v4(o + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
             } else {
               __nv_bfloat16* o = static_cast<__nv_bfloat16*>(P.out) + row * P.n + col0;
-              for (int i = 0; i < width; i += 8)
+#pragma unroll
+              for (int i = 0; i < 16; i += 8)
                 st_na_v4(o + i, pack_bf16(v[i], v[i + 1]), pack_bf16(v[i + 2], v[i + 3]),
                          pack_bf16(v[i + 4], v[i + 5]), pack_bf16(v[i + 6], v[i + 7]));
             }
@@ -858,8 +934,18 @@ static gm_status segment_matmul_impl(const void* x, const int64_t* ptr_host, int
   P.ptr[groups] = ptr_host[groups];
   P.tile_start[groups] = tiles;
   P.num_tiles = tiles;
+  // fp32-accurate split: separate hi*hi / correction accumulators, spread over
+  // as many k-block sets as TMEM's 512 columns hold (two buffered tiles)
+  P.acc_sets = 0;
+  if (a_f32 && a_pieces == 3) {
+    static const int sets_env = [] { const char* e = getenv("GM_GEMM_ACC_SETS"); return e ? atoi(e) : 4; }();
+    int sets = std::max(0, std::min(sets_env, 512 / (4 * P.bn)));
+    sets = std::min(sets, P.k_blocks);
+    P.acc_sets = sets;
+  }
+  P.acc_cols = P.acc_sets > 0 ? 2 * P.acc_sets * P.bn : P.bn;
   uint32_t cols = 32;
-  while (cols < static_cast<uint32_t>(2 * P.bn)) cols <<= 1;
+  while (cols < static_cast<uint32_t>(2 * P.acc_cols)) cols <<= 1;
   P.tmem_cols = cols;
 
   const size_t b_full_bytes = static_cast<size_t>(pieces) * P.k_blocks * P.bn * kblk * 2;

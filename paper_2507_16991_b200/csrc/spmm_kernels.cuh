@@ -251,56 +251,6 @@ __device__ __forceinline__ unsigned short ldg_hot_cs_v<unsigned short>(const uns
   return r;
 }
 
-// Descriptor-free hot / cold pair with the column validity folded in:
-// hot ? default L2 policy : evict-first streaming (ld.global.cs). No 64-bit
-// createpolicy operand, so no uniform-register descriptor per gather.
-template <typename R>
-__device__ __forceinline__ R ldg_nc_cs_v(const R* p, bool valid, bool hot);
-template <>
-__device__ __forceinline__ uint4 ldg_nc_cs_v<uint4>(const uint4* p, bool valid, bool hot) {
-  uint4 r;
-  asm("{\n\t.reg .pred v, h, a, b;\n\tsetp.ne.b32 v, %5, 0;\n\tsetp.ne.b32 h, %6, 0;\n\t"
-      "and.pred a, v, h;\n\tand.pred b, v, !h;\n\t"
-      "@a ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\n\t"
-      "@b ld.global.cs.nc.v4.u32 {%0,%1,%2,%3}, [%4];\n\t}"
-      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-      : "l"(p), "r"(static_cast<int>(valid)), "r"(static_cast<int>(hot)));
-  return r;
-}
-template <>
-__device__ __forceinline__ uint2 ldg_nc_cs_v<uint2>(const uint2* p, bool valid, bool hot) {
-  uint2 r;
-  asm("{\n\t.reg .pred v, h, a, b;\n\tsetp.ne.b32 v, %3, 0;\n\tsetp.ne.b32 h, %4, 0;\n\t"
-      "and.pred a, v, h;\n\tand.pred b, v, !h;\n\t"
-      "@a ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];\n\t"
-      "@b ld.global.cs.nc.v2.u32 {%0,%1}, [%2];\n\t}"
-      : "=r"(r.x), "=r"(r.y)
-      : "l"(p), "r"(static_cast<int>(valid)), "r"(static_cast<int>(hot)));
-  return r;
-}
-template <>
-__device__ __forceinline__ uint32_t ldg_nc_cs_v<uint32_t>(const uint32_t* p, bool valid, bool hot) {
-  uint32_t r;
-  asm("{\n\t.reg .pred v, h, a, b;\n\tsetp.ne.b32 v, %2, 0;\n\tsetp.ne.b32 h, %3, 0;\n\t"
-      "and.pred a, v, h;\n\tand.pred b, v, !h;\n\t"
-      "@a ld.global.nc.L1::no_allocate.u32 %0, [%1];\n\t"
-      "@b ld.global.cs.nc.u32 %0, [%1];\n\t}"
-      : "=r"(r)
-      : "l"(p), "r"(static_cast<int>(valid)), "r"(static_cast<int>(hot)));
-  return r;
-}
-template <>
-__device__ __forceinline__ unsigned short ldg_nc_cs_v<unsigned short>(const unsigned short* p, bool valid, bool hot) {
-  unsigned short r;
-  asm("{\n\t.reg .pred v, h, a, b;\n\tsetp.ne.b32 v, %2, 0;\n\tsetp.ne.b32 h, %3, 0;\n\t"
-      "and.pred a, v, h;\n\tand.pred b, v, !h;\n\t"
-      "@a ld.global.nc.L1::no_allocate.u16 %0, [%1];\n\t"
-      "@b ld.global.cs.nc.u16 %0, [%1];\n\t}"
-      : "=h"(r)
-      : "l"(p), "r"(static_cast<int>(valid)), "r"(static_cast<int>(hot)));
-  return r;
-}
-
 // ldg_hint2 with the lane's column-validity folded into the predicates: no
 // branch at all per gather (invalid lanes issue nothing, their register is
 // never read).
@@ -674,10 +624,8 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 8 || (SCALED && (MODE >= 2 
   };
 
   constexpr bool HINT = LM >= 1;  // per-entry hot flag (false when the plan's classes are off)
-  // LM = 3: hot rows default policy, cold rows ld.global.cs — no descriptors
-  const uint64_t pol_hot = (LM == 1 || LM == 2) ? policy_evict_last() : 0;
-  const uint64_t pol_cold = (LM == 1 || LM == 2) ? policy_evict_first() : 0;
-  constexpr bool GUARD = LM != 3;  // LM = 3 accumulates invalid lanes' (unloaded) vectors too; never stored
+  const uint64_t pol_hot = HINT ? policy_evict_last() : 0;
+  const uint64_t pol_cold = HINT ? policy_evict_first() : 0;
   int32_t c_next = 0, p_next = -1;
   bool h_next = false;
   A w_next = A(1);
@@ -706,14 +654,7 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 8 || (SCALED && (MODE >= 2 
     for (int u = 0; u < U; ++u) {
       const T* xr = x + static_cast<uint64_t>(static_cast<uint32_t>(__shfl_sync(FULL, c_cur, u))) * fu;
       const bool hot = (hmask >> u) & 1u;
-      if constexpr (LM == 3) {
-        // descriptor-free hot/cold pair, column validity folded in, lane base
-        // pointer: one IMAD.WIDE + two predicated loads per gather, no branch
-        const unsigned char* xs = xlane + static_cast<uint64_t>(static_cast<uint32_t>(__shfl_sync(FULL, c_cur, u))) * rowb;
-#pragma unroll
-        for (int j = 0; j < NV; ++j)
-          buf[u][j] = ldg_nc_cs_v<R>(reinterpret_cast<const R*>(xs + j * 32 * VB), valid[j], hot);
-      } else if constexpr (LM >= 1 && !MAXMIN && VB <= 8) {
+      if constexpr (LM >= 1 && !MAXMIN && VB <= 8) {
         // predicated evict_last / evict_first pair with the column validity
         // folded in and a precomputed lane base: no branch, one IMAD.WIDE per
         // gather (8-byte vectors: C5 87 -> 79 ms, C2 55 -> 51 ms in A/B runs;
@@ -766,7 +707,7 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 8 || (SCALED && (MODE >= 2 
         const int32_t pm = MAXMIN ? __shfl_sync(FULL, p_cur, u) : -1;
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
-          if (!GUARD || valid[j]) {
+          if (valid[j]) {
             A vals[V];
             VecT::unpack(buf[u][j], vals);
             acc.add(j, vals, SCALED, sc, first && u == 0, IS_MIN, pm, lex);
@@ -791,7 +732,7 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 8 || (SCALED && (MODE >= 2 
             const int32_t pm = MAXMIN ? __shfl_sync(FULL, p_cur, u) : -1;
 #pragma unroll
             for (int j = 0; j < NV; ++j)
-              if (!GUARD || valid[j]) {
+              if (valid[j]) {
                 A vals[V];
                 VecT::unpack(buf[u][j], vals);
                 acc.add(j, vals, SCALED, sc, first && u == u0, IS_MIN, pm, lex);
@@ -812,7 +753,7 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 8 || (SCALED && (MODE >= 2 
           while (k0 + u >= row_end) flush();
 #pragma unroll
           for (int j = 0; j < NV; ++j)
-            if (!GUARD || valid[j]) {
+            if (valid[j]) {
               A vals[V];
               VecT::unpack(buf[u][j], vals);
               acc.add(j, vals, SCALED, sc, first, IS_MIN, pm, lex);
@@ -838,16 +779,6 @@ inline int flat_max_nv() {
   return nv;
 }
 constexpr int kRing = 4;
-// GM_FLAT_LM3=1: the hinted flat path uses descriptor-free hot/cold gathers
-// (default policy / ld.global.cs) instead of evict_last / evict_first policies.
-inline int flat_max_u() {
-  static const int u = [] { const char* e = getenv("GM_FLAT_MAX_U"); return e ? atoi(e) : 8; }();
-  return u;
-}
-inline bool flat_lm3() {
-  static const bool on = [] { const char* e = getenv("GM_FLAT_LM3"); return e && atoi(e) != 0; }();
-  return on;
-}
 
 __device__ __forceinline__ void cp_async(void* smem, const void* gmem, int bytes) {
   const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
@@ -1307,7 +1238,7 @@ gm_status launch_flat(const SpmmArgs& p0, int64_t ns, cudaStream_t st) {
   const int64_t chunk = std::min<int64_t>(kChunk, 32 * std::max(1, flat_max_nv()));
   // streaming gathers unless X is small enough to live in L2; hot rows keep
   // an evict_last policy on the plain (unscaled, fresh) path when hinted
-  const int lm = p0.stream_x == 0 ? 0 : (p0.src_class != nullptr && !p0.accum) ? (flat_lm3() ? 3 : 2) : 1;
+  const int lm = p0.stream_x == 0 ? 0 : (p0.src_class != nullptr && !p0.accum) ? 2 : 1;
   for (int64_t base = 0; base < ns; base += chunk) {
     SpmmArgs p = p0;
     p.slot_base = base;
@@ -1326,11 +1257,7 @@ gm_status launch_flat(const SpmmArgs& p0, int64_t ns, cudaStream_t st) {
   } while (0)
 #define GM_FLAT_K(NV_, U_, M_)                                                                     \
   do {                                                                                             \
-    if (lm == 3) {                                                                                 \
-      if (scaled) spmm_flat_kernel<T, VB, NV_, U_, M_, true, false, 3><<<grid, 256, 0, st>>>(p);     \
-      else spmm_flat_kernel<T, VB, NV_, U_, M_, false, false, 3><<<grid, 256, 0, st>>>(p);           \
-    }                                                                                              \
-    else if (lm == 2) {                                                                            \
+    if (lm == 2) {                                                                                 \
       if (scaled) spmm_flat_kernel<T, VB, NV_, U_, M_, true, false, 2><<<grid, 256, 0, st>>>(p);     \
       else spmm_flat_kernel<T, VB, NV_, U_, M_, false, false, 2><<<grid, 256, 0, st>>>(p);           \
     }                                                                                              \
@@ -1355,17 +1282,7 @@ gm_status launch_flat(const SpmmArgs& p0, int64_t ns, cudaStream_t st) {
       else if (nv == 4 || kChunk <= 128) GM_FLAT(4, 2);
       else if constexpr (kChunk > 128) GM_FLAT(8, 1);
     } else {
-      if (nv == 1) {
-        if constexpr (MAXMIN) {
-          // max/min are issue-bound at 64 registers: fewer edges in flight
-          // per batch frees the gather registers (GM_FLAT_MAX_U = 4 / 6 / 8)
-          if (flat_max_u() == 4) GM_FLAT(1, 4);
-          else if (flat_max_u() == 6) GM_FLAT(1, 6);
-          else GM_FLAT(1, 8);
-        } else {
-          GM_FLAT(1, 8);
-        }
-      }
+      if (nv == 1) GM_FLAT(1, 8);
       else if (nv == 2) GM_FLAT(2, 4);
       else if (nv == 4 || kChunk <= 128) GM_FLAT(4, 2);
       else if constexpr (kChunk > 128) GM_FLAT(8, 1);

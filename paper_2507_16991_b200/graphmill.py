@@ -240,6 +240,26 @@ class EdgeIndex:
             self._cache.exact = build_compressed(self.dst(), self.src(), self._num_dst, self._num_src)
         return self._cache.exact
 
+    def source_view(self) -> CsrView:
+        """Per source node, its entries in ascending CSC position (gm_source_view),
+        with COO edge ids as perm: the gather order of the max/min backward.
+        Built once from the CSC and cached beside it."""
+        if self._cache.source is None:
+            csc = self.to_csc()
+            lib = L.lib()
+            e, n = csc.num_entries(), self._num_src
+            dev = csc.rowptr.device
+            rowptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
+            col = torch.empty(max(e, 1), dtype=torch.int32, device=dev)
+            eid = torch.empty(max(e, 1), dtype=torch.int32, device=dev)
+            nb = lib.gm_source_view_workspace(e, n)
+            ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=dev)
+            cs = csc.c_struct()
+            L.check(lib.gm_source_view(C.byref(cs), n, _p(rowptr), _p(col), _p(eid), _p(ws), nb, _stream()),
+                    "gm_source_view")
+            self._cache.source = CsrView(rowptr, col, eid, self._num_dst)
+        return self._cache.source
+
     def has_csr_cache(self) -> bool:
         return self._cache.csr is not None
 
@@ -315,6 +335,7 @@ class _CacheSlot:
         self.csr_builds = 0
         self.csc_builds = 0
         self.exact: Optional[CsrView] = None
+        self.source: Optional[CsrView] = None
         self.gcn_deg: dict = {}
 
 
@@ -452,6 +473,35 @@ def neighbor_aggregate(e: EdgeIndex, x: torch.Tensor, kind: str,
         w_csr = _permute(edge_weight.to(_acc_dtype(x.dtype)).contiguous(), grouping.perm)
     want = return_argmax and kind in ("max", "min")
     return _run_spmm(grouping, x, kind, w_csr=w_csr, want_arg=want, num_rows=e.num_dst_nodes())
+
+
+def neighbor_aggregate_backward(e: EdgeIndex, kind: str, grad_out: torch.Tensor,
+                                argmax: torch.Tensor) -> torch.Tensor:
+    """Backward of neighbor_aggregate max/min (message_passing.hpp:508-514):
+    aggregate's argpos scatter (aggregate.hpp:295-308) then the gather_rows
+    adjoint (tensor.hpp:510-524), fused into one gather over the source view.
+    argmax: the COO edge ids returned by neighbor_aggregate(..., return_argmax=True).
+    Returns dx [num_src_nodes, F], bit-identical to the reference tape."""
+    if kind not in ("max", "min"):
+        raise ValueError("neighbor_aggregate_backward: max or min")
+    if grad_out.dtype not in (torch.float32, torch.float64):
+        raise ValueError("neighbor_aggregate_backward: f32/f64 only")
+    if grad_out.dim() != 2 or grad_out.shape[0] != e.num_dst_nodes():
+        raise ValueError("neighbor_aggregate_backward: grad_out must be [num_dst_nodes, F]")
+    if tuple(argmax.shape) != tuple(grad_out.shape) or argmax.dtype != torch.int32:
+        raise ValueError("neighbor_aggregate_backward: argmax must be int32 like grad_out")
+    if e.is_undirected():
+        raise ValueError("neighbor_aggregate_backward: undirected views group by the CSR; "
+                         "build the index without the is_undirected claim")
+    g = grad_out.contiguous()
+    f = g.shape[1]
+    view = e.source_view()
+    dx = torch.empty((e.num_src_nodes(), f), dtype=g.dtype, device=g.device)
+    cs = view.c_struct()
+    plan = view.plan(row_bytes=f * g.element_size())
+    L.check(L.lib().gm_spmm_max_backward(C.byref(cs), C.byref(plan), _DT[g.dtype], _p(argmax.contiguous()), _p(g),
+                                         f, _p(dx), _stream()), "gm_spmm_max_backward")
+    return dx
 
 
 def gcn_degrees(e: EdgeIndex, square: bool):

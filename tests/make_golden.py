@@ -199,11 +199,43 @@ def hetero_fixtures(ref: Reference) -> dict:
                 w_neigh=w_neigh, w_self=w_self, bias=bias, out=out)
 
 
+def maxbwd_fixtures(ref: Reference) -> dict:
+    """Backward of the layer max/min path through the reference's own tape
+    (aggregate.hpp:295-308 + gather_rows adjoint): quantised features (ties,
+    +-0), a source hub (out-degree > the 1024-edge heavy threshold of the
+    source view), a destination hub, duplicate edges, empty rows; f32 and f64."""
+    d = {}
+    rng = np.random.default_rng(4321)
+    n = 3000
+    src = np.concatenate([np.full(4000, 11), rng.integers(0, n, 14000), np.full(1500, 2222)])
+    dst = np.concatenate([rng.integers(0, n, 4000), rng.integers(0, n - 100, 14000), rng.integers(0, 40, 1500)])
+    dup = rng.integers(0, src.size, 800)
+    src, dst = np.concatenate([src, src[dup]]), np.concatenate([dst, dst[dup]])
+    order = rng.permutation(src.size)
+    src, dst = src[order].astype(np.int64), dst[order].astype(np.int64)
+    d.update(src=src, dst=dst, n=np.array([n]))
+    for dt, f in (("f32", 12), ("f64", 5)):
+        x = np.floor(rng.uniform(-1, 1, (n, f)) * 8) / 8
+        x[rng.random((n, f)) < 0.1] = -0.0
+        g = rng.uniform(-1, 1, (n, f))
+        npdt = np.float32 if dt == "f32" else np.float64
+        x, g = x.astype(npdt), g.astype(npdt)
+        d[f"{dt}_x"], d[f"{dt}_g"] = x, g
+        for kind in ("max", "min"):
+            d[f"{dt}_{kind}_dx"] = ref.max_backward(src, dst, n, n, x, g, is_min=(kind == "min"))
+            d[f"{dt}_{kind}_arg"] = ref.max_path(src, dst, n, n, x, is_min=(kind == "min"))[1]
+    return d
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     ref = Reference()
-    for name, fn in (("csr", csr_fixtures), ("spmm", spmm_fixtures), ("gemm", gemm_fixtures),
-                     ("hetero", hetero_fixtures)):
+    fixtures = (("csr", csr_fixtures), ("spmm", spmm_fixtures), ("gemm", gemm_fixtures),
+                ("hetero", hetero_fixtures), ("maxbwd", maxbwd_fixtures))
+    only = sys.argv[sys.argv.index("--only") + 1].split(",") if "--only" in sys.argv else None
+    for name, fn in fixtures:
+        if only and name not in only:
+            continue
         data = fn(ref)
         path = os.path.join(OUT, f"{name}.npz")
         np.savez_compressed(path, **data)
