@@ -125,10 +125,20 @@ __global__ void __launch_bounds__(kTileThreads) tile_scatter_kernel(
   for (int i = threadIdx.x; i < kTileWarps * nb_max; i += kTileThreads) whist[i] = 0;
   const int64_t wbase = t * kTileItems + static_cast<int64_t>(w) * (32 * kRounds);
   uint32_t c[kRounds];  // bucket << 16 | local row, then rank << 22 | bucket << 10 | local row
+  int32_t val[kRounds];  // values < 2^31 (int32 col)
 #pragma unroll
   for (int j = 0; j < kRounds; ++j) {
     const int64_t i = wbase + j * 32 + lane;
     c[j] = i < e ? __ldcs(code + i) : 0xffffffffu;
+    val[j] = i < e ? static_cast<int32_t>(__ldcs(values + i)) : 0;
+  }
+  // this tile's first slot of every bucket, fetched while the ranking runs
+  constexpr int kOffPer = kMaxBuckets / kTileThreads;
+  int32_t toff[kOffPer];
+#pragma unroll
+  for (int q = 0; q < kOffPer; ++q) {
+    const int d = threadIdx.x + q * kTileThreads;
+    toff[q] = d < nb_max ? table_off[static_cast<int64_t>(d) * tiles + t] : 0;
   }
   __syncthreads();
   uint16_t* my = whist + w * nb_max;
@@ -150,15 +160,19 @@ __global__ void __launch_bounds__(kTileThreads) tile_scatter_kernel(
   __syncthreads();
   // per bucket: exclusive prefix over the warps (tile totals <= 8192 fit u16)
   // and this tile's first output slot
-  for (int d = threadIdx.x; d < nb_max; d += kTileThreads) {
-    uint16_t run = 0;
 #pragma unroll
-    for (int ww = 0; ww < kTileWarps; ++ww) {
-      const uint16_t cnt = whist[ww * nb_max + d];
-      whist[ww * nb_max + d] = run;
-      run = static_cast<uint16_t>(run + cnt);
+  for (int q = 0; q < kOffPer; ++q) {
+    const int d = threadIdx.x + q * kTileThreads;
+    if (d < nb_max) {
+      uint16_t run = 0;
+#pragma unroll
+      for (int ww = 0; ww < kTileWarps; ++ww) {
+        const uint16_t cnt = whist[ww * nb_max + d];
+        whist[ww * nb_max + d] = run;
+        run = static_cast<uint16_t>(run + cnt);
+      }
+      tile_off[d] = toff[q];
     }
-    tile_off[d] = run ? table_off[static_cast<int64_t>(d) * tiles + t] : 0;
   }
   __syncthreads();
 #pragma unroll
@@ -168,7 +182,7 @@ __global__ void __launch_bounds__(kTileThreads) tile_scatter_kernel(
       const int32_t d = static_cast<int32_t>((c[j] >> 10) & 0xfffu);
       const int64_t out = static_cast<int64_t>(tile_off[d]) + my[d] + (c[j] >> 22);
       st_row[out] = static_cast<uint16_t>(c[j] & 0x3ffu);
-      st_pv[out] = make_int2(static_cast<int32_t>(i), static_cast<int32_t>(values[i]));
+      st_pv[out] = make_int2(static_cast<int32_t>(i), val[j]);
     }
   }
 }
@@ -199,7 +213,18 @@ __global__ void __launch_bounds__(32 * kFinWarps) bucket_finalize_kernel(
   __syncthreads();
   const int64_t len = e - s;
   const int64_t ws = s + len * w / kFinWarps, we = s + len * (w + 1) / kFinWarps;
-  for (int64_t k = ws + lane; k < we; k += 32) atomicAdd(&cnt[w][st_row[k]], 1);
+  constexpr int kFinU = 4;  // 32-entry batches in flight per warp
+  for (int64_t k0 = ws; k0 < we; k0 += 32 * kFinU) {
+    uint16_t rr[kFinU];
+#pragma unroll
+    for (int u = 0; u < kFinU; ++u) {
+      const int64_t k = k0 + u * 32 + lane;
+      rr[u] = k < we ? st_row[k] : 0xffff;
+    }
+#pragma unroll
+    for (int u = 0; u < kFinU; ++u)
+      if (rr[u] != 0xffff) atomicAdd(&cnt[w][rr[u]], 1);
+  }
   __syncthreads();
   for (int r = threadIdx.x; r < nr; r += blockDim.x) {
     int32_t run = static_cast<int32_t>(rowptr[r0 + r] - s);
@@ -212,21 +237,31 @@ __global__ void __launch_bounds__(32 * kFinWarps) bucket_finalize_kernel(
   }
   __syncthreads();
   const unsigned lt = (1u << lane) - 1u;
-  for (int64_t k0 = ws; k0 < we; k0 += 32) {
-    const int64_t k = k0 + lane;
-    const bool valid = k < we;
-    const uint32_t r = valid ? static_cast<uint32_t>(st_row[k]) : 0u;
-    const int2 pv = valid ? st_pv[k] : make_int2(0, 0);
-    const unsigned peers = peers_of<10>(r, valid);
-    int32_t old = 0;
-    if (valid) old = cnt[w][r];
-    __syncwarp();
-    if (valid && (peers & lt) == 0) cnt[w][r] = old + __popc(peers);
-    __syncwarp();
-    if (valid) {
-      const int64_t dst = s + old + __popc(peers & lt);
-      perm[dst] = pv.x;
-      col[dst] = pv.y;
+  for (int64_t k1 = ws; k1 < we; k1 += 32 * kFinU) {
+    uint32_t rr[kFinU];
+    int2 pv[kFinU];
+#pragma unroll
+    for (int u = 0; u < kFinU; ++u) {
+      const int64_t k = k1 + u * 32 + lane;
+      const bool valid = k < we;
+      rr[u] = valid ? static_cast<uint32_t>(st_row[k]) : 0xffffffffu;
+      pv[u] = valid ? st_pv[k] : make_int2(0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < kFinU; ++u) {
+      const bool valid = rr[u] != 0xffffffffu;
+      const uint32_t r = valid ? rr[u] : 0u;
+      const unsigned peers = peers_of<10>(r, valid);
+      int32_t old = 0;
+      if (valid) old = cnt[w][r];
+      __syncwarp();
+      if (valid && (peers & lt) == 0) cnt[w][r] = old + __popc(peers);
+      __syncwarp();
+      if (valid) {
+        const int64_t dst = s + old + __popc(peers & lt);
+        perm[dst] = pv[u].x;
+        col[dst] = pv[u].y;
+      }
     }
   }
 }

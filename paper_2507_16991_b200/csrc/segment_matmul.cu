@@ -429,11 +429,22 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
           const uint32_t a_addr = smem_u32(a_ring + static_cast<size_t>(s) * kAStage);
           const uint32_t b_addr = P.b_resident ? smem_u32(b_buf + static_cast<size_t>(kb) * b_kblock_bytes)
                                                : smem_u32(b_buf + static_cast<size_t>(s) * b_kblock_bytes);
+          uint32_t d = tmem_d;
+          bool fresh = kb == 0;
+          if (CVT == 0 && P.acc_sets > 0) {
+            // staged fp32 split: k-blocks of segment 0 (hi*hi) -> main sets,
+            // segments 1..5 (corrections) -> correction sets
+            const int segb = P.a_seg_k / KBLK;
+            const int part = kb >= segb ? 1 : 0;
+            const int kk = part ? kb - segb : kb;
+            d = tmem_d + static_cast<uint32_t>((2 * (kk % P.acc_sets) + part) * P.bn);
+            fresh = kk < P.acc_sets;
+          }
 #pragma unroll
           for (int k = 0; k < KBLK / 16; ++k) {
             // advancing 16 bf16 = 32 B inside the swizzle atom
-            tc_mma(tmem_d, sdesc_k<KBLK>(a_addr + k * 32), sdesc_k<KBLK>(b_addr + k * 32), idesc,
-                   (kb > 0 || k > 0) ? 1u : 0u);
+            tc_mma(d, sdesc_k<KBLK>(a_addr + k * 32), sdesc_k<KBLK>(b_addr + k * 32), idesc,
+                   (!fresh || k > 0) ? 1u : 0u);
           }
           tc_commit(&empty[s]);  // smem stage free once these MMAs retire
         }
@@ -487,7 +498,7 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
       // split accumulators: (sum of the hi*hi sets) + (sum of the correction sets), fp32 RN
       auto load_cols = [&](uint32_t col, uint32_t* v, auto width_c) {
         constexpr int W = decltype(width_c)::value;
-        if (!(CVT == 3 && P.acc_sets > 0)) {
+        if (CVT == 1 || P.acc_sets == 0) {
           tmem_ld32<W>(tbase + col, v);
           tmem_wait_ld();
           return;
@@ -519,7 +530,7 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
       };
       if (full_tile) {
         for (int c = c_lo; c < c_hi; c += chunk_cols) {
-          if (CVT == 3 && P.acc_sets > 0) {
+          if ((CVT == 3 || (CVT == 0 && out_f32)) && P.acc_sets > 0) {
             // split accumulators: summed and staged 16 columns at a time
             if (lane == 0 && nstore >= 1) bulk_wait_read<0>();  // the previous store has read the box
             __syncwarp();
@@ -937,10 +948,10 @@ static gm_status segment_matmul_impl(const void* x, const int64_t* ptr_host, int
   // fp32-accurate split: separate hi*hi / correction accumulators, spread over
   // as many k-block sets as TMEM's 512 columns hold (two buffered tiles)
   P.acc_sets = 0;
-  if (a_f32 && a_pieces == 3) {
+  if ((a_f32 && a_pieces == 3) || (a_seg_k > 0 && out_dtype == GM_F32)) {
     static const int sets_env = [] { const char* e = getenv("GM_GEMM_ACC_SETS"); return e ? atoi(e) : 4; }();
     int sets = std::max(0, std::min(sets_env, 512 / (4 * P.bn)));
-    sets = std::min(sets, P.k_blocks);
+    sets = std::min(sets, a_f32 ? P.k_blocks : static_cast<int>(a_seg_k / kblk));
     P.acc_sets = sets;
   }
   P.acc_cols = P.acc_sets > 0 ? 2 * P.acc_sets * P.bn : P.bn;
