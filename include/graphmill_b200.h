@@ -38,7 +38,8 @@ typedef enum gm_status {
   GM_ERR_CUDA = 3,
   GM_ERR_UNSUPPORTED = 4,
   GM_ERR_LOGIC = 5,            /* reference: std::logic_error */
-  GM_ERR_RUNTIME = 6           /* reference: std::runtime_error (dataset IO) */
+  GM_ERR_RUNTIME = 6,          /* reference: std::runtime_error (dataset IO) */
+  GM_ERR_NCCL = 7
 } gm_status;
 
 typedef enum gm_dtype { GM_F32 = 0, GM_F64 = 1, GM_BF16 = 2 } gm_dtype;
@@ -317,6 +318,23 @@ GM_API gm_status gm_segment_matmul_f32(const float* x, const int64_t* ptr_host, 
                                        int64_t n, const float* w, float* out, void* workspace, size_t workspace_bytes,
                                        gm_stream_t stream);
 
+/* grouped_matmul over SEPARATE per-group tensors — the reference's
+ * grouped_matmul(vector<Tensor> inputs, Tensor W[G,F,F']) (hetero.hpp:134-157):
+ * out_host[g] = x_host[g] @ w[g] for groups of rows_host[g] rows (host arrays
+ * of device pointers). Operands (x_dtype, w_dtype): (F32, F32) fp32-accurate
+ * split route, out F32; (F32, BF16) x rounded to bf16 inside the kernel, out
+ * F32; (BF16, BF16) out BF16 or F32. With <= 8 groups, n % 16 == 0, x f32
+ * k % 4 == 0 / x bf16 k % 64 == 0 and 16-byte aligned pointers, one kernel
+ * reads and writes every group in place through per-group TMA maps (no
+ * concatenation); otherwise the groups are gathered into the workspace and
+ * scattered back (stream-ordered copies). */
+GM_API size_t gm_grouped_matmul_workspace(const int64_t* rows_host, int64_t groups, int64_t k, int64_t n,
+                                          gm_dtype x_dtype, gm_dtype w_dtype, gm_dtype out_dtype);
+GM_API gm_status gm_grouped_matmul(const void* const* x_host, const int64_t* rows_host, int64_t groups, int64_t k,
+                                   int64_t n, const void* w, gm_dtype x_dtype, gm_dtype w_dtype,
+                                   void* const* out_host, gm_dtype out_dtype, void* workspace, size_t workspace_bytes,
+                                   gm_stream_t stream);
+
 /* ------------------------------------------------------------------------ */
 /* Multi-GPU partitioning (north_star: dst-row partition + source all-gather) */
 /* ------------------------------------------------------------------------ */
@@ -365,6 +383,63 @@ GM_API gm_status gm_spmm_accumulate(const gm_csr* csr, const gm_spmm_plan* plan,
                                     const void* x, int64_t f, const void* edge_weight, gm_reduce reduce,
                                     const int32_t* mean_deg, void* out, int32_t* arg_out,
                                     gm_stream_t stream);
+
+/* Multi-GPU SpMM over NCCL (north_star: dst-row partition + source exchange).
+ * ncclComm_t is NCCL's own handle (struct ncclComm*); the library resolves
+ * NCCL at run time (dlopen libnccl.so.2). Hosts without their own NCCL
+ * bootstrap can use gm_nccl_unique_id (128 bytes, to broadcast out of band)
+ * and gm_nccl_comm_init. */
+typedef struct ncclComm* ncclComm_t;
+GM_API gm_status gm_nccl_unique_id(void* id_out);
+GM_API gm_status gm_nccl_comm_init(int32_t world, const void* id, int32_t rank, ncclComm_t* comm);
+GM_API gm_status gm_nccl_comm_destroy(ncclComm_t comm);
+
+typedef enum gm_dist_mode {
+  GM_DIST_EXACT = 0,   /* one all-gather, one gm_spmm: bit-identical to one GPU */
+  GM_DIST_BLOCKED = 1, /* `chunks` all-gathers overlapped with source-blocked aggregation */
+  GM_DIST_HALO = 2     /* ncclSend/Recv of the referenced remote rows only, overlapped */
+} gm_dist_mode;
+
+/* One rank's view of the partitioned SpMM. X is row-sharded: rank q owns
+ * shard rows [q * shard_rows, (q+1) * shard_rows) (last padded).
+ *  EXACT:   blocks[0] = this rank's destination rows with GLOBAL source ids
+ *           (the gathered X is [world * shard_rows, f]);
+ *  BLOCKED: blocks[0..chunks] from gm_csr_split_blocks: block 0 = sources in
+ *           the own shard (column = row inside x_shard, which is padded to
+ *           chunks * chunk_rows rows), block 1+c = sources of exchange chunk c
+ *           (column = q * chunk_rows + row inside the chunk);
+ *  HALO:    blocks[0] = own shard, blocks[1] = halo rows (column = position in
+ *           the receive buffer: peers in rank order, each ascending);
+ *           halo_send_idx = rows of my shard each peer needs (peers in rank
+ *           order), per-peer HOST counts of what I send / receive.
+ * plans: gm_spmm_plan_build of each block. mean_deg: FULL row degrees (MEAN). */
+typedef struct gm_dist_layout {
+  int32_t rank;
+  int32_t world;
+  gm_dist_mode mode;
+  int32_t chunks;
+  int64_t shard_rows;
+  int64_t chunk_rows;
+  const gm_csr* blocks;
+  const gm_spmm_plan* plans;
+  const int32_t* mean_deg;
+  const int32_t* halo_send_idx;
+  const int64_t* halo_send_counts_host;
+  const int64_t* halo_recv_counts_host;
+} gm_dist_layout;
+
+/* The exchange runs on comm_stream (gated on `stream` having reached the
+ * call), aggregation on `stream`, each block waiting (device-side event) for
+ * only the chunk it reads. Numerics: EXACT bit-identical to gm_spmm on the
+ * full graph; BLOCKED/HALO: max/min + argmax bit-identical (NaN-free), sums
+ * continued across blocks (fp32 tolerance; bf16 sum/mean refused — use EXACT).
+ * workspace: gm_dist_spmm_workspace bytes (receive buffers); keep it alive
+ * until `stream` has passed the call. */
+GM_API size_t gm_dist_spmm_workspace(const gm_dist_layout* layout, gm_dtype dtype, int64_t f);
+GM_API gm_status gm_dist_spmm(const gm_dist_layout* layout, gm_dtype dtype, const void* x_shard, int64_t f,
+                              gm_reduce reduce, void* out, int32_t* arg_out, void* workspace,
+                              size_t workspace_bytes, ncclComm_t comm, gm_stream_t comm_stream,
+                              gm_stream_t stream);
 
 /* ------------------------------------------------------------------------ */
 /* Dataset ingestion (L5): dataset_io.hpp:14-20 layout, load_dataset          */

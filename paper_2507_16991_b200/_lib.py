@@ -22,6 +22,7 @@ GM_ERR_CUDA = 3
 GM_ERR_UNSUPPORTED = 4
 GM_ERR_LOGIC = 5
 GM_ERR_RUNTIME = 6
+GM_ERR_NCCL = 7
 
 GM_F32, GM_F64, GM_BF16 = 0, 1, 2
 GM_SUM, GM_MEAN, GM_MAX, GM_MIN = 0, 1, 2, 3
@@ -57,6 +58,26 @@ class gm_spmm_plan(C.Structure):
 class gm_gcn_norm(C.Structure):
     _fields_ = [("deg_src", C.c_void_p), ("deg_dst", C.c_void_p), ("self_loops", C.c_int),
                 ("bias", C.c_void_p), ("relu", C.c_int)]
+
+
+GM_DIST_EXACT, GM_DIST_BLOCKED, GM_DIST_HALO = 0, 1, 2
+
+
+class gm_dist_layout(C.Structure):
+    _fields_ = [
+        ("rank", C.c_int32),
+        ("world", C.c_int32),
+        ("mode", C.c_int),
+        ("chunks", C.c_int32),
+        ("shard_rows", C.c_int64),
+        ("chunk_rows", C.c_int64),
+        ("blocks", C.POINTER(gm_csr)),
+        ("plans", C.POINTER(gm_spmm_plan)),
+        ("mean_deg", C.c_void_p),
+        ("halo_send_idx", C.c_void_p),
+        ("halo_send_counts_host", C.POINTER(C.c_int64)),
+        ("halo_recv_counts_host", C.POINTER(C.c_int64)),
+    ]
 
 
 # name -> (restype, argtypes); mirrors include/graphmill_b200.h one to one.
@@ -106,8 +127,17 @@ SIGNATURES = {
                                                 _P]),
     "gm_segment_matmul_f32_workspace": (C.c_size_t, [_I64, _I64, _I64, _I64]),
     "gm_segment_matmul_f32": (C.c_int, [_P, C.POINTER(C.c_int64), _I64, _I64, _I64, _P, _P, _P, C.c_size_t, _P]),
+    "gm_grouped_matmul_workspace": (C.c_size_t, [C.POINTER(C.c_int64), _I64, _I64, _I64, C.c_int, C.c_int, C.c_int]),
+    "gm_grouped_matmul": (C.c_int, [C.POINTER(C.c_void_p), C.POINTER(C.c_int64), _I64, _I64, _I64, _P, C.c_int,
+                                    C.c_int, C.POINTER(C.c_void_p), C.c_int, _P, C.c_size_t, _P]),
     "gm_partition_rows_by_nnz": (C.c_int, [C.POINTER(C.c_int64), _I64, C.c_int32,
                                            C.POINTER(C.c_int64)]),
+    "gm_nccl_unique_id": (C.c_int, [_P]),
+    "gm_nccl_comm_init": (C.c_int, [C.c_int32, _P, C.c_int32, C.POINTER(C.c_void_p)]),
+    "gm_nccl_comm_destroy": (C.c_int, [_P]),
+    "gm_dist_spmm_workspace": (C.c_size_t, [C.POINTER(gm_dist_layout), C.c_int, _I64]),
+    "gm_dist_spmm": (C.c_int, [C.POINTER(gm_dist_layout), C.c_int, _P, _I64, C.c_int, _P, _P, _P, C.c_size_t, _P, _P,
+                               _P]),
     "gm_read_file_to_device": (C.c_int, [C.c_char_p, _I64, _P, _P, C.c_size_t, _P]),
     "gm_read_edge_pairs_workspace": (C.c_size_t, [C.c_size_t]),
     "gm_read_edge_pairs_to_device": (C.c_int, [C.c_char_p, _I64, _P, _P, _P, C.c_size_t, _P, C.c_size_t, _P]),

@@ -111,79 +111,98 @@ __device__ __forceinline__ unsigned peers_of(uint32_t key, bool valid) {
   return m;
 }
 
-// 3. stable scatter of each tile's entries into their buckets' runs. The
-// codes of a warp's 512 positions are loaded up front (independent loads); the
-// 16 ranking rounds then only touch registers and shared memory. Staged as
+// 3. stable scatter of each tile's entries into their buckets' runs.
+// Persistent CTAs (one per SM: the per-warp histograms fill shared memory)
+// walk tiles blockIdx.x, +gridDim.x, ...; the next tile's codes, values and
+// table offsets are loaded into registers while the current tile is ranked
+// and scattered, so the SM's memory pipe never idles between phases. Staged as
 // (local row u16) and (COO position, value) int2.
-__global__ void __launch_bounds__(kTileThreads) tile_scatter_kernel(
+__global__ void __launch_bounds__(kTileThreads, 1) tile_scatter_kernel(
     const uint32_t* __restrict__ code, const int64_t* __restrict__ values, int64_t e, int32_t nb_max, int64_t tiles,
     const int32_t* __restrict__ table_off, uint16_t* __restrict__ st_row, int2* __restrict__ st_pv) {
   extern __shared__ int32_t tile_off[];  // [nb_max] this tile's first slot per bucket, then whist
   uint16_t* whist = reinterpret_cast<uint16_t*>(tile_off + nb_max);  // [kTileWarps][nb_max]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t t = blockIdx.x;
-  for (int i = threadIdx.x; i < kTileWarps * nb_max; i += kTileThreads) whist[i] = 0;
-  const int64_t wbase = t * kTileItems + static_cast<int64_t>(w) * (32 * kRounds);
-  uint32_t c[kRounds];  // bucket << 16 | local row, then rank << 22 | bucket << 10 | local row
-  int32_t val[kRounds];  // values < 2^31 (int32 col)
-#pragma unroll
-  for (int j = 0; j < kRounds; ++j) {
-    const int64_t i = wbase + j * 32 + lane;
-    c[j] = i < e ? __ldcs(code + i) : 0xffffffffu;
-    val[j] = i < e ? static_cast<int32_t>(__ldcs(values + i)) : 0;
-  }
-  // this tile's first slot of every bucket, fetched while the ranking runs
-  constexpr int kOffPer = kMaxBuckets / kTileThreads;
-  int32_t toff[kOffPer];
-#pragma unroll
-  for (int q = 0; q < kOffPer; ++q) {
-    const int d = threadIdx.x + q * kTileThreads;
-    toff[q] = d < nb_max ? table_off[static_cast<int64_t>(d) * tiles + t] : 0;
-  }
-  __syncthreads();
   uint16_t* my = whist + w * nb_max;
   const unsigned lt = (1u << lane) - 1u;
+  constexpr int kOffPer = kMaxBuckets / kTileThreads;
+  uint32_t c[kRounds], cn[kRounds];  // bucket << 16 | local row (ranked: rank << 22 | bucket << 10 | row)
+  int32_t val[kRounds], valn[kRounds];
+  int32_t toff[kOffPer], toffn[kOffPer];
+  auto load = [&](int64_t t, uint32_t* cc, int32_t* vv, int32_t* oo) {
+    const int64_t wbase = t * kTileItems + static_cast<int64_t>(w) * (32 * kRounds);
 #pragma unroll
-  for (int j = 0; j < kRounds; ++j) {
-    const bool valid = c[j] != 0xffffffffu;
-    const uint32_t d = valid ? (c[j] >> 16) : 0u;
-    const unsigned peers = peers_of<12>(d, valid);
-    uint16_t old = 0;
-    if (valid) old = my[d];
-    __syncwarp();
-    if (valid && (peers & lt) == 0) my[d] = static_cast<uint16_t>(old + __popc(peers));
-    __syncwarp();
-    // rank inside the warp's 512 positions (< 512) in bits 22..31, bucket in
-    // bits 10..21, local row (kBucketRows = 1024) in bits 0..9
-    if (valid) c[j] = (static_cast<uint32_t>(old + __popc(peers & lt)) << 22) | (d << 10) | (c[j] & 0x3ffu);
-  }
-  __syncthreads();
-  // per bucket: exclusive prefix over the warps (tile totals <= 8192 fit u16)
-  // and this tile's first output slot
+    for (int j = 0; j < kRounds; ++j) {
+      const int64_t i = wbase + j * 32 + lane;
+      const bool ok = t < tiles && i < e;
+      cc[j] = ok ? __ldcs(code + i) : 0xffffffffu;
+      vv[j] = ok ? static_cast<int32_t>(__ldcs(values + i)) : 0;
+    }
 #pragma unroll
-  for (int q = 0; q < kOffPer; ++q) {
-    const int d = threadIdx.x + q * kTileThreads;
-    if (d < nb_max) {
-      uint16_t run = 0;
+    for (int q = 0; q < kOffPer; ++q) {
+      const int d = threadIdx.x + q * kTileThreads;
+      oo[q] = (t < tiles && d < nb_max) ? table_off[static_cast<int64_t>(d) * tiles + t] : 0;
+    }
+  };
+  int64_t t = blockIdx.x;
+  load(t, c, val, toff);
+  for (int i = threadIdx.x; i < (kTileWarps * nb_max + 1) / 2; i += kTileThreads) reinterpret_cast<uint32_t*>(whist)[i] = 0u;
+  for (; t < tiles; t += gridDim.x) {
+    __syncthreads();  // counters zeroed, previous tile's scatter done
+    load(t + gridDim.x, cn, valn, toffn);  // next tile, in flight during this one
 #pragma unroll
-      for (int ww = 0; ww < kTileWarps; ++ww) {
-        const uint16_t cnt = whist[ww * nb_max + d];
-        whist[ww * nb_max + d] = run;
-        run = static_cast<uint16_t>(run + cnt);
+    for (int j = 0; j < kRounds; ++j) {
+      const bool valid = c[j] != 0xffffffffu;
+      const uint32_t d = valid ? (c[j] >> 16) : 0u;
+      const unsigned peers = peers_of<12>(d, valid);
+      uint16_t old = 0;
+      if (valid) old = my[d];
+      __syncwarp();
+      if (valid && (peers & lt) == 0) my[d] = static_cast<uint16_t>(old + __popc(peers));
+      __syncwarp();
+      // rank inside the warp's 512 positions (< 512) in bits 22..31, bucket in
+      // bits 10..21, local row (kBucketRows = 1024) in bits 0..9
+      if (valid) c[j] = (static_cast<uint32_t>(old + __popc(peers & lt)) << 22) | (d << 10) | (c[j] & 0x3ffu);
+    }
+    __syncthreads();
+    // per bucket: exclusive prefix over the warps (tile totals <= 8192 fit
+    // u16) and this tile's first output slot
+#pragma unroll
+    for (int q = 0; q < kOffPer; ++q) {
+      const int d = threadIdx.x + q * kTileThreads;
+      if (d < nb_max) {
+        uint16_t run = 0;
+#pragma unroll
+        for (int ww = 0; ww < kTileWarps; ++ww) {
+          const uint16_t cnt = whist[ww * nb_max + d];
+          whist[ww * nb_max + d] = run;
+          run = static_cast<uint16_t>(run + cnt);
+        }
+        tile_off[d] = toff[q];
       }
-      tile_off[d] = toff[q];
     }
-  }
-  __syncthreads();
+    __syncthreads();
+    const int64_t wbase = t * kTileItems + static_cast<int64_t>(w) * (32 * kRounds);
 #pragma unroll
-  for (int j = 0; j < kRounds; ++j) {
-    const int64_t i = wbase + j * 32 + lane;
-    if (i < e) {
-      const int32_t d = static_cast<int32_t>((c[j] >> 10) & 0xfffu);
-      const int64_t out = static_cast<int64_t>(tile_off[d]) + my[d] + (c[j] >> 22);
-      st_row[out] = static_cast<uint16_t>(c[j] & 0x3ffu);
-      st_pv[out] = make_int2(static_cast<int32_t>(i), val[j]);
+    for (int j = 0; j < kRounds; ++j) {
+      const int64_t i = wbase + j * 32 + lane;
+      if (i < e) {
+        const int32_t d = static_cast<int32_t>((c[j] >> 10) & 0xfffu);
+        const int64_t out = static_cast<int64_t>(tile_off[d]) + my[d] + (c[j] >> 22);
+        st_row[out] = static_cast<uint16_t>(c[j] & 0x3ffu);
+        st_pv[out] = make_int2(static_cast<int32_t>(i), val[j]);
+      }
     }
+    __syncthreads();
+    for (int i = threadIdx.x; i < (kTileWarps * nb_max + 1) / 2; i += kTileThreads)
+      reinterpret_cast<uint32_t*>(whist)[i] = 0u;
+#pragma unroll
+    for (int j = 0; j < kRounds; ++j) {
+      c[j] = cn[j];
+      val[j] = valn[j];
+    }
+#pragma unroll
+    for (int q = 0; q < kOffPer; ++q) toff[q] = toffn[q];
   }
 }
 
@@ -420,11 +439,11 @@ inline gm_status bucket_build(const int64_t* keys, const int64_t* values, int64_
   GM_CHECK_LAUNCH("tile_hist_kernel");
   s = scan32_exclusive(w.table, nb * tiles, w.partial, st);
   if (s != GM_OK) return s;
-  const size_t smem = (sizeof(int32_t) + sizeof(uint16_t) * kTileWarps) * static_cast<size_t>(nb);
+  const size_t smem = (sizeof(int32_t) + sizeof(uint16_t) * kTileWarps) * static_cast<size_t>(nb) + 4;
   if (smem > 48 * 1024)
     GM_TRY_CUDA(cudaFuncSetAttribute(tile_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
-  tile_scatter_kernel<<<static_cast<unsigned>(tiles), kTileThreads, smem, st>>>(
+  tile_scatter_kernel<<<static_cast<unsigned>(std::min<int64_t>(tiles, kNumSMs)), kTileThreads, smem, st>>>(
       w.code, values, e, static_cast<int32_t>(nb), tiles, w.table, w.st_row, w.st_pv);
   GM_CHECK_LAUNCH("tile_scatter_kernel");
   // GM_CSR_FIN_SMEM (bytes, tuning only) can reserve more shared memory to

@@ -357,13 +357,22 @@ static BuildWs build_layout(void* base, int64_t e, int64_t n) {
 
 }  // namespace gm
 #include "csr_bucket.cuh"
+#include "csr_radix.cuh"
 namespace gm {
 
-// GM_CSR_BUCKET=0 keeps the scatter + per-row sort build (A/B comparison only).
-static bool use_bucket_build(int64_t e, int64_t rows) {
-  static const bool on = [] { const char* v = getenv("GM_CSR_BUCKET"); return !(v && v[0] == '0'); }();
-  return on && cb::bucket_path_ok(e, rows);
+// GM_CSR_ALGO (A/B comparison only): radix (default) | bucket | sort
+// (scatter + per-row sort).
+static int csr_algo() {
+  static const int a = [] {
+    const char* v = getenv("GM_CSR_ALGO");
+    if (!v) return 0;
+    const std::string s(v);
+    return s == "bucket" ? 1 : s == "sort" ? 2 : 0;
+  }();
+  return a;
 }
+static bool use_bucket_build(int64_t e, int64_t rows) { return csr_algo() == 1 && cb::bucket_path_ok(e, rows); }
+static bool use_radix_build(int64_t e, int64_t rows) { return csr_algo() == 0 && e > 0 && rows > 0; }
 
 // ---------------------------------------------------------------------------
 // Stable split of a CSR's entries into source blocks (multi-GPU overlap):
@@ -754,8 +763,10 @@ GM_API gm_status gm_gcn_degrees(const int64_t* full_src, const int64_t* full_dst
 GM_API size_t gm_build_compressed_workspace(int64_t num_edges, int64_t num_rows) {
   if (num_edges < 0 || num_rows < 0) return 0;
   size_t b = build_layout(nullptr, num_edges, num_rows).bytes;
-  if (cb::bucket_path_ok(num_edges, num_rows)) b += cb::bucket_layout(nullptr, num_edges, num_rows).bytes;
-  return b;
+  size_t extra = 0;
+  if (cb::bucket_path_ok(num_edges, num_rows)) extra = cb::bucket_layout(nullptr, num_edges, num_rows).bytes;
+  if (num_edges > 0) extra = std::max(extra, rx::radix_layout(nullptr, num_edges).bytes);
+  return b + extra;
 }
 
 GM_API gm_status gm_build_compressed(const int64_t* keys, const int64_t* values,
@@ -775,6 +786,11 @@ GM_API gm_status gm_build_compressed(const int64_t* keys, const int64_t* values,
   if (num_rows == 0) {  // rowptr = {0}
     GM_TRY_CUDA(cudaMemsetAsync(rowptr, 0, sizeof(int64_t), st));
     return GM_OK;
+  }
+  if (use_radix_build(num_edges, num_rows)) {  // needs no count pass: rowptr comes from the sorted keys
+    const rx::RadixWs rw = rx::radix_layout(static_cast<unsigned char*>(workspace) +
+                                                build_layout(nullptr, num_edges, num_rows).bytes, num_edges);
+    return rx::radix_build(keys, values, num_edges, num_rows, rowptr, col, perm, rw, st);
   }
   const BuildWs w = build_layout(workspace, num_edges, num_rows);
   GM_TRY_CUDA(cudaMemsetAsync(w.cnt, 0, sizeof(int32_t) * static_cast<size_t>(num_rows), st));

@@ -44,6 +44,15 @@ constexpr uint32_t kCStageBytes = kEpiWarps * kCBoxBytes;  // one 4 KB staging b
 #endif
 constexpr int kCvtWarps = GM_CVT_WARPS;     // fp32 split path: warps converting x tiles into bf16 pieces in smem
 
+// Pointer-array mode (grouped_matmul over separate tensors, hetero.hpp:134-157):
+// one TMA map per group for x and for out, rows addressed group-locally.
+constexpr int kMaxPtrGroups = 8;
+struct GroupMaps {
+  CUtensorMap a[kMaxPtrGroups];
+  CUtensorMap c[kMaxPtrGroups];
+  void* out[kMaxPtrGroups];
+};
+
 struct Params {
   int64_t ptr[kMaxGroups + 1];        // group row offsets
   int32_t tile_start[kMaxGroups + 1]; // first m-tile id of each group (n-tiles folded in)
@@ -75,6 +84,7 @@ struct Params {
   // the tensor pipe's per-step accumulation error grows that much slower.
   int32_t acc_sets;
   int32_t acc_cols;                   // TMEM columns per double-buffer slot
+  int32_t ptr_groups;                 // 1: x / out per group (GroupMaps), rows group-local
   void* out;
 };
 
@@ -236,7 +246,8 @@ __device__ __forceinline__ void split3x2(float a, float b, uint32_t& hw, uint32_
 template <int KBLK, int CVT>
 __global__ void __launch_bounds__(CVT > 0 ? kThreads + 32 * kCvtWarps : kThreads, 1)
 segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ CUtensorMap map_a,
-                      const __grid_constant__ CUtensorMap map_b, const __grid_constant__ CUtensorMap map_c) {
+                      const __grid_constant__ CUtensorMap map_b, const __grid_constant__ CUtensorMap map_c,
+                      const __grid_constant__ GroupMaps G) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-B alignment for the SWIZZLE_128B atoms
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -311,7 +322,9 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
       for (int t = blockIdx.x; t < P.num_tiles; t += gridDim.x) {
         int g, mt, nt;
         decode_tile(P, t, g, mt, nt);
-        const int row0 = static_cast<int>(P.ptr[g]) + mt * BM;
+        // A rows: global (one matrix) or group-local (pointer-array mode)
+        const int row0 = P.ptr_groups ? mt * BM : static_cast<int>(P.ptr[g]) + mt * BM;
+        const CUtensorMap* ma = P.ptr_groups ? &G.a[g] : &map_a;
         const int brow0 = g * P.n + nt * P.bn;
         if (P.b_resident && g != cur_g) {
           if (nbload > 0) mbar_wait(bempty, (nbload - 1) & 1);
@@ -328,7 +341,7 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
             // fp32 x tile -> staging ring (rows / columns past the end read as zero)
             mbar_wait(&xempty[sx], xph ^ 1);
             mbar_expect_tx(&xfull[sx], kXStage);
-            tma_load_2d(x_ring + static_cast<size_t>(sx) * kXStage, &map_a, &xfull[sx], kb * KBLK, row0);
+            tma_load_2d(x_ring + static_cast<size_t>(sx) * kXStage, ma, &xfull[sx], kb * KBLK, row0);
             if (++sx == SX) {
               sx = 0;
               xph ^= 1;
@@ -360,7 +373,7 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
             const int seg = ac / P.a_seg_k;
             ac += (static_cast<int>((P.a_seg_map >> (2 * seg)) & 3u) - seg) * P.a_seg_k;
           }
-          tma_load_2d(a_ring + static_cast<size_t>(s) * kAStage, &map_a, &full[s], ac, row0);
+          tma_load_2d(a_ring + static_cast<size_t>(s) * kAStage, ma, &full[s], ac, row0);
           if (++s == S) {
             s = 0;
             ph ^= 1;
@@ -492,6 +505,11 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
       const int64_t row0 = P.ptr[g] + static_cast<int64_t>(mt) * BM;
       const int64_t row = row0 + q * 32 + lane;
       const bool full_tile = P.tma_store && row0 + BM <= grow_end;  // else: masked direct stores
+      // output rows: global, or group-local in pointer-array mode
+      const CUtensorMap* mc = P.ptr_groups ? &G.c[g] : &map_c;
+      const int64_t orow0 = P.ptr_groups ? static_cast<int64_t>(mt) * BM : row0;
+      void* const obase = P.ptr_groups ? G.out[g] : P.out;
+      const int64_t orow = orow0 + q * 32 + lane;
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * P.acc_cols);
@@ -547,7 +565,7 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
             fence_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_2d(&map_c, my_stage, nt * P.bn + c, static_cast<int32_t>(row0 + q * 32));
+              tma_store_2d(mc, my_stage, nt * P.bn + c, static_cast<int32_t>(orow0 + q * 32));
               bulk_commit();
             }
             ++nstore;
@@ -579,7 +597,7 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
           fence_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&map_c, my_stage + b * kCBoxBytes, nt * P.bn + c, static_cast<int32_t>(row0 + q * 32));
+            tma_store_2d(mc, my_stage + b * kCBoxBytes, nt * P.bn + c, static_cast<int32_t>(orow0 + q * 32));
             bulk_commit();
           }
           ++nstore;
@@ -592,11 +610,11 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
           if (live) {
             const int64_t col0 = static_cast<int64_t>(nt) * P.bn + c;
             if (out_f32) {
-              float* o = static_cast<float*>(P.out) + row * P.n + col0;
+              float* o = static_cast<float*>(obase) + orow * P.n + col0;
 #pragma unroll
               for (int i = 0; i < 16; i += 4) st_na_v4(o + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
             } else {
-              __nv_bfloat16* o = static_cast<__nv_bfloat16*>(P.out) + row * P.n + col0;
+              __nv_bfloat16* o = static_cast<__nv_bfloat16*>(obase) + orow * P.n + col0;
 #pragma unroll
               for (int i = 0; i < 16; i += 8)
                 st_na_v4(o + i, pack_bf16(v[i], v[i + 1]), pack_bf16(v[i + 2], v[i + 3]),
@@ -870,7 +888,8 @@ static gm_status segment_matmul_impl(const void* x, const int64_t* ptr_host, int
                                      int64_t n_in, const void* w, const void* w_packed, gm_dtype out_dtype, void* out,
                                      void* workspace, size_t workspace_bytes, gm_stream_t stream,
                                      int64_t a_seg_k = 0, uint32_t a_seg_map = 0, int64_t a_cols = 0,
-                                     const float* a_f32 = nullptr, int64_t a_ld = 0, int a_pieces = 3) {
+                                     const float* a_f32 = nullptr, int64_t a_ld = 0, int a_pieces = 3,
+                                     const void* const* gx = nullptr, void* const* gout = nullptr) {
   using namespace gm::gmm;
   GM_REQUIRE(ptr_host && groups >= 1 && groups <= kMaxGroups, GM_ERR_INVALID_ARGUMENT,
              "segment_matmul: groups must be in [1, " + std::to_string(kMaxGroups) + "]");
@@ -913,6 +932,9 @@ static gm_status segment_matmul_impl(const void* x, const int64_t* ptr_host, int
   }
   GM_REQUIRE((reinterpret_cast<uintptr_t>(xk) | reinterpret_cast<uintptr_t>(outk)) % 16 == 0,
              GM_ERR_INVALID_ARGUMENT, "segment_matmul: x and out must be 16-byte aligned");
+  const bool ptr_mode = gx != nullptr;
+  GM_REQUIRE(!ptr_mode || (gout && groups <= kMaxPtrGroups && k == k_in && n == n_in && a_seg_k == 0),
+             GM_ERR_INVALID_ARGUMENT, "segment_matmul: pointer-array groups need <= 8 groups and unpadded shapes");
 
   Params P{};
   P.groups = static_cast<int32_t>(groups);
@@ -930,6 +952,7 @@ static gm_status segment_matmul_impl(const void* x, const int64_t* ptr_host, int
   P.n = static_cast<int32_t>(n);
   P.out_f32 = out_dtype == GM_F32;
   P.out = outk;
+  P.ptr_groups = ptr_mode ? 1 : 0;
   P.tma_store = (P.bn % (128 / static_cast<int>(out_dtype == GM_F32 ? 4 : 2))) == 0 ? 1 : 0;
   P.a_seg_k = static_cast<int32_t>(a_f32 ? k : a_seg_k);
   P.a_seg_map = a_seg_map;
@@ -1020,13 +1043,38 @@ static gm_status segment_matmul_impl(const void* x, const int64_t* ptr_host, int
                static_cast<uint64_t>(esz));
   if (s != GM_OK) return s;
 
+  GroupMaps G{};
+  if (ptr_mode) {
+    for (int64_t g = 0; g < groups; ++g) {
+      const int64_t rg = ptr_host[g + 1] - ptr_host[g];
+      G.a[g] = map_a;  // empty groups own no tiles; any valid map
+      G.c[g] = map_c;
+      G.out[g] = gout[g];
+      if (rg == 0) continue;
+      GM_REQUIRE((reinterpret_cast<uintptr_t>(gx[g]) | reinterpret_cast<uintptr_t>(gout[g])) % 16 == 0,
+                 GM_ERR_INVALID_ARGUMENT, "grouped_matmul: every x / out must be 16-byte aligned");
+      if (a_f32)
+        s = make_map(&G.a[g], gx[g], static_cast<uint64_t>(a_ld), static_cast<uint64_t>(rg), kblk, BM,
+                     CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, CU_TENSOR_MAP_SWIZZLE_NONE);
+      else
+        s = make_map(&G.a[g], gx[g], static_cast<uint64_t>(k), static_cast<uint64_t>(rg), kblk, BM,
+                     CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, swz);
+      if (s != GM_OK) return s;
+      s = make_map(&G.c[g], gout[g], static_cast<uint64_t>(n), static_cast<uint64_t>(rg),
+                   128 / static_cast<uint32_t>(esz), 32,
+                   out_dtype == GM_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                   static_cast<uint64_t>(esz));
+      if (s != GM_OK) return s;
+    }
+  }
+
   // per call: the attribute is per device, and a process may drive several
   auto kern = a_f32 ? (a_pieces == 3 ? (kblk == 64 ? segment_matmul_kernel<64, 3> : segment_matmul_kernel<32, 3>)
                                       : (kblk == 64 ? segment_matmul_kernel<64, 1> : segment_matmul_kernel<32, 1>))
                     : (kblk == 64 ? segment_matmul_kernel<64, 0> : segment_matmul_kernel<32, 0>);
   GM_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   const unsigned grid = static_cast<unsigned>(std::min<int32_t>(tiles, kNumSMs));
-  kern<<<grid, a_f32 ? kThreads + 32 * kCvtWarps : kThreads, smem, st>>>(P, map_a, map_b, map_c);
+  kern<<<grid, a_f32 ? kThreads + 32 * kCvtWarps : kThreads, smem, st>>>(P, map_a, map_b, map_c, G);
   GM_CHECK_LAUNCH("segment_matmul_kernel");
   if (n != n_in) {
     unpad_cols_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(rows * n_in, 256), 8192)), 256, 0, st>>>(
@@ -1094,9 +1142,10 @@ GM_API size_t gm_segment_matmul_f32_workspace(int64_t rows, int64_t groups, int6
          gm_segment_matmul_workspace(rows, groups, kSplit * kp, n);
 }
 
-GM_API gm_status gm_segment_matmul_f32(const float* x, const int64_t* ptr_host, int64_t groups, int64_t k,
-                                       int64_t n, const float* w, float* out, void* workspace, size_t workspace_bytes,
-                                       gm_stream_t stream) {
+static gm_status segment_matmul_f32_impl(const float* x, const int64_t* ptr_host, int64_t groups, int64_t k,
+                                         int64_t n, const float* w, float* out, void* workspace,
+                                         size_t workspace_bytes, gm_stream_t stream, const void* const* gx,
+                                         void* const* gout) {
   GM_REQUIRE(ptr_host && groups >= 1, GM_ERR_INVALID_ARGUMENT, "segment_matmul: bad groups");
   GM_REQUIRE(k > 0 && n > 0, GM_ERR_INVALID_ARGUMENT, "segment_matmul: K and N must be positive");
   const int64_t rows = ptr_host[groups];
@@ -1111,7 +1160,7 @@ GM_API gm_status gm_segment_matmul_f32(const float* x, const int64_t* ptr_host, 
   // fused split (x read once by TMA, pieces formed in shared memory) when x
   // rows meet TMA's 16-byte stride rule; GM_GEMM_FUSED_SPLIT=0 selects the staged path below
   static const bool fused_env = [] { const char* e = getenv("GM_GEMM_FUSED_SPLIT"); return !(e && e[0] == '0'); }();
-  if (fused_env && k % 4 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0) {
+  if (fused_env && k % 4 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0 && (!gx || n % 16 == 0)) {
     const int64_t np = pad_to(n, 16);
     auto* wt = static_cast<__nv_bfloat16*>(workspace);
     const size_t wt_bytes = align_up(static_cast<size_t>(groups * np * 3 * kp) * 2, 256);
@@ -1121,8 +1170,9 @@ GM_API gm_status gm_segment_matmul_f32(const float* x, const int64_t* ptr_host, 
     GM_CHECK_LAUNCH("split_wt_kernel");
     return segment_matmul_impl(x, ptr_host, groups, kp, n, nullptr, wt, GM_F32, out,
                                static_cast<unsigned char*>(workspace) + wt_bytes, workspace_bytes - wt_bytes, stream,
-                               0, 0, 0, x, k);
+                               0, 0, 0, x, k, 3, gx, gout);
   }
+  GM_REQUIRE(!gx, GM_ERR_INVALID_ARGUMENT, "grouped_matmul: pointer-array route needs k % 4 == 0, n % 16 == 0");
   unsigned char* b = static_cast<unsigned char*>(workspace);
   auto* xs = reinterpret_cast<__nv_bfloat16*>(b);
   b += align_up(static_cast<size_t>(rows * 3 * kp) * 2, 256);
@@ -1137,6 +1187,115 @@ GM_API gm_status gm_segment_matmul_f32(const float* x, const int64_t* ptr_host, 
   return segment_matmul_impl(xs, ptr_host, groups, kSplit * kp, n, ws, nullptr, GM_F32, out, b,
                              workspace_bytes - static_cast<size_t>(b - static_cast<unsigned char*>(workspace)), stream,
                              kp, kSplitSegMap, 3 * kp);
+}
+
+GM_API gm_status gm_segment_matmul_f32(const float* x, const int64_t* ptr_host, int64_t groups, int64_t k,
+                                       int64_t n, const float* w, float* out, void* workspace, size_t workspace_bytes,
+                                       gm_stream_t stream) {
+  return segment_matmul_f32_impl(x, ptr_host, groups, k, n, w, out, workspace, workspace_bytes, stream, nullptr,
+                                 nullptr);
+}
+
+// grouped_matmul over separate per-group tensors (hetero.hpp:134-157): one
+// TMA map per group for x and out, so nothing is concatenated when the shapes
+// run unpadded (<= 8 groups, n % 16 == 0, 16-byte aligned; x f32: k % 4 == 0,
+// x bf16: k % 64 == 0); otherwise the groups are gathered into the workspace
+// (stream-ordered copies) and the results copied back.
+// Operand routes: (f32 x, f32 w) fp32-accurate split; (f32 x, bf16 w) x
+// rounded to bf16 inside the kernel; (bf16, bf16).
+static bool grouped_direct(int64_t groups, int64_t k, int64_t n, gm_dtype x_dtype) {
+  if (groups > gm::gmm::kMaxPtrGroups || n % 16 != 0) return false;
+  return x_dtype == GM_F32 ? k % 4 == 0 : k % 64 == 0;
+}
+
+static size_t grouped_inner_ws(int64_t rows, int64_t groups, int64_t k, int64_t n, gm_dtype x_dtype,
+                               gm_dtype w_dtype) {
+  if (x_dtype == GM_F32 && w_dtype == GM_F32) return gm_segment_matmul_f32_workspace(rows, groups, k, n);
+  if (x_dtype == GM_F32)  // packed bf16 W + the packed route's workspace
+    return align_up(gm_segment_matmul_packed_w_bytes(groups, k, n), 256) +
+           gm_segment_matmul_packed_workspace(rows, groups, k, n);
+  return gm_segment_matmul_workspace(rows, groups, k, n);
+}
+
+GM_API size_t gm_grouped_matmul_workspace(const int64_t* rows_host, int64_t groups, int64_t k, int64_t n,
+                                          gm_dtype x_dtype, gm_dtype w_dtype, gm_dtype out_dtype) {
+  if (!rows_host || groups < 1 || k < 1 || n < 1) return 0;
+  int64_t rows = 0;
+  for (int64_t g = 0; g < groups; ++g) rows += rows_host[g];
+  const size_t inner = grouped_inner_ws(rows, groups, k, n, x_dtype, w_dtype);
+  if (grouped_direct(groups, k, n, x_dtype)) return inner;
+  const size_t xe = x_dtype == GM_F32 ? 4 : 2, oe = out_dtype == GM_F32 ? 4 : 2;
+  return inner + align_up(static_cast<size_t>(rows * k) * xe, 256) + align_up(static_cast<size_t>(rows * n) * oe, 256);
+}
+
+// one launch over the groups described by (x, out) — contiguous, or per-group
+// pointers when gx / gout are given
+static gm_status grouped_run(const void* x, const int64_t* ptr, int64_t groups, int64_t k, int64_t n, const void* w,
+                             gm_dtype x_dtype, gm_dtype w_dtype, void* out, gm_dtype out_dtype, void* ws,
+                             size_t ws_bytes, gm_stream_t stream, const void* const* gx, void* const* gout) {
+  if (x_dtype == GM_F32 && w_dtype == GM_F32)
+    return segment_matmul_f32_impl(static_cast<const float*>(x), ptr, groups, k, n, static_cast<const float*>(w),
+                                   static_cast<float*>(out), ws, ws_bytes, stream, gx, gout);
+  if (x_dtype == GM_F32) {
+    unsigned char* packed = static_cast<unsigned char*>(ws);
+    const size_t pb = align_up(gm_segment_matmul_packed_w_bytes(groups, k, n), 256);
+    gm_status s = gm_segment_matmul_pack_w(w, groups, k, n, packed, stream);
+    if (s != GM_OK) return s;
+    GM_REQUIRE(k % 4 == 0 && out_dtype == GM_F32, GM_ERR_INVALID_ARGUMENT,
+               "grouped_matmul: f32 x with bf16 weights needs k % 4 == 0 and f32 out");
+    const int64_t kp = pad_to(k, 64);
+    return segment_matmul_impl(x, ptr, groups, kp, n, nullptr, packed, GM_F32, out, packed + pb, ws_bytes - pb,
+                               stream, 0, 0, 0, static_cast<const float*>(x), k, 1, gx, gout);
+  }
+  return segment_matmul_impl(x, ptr, groups, k, n, w, nullptr, out_dtype, out, ws, ws_bytes, stream, 0, 0, 0,
+                             nullptr, 0, 3, gx, gout);
+}
+
+GM_API gm_status gm_grouped_matmul(const void* const* x_host, const int64_t* rows_host, int64_t groups, int64_t k,
+                                   int64_t n, const void* w, gm_dtype x_dtype, gm_dtype w_dtype, void* const* out_host,
+                                   gm_dtype out_dtype, void* workspace, size_t workspace_bytes, gm_stream_t stream) {
+  GM_REQUIRE(x_host && rows_host && out_host && groups >= 1, GM_ERR_INVALID_ARGUMENT,
+             "grouped_matmul: null group arrays");
+  GM_REQUIRE((x_dtype == GM_F32 || x_dtype == GM_BF16) && (w_dtype == GM_F32 || w_dtype == GM_BF16) &&
+                 !(x_dtype == GM_BF16 && w_dtype == GM_F32),
+             GM_ERR_INVALID_ARGUMENT, "grouped_matmul: operands (f32, f32), (f32, bf16) or (bf16, bf16)");
+  GM_REQUIRE(x_dtype == GM_BF16 || out_dtype == GM_F32, GM_ERR_INVALID_ARGUMENT,
+             "grouped_matmul: f32 activations produce f32");
+  GM_REQUIRE(workspace_bytes >= gm_grouped_matmul_workspace(rows_host, groups, k, n, x_dtype, w_dtype, out_dtype),
+             GM_ERR_INVALID_ARGUMENT, "grouped_matmul: workspace too small");
+  std::vector<int64_t> ptr(static_cast<size_t>(groups) + 1, 0);
+  for (int64_t g = 0; g < groups; ++g) {
+    GM_REQUIRE(rows_host[g] >= 0, GM_ERR_INVALID_ARGUMENT, "grouped_matmul: negative group rows");
+    ptr[static_cast<size_t>(g) + 1] = ptr[static_cast<size_t>(g)] + rows_host[g];
+  }
+  const int64_t rows = ptr.back();
+  if (rows == 0) return GM_OK;
+  int64_t first = 0;
+  while (rows_host[first] == 0) ++first;
+  if (grouped_direct(groups, k, n, x_dtype))
+    return grouped_run(x_host[first], ptr.data(), groups, k, n, w, x_dtype, w_dtype, out_host[first], out_dtype,
+                       workspace, workspace_bytes, stream, x_host, out_host);
+  // gathered route
+  cudaStream_t st = as_stream(stream);
+  const size_t xe = x_dtype == GM_F32 ? 4 : 2, oe = out_dtype == GM_F32 ? 4 : 2;
+  unsigned char* xb = static_cast<unsigned char*>(workspace);
+  unsigned char* ob = xb + align_up(static_cast<size_t>(rows * k) * xe, 256);
+  unsigned char* inner = ob + align_up(static_cast<size_t>(rows * n) * oe, 256);
+  const size_t inner_bytes = workspace_bytes - static_cast<size_t>(inner - xb);
+  for (int64_t g = 0; g < groups; ++g)
+    if (rows_host[g] > 0)
+      GM_TRY_CUDA(cudaMemcpyAsync(xb + ptr[static_cast<size_t>(g)] * k * xe, x_host[g],
+                                  static_cast<size_t>(rows_host[g] * k) * xe, cudaMemcpyDeviceToDevice, st));
+  gm_status s = x_dtype == GM_F32 && w_dtype == GM_BF16 && k % 4 != 0
+                    ? fail(GM_ERR_INVALID_ARGUMENT, "grouped_matmul: f32 x with bf16 weights needs k % 4 == 0")
+                    : grouped_run(xb, ptr.data(), groups, k, n, w, x_dtype, w_dtype, ob, out_dtype, inner,
+                                  inner_bytes, stream, nullptr, nullptr);
+  if (s != GM_OK) return s;
+  for (int64_t g = 0; g < groups; ++g)
+    if (rows_host[g] > 0)
+      GM_TRY_CUDA(cudaMemcpyAsync(out_host[g], ob + ptr[static_cast<size_t>(g)] * n * oe,
+                                  static_cast<size_t>(rows_host[g] * n) * oe, cudaMemcpyDeviceToDevice, st));
+  return GM_OK;
 }
 
 }  // extern "C"

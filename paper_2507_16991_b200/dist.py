@@ -325,3 +325,137 @@ class HaloSpmm:
                                        _p(self.mean_deg) if kind == L.GM_MEAN else None, _p(out),
                                        _p(arg) if maxmin else None, _stream()), "gm_spmm_accumulate (halo)")
         return (out, arg) if maxmin else out
+
+
+# ---------------------------------------------------------------------------
+# The same three modes through the library's own C-ABI over NCCL
+# (gm_dist_spmm): the exchange is issued by the library on a comm stream and
+# each source block waits on a device event for just its chunk — no host
+# synchronisation per step. The communicator is NCCL's own (bootstrapped here
+# over torch.distributed); a C++ host passes its ncclComm_t directly.
+# ---------------------------------------------------------------------------
+class NcclComm:
+    """An NCCL communicator created through gm_nccl_comm_init; the 128-byte
+    unique id travels over the torch.distributed group (any backend)."""
+
+    def __init__(self, rank: int, world: int, group=None):
+        lib = L.lib()
+        uid = (C.c_ubyte * 128)()
+        if rank == 0:
+            L.check(lib.gm_nccl_unique_id(C.cast(uid, C.c_void_p)), "gm_nccl_unique_id")
+        if world > 1:
+            box = [bytes(uid)]
+            dist.broadcast_object_list(box, src=0, group=group)
+            C.memmove(uid, box[0], 128)
+        self.comm = C.c_void_p()
+        L.check(lib.gm_nccl_comm_init(world, C.cast(uid, C.c_void_p), rank, C.byref(self.comm)), "gm_nccl_comm_init")
+        self.rank, self.world = rank, world
+
+    def close(self):
+        if self.comm:
+            L.check(L.lib().gm_nccl_comm_destroy(self.comm), "gm_nccl_comm_destroy")
+            self.comm = C.c_void_p()
+
+
+class DistSpmm:
+    """One rank's partitioned SpMM through gm_dist_spmm.
+
+    mode "exact": view = the rank's row slice with global source ids;
+    "blocked": view split into 1 + chunks source blocks (as BlockedSpmm);
+    "halo": need = halo_need(...), send = exchange_need_lists(need)."""
+
+    def __init__(self, rows, num_src_rows: int, comm: NcclComm, mode: str = "blocked", chunks: int = 4,
+                 need=None, send=None):
+        from .graphmill import CsrView, _p, _stream
+        self.comm, self.mode = comm, mode
+        rank, world = comm.rank, comm.world
+        self.rank, self.world = rank, world
+        lib = L.lib()
+        dev = rows.rowptr.device
+        n, nnz = rows.num_rows(), rows.num_entries()
+        self.s_rows = -(-num_src_rows // world)
+        self._keep = []
+        if mode == "exact":
+            views = [rows]
+            self.chunks, self.cs = 0, 0
+        else:
+            if mode == "blocked":
+                self.chunks = chunks
+                self.s_rows, self.cs = chunk_layout(num_src_rows, world, chunks)
+                blk, colmap = source_blocks(num_src_rows, rank, world, chunks, dev)
+                nb = chunks + 1
+            elif mode == "halo":
+                self.chunks, self.cs = 0, 0
+                blk, colmap = halo_blocks(need, num_src_rows, rank, world, dev)
+                nb = 2
+            else:
+                raise ValueError(f"DistSpmm: unknown mode {mode}")
+            rowptr_b = torch.empty(nb * (n + 1), dtype=torch.int64, device=dev)
+            col_b = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+            perm_b = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+            wsb = lib.gm_csr_split_blocks_workspace(n, nb)
+            ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+            cs = rows.c_struct()
+            L.check(lib.gm_csr_split_blocks(C.byref(cs), _p(blk), _p(colmap), nb, _p(rowptr_b), _p(col_b),
+                                            _p(perm_b), _p(ws), wsb, _stream()), "gm_csr_split_blocks")
+            rp = rowptr_b.view(nb, n + 1)
+            ends, starts = rp[:, n].cpu().tolist(), rp[:, 0].cpu().tolist()
+            views = []
+            for b in range(nb):
+                if mode == "blocked":
+                    ncols = chunks * self.cs if b == 0 else world * self.cs
+                else:
+                    ncols = self.s_rows if b == 0 else max(1, sum(int(t.numel()) for t in need))
+                views.append(CsrView(rp[b], col_b, perm_b, ncols, int(ends[b] - starts[b])))
+            self._keep += [rowptr_b, col_b, perm_b]
+        self.views = views
+        self.mean_deg = (rows.rowptr[1:] - rows.rowptr[:-1]).to(torch.int32)
+        self._ws = {}
+        self.comm_stream = torch.cuda.Stream(device=dev)
+        lay = L.gm_dist_layout()
+        lay.rank, lay.world = rank, world
+        lay.mode = {"exact": L.GM_DIST_EXACT, "blocked": L.GM_DIST_BLOCKED, "halo": L.GM_DIST_HALO}[mode]
+        lay.chunks = self.chunks
+        lay.shard_rows = self.s_rows
+        lay.chunk_rows = self.cs
+        self._blocks = (L.gm_csr * len(views))(*[v.c_struct() for v in views])
+        lay.blocks = self._blocks
+        lay.mean_deg = self.mean_deg.data_ptr()
+        if mode == "halo":
+            self.send_idx = torch.cat(send).to(torch.int32) if send else torch.empty(0, dtype=torch.int32, device=dev)
+            self._send_counts = (C.c_int64 * world)(*[int(t.numel()) for t in send])
+            self._recv_counts = (C.c_int64 * world)(*[int(t.numel()) for t in need])
+            lay.halo_send_idx = self.send_idx.data_ptr() if self.send_idx.numel() else None
+            lay.halo_send_counts_host = self._send_counts
+            lay.halo_recv_counts_host = self._recv_counts
+        self.layout = lay
+        self._plans = {}
+
+    def _plans_for(self, row_bytes):
+        key = 4096 if row_bytes >= 1024 else 0
+        if key not in self._plans:
+            self._plans[key] = (L.gm_spmm_plan * len(self.views))(*[v.plan(row_bytes) for v in self.views])
+        return self._plans[key]
+
+    def __call__(self, x_shard: torch.Tensor, reduce: str = "sum", out: Optional[torch.Tensor] = None,
+                 arg: Optional[torch.Tensor] = None):
+        from .graphmill import _DT, _KIND, _p, _stream
+        x_shard = x_shard.contiguous()
+        f = x_shard.shape[1]
+        n = self.views[0].num_rows()
+        maxmin = reduce in ("max", "min")
+        if out is None:
+            out = torch.empty(n, f, dtype=x_shard.dtype, device=x_shard.device)
+        if maxmin and arg is None:
+            arg = torch.empty(n, f, dtype=torch.int32, device=x_shard.device)
+        self.layout.plans = self._plans_for(f * x_shard.element_size())
+        key = (f, x_shard.dtype)
+        lib = L.lib()
+        if key not in self._ws:
+            nb = lib.gm_dist_spmm_workspace(C.byref(self.layout), _DT[x_shard.dtype], f)
+            self._ws[key] = torch.empty(max(nb, 1), dtype=torch.uint8, device=x_shard.device)
+        ws = self._ws[key]
+        L.check(lib.gm_dist_spmm(C.byref(self.layout), _DT[x_shard.dtype], _p(x_shard), f, _KIND[reduce], _p(out),
+                                 _p(arg) if maxmin else None, _p(ws), ws.numel(), self.comm.comm,
+                                 C.c_void_p(self.comm_stream.cuda_stream), _stream()), "gm_dist_spmm")
+        return (out, arg) if maxmin else out

@@ -666,18 +666,47 @@ def _packed_weights(w: torch.Tensor, groups: int, k: int, n: int) -> torch.Tenso
 
 
 def grouped_matmul(inputs: Sequence[torch.Tensor], weights: torch.Tensor,
-                   out_dtype: Optional[torch.dtype] = None):
-    """List form of hetero.hpp:134-157 (validates like the reference)."""
+                   out_dtype: Optional[torch.dtype] = None, out: Optional[Sequence[torch.Tensor]] = None):
+    """List form of hetero.hpp:134-157 (validates like the reference): one
+    gm_grouped_matmul launch reads every group's tensor in place and writes
+    every group's output in place (per-group TMA maps; no concatenation).
+    fp32 inputs and weights take the fp32-accurate route; otherwise bf16.
+    out (optional): per-group destination tensors."""
     if weights.dim() != 3:
         raise ValueError("grouped_matmul: weights must be [groups, F, F']")
-    groups, k, _ = weights.shape
+    groups, k, n = weights.shape
     if len(inputs) != groups:
         raise ValueError(f"grouped_matmul: group count mismatch ({len(inputs)} inputs, {groups} weight slabs)")
     for g, h in enumerate(inputs):
         if h.dim() != 2 or h.shape[1] != k:
             raise ValueError(f"grouped_matmul: group {g} inner dimension mismatch")
-    ptr = [0]
-    for h in inputs:
-        ptr.append(ptr[-1] + h.shape[0])
-    out = segment_matmul(torch.cat(list(inputs), 0), ptr, weights, out_dtype)
-    return [out[ptr[g]:ptr[g + 1]] for g in range(groups)]
+    dev = weights.device
+    x32 = all(h.dtype == torch.float32 for h in inputs)
+    if x32 and weights.dtype == torch.float32 and out_dtype in (None, torch.float32):
+        # the reference's grouped_matmul<float>: fp32-accurate split route
+        xs, w = [h.contiguous() for h in inputs], weights.contiguous()
+        odt, xdt, wdt = torch.float32, L.GM_F32, L.GM_F32
+    elif x32 and out_dtype in (None, torch.float32) and k % 4 == 0:
+        # fp32 activations x bf16 weights: rounded to bf16 inside the kernel
+        xs, w = [h.contiguous() for h in inputs], weights.to(torch.bfloat16).contiguous()
+        odt, xdt, wdt = torch.float32, L.GM_F32, L.GM_BF16
+    else:
+        xs = [h.to(torch.bfloat16).contiguous() for h in inputs]
+        w = weights.to(torch.bfloat16).contiguous()
+        odt, xdt, wdt = out_dtype or torch.bfloat16, L.GM_BF16, L.GM_BF16
+    if out is None:
+        outs = [torch.empty((h.shape[0], n), dtype=odt, device=dev) for h in xs]
+    else:
+        outs = list(out)
+        for g, o in enumerate(outs):
+            if tuple(o.shape) != (xs[g].shape[0], n) or o.dtype != odt or not o.is_contiguous():
+                raise ValueError(f"grouped_matmul: out[{g}] must be a contiguous [{xs[g].shape[0]}, {n}] {odt}")
+    rows = (C.c_int64 * groups)(*[int(h.shape[0]) for h in xs])
+    xp = (C.c_void_p * groups)(*[h.data_ptr() for h in xs])
+    op = (C.c_void_p * groups)(*[o.data_ptr() for o in outs])
+    lib = L.lib()
+    nb = lib.gm_grouped_matmul_workspace(rows, groups, k, n, xdt, wdt, _DT[odt])
+    ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=dev)
+    L.check(lib.gm_grouped_matmul(xp, rows, groups, k, n, _p(w), xdt, wdt, op, _DT[odt], _p(ws), nb, _stream()),
+            "gm_grouped_matmul")
+    return outs

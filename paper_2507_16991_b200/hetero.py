@@ -8,7 +8,8 @@
        P = segment_matmul(cat(agg_et), stack(w_neigh_et))  tcgen05 grouped GEMM
      (message_passing.hpp:520, one matmul per edge type in the reference)
   3. self projection for ALL node types at once:
-       S = segment_matmul(cat(h_nt), stack(w_self_nt))     tcgen05 grouped GEMM
+       S = grouped_matmul([h_nt], stack(w_self_nt))        tcgen05 grouped GEMM,
+     every h_nt read in place (per-group TMA maps)
      (layer_update message_passing.hpp:579-580, one matmul per node type)
   4. out_nt = ((sum_et P_et) + S_nt) + bias_nt              gm_hetero_combine,
      in the reference's add order (hetero.hpp:338-343, :362)
@@ -24,7 +25,7 @@ from typing import Dict, Tuple
 import torch
 
 from . import _lib as L
-from .graphmill import EdgeIndex, _stream, segment_matmul, spmm
+from .graphmill import EdgeIndex, _stream, grouped_matmul, segment_matmul, spmm
 
 EdgeKey = Tuple[str, str, str]  # (src, rel, dst) — EdgeType
 
@@ -48,6 +49,10 @@ def hetero_sage_layer(edges: Dict[EdgeKey, EdgeIndex], h: Dict[str, torch.Tensor
         if et not in w_neigh:
             raise ValueError(f"hetero_propagate: model lacks a replica for edge type {canonical(et)}")
     f_out = next(iter(w_self.values())).shape[1]
+    f_in = next(iter(h.values())).shape[1]
+    for nt in node_types:  # one feature width for every node type (the stacked weights' inner dimension)
+        if h[nt].dim() != 2 or h[nt].shape[1] != f_in or w_self[nt].shape[0] != f_in:
+            raise ValueError(f"hetero_propagate: node type {nt} feature width differs from {f_in}")
     dev = next(iter(h.values())).device
 
     # 1. per-edge-type mean aggregation (exact), written straight into the
@@ -55,7 +60,6 @@ def hetero_sage_layer(edges: Dict[EdgeKey, EdgeIndex], h: Dict[str, torch.Tensor
     ptr = [0]
     for et in edge_types:
         ptr.append(ptr[-1] + edges[et].num_dst_nodes())
-    f_in = next(iter(h.values())).shape[1]
     agg_all = torch.empty(ptr[-1], f_in, dtype=next(iter(h.values())).dtype, device=dev)
     for i, et in enumerate(edge_types):
         spmm(edges[et], h[et[0]], None, "mean", out=agg_all[ptr[i]:ptr[i + 1]])
@@ -66,12 +70,10 @@ def hetero_sage_layer(edges: Dict[EdgeKey, EdgeIndex], h: Dict[str, torch.Tensor
                               out_dtype=torch.float32)
         for i, et in enumerate(edge_types):
             parts_by_dst[et[2]].append(proj[ptr[i]:ptr[i + 1]])
-    # 3. one grouped GEMM over node types (tcgen05)
-    nptr = [0]
-    for nt in node_types:
-        nptr.append(nptr[-1] + h[nt].shape[0])
-    selfp = segment_matmul(torch.cat([h[nt] for nt in node_types], 0), nptr,
-                           torch.stack([w_self[nt] for nt in node_types]), out_dtype=torch.float32)
+    # 3. one grouped GEMM over node types (tcgen05), reading every node type's
+    #    features in place (per-group TMA maps, no concatenation)
+    selfp = grouped_matmul([h[nt] for nt in node_types], torch.stack([w_self[nt] for nt in node_types]),
+                           out_dtype=torch.float32)
     # 4. combine in the reference's order
     out = {}
     lib = L.lib()
@@ -80,7 +82,7 @@ def hetero_sage_layer(edges: Dict[EdgeKey, EdgeIndex], h: Dict[str, torch.Tensor
         o = torch.empty(rows, f_out, dtype=torch.float32, device=dev)
         parts = [p.contiguous() for p in parts_by_dst[nt]]
         arr = (C.c_void_p * max(1, len(parts)))(*[p.data_ptr() for p in parts])
-        s = selfp[nptr[i]:nptr[i + 1]]
+        s = selfp[i]
         b = bias[nt].to(torch.float32).contiguous()
         L.check(lib.gm_hetero_combine(arr, len(parts), C.c_void_p(s.data_ptr()), C.c_void_p(b.data_ptr()),
                                       rows, f_out, C.c_void_p(o.data_ptr()), _stream()), "gm_hetero_combine")

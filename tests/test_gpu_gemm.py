@@ -179,3 +179,48 @@ def test_fp32_activations_bf16_weights_match_cast_route(k, n):
     torch.cuda.synchronize()
     assert got.dtype == torch.float32
     assert torch.equal(got, want), float((got - want).abs().max())
+
+
+# ---------------------------------------------------------------------------
+# grouped_matmul over separate tensors (hetero.hpp:134-157) through the
+# pointer-array entry gm_grouped_matmul: per-group TMA maps, outputs written
+# in place; the gathered fallback for shapes that need padding
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("k,n,groups", [(128, 128, 4), (64, 48, 3), (128, 256, 8), (100, 32, 3), (36, 40, 9)])
+@pytest.mark.parametrize("route", ["f32", "f32x_bf16w", "bf16"])
+def test_grouped_matmul_pointer_array(k, n, groups, route):
+    torch.manual_seed(k + n + groups)
+    rows = [0 if g == 1 else 300 * g + 7 for g in range(groups)]
+    xs = [torch.randn(r, k, device="cuda") for r in rows]
+    w = torch.randn(groups, k, n, device="cuda") / k ** 0.5
+    if route == "f32x_bf16w":
+        w = w.to(torch.bfloat16)
+    if route == "bf16":
+        xs = [x.to(torch.bfloat16) for x in xs]
+        w = w.to(torch.bfloat16)
+    odt = torch.float32
+    outs = [torch.full((r, n), float("nan"), device="cuda") for r in rows]
+    got = gm.grouped_matmul(xs, w, out_dtype=odt, out=outs)
+    torch.cuda.synchronize()
+    for g in range(groups):
+        assert got[g].data_ptr() == outs[g].data_ptr()  # written in place
+        xg = xs[g].double().cpu().numpy()
+        if route != "f32":  # the bf16 operands the kernel multiplies
+            xg = xs[g].to(torch.bfloat16).double().cpu().numpy()
+        wg = w[g].double().cpu().numpy()
+        ref = xg @ wg
+        scale = np.abs(xg) @ np.abs(wg)
+        assert np.all(np.abs(got[g].double().cpu().numpy() - ref) <= 1e-5 * scale + 1e-6), (route, g)
+
+
+def test_grouped_matmul_matches_segment_matmul_bitwise():
+    torch.manual_seed(9)
+    rows = [700, 1, 0, 1234]
+    xs = [torch.randn(r, 128, device="cuda") for r in rows]
+    w = torch.randn(4, 128, 128, device="cuda") / 11
+    got = gm.grouped_matmul(xs, w)
+    ptr = np.concatenate([[0], np.cumsum(rows)]).tolist()
+    want = gm.segment_matmul(torch.cat(xs), ptr, w)
+    torch.cuda.synchronize()
+    for g in range(4):
+        assert torch.equal(got[g], want[ptr[g]:ptr[g + 1]])
