@@ -230,10 +230,13 @@ GM_API gm_status gm_edge_dot(gm_dtype dtype, const int64_t* src, const int64_t* 
  * and writes out[perm[k]] (COO order). Consecutive entries share the
  * destination row, so its gradient row is fetched once per row run instead of
  * once per edge. entry_rows: gm_csr_entry_rows of the same view (int32 per
- * entry, indexed from the view's first entry); cache it beside the view. */
+ * entry, indexed from the view's first entry); cache it beside the view.
+ * plan (optional, gm_spmm_plan_build of the same view): its source hotness
+ * classes give the source-row gathers gm_spmm's L2 residency policy. */
 GM_API gm_status gm_csr_entry_rows(const gm_csr* csr, int32_t* rows_out, gm_stream_t stream);
-GM_API gm_status gm_edge_dot_csc(gm_dtype dtype, const gm_csr* csc, const int32_t* entry_rows, const void* a_by_dst,
-                                 const void* b_by_src, int64_t f, void* out, gm_stream_t stream);
+GM_API gm_status gm_edge_dot_csc(gm_dtype dtype, const gm_csr* csc, const gm_spmm_plan* plan,
+                                 const int32_t* entry_rows, const void* a_by_dst, const void* b_by_src, int64_t f,
+                                 void* out, gm_stream_t stream);
 
 /* Backward of the max/min aggregation path (message_passing.hpp:508-514):
  * the argpos scatter of aggregate's closure (aggregate.hpp:295-308) followed by

@@ -7,9 +7,11 @@
 //   build_compressed                                    edge_index.hpp:120-121
 //   spmm (sum | mean, optional edge weight)             message_passing.hpp:92-169
 //   neighbor_aggregate (sum | mean | max | min)         message_passing.hpp:500-514
-//   gcn_aggregate                                       message_passing.hpp:490-495
+//   gcn_aggregate / gcn_layer / gcn_forward             message_passing.hpp:490-499, 578, 631-641
+//   neighbor_aggregate_backward (max | min)             aggregate.hpp:295-308 + tensor.hpp:510-524
 //   aggregate (edge rows by index)                      aggregate.hpp:154-215
-//   grouped_matmul                                      hetero.hpp:134-157
+//   grouped_matmul (bf16 and fp32, per-group tensors)   hetero.hpp:134-157
+//   DistSpmm (dst-row partition over an ncclComm_t)
 // Data lives on the device (DeviceMatrix / DeviceArray); std::invalid_argument,
 // std::out_of_range and std::logic_error carry the reference's message shapes.
 #pragma once
@@ -25,7 +27,6 @@
 #include <stdexcept>
 #include <string>
 #include <type_traits>
-#include <unordered_map>
 #include <utility>
 #include <vector>
 
@@ -235,6 +236,39 @@ class EdgeIndex {
   int csr_build_count() const { return cache_->csr_builds.load(); }
   int csc_build_count() const { return cache_->csc_builds.load(); }
 
+  // Effective GCN degrees of this index's FULL arrays, computed once and kept
+  // beside its caches (they depend only on the immutable COO arrays).
+  std::pair<const std::int32_t*, const std::int32_t*> gcn_degrees() const {
+    std::call_once(cache_->gcn_once, [&] {
+      const bool square = num_src_ == num_dst_;
+      cache_->gcn_dst = DeviceArray<std::int32_t>(static_cast<std::size_t>(num_dst_));
+      cache_->gcn_src = square ? cache_->gcn_dst : DeviceArray<std::int32_t>(static_cast<std::size_t>(num_src_));
+      detail::check(gm_gcn_degrees(src_.data(), dst_.data(), num_edges_, num_src_, num_dst_, square,
+                                   cache_->gcn_src.data(), cache_->gcn_dst.data(), stream()));
+    });
+    return {cache_->gcn_src.data(), cache_->gcn_dst.data()};
+  }
+
+  // Source view (gm_source_view): the gather order of the max/min backward.
+  const CsrView& source_view() const {
+    std::call_once(cache_->source_once, [&] {
+      const CsrView& csc = to_csc();
+      auto v = std::make_unique<CsrView>();
+      v->rowptr = DeviceArray<Index>(static_cast<std::size_t>(num_src_ + 1));
+      v->col = DeviceArray<std::int32_t>(static_cast<std::size_t>(num_edges_));
+      v->perm = DeviceArray<std::int32_t>(static_cast<std::size_t>(num_edges_));
+      v->num_cols = num_dst_;
+      const gm_csr c = csc.c_struct();
+      const std::size_t wsb = gm_source_view_workspace(num_edges_, num_src_);
+      DeviceArray<unsigned char> w(wsb ? wsb : 1);
+      detail::check(gm_source_view(&c, num_src_, v->rowptr.data(), v->col.data(), v->perm.data(), w.data(), wsb,
+                                   stream()));
+      detail::check_cuda(cudaStreamSynchronize(stream()), "sync");  // workspace dies here
+      cache_->source = std::move(v);
+    });
+    return *cache_->source;
+  }
+
   // Destination grouping used when the per-edge association matters on an
   // undirected index (the reference's COO sweep, message_passing.hpp:51-59):
   // built once, kept OUT of the public CSC cache like the reference.
@@ -253,6 +287,10 @@ class EdgeIndex {
     std::atomic<int> csc_builds{0};
     std::once_flag exact_once;
     std::unique_ptr<CsrView> exact;
+    std::once_flag gcn_once;
+    DeviceArray<std::int32_t> gcn_src, gcn_dst;  // effective GCN degrees (message_passing.hpp:441-460)
+    std::once_flag source_once;
+    std::unique_ptr<CsrView> source;             // per source, entries in ascending CSC position
     ~CacheSlot() {
       delete csr.load();
       delete csc.load();
@@ -294,23 +332,16 @@ class EdgeIndex {
     if (claims.is_undirected && *claims.is_undirected) {
       if (num_src_ != num_dst_)
         throw std::invalid_argument("EdgeIndex: is_undirected claim requires num_src_nodes == num_dst_nodes");
-      // Multiset symmetry (edge_index.cpp:98-118) — input validation on the
-      // caller's host arrays, as in the reference constructor.
-      struct H {
-        std::size_t operator()(const std::pair<Index, Index>& p) const {
-          return std::hash<Index>()(p.first * 0x9e3779b97f4a7c15ll ^ p.second);
-        }
-      };
-      std::unordered_map<std::pair<Index, Index>, Index, H> counts;
-      for (std::size_t i = 0; i < hs.size(); ++i) ++counts[{hs[i], hd[i]}];
-      for (std::size_t i = 0; i < hs.size(); ++i) {
-        auto it = counts.find({hd[i], hs[i]});
-        const Index mirror = it == counts.end() ? 0 : it->second;
-        if (mirror != counts[{hs[i], hd[i]}])
-          throw std::invalid_argument("EdgeIndex: is_undirected claim violated at position " + std::to_string(i) +
-                                      " (edge " + std::to_string(hs[i]) + "->" + std::to_string(hd[i]) +
-                                      " lacks a matching reverse)");
-      }
+      // Multiset symmetry (edge_index.cpp:98-118) on the device: the first
+      // position whose pair multiplicity differs from its reverse's
+      const std::size_t wsb = gm_first_asymmetric_workspace(num_edges_);
+      DeviceArray<unsigned char> aw(wsb ? wsb : 1);
+      Index bad = -1;
+      detail::check(gm_first_asymmetric(src_.data(), dst_.data(), num_edges_, num_src_, &bad, aw.data(), wsb, stream()));
+      if (bad >= 0)
+        throw std::invalid_argument("EdgeIndex: is_undirected claim violated at position " + std::to_string(bad) +
+                                    " (edge " + std::to_string(hs[static_cast<std::size_t>(bad)]) + "->" +
+                                    std::to_string(hd[static_cast<std::size_t>(bad)]) + " lacks a matching reverse)");
       undirected_ = true;
     }
   }
@@ -375,18 +406,65 @@ DeviceMatrix<S> neighbor_aggregate(const EdgeIndex& e, const DeviceMatrix<S>& x,
   return detail::run_spmm<S>(e.transpose_view(), x, kind, nullptr, nullptr, e.num_dst_nodes(), mm ? argmax : nullptr);
 }
 
-// GCN neighbour side after the transform (message_passing.hpp:490-495).
+// GCN neighbour side after the transform (message_passing.hpp:490-495), with
+// layer_update's bias (:578) and optionally the model's inter-layer relu (:637)
+// fused into the aggregate's epilogue. Degrees are cached on the index.
 template <class S>
-DeviceMatrix<S> gcn_aggregate(const EdgeIndex& e, const DeviceMatrix<S>& xw) {
+DeviceMatrix<S> gcn_aggregate(const EdgeIndex& e, const DeviceMatrix<S>& xw,
+                              const DeviceArray<detail::Acc<S>>* bias = nullptr, bool relu = false) {
+  if (xw.rows() != e.num_src_nodes()) throw std::invalid_argument("spmm: feature rows != num_src_nodes");
+  if (bias && static_cast<Index>(bias->size()) != xw.cols())
+    throw std::invalid_argument("layer_update: bias length != feature width");
   const bool square = e.num_src_nodes() == e.num_dst_nodes();
-  DeviceArray<std::int32_t> dd(static_cast<std::size_t>(e.num_dst_nodes()));
-  DeviceArray<std::int32_t> ds = square ? dd : DeviceArray<std::int32_t>(static_cast<std::size_t>(e.num_src_nodes()));
-  detail::check(gm_gcn_degrees(e.src().data(), e.dst().data(), e.num_edges(), e.num_src_nodes(), e.num_dst_nodes(),
-                               square, ds.data(), dd.data(), stream()));
-  const gm_gcn_norm g{ds.data(), dd.data(), square ? 1 : 0};
-  auto out = detail::run_spmm<S>(e.to_csc(), xw, AggKind::sum, nullptr, &g, e.num_dst_nodes(), nullptr);
-  detail::check_cuda(cudaStreamSynchronize(stream()), "sync");  // degree arrays die here
+  const auto deg = e.gcn_degrees();
+  const gm_gcn_norm g{deg.first, deg.second, square ? 1 : 0, bias ? bias->data() : nullptr, relu ? 1 : 0};
+  return detail::run_spmm<S>(e.to_csc(), xw, AggKind::sum, nullptr, &g, e.num_dst_nodes(), nullptr);
+}
+
+// layer_forward for LayerKind::gcn (message_passing.hpp:490-499, 578): the
+// transform on the tcgen05 GEMM (fp32-accurate split route for float), then
+// the fused aggregate + bias (+ relu).
+inline DeviceMatrix<float> gcn_layer(const EdgeIndex& e, const DeviceMatrix<float>& h, const DeviceMatrix<float>& w,
+                                     const DeviceArray<float>& bias, bool relu = false) {
+  if (h.rows() != e.num_src_nodes() || e.num_src_nodes() != e.num_dst_nodes())
+    throw std::invalid_argument("layer_forward: square index matching h required");
+  if (w.rows() != h.cols()) throw std::invalid_argument("matmul: inner dimension mismatch");
+  DeviceMatrix<float> xw(h.rows(), w.cols());
+  const Index ptr[2] = {0, h.rows()};
+  const std::size_t wsb = gm_segment_matmul_f32_workspace(h.rows(), 1, h.cols(), w.cols());
+  DeviceArray<unsigned char> ws(wsb ? wsb : 1);
+  detail::check(gm_segment_matmul_f32(h.data(), ptr, 1, h.cols(), w.cols(), w.data(), xw.data(), ws.data(), wsb,
+                                      stream()));
+  auto out = gcn_aggregate<float>(e, xw, &bias, relu);
+  detail::check_cuda(cudaStreamSynchronize(stream()), "sync");  // the GEMM workspace dies here
   return out;
+}
+
+// Model::forward of a GCN stack (message_passing.hpp:631-641): relu between layers.
+inline DeviceMatrix<float> gcn_forward(const EdgeIndex& e, const DeviceMatrix<float>& x,
+                                       const std::vector<std::pair<DeviceMatrix<float>, DeviceArray<float>>>& layers) {
+  DeviceMatrix<float> h = x;
+  for (std::size_t i = 0; i < layers.size(); ++i)
+    h = gcn_layer(e, h, layers[i].first, layers[i].second, i + 1 < layers.size());
+  return h;
+}
+
+// Backward of neighbor_aggregate max/min: dx [num_src, F] from the output
+// gradient and the argmax of the forward (aggregate.hpp:295-308, tensor.hpp:510-524).
+template <class S>
+DeviceMatrix<S> neighbor_aggregate_backward(const EdgeIndex& e, const DeviceMatrix<S>& grad_out,
+                                            const DeviceArray<std::int32_t>& argmax) {
+  static_assert(!std::is_same_v<S, bf16>, "f32/f64 only");
+  if (grad_out.rows() != e.num_dst_nodes())
+    throw std::invalid_argument("neighbor_aggregate_backward: grad_out must be [num_dst_nodes, F]");
+  if (static_cast<Index>(argmax.size()) != grad_out.rows() * grad_out.cols())
+    throw std::invalid_argument("neighbor_aggregate_backward: argmax must match grad_out");
+  const CsrView& v = e.source_view();
+  DeviceMatrix<S> dx(e.num_src_nodes(), grad_out.cols());
+  const gm_csr c = v.c_struct();
+  detail::check(gm_spmm_max_backward(&c, &v.plan(), detail::dtype_of<S>(), argmax.data(), grad_out.data(),
+                                     grad_out.cols(), dx.data(), stream()));
+  return dx;
 }
 
 // aggregate.hpp:154-215 for edge-level rows (sum/mean/max/min).
@@ -405,48 +483,98 @@ DeviceMatrix<S> aggregate(const DeviceMatrix<S>& values, const std::vector<Index
   return detail::run_spmm<S>(g, values, kind, nullptr, nullptr, num_groups, nullptr);
 }
 
-// hetero.hpp:134-157: { H_T W_T } for W = [G, F, F'] (bf16 operands, fp32
-// accumulation; output float).
-inline std::vector<DeviceMatrix<float>> grouped_matmul(const std::vector<DeviceMatrix<bf16>>& inputs,
-                                                       const DeviceArray<bf16>& weights, Index groups, Index f_in,
-                                                       Index f_out) {
+// hetero.hpp:134-157: { H_T W_T } for W = [G, F, F'] over separate per-group
+// tensors, one gm_grouped_matmul launch (per-group TMA maps: no concatenation,
+// no copies). bf16 operands with fp32 output, or fp32 operands on the
+// fp32-accurate route (the reference's grouped_matmul<float>).
+namespace detail {
+template <class X>
+std::vector<DeviceMatrix<float>> grouped(const std::vector<DeviceMatrix<X>>& inputs, const void* w, Index groups,
+                                         Index f_in, Index f_out) {
   if (static_cast<Index>(inputs.size()) != groups)
     throw std::invalid_argument("grouped_matmul: group count mismatch (" + std::to_string(inputs.size()) +
                                 " inputs, " + std::to_string(groups) + " weight slabs)");
-  std::vector<Index> ptr{0};
-  for (Index g = 0; g < groups; ++g) {
-    if (inputs[static_cast<std::size_t>(g)].cols() != f_in)
-      throw std::invalid_argument("grouped_matmul: group " + std::to_string(g) + " inner dimension mismatch");
-    ptr.push_back(ptr.back() + inputs[static_cast<std::size_t>(g)].rows());
-  }
-  const Index rows = ptr.back();
-  DeviceMatrix<bf16> x(rows, f_in);
-  for (Index g = 0; g < groups; ++g) {
-    const auto& h = inputs[static_cast<std::size_t>(g)];
-    if (h.rows())
-      detail::check_cuda(cudaMemcpyAsync(x.data() + ptr[static_cast<std::size_t>(g)] * f_in, h.data(),
-                                         static_cast<std::size_t>(h.rows() * f_in) * sizeof(bf16),
-                                         cudaMemcpyDeviceToDevice, stream()),
-                         "D2D");
-  }
-  DeviceMatrix<float> out(rows, f_out);
-  const std::size_t wsb = gm_segment_matmul_workspace(rows, groups, f_in, f_out);
-  DeviceArray<unsigned char> ws(wsb ? wsb : 1);
-  detail::check(gm_segment_matmul(x.data(), ptr.data(), groups, f_in, f_out, weights.data(), GM_F32, out.data(),
-                                  ws.data(), wsb, stream()));
+  std::vector<Index> rows;
+  std::vector<const void*> xs;
+  std::vector<void*> os;
   std::vector<DeviceMatrix<float>> outs;
   for (Index g = 0; g < groups; ++g) {
-    const Index r = ptr[static_cast<std::size_t>(g) + 1] - ptr[static_cast<std::size_t>(g)];
-    DeviceMatrix<float> o(r, f_out);
-    if (r)
-      detail::check_cuda(cudaMemcpyAsync(o.data(), out.data() + ptr[static_cast<std::size_t>(g)] * f_out,
-                                         static_cast<std::size_t>(r * f_out) * sizeof(float), cudaMemcpyDeviceToDevice,
-                                         stream()),
-                         "D2D");
-    outs.push_back(std::move(o));
+    const auto& h = inputs[static_cast<std::size_t>(g)];
+    if (h.cols() != f_in)
+      throw std::invalid_argument("grouped_matmul: group " + std::to_string(g) + " inner dimension mismatch");
+    rows.push_back(h.rows());
+    outs.emplace_back(h.rows(), f_out);
+    xs.push_back(h.data());
+    os.push_back(outs.back().data());
   }
-  detail::check_cuda(cudaStreamSynchronize(stream()), "sync");
+  const gm_dtype dt = dtype_of<X>();
+  const std::size_t wsb = gm_grouped_matmul_workspace(rows.data(), groups, f_in, f_out, dt, dt, GM_F32);
+  DeviceArray<unsigned char> ws(wsb ? wsb : 1);
+  check(gm_grouped_matmul(xs.data(), rows.data(), groups, f_in, f_out, w, dt, dt, os.data(), GM_F32, ws.data(), wsb,
+                          stream()));
+  check_cuda(cudaStreamSynchronize(stream()), "sync");  // the workspace dies here
   return outs;
 }
+}  // namespace detail
+
+inline std::vector<DeviceMatrix<float>> grouped_matmul(const std::vector<DeviceMatrix<bf16>>& inputs,
+                                                       const DeviceArray<bf16>& weights, Index groups, Index f_in,
+                                                       Index f_out) {
+  return detail::grouped<bf16>(inputs, weights.data(), groups, f_in, f_out);
+}
+
+inline std::vector<DeviceMatrix<float>> grouped_matmul(const std::vector<DeviceMatrix<float>>& inputs,
+                                                       const DeviceArray<float>& weights, Index groups, Index f_in,
+                                                       Index f_out) {
+  return detail::grouped<float>(inputs, weights.data(), groups, f_in, f_out);
+}
+
+// One rank of the destination-row partitioned SpMM over a caller-owned NCCL
+// communicator (gm_dist_spmm). EXACT mode: `rows` is the rank's row slice of
+// the CSC with global source ids; every rank passes its X shard of
+// shard_rows rows (row-sharded X, last shard zero-padded).
+class DistSpmm {
+ public:
+  DistSpmm(const CsrView& rows, Index shard_rows, int rank, int world, ncclComm_t comm)
+      : rows_(rows), comm_(comm) {
+    layout_.rank = rank;
+    layout_.world = world;
+    layout_.mode = GM_DIST_EXACT;
+    layout_.shard_rows = shard_rows;
+    block_ = rows_.c_struct();
+    detail::check_cuda(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking), "stream");
+  }
+  DistSpmm(const DistSpmm&) = delete;
+  DistSpmm& operator=(const DistSpmm&) = delete;
+  ~DistSpmm() { cudaStreamDestroy(comm_stream_); }
+
+  template <class S>
+  DeviceMatrix<S> operator()(const DeviceMatrix<S>& x_shard, AggKind kind, DeviceArray<std::int32_t>* argmax = nullptr) {
+    if (x_shard.rows() != layout_.shard_rows) throw std::invalid_argument("DistSpmm: x_shard rows != shard_rows");
+    plan_ = rows_.plan();
+    layout_.blocks = &block_;
+    layout_.plans = &plan_;
+    const gm_dtype dt = detail::dtype_of<S>();
+    const std::size_t wsb = gm_dist_spmm_workspace(&layout_, dt, x_shard.cols());
+    if (ws_.size() < wsb) ws_ = DeviceArray<unsigned char>(wsb);
+    DeviceMatrix<S> out(rows_.num_rows(), x_shard.cols());
+    const bool mm = kind == AggKind::max || kind == AggKind::min;
+    if (mm && argmax) *argmax = DeviceArray<std::int32_t>(static_cast<std::size_t>(out.rows() * out.cols()));
+    const gm_reduce r = kind == AggKind::sum ? GM_SUM : kind == AggKind::mean ? GM_MEAN : kind == AggKind::max ? GM_MAX : GM_MIN;
+    detail::check(gm_dist_spmm(&layout_, dt, x_shard.data(), x_shard.cols(), r, out.data(),
+                               mm && argmax ? argmax->data() : nullptr, ws_.data(), ws_.size(), comm_, comm_stream_,
+                               stream()));
+    return out;
+  }
+
+ private:
+  CsrView rows_;
+  ncclComm_t comm_;
+  gm_dist_layout layout_{};
+  gm_csr block_{};
+  gm_spmm_plan plan_{};
+  cudaStream_t comm_stream_ = nullptr;
+  DeviceArray<unsigned char> ws_;
+};
 
 }  // namespace b200

@@ -110,7 +110,7 @@ SIGNATURES = {
     "gm_scale_rows_div": (C.c_int, [C.c_int, _P, _I64, _I64, _P, _P, _P]),
     "gm_edge_dot": (C.c_int, [C.c_int, _P, _P, _I64, _P, _P, _I64, _P, _P]),
     "gm_csr_entry_rows": (C.c_int, [C.POINTER(gm_csr), _P, _P]),
-    "gm_edge_dot_csc": (C.c_int, [C.c_int, C.POINTER(gm_csr), _P, _P, _P, _I64, _P, _P]),
+    "gm_edge_dot_csc": (C.c_int, [C.c_int, C.POINTER(gm_csr), C.POINTER(gm_spmm_plan), _P, _P, _P, _I64, _P, _P]),
     "gm_source_view_workspace": (C.c_size_t, [_I64, _I64]),
     "gm_source_view": (C.c_int, [C.POINTER(gm_csr), _I64, _P, _P, _P, _P, C.c_size_t, _P]),
     "gm_spmm_max_backward": (C.c_int, [C.POINTER(gm_csr), C.POINTER(gm_spmm_plan), C.c_int, _P, _P, _I64, _P, _P]),

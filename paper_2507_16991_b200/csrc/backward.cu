@@ -6,6 +6,7 @@
 // All arithmetic is IEEE round-to-nearest with no contraction, in the
 // reference's order (sequential in j), so results are bit-identical.
 #include <algorithm>
+#include <cmath>
 
 #include "vec.cuh"
 
@@ -180,13 +181,30 @@ constexpr int kDotV4Warps = 4;
 #endif
 constexpr int kDotBufs = GM_DOT_BUFS;  // staged units per warp (3 and 4 measured slower: fewer resident warps)
 // stage unit u = (batch u / nc, column chunk u % nc) of this warp into buffer u % kDotBufs
+// 16-byte cp.async with an L2 eviction policy chosen per row: hot source rows
+// (the plan's classes) evict_last, all others evict_first — the forward
+// SpMM's residency scheme, so power-law hub rows stay in L2 across the sweep.
+__device__ __forceinline__ void cp_async_16_hint(uint32_t dst, const void* src, bool hot, uint64_t ph, uint64_t pc) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+               "@q cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %3;\n\t"
+               "@!q cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %4;\n\t}" ::"r"(dst),
+               "l"(src), "r"(static_cast<int>(hot)), "l"(ph), "l"(pc)
+               : "memory");
+}
+
 template <int kDotChunk>
 __device__ __forceinline__ void dot_v4_issue(int64_t u, int64_t gw, int64_t nw, int nc, int64_t e, int64_t k0,
                                              int64_t f, int stride, const int32_t* __restrict__ col,
-                                             const float* __restrict__ b, float* buf, int lane, int32_t& rb_iss) {
+                                             const float* __restrict__ b, float* buf, int lane, int32_t& rb_iss,
+                                             const uint8_t* __restrict__ src_class, int hot_limit, uint32_t& hot_iss,
+                                             uint64_t ph, uint64_t pc) {
   const int64_t base = (gw + (u / nc) * nw) * 32;
   const int ci = static_cast<int>(u % nc);
-  if (ci == 0) rb_iss = base + lane < e ? col[k0 + base + lane] : 0;
+  if (ci == 0) {
+    rb_iss = base + lane < e ? col[k0 + base + lane] : 0;
+    const bool hot = src_class && base + lane < e && src_class[k0 + base + lane] < hot_limit;
+    hot_iss = __ballot_sync(0xffffffffu, hot);
+  }
   const int ne = static_cast<int>(e - base < 32 ? e - base : 32);
   const int64_t c0 = static_cast<int64_t>(ci) * kDotChunk;
   const int n16 = static_cast<int>((f - c0 < kDotChunk ? f - c0 : kDotChunk) / 4);  // 16-B pieces per row
@@ -196,8 +214,7 @@ __device__ __forceinline__ void dot_v4_issue(int64_t u, int64_t gw, int64_t nw, 
     const int32_t rbt = __shfl_sync(0xffffffffu, rb_iss, t);  // every lane reaches the shuffle
     if (t < ne) {
       const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(stage + t * stride + pc * 4));
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(b + static_cast<int64_t>(rbt) * f + c0 + pc * 4)
-                   : "memory");
+      cp_async_16_hint(d, b + static_cast<int64_t>(rbt) * f + c0 + pc * 4, (hot_iss >> t) & 1u, ph, pc);
     }
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
@@ -206,7 +223,7 @@ template <int kDotChunk>  // floats of a row staged per unit
 __global__ void __launch_bounds__(kDotV4Warps * 32) edge_dot_csc_v4_kernel(
     const int32_t* __restrict__ rows, const int32_t* __restrict__ col, const int32_t* __restrict__ perm, int64_t k0,
     int64_t e, const float* __restrict__ a, const float* __restrict__ b, int64_t f, int stride,
-    float* __restrict__ out) {
+    float* __restrict__ out, const uint8_t* __restrict__ src_class, int hot_limit) {
   extern __shared__ __align__(16) unsigned char dot_smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -219,15 +236,22 @@ __global__ void __launch_bounds__(kDotV4Warps * 32) edge_dot_csc_v4_kernel(
   const int64_t units = ((nb_all - gw + nw - 1) / nw) * nc;
 
   int32_t rb_iss = 0;
+  uint32_t hot_iss = 0;
+  uint64_t ph, pcold;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(ph));
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pcold));
   float acc = 0.f;
   int32_t ra = 0;
   for (int64_t u = 0; u < kDotBufs - 1; ++u) {
-    if (u < units) dot_v4_issue<kDotChunk>(u, gw, nw, nc, e, k0, f, stride, col, b, buf, lane, rb_iss);
+    if (u < units)
+      dot_v4_issue<kDotChunk>(u, gw, nw, nc, e, k0, f, stride, col, b, buf, lane, rb_iss, src_class, hot_limit, hot_iss,
+                              ph, pcold);
     else asm volatile("cp.async.commit_group;" ::: "memory");
   }
   for (int64_t u = 0; u < units; ++u) {
     if (u + kDotBufs - 1 < units)
-      dot_v4_issue<kDotChunk>(u + kDotBufs - 1, gw, nw, nc, e, k0, f, stride, col, b, buf, lane, rb_iss);
+      dot_v4_issue<kDotChunk>(u + kDotBufs - 1, gw, nw, nc, e, k0, f, stride, col, b, buf, lane, rb_iss, src_class,
+                              hot_limit, hot_iss, ph, pcold);
     else asm volatile("cp.async.commit_group;" ::: "memory");
     const int64_t base = (gw + (u / nc) * nw) * 32;
     const int ci = static_cast<int>(u % nc);
@@ -310,8 +334,9 @@ GM_API gm_status gm_csr_entry_rows(const gm_csr* csr, int32_t* rows_out, gm_stre
   return GM_OK;
 }
 
-GM_API gm_status gm_edge_dot_csc(gm_dtype dtype, const gm_csr* csc, const int32_t* entry_rows, const void* a_by_dst,
-                                 const void* b_by_src, int64_t f, void* out, gm_stream_t stream) {
+GM_API gm_status gm_edge_dot_csc(gm_dtype dtype, const gm_csr* csc, const gm_spmm_plan* plan,
+                                 const int32_t* entry_rows, const void* a_by_dst, const void* b_by_src, int64_t f,
+                                 void* out, gm_stream_t stream) {
   GM_REQUIRE(csc && entry_rows, GM_ERR_INVALID_ARGUMENT, "gm_edge_dot_csc: null argument");
   GM_REQUIRE(dtype == GM_F32 || dtype == GM_F64, GM_ERR_INVALID_ARGUMENT, "gm_edge_dot_csc: f32/f64 only");
   GM_REQUIRE(csc->nnz == 0 || csc->perm, GM_ERR_INVALID_ARGUMENT, "gm_edge_dot_csc: csc->perm required");
@@ -339,9 +364,17 @@ GM_API gm_status gm_edge_dot_csc(gm_dtype dtype, const gm_csr* csc, const int32_
     GM_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDotV4Warps * 32, smem));
     const unsigned blocks = static_cast<unsigned>(
         std::min<int64_t>(ceil_div(csc->nnz, 32 * kDotV4Warps), static_cast<int64_t>(kNumSMs) * std::max(per_sm, 1)));
+    // L2 residency of hot source rows: the same budget rule as gm_spmm
+    const uint8_t* cls = nullptr;
+    int limit = 0;
+    if (plan && plan->src_class && plan->l2_hot_bytes > 0) {
+      const double hot_rows = static_cast<double>(plan->l2_hot_bytes) / static_cast<double>(f * 4);
+      limit = static_cast<int>(std::floor(4.0 * std::log2(1.0 + hot_rows)));
+      if (plan->hot_edge_frac[std::min(limit, GM_PLAN_CLASSES - 1)] >= 0.15) cls = plan->src_class;
+    }
     kern<<<blocks, kDotV4Warps * 32, smem, st>>>(
         entry_rows - k0, csc->col, csc->perm, k0, csc->nnz, static_cast<const float*>(a_by_dst),
-        static_cast<const float*>(b_by_src), f, stride, static_cast<float*>(out));
+        static_cast<const float*>(b_by_src), f, stride, static_cast<float*>(out), cls, limit);
     GM_CHECK_LAUNCH("edge_dot_csc_v4_kernel");
     return GM_OK;
   }

@@ -5,15 +5,15 @@
 // The reference is a stable counting sort by key: within a row, entries keep
 // ascending COO position. An LSD radix sort whose every pass is stable yields
 // exactly that order, so col / perm come out bit-identical to the reference
-// for any input. Per pass (8-bit digit, 2048-entry tiles of 8 warps):
+// for any input. Per pass (8-bit digit, 4096-entry tiles of 8 warps):
 //   1. radix_hist: per-tile digit counts -> table[digit][tile];
 //   2. exclusive scan of the table (digit-major) = each (digit, tile) run's
 //      first output slot;
-//   3. radix_scatter: every warp ranks its 256 entries round by round
+//   3. radix_scatter: every warp ranks its 512 entries round by round
 //      (ballot multisplit: one ballot per digit bit, per-warp u16 counters), a
 //      per-digit prefix over warps and over digits gives each entry's slot in a
 //      digit-sorted copy of the tile in shared memory, and the tile leaves as
-//      contiguous digit runs (coalesced stores, ~8 entries per run).
+//      contiguous digit runs (coalesced stores, ~16 entries per run).
 // rowptr comes from the sorted keys of the last pass (row boundaries), so no
 // atomics anywhere: the result does not depend on scheduling.
 #pragma once
@@ -25,8 +25,8 @@ constexpr int kBits = 8;
 constexpr int kBins = 1 << kBits;
 constexpr int kWarps = 8;
 constexpr int kThreads = 32 * kWarps;
-constexpr int kRounds = 8;
-constexpr int kTile = kThreads * kRounds;  // 2048 entries
+constexpr int kRounds = 16;
+constexpr int kTile = kThreads * kRounds;  // 4096 entries
 
 // lanes holding the same BITS-bit digit (invalid lanes excluded)
 template <int BITS>

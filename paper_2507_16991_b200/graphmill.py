@@ -245,7 +245,8 @@ class EdgeIndex:
         with COO edge ids as perm: the gather order of the max/min backward.
         Built once from the CSC and cached beside it."""
         if self._cache.source is None:
-            csc = self.to_csc()
+            # undirected indices group exactly without publishing a CSC (as the forward)
+            csc = self._exact_dst_grouping() if self._undirected else self.to_csc()
             lib = L.lib()
             e, n = csc.num_entries(), self._num_src
             dev = csc.rowptr.device
@@ -448,8 +449,9 @@ def spmm_backward(e: EdgeIndex, x: torch.Tensor, edge_weight: Optional[torch.Ten
         dw = torch.empty(e.num_edges(), dtype=x.dtype, device=x.device)
         csc = e.to_csc()
         cs = csc.c_struct()
-        L.check(lib.gm_edge_dot_csc(_DT[x.dtype], C.byref(cs), _p(csc.entry_rows()), _p(gs), _p(x.contiguous()),
-                                    f, _p(dw), _stream()), "edge_dot_csc")
+        plan = csc.plan(row_bytes=f * x.element_size())
+        L.check(lib.gm_edge_dot_csc(_DT[x.dtype], C.byref(cs), C.byref(plan), _p(csc.entry_rows()), _p(gs),
+                                    _p(x.contiguous()), f, _p(dw), _stream()), "edge_dot_csc")
     return dx, dw
 
 
@@ -467,7 +469,14 @@ def neighbor_aggregate(e: EdgeIndex, x: torch.Tensor, kind: str,
         raise ValueError(f"unknown aggregation kind: {kind}")
     if x.shape[0] != e.num_src_nodes():
         raise ValueError("propagate: h_src rows != num_src_nodes")
-    grouping = e.transpose_view()
+    # Undirected indices: sum/mean follow the reference's CSR order
+    # (A = A^T, message_passing.hpp:47-85). max/min use the exact destination
+    # grouping: the reference's dst_grouped_order would gather e.src()[perm]
+    # over the CSR — the row node itself, not its neighbour (:205-212) — a
+    # divergence kept deliberately so the fused path equals the edge path and
+    # argmax names the forward edge (u -> v).
+    maxmin = kind in ("max", "min")
+    grouping = e._exact_dst_grouping() if (e.is_undirected() and maxmin) else e.transpose_view()
     w_csr = None
     if edge_weight is not None:
         w_csr = _permute(edge_weight.to(_acc_dtype(x.dtype)).contiguous(), grouping.perm)
@@ -490,9 +499,6 @@ def neighbor_aggregate_backward(e: EdgeIndex, kind: str, grad_out: torch.Tensor,
         raise ValueError("neighbor_aggregate_backward: grad_out must be [num_dst_nodes, F]")
     if tuple(argmax.shape) != tuple(grad_out.shape) or argmax.dtype != torch.int32:
         raise ValueError("neighbor_aggregate_backward: argmax must be int32 like grad_out")
-    if e.is_undirected():
-        raise ValueError("neighbor_aggregate_backward: undirected views group by the CSR; "
-                         "build the index without the is_undirected claim")
     g = grad_out.contiguous()
     f = g.shape[1]
     view = e.source_view()
@@ -502,6 +508,105 @@ def neighbor_aggregate_backward(e: EdgeIndex, kind: str, grad_out: torch.Tensor,
     L.check(L.lib().gm_spmm_max_backward(C.byref(cs), C.byref(plan), _DT[g.dtype], _p(argmax.contiguous()), _p(g),
                                          f, _p(dx), _stream()), "gm_spmm_max_backward")
     return dx
+
+
+# ---------------------------------------------------------------------------
+# Generic message passing: select_path / propagate (message_passing.hpp:14-36,
+# 176-258) over this library's gather, grouping and aggregation kernels.
+# ---------------------------------------------------------------------------
+EDGE_MATERIALIZE = "edge_materialize"
+SEGMENT_FUSED = "segment_fused"
+
+
+@dataclass
+class MessageFns:
+    """message(h_w, edge_attr, h_v) -> messages (edge-aligned) and
+    update(h_v, aggregated) (message_passing.hpp:176-182). None = identity
+    message (h_w) / update returning the aggregate."""
+    message: Optional[object] = None
+    update: Optional[object] = None
+
+
+def select_path(e: EdgeIndex, needs_edge_callback: bool) -> str:
+    """message_passing.hpp:31-36: an edge callback forces materialisation; the
+    fused path needs a destination grouping (by_dst claim, CSC cache, or an
+    undirected index's CSR cache)."""
+    if needs_edge_callback:
+        return EDGE_MATERIALIZE
+    grouped = e.sort_order() == "by_dst" or e.has_csc_cache() or (e.is_undirected() and e.has_csr_cache())
+    return SEGMENT_FUSED if grouped else EDGE_MATERIALIZE
+
+
+def gather_rows(src: torch.Tensor, index, name: str = "gather_rows:") -> torch.Tensor:
+    """tensor.hpp:499-530: out[i] = src[index[i]] after the bounds check of
+    tensor.hpp:489-495 (std::out_of_range naming the first bad position)."""
+    if src.dim() < 1:
+        raise ValueError("gather_rows: rank >= 1 required")
+    n = src.shape[0]
+    idx = index if isinstance(index, torch.Tensor) else torch.as_tensor(index)
+    idx = idx.to(device=src.device)
+    lib = L.lib()
+    if idx.dtype == torch.int64:
+        ws = torch.empty(64, dtype=torch.uint8, device=src.device)
+        L.check(lib.gm_check_index_bounds(_p(idx), idx.numel(), n, name.encode(), _p(ws), _stream()), "bounds")
+        idx = idx.to(torch.int32)
+    idx = idx.contiguous()
+    x = src.contiguous()
+    f = 1
+    for d in x.shape[1:]:
+        f *= int(d)
+    out = torch.empty((idx.numel(),) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+    if idx.numel() and f:
+        L.check(lib.gm_gather_rows(_DT[x.dtype], _p(x), f, _p(idx), idx.numel(), _p(out), _stream()),
+                "gm_gather_rows")
+    return out
+
+
+def _entry_dst(grouping: CsrView) -> torch.Tensor:
+    return grouping.entry_rows()[: grouping.num_entries()]
+
+
+def propagate(e: EdgeIndex, h_src: torch.Tensor, h_dst: torch.Tensor, edge_attr: Optional[torch.Tensor],
+              fns: MessageFns, agg: str, path: str, callback=None, edge_type_name: str = "") -> torch.Tensor:
+    """message_passing.hpp:220-258: h'_v = update(h_v, agg_{w in N(v)} c(message(h_w, e_wv, h_v))).
+    edge_materialize: messages in COO order, aggregated in ascending position
+    per destination (aggregate's unsorted_scatter); segment_fused: messages in
+    destination-grouped order (the CSC, or the exact grouping when an edge
+    attribute meets an undirected index), sorted-segment aggregate. With an
+    identity message and no edge attribute the fused path is one SpMM kernel
+    (no E x F temporary)."""
+    if h_src.shape[0] != e.num_src_nodes():
+        raise ValueError("propagate: h_src rows != num_src_nodes")
+    if h_dst.shape[0] != e.num_dst_nodes():
+        raise ValueError("propagate: h_dst rows != num_dst_nodes")
+    if edge_attr is not None and edge_attr.shape[0] != e.num_edges():
+        raise ValueError("propagate: edge_attr rows != num_edges")
+    if path == SEGMENT_FUSED and callback is not None:
+        raise ValueError("propagate: edge callbacks require the edge_materialize path")
+    if path not in (EDGE_MATERIALIZE, SEGMENT_FUSED):
+        raise ValueError(f"propagate: unknown path {path}")
+    message = fns.message or (lambda hw, ea, hv: hw)
+    update = fns.update or (lambda hv, a: a)
+    n_dst = e.num_dst_nodes()
+    if path == EDGE_MATERIALIZE:
+        hw = gather_rows(h_src, e.src())
+        hv = gather_rows(h_dst, e.dst())
+        m = message(hw, edge_attr, hv)
+        if callback is not None:
+            m = callback(m, edge_type_name)
+        return update(h_dst, aggregate(m, e.dst(), n_dst, agg))
+    if fns.message is None and edge_attr is None:
+        return update(h_dst, neighbor_aggregate(e, h_src, agg))
+    # the exact grouping on undirected indices: gathers the true in-neighbour
+    # (see neighbor_aggregate), for every message function
+    grouping = e._exact_dst_grouping() if e.is_undirected() else e.transpose_view()
+    k = grouping.num_entries()
+    hw = gather_rows(h_src, grouping.col[:k])
+    grouped_dst = _entry_dst(grouping)
+    hv = gather_rows(h_dst, grouped_dst)
+    ea = gather_rows(edge_attr, grouping.perm[:k]) if edge_attr is not None else None
+    m = message(hw, ea, hv)
+    return update(h_dst, aggregate(m, grouped_dst, n_dst, agg))
 
 
 def gcn_degrees(e: EdgeIndex, square: bool):
@@ -577,7 +682,7 @@ def aggregate(values: torch.Tensor, index: torch.Tensor, num_groups: int, kind: 
     visited in ascending position, exactly the reference's scatter order."""
     if kind not in _KIND:
         raise ValueError(f"unknown aggregation kind: {kind}")
-    index = index.to(dtype=torch.int64).contiguous()
+    index = index.to(device=values.device, dtype=torch.int64).contiguous()
     if values.shape[0] != index.numel():
         raise ValueError("aggregate: values rows != index length")
     lib = L.lib()

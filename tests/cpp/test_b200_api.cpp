@@ -297,3 +297,87 @@ TEST_CASE("grouped_matmul equals independent per-group matmuls; empty groups; er
   CHECK_THROWS_AS(grouped_matmul({ins[0], DeviceMatrix<bf16>(2, 4)}, DeviceArray<bf16>::from_host(wb), 2, 3, 5),
                   std::invalid_argument);
 }
+
+TEST_CASE("gcn layer: tcgen05 transform + fused bias/relu epilogue (message_passing.hpp:490-499, 578)") {
+  // 3-node path with self loops: out = A_hat (h W) + b, relu when asked
+  EdgeIndex e({0, 1, 1, 2}, {1, 0, 2, 1}, 3, 3);
+  const std::vector<float> h{1, 2, -1, 0.5f, 3, -2}, w{0.5f, -1, 2, 0.25f}, b{0.1f, -5};
+  auto hm = DeviceMatrix<float>::from_host(3, 2, h);
+  auto wm = DeviceMatrix<float>::from_host(2, 2, w);
+  auto bias = DeviceArray<float>::from_host(b);
+  std::vector<double> xw(6, 0);
+  for (int r = 0; r < 3; ++r)
+    for (int j = 0; j < 2; ++j)
+      for (int k = 0; k < 2; ++k) xw[r * 2 + j] += double(h[r * 2 + k]) * w[k * 2 + j];
+  const double deg[3] = {2, 3, 2};  // in-degree + self loop
+  const std::vector<std::vector<int>> in{{1}, {0, 2}, {1}};
+  const auto got = gcn_layer(e, hm, wm, bias).to_host();
+  const auto got_relu = gcn_layer(e, hm, wm, bias, true).to_host();
+  for (int v = 0; v < 3; ++v)
+    for (int j = 0; j < 2; ++j) {
+      double want = xw[v * 2 + j] / deg[v];
+      for (int s : in[v]) want += xw[s * 2 + j] / std::sqrt(deg[s] * deg[v]);
+      want += b[j];
+      CHECK(std::abs(got[v * 2 + j] - want) <= 1e-5 * (std::abs(want) + 1));
+      CHECK(got_relu[v * 2 + j] == (got[v * 2 + j] > 0 ? got[v * 2 + j] : 0.0f));
+    }
+}
+
+TEST_CASE("fp32 grouped_matmul over separate tensors (hetero.hpp:134-157, grouped_matmul<float>)") {
+  const auto h0 = random_values(300 * 128, 301), h1 = random_values(7 * 128, 302), w = random_values(2 * 128 * 64, 303);
+  auto f = [](const std::vector<double>& v) { return std::vector<float>(v.begin(), v.end()); };
+  std::vector<DeviceMatrix<float>> ins{DeviceMatrix<float>::from_host(300, 128, f(h0)),
+                                       DeviceMatrix<float>::from_host(7, 128, f(h1))};
+  auto outs = grouped_matmul(ins, DeviceArray<float>::from_host(f(w)), 2, 128, 64);
+  const std::vector<const std::vector<double>*> hs{&h0, &h1};
+  for (std::size_t g = 0; g < 2; ++g) {
+    const auto got = outs[g].to_host();
+    for (Index r = 0; r < outs[g].rows(); ++r)
+      for (Index j = 0; j < 64; ++j) {
+        double want = 0, scale = 0;
+        for (Index k = 0; k < 128; ++k) {
+          const double a = float((*hs[g])[static_cast<std::size_t>(r * 128 + k)]);
+          const double bb = float(w[g * 128 * 64 + static_cast<std::size_t>(k * 64 + j)]);
+          want += a * bb;
+          scale += std::abs(a * bb);
+        }
+        CHECK(std::abs(got[static_cast<std::size_t>(r * 64 + j)] - want) <= 1e-5 * scale + 1e-7);
+      }
+  }
+}
+
+TEST_CASE("max backward lands on the first attaining edge (aggregate.hpp:295-308)") {
+  // destinations 0 and 1; edges (src -> dst): 0->0, 1->0, 2->0, 2->1, 0->1
+  EdgeIndex e({0, 1, 2, 2, 0}, {0, 0, 0, 1, 1}, 3, 2);
+  auto x = DeviceMatrix<double>::from_host(3, 1, std::vector<double>{5, 5, 1});
+  DeviceArray<std::int32_t> arg;
+  neighbor_aggregate(e, x, AggKind::max, &arg);
+  auto g = DeviceMatrix<double>::from_host(2, 1, std::vector<double>{10, 7});
+  const auto dx = neighbor_aggregate_backward(e, g, arg).to_host();
+  // row 0: tie 5/5 -> edge 0 (src 0); row 1: max(1, 5) -> edge 4 (src 0)
+  CHECK(dx == std::vector<double>{17, 0, 0});
+}
+
+TEST_CASE("DistSpmm over a 1-rank NCCL communicator equals the single-GPU spmm") {
+  unsigned char id[128];
+  REQUIRE(gm_nccl_unique_id(id) == GM_OK);
+  ncclComm_t comm = nullptr;
+  REQUIRE(gm_nccl_comm_init(1, id, 0, &comm) == GM_OK);
+  {
+    Stream s = test_stream(77);
+    std::vector<Index> src(20000), dst(20000);
+    for (std::size_t i = 0; i < src.size(); ++i) {
+      src[i] = static_cast<Index>(s.next_below(3000));
+      dst[i] = static_cast<Index>(s.next_below(3000));
+    }
+    EdgeIndex e(src, dst, 3000, 3000);
+    const auto xh = random_values(3000 * 16, 78);
+    auto x = DeviceMatrix<double>::from_host(3000, 16, xh);
+    DistSpmm ds(e.to_csc(), 3000, 0, 1, comm);
+    CHECK(ds(x, AggKind::sum).to_host() == neighbor_aggregate(e, x, AggKind::sum).to_host());
+    DeviceArray<std::int32_t> a1, a2;
+    CHECK(ds(x, AggKind::max, &a1).to_host() == neighbor_aggregate(e, x, AggKind::max, &a2).to_host());
+    CHECK(a1.to_host() == a2.to_host());
+  }
+  CHECK(gm_nccl_comm_destroy(comm) == GM_OK);
+}

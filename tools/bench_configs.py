@@ -155,7 +155,7 @@ def products_backward():
     cs = csc.c_struct()
     er = csc.entry_rows()
     import ctypes as _C
-    dot_csc_ms = timed(lambda: L.check(L.lib().gm_edge_dot_csc(L.GM_F32, _C.byref(cs), er.data_ptr(), gout.data_ptr(),
+    dot_csc_ms = timed(lambda: L.check(L.lib().gm_edge_dot_csc(L.GM_F32, _C.byref(cs), _C.byref(csc.plan()), er.data_ptr(), gout.data_ptr(),
                                                                x.data_ptr(), f, dw.data_ptr(),
                                                                torch.cuda.current_stream().cuda_stream)), reps=5)
     r = {"config": "C4 backward (sum)", "edge_dot_csc_ms": dot_csc_ms, "dx_ms": dx_ms, "dx_gedges_s": e / dx_ms / 1e6, "dx_and_dw_ms": full_ms,

@@ -26,6 +26,6 @@ csc = g.to_csc()
 cs = csc.c_struct()
 rows = csc.entry_rows()
 for _ in range(2):
-    L.check(L.lib().gm_edge_dot_csc(L.GM_F32, C.byref(cs), rows.data_ptr(), gout.data_ptr(), x.data_ptr(), f,
+    L.check(L.lib().gm_edge_dot_csc(L.GM_F32, C.byref(cs), C.byref(csc.plan()), rows.data_ptr(), gout.data_ptr(), x.data_ptr(), f,
                                     dw.data_ptr(), torch.cuda.current_stream().cuda_stream))
 torch.cuda.synchronize()
