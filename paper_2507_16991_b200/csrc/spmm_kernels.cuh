@@ -157,6 +157,22 @@ __device__ __forceinline__ unsigned short ldg_hot_cs<unsigned short>(const unsig
   return r;
 }
 
+// hot ? normal-priority : evict-first (ld.global.cs), predicated pair with no
+// cache-policy operand: nothing 64-bit stays live across the batch (the
+// policy-register form spilled at the max path's 64-register cap).
+template <typename R>
+__device__ __forceinline__ R ldg_na_cs(const R* p, bool hot);
+template <>
+__device__ __forceinline__ uint4 ldg_na_cs<uint4>(const uint4* p, bool hot) {
+  uint4 r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+      "@q ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\n\t"
+      "@!q ld.global.cs.nc.v4.u32 {%0,%1,%2,%3}, [%4];\n\t}"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p), "r"(static_cast<int>(hot)));
+  return r;
+}
+
 // Both policies as predicated loads (no branch per gather): hot ? evict_last : evict_first.
 template <typename R>
 __device__ __forceinline__ R ldg_hint2(const R* p, bool hot, uint64_t ph, uint64_t pc);
@@ -526,6 +542,20 @@ __global__ void __launch_bounds__(256) spmm_light_kernel(const SpmmArgs p) {
 // stream the cold arm with ld.global.cs. 0 = default loads (X fits L2).
 // Measured on C4 (sum): default 6.2 ms, all-cs 6.2, all-evict_first 4.8,
 // hot evict_last + cold evict_first 4.25.
+#ifndef GM_FLAT_GATHER_V
+#define GM_FLAT_GATHER_V 3
+#endif
+// gather form of the 16-byte one-vector flat path (same-box A/B builds,
+// tools/build_variant.sh): 0 validity-predicated policy pair; 1 max/min with
+// clamped lanes (no predicate) + normal / evict-first; 2 the same for sum/mean
+// (C4 sum 4.27 -> 4.89 ms: the hot rows need evict_last); 3 (default) max/min
+// with clamped lanes + evict_last / evict-first. With 6 edges per batch
+// (GM_FLAT_MAX_U) C4 max + argmax went 5.13 -> 4.72 ms: 8 edges spilled the
+// batch at the 64-register cap, 4-5 left too few gathers in flight.
+constexpr int kFlatGather = GM_FLAT_GATHER_V;
+#ifndef GM_FLAT_MAX_U
+#define GM_FLAT_MAX_U 6  // edges per batch of the 16-byte one-vector max/min path
+#endif
 template <typename T, int VB, int NV, int U, int MODE, bool SCALED, bool ACC, int LM>
 __global__ void __launch_bounds__(256, (sizeof(T) == 8 || (SCALED && (MODE >= 2 || NV > 1 || VB <= 8))) ? 3 : 4) spmm_flat_kernel(const SpmmArgs p) {
   constexpr bool MAXMIN = MODE >= 2;
@@ -536,6 +566,9 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 8 || (SCALED && (MODE >= 2 
   using R = typename VecT::R;
   constexpr int V = VecT::V;
   constexpr unsigned FULL = 0xffffffffu;
+  // clamped one-vector gathers: every lane consumes a real row slice, only
+  // the valid ones store
+  constexpr bool kClamped = kFlatGather >= 1 && VB == 16 && NV == 1 && LM >= 1 && (MAXMIN || kFlatGather == 2);
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (warp >= p.num_light_windows) return;
@@ -556,6 +589,12 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 8 || (SCALED && (MODE >= 2 
   }
   // gather address = this lane's slice base + source * row bytes: one IMAD.WIDE
   const unsigned char* xlane = reinterpret_cast<const unsigned char*>(x) + static_cast<size_t>(soff[0]) * sizeof(T);
+  // lanes past the row's last slot gather that slot again (same sectors as
+  // the last valid lane: no extra traffic) and never store, so the one-vector
+  // gathers need no validity predicate
+  const unsigned char* xlane_c =
+      reinterpret_cast<const unsigned char*>(x) +
+      static_cast<size_t>((p.slot_base + min(lane, max(nsl - 1, 0))) * V) * sizeof(T);
   const uint32_t rowb = fu * static_cast<uint32_t>(sizeof(T));
 
   // Positions fit int32: gm_build_compressed / plan_build require nnz < 2^31.
@@ -654,7 +693,13 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 8 || (SCALED && (MODE >= 2 
     for (int u = 0; u < U; ++u) {
       const T* xr = x + static_cast<uint64_t>(static_cast<uint32_t>(__shfl_sync(FULL, c_cur, u))) * fu;
       const bool hot = (hmask >> u) & 1u;
-      if constexpr (LM >= 1 && !MAXMIN && VB <= 8) {
+      if constexpr (kFlatGather >= 1 && VB == 16 && NV == 1 && LM >= 1 && (MAXMIN || kFlatGather == 2)) {
+        // one 16-byte vector per lane: clamped lane base (no predicate), hot
+        // rows at normal L2 priority, the rest evict-first, no policy register
+        const unsigned char* xs = xlane_c + static_cast<uint64_t>(static_cast<uint32_t>(__shfl_sync(FULL, c_cur, u))) * rowb;
+        if constexpr (kFlatGather == 3) buf[u][0] = ldg_hot_cs<R>(reinterpret_cast<const R*>(xs), hot, pol_hot);
+        else buf[u][0] = ldg_na_cs<R>(reinterpret_cast<const R*>(xs), hot);
+      } else if constexpr (LM >= 1 && !MAXMIN && VB <= 8) {
         // predicated evict_last / evict_first pair with the column validity
         // folded in and a precomputed lane base: no branch, one IMAD.WIDE per
         // gather (8-byte vectors: C5 87 -> 79 ms, C2 55 -> 51 ms in A/B runs;
@@ -707,7 +752,7 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 8 || (SCALED && (MODE >= 2 
         const int32_t pm = MAXMIN ? __shfl_sync(FULL, p_cur, u) : -1;
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
-          if (valid[j]) {
+          if (kClamped || valid[j]) {
             A vals[V];
             VecT::unpack(buf[u][j], vals);
             acc.add(j, vals, SCALED, sc, first && u == 0, IS_MIN, pm, lex);
@@ -732,7 +777,7 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 8 || (SCALED && (MODE >= 2 
             const int32_t pm = MAXMIN ? __shfl_sync(FULL, p_cur, u) : -1;
 #pragma unroll
             for (int j = 0; j < NV; ++j)
-              if (valid[j]) {
+              if (kClamped || valid[j]) {
                 A vals[V];
                 VecT::unpack(buf[u][j], vals);
                 acc.add(j, vals, SCALED, sc, first && u == u0, IS_MIN, pm, lex);
@@ -753,7 +798,7 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 8 || (SCALED && (MODE >= 2 
           while (k0 + u >= row_end) flush();
 #pragma unroll
           for (int j = 0; j < NV; ++j)
-            if (valid[j]) {
+            if (kClamped || valid[j]) {
               A vals[V];
               VecT::unpack(buf[u][j], vals);
               acc.add(j, vals, SCALED, sc, first, IS_MIN, pm, lex);
@@ -1282,8 +1327,10 @@ gm_status launch_flat(const SpmmArgs& p0, int64_t ns, cudaStream_t st) {
       else if (nv == 4 || kChunk <= 128) GM_FLAT(4, 2);
       else if constexpr (kChunk > 128) GM_FLAT(8, 1);
     } else {
-      if (nv == 1) GM_FLAT(1, 8);
-      else if (nv == 2) GM_FLAT(2, 4);
+      if (nv == 1) {
+        if constexpr (MAXMIN) GM_FLAT(1, GM_FLAT_MAX_U);
+        else GM_FLAT(1, 8);
+      } else if (nv == 2) GM_FLAT(2, 4);
       else if (nv == 4 || kChunk <= 128) GM_FLAT(4, 2);
       else if constexpr (kChunk > 128) GM_FLAT(8, 1);
     }
