@@ -181,14 +181,15 @@ constexpr int kDotV4Warps = 4;
 #endif
 constexpr int kDotBufs = GM_DOT_BUFS;  // staged units per warp (3 and 4 measured slower: fewer resident warps)
 // stage unit u = (batch u / nc, column chunk u % nc) of this warp into buffer u % kDotBufs
-// 16-byte cp.async with an L2 eviction policy chosen per row: hot source rows
-// (the plan's classes) evict_last, all others evict_first — the forward
-// SpMM's residency scheme, so power-law hub rows stay in L2 across the sweep.
-__device__ __forceinline__ void cp_async_16_hint(uint32_t dst, const void* src, bool hot, uint64_t ph, uint64_t pc) {
+// 16-byte cp.async; hot source rows (the plan's classes) carry an evict_last
+// policy so power-law hub rows stay in L2 across the sweep, the rest default
+// priority (evict_first for them measured 7.6 -> 9.3 ms on C4: unlike the
+// forward sweep, dw re-reads cold rows within L2's lifetime).
+__device__ __forceinline__ void cp_async_16_hint(uint32_t dst, const void* src, bool hot, uint64_t ph) {
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
                "@q cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %3;\n\t"
-               "@!q cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %4;\n\t}" ::"r"(dst),
-               "l"(src), "r"(static_cast<int>(hot)), "l"(ph), "l"(pc)
+               "@!q cp.async.cg.shared.global [%0], [%1], 16;\n\t}" ::"r"(dst),
+               "l"(src), "r"(static_cast<int>(hot)), "l"(ph)
                : "memory");
 }
 
@@ -197,7 +198,7 @@ __device__ __forceinline__ void dot_v4_issue(int64_t u, int64_t gw, int64_t nw, 
                                              int64_t f, int stride, const int32_t* __restrict__ col,
                                              const float* __restrict__ b, float* buf, int lane, int32_t& rb_iss,
                                              const uint8_t* __restrict__ src_class, int hot_limit, uint32_t& hot_iss,
-                                             uint64_t ph, uint64_t pc) {
+                                             uint64_t ph) {
   const int64_t base = (gw + (u / nc) * nw) * 32;
   const int ci = static_cast<int>(u % nc);
   if (ci == 0) {
@@ -214,7 +215,7 @@ __device__ __forceinline__ void dot_v4_issue(int64_t u, int64_t gw, int64_t nw, 
     const int32_t rbt = __shfl_sync(0xffffffffu, rb_iss, t);  // every lane reaches the shuffle
     if (t < ne) {
       const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(stage + t * stride + pc * 4));
-      cp_async_16_hint(d, b + static_cast<int64_t>(rbt) * f + c0 + pc * 4, (hot_iss >> t) & 1u, ph, pc);
+      cp_async_16_hint(d, b + static_cast<int64_t>(rbt) * f + c0 + pc * 4, (hot_iss >> t) & 1u, ph);
     }
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
@@ -237,21 +238,20 @@ __global__ void __launch_bounds__(kDotV4Warps * 32) edge_dot_csc_v4_kernel(
 
   int32_t rb_iss = 0;
   uint32_t hot_iss = 0;
-  uint64_t ph, pcold;
+  uint64_t ph;
   asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(ph));
-  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pcold));
   float acc = 0.f;
   int32_t ra = 0;
   for (int64_t u = 0; u < kDotBufs - 1; ++u) {
     if (u < units)
       dot_v4_issue<kDotChunk>(u, gw, nw, nc, e, k0, f, stride, col, b, buf, lane, rb_iss, src_class, hot_limit, hot_iss,
-                              ph, pcold);
+                              ph);
     else asm volatile("cp.async.commit_group;" ::: "memory");
   }
   for (int64_t u = 0; u < units; ++u) {
     if (u + kDotBufs - 1 < units)
       dot_v4_issue<kDotChunk>(u + kDotBufs - 1, gw, nw, nc, e, k0, f, stride, col, b, buf, lane, rb_iss, src_class,
-                              hot_limit, hot_iss, ph, pcold);
+                              hot_limit, hot_iss, ph);
     else asm volatile("cp.async.commit_group;" ::: "memory");
     const int64_t base = (gw + (u / nc) * nw) * 32;
     const int ci = static_cast<int>(u % nc);

@@ -5,15 +5,18 @@
 // The reference is a stable counting sort by key: within a row, entries keep
 // ascending COO position. An LSD radix sort whose every pass is stable yields
 // exactly that order, so col / perm come out bit-identical to the reference
-// for any input. Per pass (8-bit digit, 4096-entry tiles of 8 warps):
-//   1. radix_hist: per-tile digit counts -> table[digit][tile];
-//   2. exclusive scan of the table (digit-major) = each (digit, tile) run's
-//      first output slot;
-//   3. radix_scatter: every warp ranks its 512 entries round by round
+// for any input. Digits are 8 bits wide (11 as an A/B knob). Per pass
+// (2048-entry tiles of 8 warps):
+//   1. radix_hist: per-tile digit counts -> table[tile][digit] (one contiguous
+//      row per tile);
+//   2. radix_colscan: exclusive scan of every digit's column over the tiles
+//      (in place) plus the digit totals; a one-CTA scan of the totals gives
+//      each digit's first output slot;
+//   3. radix_scatter: every warp ranks its 256 entries round by round
 //      (ballot multisplit: one ballot per digit bit, per-warp u16 counters), a
 //      per-digit prefix over warps and over digits gives each entry's slot in a
 //      digit-sorted copy of the tile in shared memory, and the tile leaves as
-//      contiguous digit runs (coalesced stores, ~16 entries per run).
+//      contiguous digit runs.
 // rowptr comes from the sorted keys of the last pass (row boundaries), so no
 // atomics anywhere: the result does not depend on scheduling.
 #pragma once
@@ -21,12 +24,17 @@
 namespace gm {
 namespace rx {
 
-constexpr int kBits = 8;
-constexpr int kBins = 1 << kBits;
+constexpr int kMaxBits = 11;
 constexpr int kWarps = 8;
 constexpr int kThreads = 32 * kWarps;
-constexpr int kRounds = 16;
-constexpr int kTile = kThreads * kRounds;  // 4096 entries
+// Entries per lane per tile and the scatter's CTAs per SM (same-box A/B on
+// C4, whole build: 16 rounds / 2 CTAs 2.06 ms, 12 / 2 2.09, 8 / 3 2.02,
+// 8 / 4 (64 registers) 1.94)
+#ifndef GM_RADIX_ROUNDS
+#define GM_RADIX_ROUNDS 8
+#endif
+constexpr int kRounds = GM_RADIX_ROUNDS;
+constexpr int kTile = kThreads * kRounds;  // entries per tile
 
 // lanes holding the same BITS-bit digit (invalid lanes excluded)
 template <int BITS>
@@ -51,42 +59,168 @@ struct In {
 };
 
 __device__ __forceinline__ uint32_t key_at(const In& in, int64_t i) {
-  return in.keys64 ? static_cast<uint32_t>(in.keys64[i]) : __ldcs(in.key + i);
+  return in.keys64 ? static_cast<uint32_t>(in.keys64[i]) : in.key[i];
 }
 
-__global__ void __launch_bounds__(kThreads) radix_hist_kernel(In in, int64_t e, int shift, int64_t tiles,
+template <int BITS>
+__global__ void __launch_bounds__(kThreads) radix_hist_kernel(In in, int64_t e, int shift,
                                                               int32_t* __restrict__ table) {
+  constexpr int kBins = 1 << BITS;
   __shared__ int32_t hist[kBins];
   const int64_t t = blockIdx.x;
-  hist[threadIdx.x] = 0;
+  for (int d = threadIdx.x; d < kBins; d += kThreads) hist[d] = 0;
   __syncthreads();
   const int64_t base = t * kTile;
   const int64_t end = min(e, base + kTile);
   for (int64_t i = base + threadIdx.x; i < end; i += kThreads)
     atomicAdd(&hist[(key_at(in, i) >> shift) & (kBins - 1)], 1);
   __syncthreads();
-  table[static_cast<int64_t>(threadIdx.x) * tiles + t] = hist[threadIdx.x];
+  for (int d = threadIdx.x; d < kBins; d += kThreads) table[t * kBins + d] = hist[d];
+}
+
+// Exclusive scan of the tile-major table over tiles, per digit, in place, in
+// three steps so every step has thousands of warps in flight:
+//   colsum:  warp (digit group of 32, chunk of kChunk tiles) -> part[chunk][d];
+//   colscan: the partial table scanned over chunks (one CTA per digit group,
+//            its warps owning contiguous chunk ranges) + the digit totals;
+//   coldown: each (group, chunk) warp rewrites its tiles as running prefixes.
+constexpr int kChunk = 16;  // tiles per warp in colsum / coldown
+constexpr int kColWarps = 32;
+__global__ void radix_colsum_kernel(const int32_t* __restrict__ table, int64_t tiles, int bins,
+                                    int32_t* __restrict__ part) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int groups = bins / 32;
+  const int64_t c = gw / groups;
+  const int d = static_cast<int>(gw % groups) * 32 + lane;
+  const int64_t t0 = c * kChunk;
+  if (t0 >= tiles) return;
+  const int64_t t1 = min(tiles, t0 + kChunk);
+  int32_t s = 0;
+#pragma unroll 4
+  for (int64_t t = t0; t < t1; ++t) s += table[t * bins + d];
+  part[c * bins + d] = s;
+}
+__global__ void radix_coldown_kernel(int32_t* __restrict__ table, int64_t tiles, int bins,
+                                     const int32_t* __restrict__ part) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int groups = bins / 32;
+  const int64_t c = gw / groups;
+  const int d = static_cast<int>(gw % groups) * 32 + lane;
+  const int64_t t0 = c * kChunk;
+  if (t0 >= tiles) return;
+  const int64_t t1 = min(tiles, t0 + kChunk);
+  int32_t v[kChunk];
+#pragma unroll
+  for (int i = 0; i < kChunk; ++i) v[i] = t0 + i < t1 ? table[(t0 + i) * bins + d] : 0;
+  int32_t run = part[c * bins + d];
+#pragma unroll
+  for (int i = 0; i < kChunk; ++i) {
+    if (t0 + i < t1) table[(t0 + i) * bins + d] = run;
+    run += v[i];
+  }
+}
+// in-place exclusive scan of a [rows][bins] table over rows, per column, plus
+// the column totals; one CTA per 32 columns (lane = column)
+__global__ void __launch_bounds__(32 * kColWarps) radix_colscan_kernel(int32_t* __restrict__ table, int64_t rows,
+                                                                       int bins, int32_t* __restrict__ total) {
+  __shared__ int32_t psum[kColWarps][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int d = blockIdx.x * 32 + lane;
+  const int64_t per = (rows + kColWarps - 1) / kColWarps;
+  const int64_t t0 = min(rows, static_cast<int64_t>(w) * per), t1 = min(rows, t0 + per);
+  int32_t s = 0;
+  for (int64_t t = t0; t < t1; ++t) s += table[t * bins + d];
+  psum[w][lane] = s;
+  __syncthreads();
+  int32_t before = 0, all = 0;
+#pragma unroll 8
+  for (int ww = 0; ww < kColWarps; ++ww) {
+    const int32_t c = psum[ww][lane];
+    before += ww < w ? c : 0;
+    all += c;
+  }
+  int32_t run = before;
+  for (int64_t t = t0; t < t1; ++t) {
+    const int32_t c = table[t * bins + d];
+    table[t * bins + d] = run;
+    run += c;
+  }
+  if (w == 0) total[d] = all;
+}
+
+// Exclusive scan of the digit totals (bins <= 2048, one CTA of 1024 threads).
+__global__ void __launch_bounds__(1024) radix_digit_scan_kernel(const int32_t* __restrict__ total, int bins,
+                                                                int32_t* __restrict__ start) {
+  __shared__ int32_t wsum[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int per = (bins + 1023) / 1024;
+  int32_t v[2] = {0, 0};
+  int32_t s = 0;
+  for (int j = 0; j < per; ++j) {
+    const int d = threadIdx.x * per + j;
+    v[j] = d < bins ? total[d] : 0;
+    s += v[j];
+  }
+  int32_t inc = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t n = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += n;
+  }
+  if (lane == 31) wsum[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    const int32_t t = wsum[lane];
+    int32_t ti = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t n = __shfl_up_sync(0xffffffffu, ti, o);
+      if (lane >= o) ti += n;
+    }
+    wsum[lane] = ti - t;
+  }
+  __syncthreads();
+  int32_t run = wsum[w] + inc - s;
+  for (int j = 0; j < per; ++j) {
+    const int d = threadIdx.x * per + j;
+    if (d < bins) start[d] = run;
+    run += v[j];
+  }
+}
+
+template <int BITS>
+constexpr size_t scatter_smem_bytes() {
+  return 3 * kTile * sizeof(uint32_t) + kWarps * (1 << BITS) * sizeof(uint16_t) + 2 * ((1 << BITS) + 1) * sizeof(int32_t);
 }
 
 // LAST: write perm / col (int32) and the sorted keys (for rowptr) instead of
 // the next pass's triples.
-template <bool LAST>
-__global__ void __launch_bounds__(kThreads) radix_scatter_kernel(In in, int64_t e, int shift, int64_t tiles,
+#ifndef GM_RADIX_MINB
+#define GM_RADIX_MINB 4
+#endif
+template <int BITS, bool LAST>
+__global__ void __launch_bounds__(kThreads, GM_RADIX_MINB) radix_scatter_kernel(In in, int64_t e, int shift,
                                                                  const int32_t* __restrict__ table_off,
+                                                                 const int32_t* __restrict__ digit_start,
                                                                  uint32_t* __restrict__ okey, uint32_t* __restrict__ opos,
                                                                  uint32_t* __restrict__ oval) {
-  __shared__ uint16_t whist[kWarps][kBins];
-  __shared__ int32_t dstart[kBins + 1];
-  __shared__ int32_t gout[kBins];
+  constexpr int kBins = 1 << BITS;
+  constexpr int kPer = kBins >= kThreads ? kBins / kThreads : 1;  // digits per thread
   __shared__ int32_t wsum[kWarps];
-  extern __shared__ uint32_t stage[];  // digit-sorted tile: key, position, value
+  extern __shared__ __align__(16) uint32_t stage[];  // digit-sorted tile: key, position, value
   uint32_t* skey = stage;
   uint32_t* spos = stage + kTile;
   uint32_t* sval = stage + 2 * kTile;
+  uint16_t* whist = reinterpret_cast<uint16_t*>(stage + 3 * kTile);  // [kWarps][kBins]
+  int32_t* dstart = reinterpret_cast<int32_t*>(whist + kWarps * kBins);  // [kBins + 1]
+  int32_t* gout = dstart + kBins + 1;                                      // [kBins]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t t = blockIdx.x;
-  for (int i = threadIdx.x; i < kWarps * kBins; i += kThreads) (&whist[0][0])[i] = 0;
-  gout[threadIdx.x] = table_off[static_cast<int64_t>(threadIdx.x) * tiles + t];
+  for (int i = threadIdx.x; i < kWarps * kBins / 2; i += kThreads) reinterpret_cast<uint32_t*>(whist)[i] = 0;
+  for (int d = threadIdx.x; d < kBins; d += kThreads)
+    gout[d] = digit_start[d] + table_off[t * kBins + d];
   const int64_t wbase = t * kTile + static_cast<int64_t>(w) * (32 * kRounds);
   uint32_t k[kRounds], p[kRounds], v[kRounds];
 #pragma unroll
@@ -106,31 +240,42 @@ __global__ void __launch_bounds__(kThreads) radix_scatter_kernel(In in, int64_t 
   __syncthreads();
   const unsigned lt = (1u << lane) - 1u;
   uint16_t rank[kRounds];
+  uint16_t* wh = whist + w * kBins;
 #pragma unroll
   for (int j = 0; j < kRounds; ++j) {
     const bool valid = wbase + j * 32 + lane < e;
     const uint32_t d = (k[j] >> shift) & (kBins - 1);
-    const unsigned peers = digit_peers<kBits>(d, valid);
+    // (one __match_any_sync instead of the ballots measured 10% slower per build)
+    const unsigned peers = digit_peers<BITS>(d, valid);
     uint16_t old = 0;
-    if (valid) old = whist[w][d];
+    if (valid) old = wh[d];
     __syncwarp();
-    if (valid && (peers & lt) == 0) whist[w][d] = static_cast<uint16_t>(old + __popc(peers));
+    if (valid && (peers & lt) == 0) wh[d] = static_cast<uint16_t>(old + __popc(peers));
     __syncwarp();
     rank[j] = static_cast<uint16_t>(old + __popc(peers & lt));
   }
   __syncthreads();
-  // per digit (one per thread): prefix over warps, then exclusive scan over digits
+  // per digit: prefix over warps (in place), then an exclusive scan over digits
+  // (thread owns kPer consecutive digits)
   {
-    const int d = threadIdx.x;
-    int32_t run = 0;
+    int32_t run_d[kPer];
+    int32_t s = 0;
 #pragma unroll
-    for (int ww = 0; ww < kWarps; ++ww) {
-      const int32_t c = whist[ww][d];
-      whist[ww][d] = static_cast<uint16_t>(run);
-      run += c;
+    for (int q = 0; q < kPer; ++q) {
+      const int d = threadIdx.x * kPer + q;
+      int32_t run = 0;
+      if (d < kBins) {
+#pragma unroll
+        for (int ww = 0; ww < kWarps; ++ww) {
+          const int32_t c = whist[ww * kBins + d];
+          whist[ww * kBins + d] = static_cast<uint16_t>(run);
+          run += c;
+        }
+      }
+      run_d[q] = run;
+      s += run;
     }
-    // block exclusive scan of the per-digit tile counts
-    int32_t inc = run;
+    int32_t inc = s;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int32_t n = __shfl_up_sync(0xffffffffu, inc, o);
@@ -140,8 +285,14 @@ __global__ void __launch_bounds__(kThreads) radix_scatter_kernel(In in, int64_t 
     __syncthreads();
     int32_t before = 0;
     for (int ww = 0; ww < w; ++ww) before += wsum[ww];
-    dstart[d] = before + inc - run;
-    if (d == kBins - 1) dstart[kBins] = before + inc;
+    int32_t r = before + inc - s;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int d = threadIdx.x * kPer + q;
+      if (d < kBins) dstart[d] = r;
+      r += run_d[q];
+    }
+    if (threadIdx.x == kThreads - 1) dstart[kBins] = r;
   }
   __syncthreads();
   // digit-sorted copy of the tile in shared memory
@@ -149,7 +300,7 @@ __global__ void __launch_bounds__(kThreads) radix_scatter_kernel(In in, int64_t 
   for (int j = 0; j < kRounds; ++j) {
     if (wbase + j * 32 + lane < e) {
       const uint32_t d = (k[j] >> shift) & (kBins - 1);
-      const int s = dstart[d] + whist[w][d] + rank[j];
+      const int s = dstart[d] + wh[d] + rank[j];
       skey[s] = k[j];
       spos[s] = p[j];
       sval[s] = v[j];
@@ -174,17 +325,19 @@ __global__ void __launch_bounds__(kThreads) radix_scatter_kernel(In in, int64_t 
   }
 }
 
-// rowptr from the sorted keys: rowptr[r] = first slot with key >= r. Each
-// thread owns 4 consecutive slots (one 16-byte load + the previous key).
+// rowptr from the sorted keys: rowptr[r] = first slot with key >= r. Thread q
+// owns slots [4q, 4q+4): one 16-byte load plus the previous key; the row
+// starts inside the range (usually zero or one) are written directly.
 __global__ void rowptr_from_sorted_kernel(const uint32_t* __restrict__ key, int64_t e, int64_t rows,
                                           int64_t* __restrict__ rowptr) {
   const int64_t quads = (e + 4) / 4;  // slots 0..e (slot e closes the last rows)
+  const bool aligned = (reinterpret_cast<uintptr_t>(key) & 15) == 0;
   for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < quads;
        q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t k0 = q * 4;
     int64_t kk[5];
-    kk[0] = k0 == 0 ? -1 : static_cast<int64_t>(key[k0 - 1]);
-    if (k0 + 4 <= e && (reinterpret_cast<uintptr_t>(key + k0) & 15) == 0) {
+    kk[0] = k0 == 0 ? -1 : static_cast<int64_t>(__ldg(key + k0 - 1));
+    if (k0 + 4 <= e && aligned) {
       const uint4 v = __ldg(reinterpret_cast<const uint4*>(key + k0));
       kk[1] = v.x;
       kk[2] = v.y;
@@ -192,8 +345,9 @@ __global__ void rowptr_from_sorted_kernel(const uint32_t* __restrict__ key, int6
       kk[4] = v.w;
     } else {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) kk[j + 1] = k0 + j < e ? static_cast<int64_t>(key[k0 + j]) : rows;
+      for (int j = 0; j < 4; ++j) kk[j + 1] = k0 + j < e ? static_cast<int64_t>(__ldg(key + k0 + j)) : rows;
     }
+    if (kk[4] == kk[0] && k0 + 4 <= e) continue;  // no row starts in this quad
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int64_t k = k0 + j;
@@ -204,8 +358,10 @@ __global__ void rowptr_from_sorted_kernel(const uint32_t* __restrict__ key, int6
 }
 
 struct RadixWs {
-  int32_t* table;    // [kBins * tiles]
-  int32_t* partial;  // scan block sums
+  int32_t* table;    // [bins * tiles]
+  int32_t* part;     // [chunks * bins] (scan partials)
+  int32_t* total;    // [bins]
+  int32_t* start;    // [bins]
   uint32_t* buf[2][3];  // ping-pong (key, pos, val)
   size_t bytes;
 };
@@ -220,8 +376,11 @@ inline RadixWs radix_layout(void* base, int64_t e) {
     return q;
   };
   const int64_t tiles = std::max<int64_t>(1, ceil_div(e, kTile));
-  w.table = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(kBins * tiles)));
-  w.partial = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(cb::scan32_blocks(kBins * tiles))));
+  constexpr int64_t bins = int64_t{1} << kMaxBits;
+  w.table = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(bins * tiles)));  // [tile][digit]
+  w.part = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(bins * ceil_div(tiles, kChunk))));
+  w.total = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(bins)));
+  w.start = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(bins)));
   for (int b = 0; b < 2; ++b)
     for (int a = 0; a < 3; ++a) w.buf[b][a] = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * static_cast<size_t>(e)));
   w.bytes = off;
@@ -234,43 +393,74 @@ inline int key_bits(int64_t rows) {
   return b;
 }
 
+template <int BITS>
+inline gm_status radix_pass(const In& in, int64_t e, int shift, bool last, const RadixWs& w, uint32_t* ok,
+                            uint32_t* op, uint32_t* ov, cudaStream_t st) {
+  const int64_t tiles = ceil_div(e, kTile);
+  constexpr int bins = 1 << BITS;
+  radix_hist_kernel<BITS><<<static_cast<unsigned>(tiles), kThreads, 0, st>>>(in, e, shift, w.table);
+  GM_CHECK_LAUNCH("radix_hist_kernel");
+  const int64_t chunks = ceil_div(tiles, kChunk);
+  const unsigned col_grid = static_cast<unsigned>(ceil_div(chunks * (bins / 32) * 32, 256));
+  radix_colsum_kernel<<<col_grid, 256, 0, st>>>(w.table, tiles, bins, w.part);
+  GM_CHECK_LAUNCH("radix_colsum_kernel");
+  radix_colscan_kernel<<<static_cast<unsigned>(bins / 32), 32 * kColWarps, 0, st>>>(w.part, chunks, bins, w.total);
+  GM_CHECK_LAUNCH("radix_colscan_kernel");
+  radix_coldown_kernel<<<col_grid, 256, 0, st>>>(w.table, tiles, bins, w.part);
+  GM_CHECK_LAUNCH("radix_coldown_kernel");
+  radix_digit_scan_kernel<<<1, 1024, 0, st>>>(w.total, bins, w.start);
+  GM_CHECK_LAUNCH("radix_digit_scan_kernel");
+  constexpr size_t smem = scatter_smem_bytes<BITS>();
+  if (last) {
+    GM_TRY_CUDA(cudaFuncSetAttribute(radix_scatter_kernel<BITS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+    GM_TRY_CUDA(cudaFuncSetAttribute(radix_scatter_kernel<BITS, true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared));
+    radix_scatter_kernel<BITS, true><<<static_cast<unsigned>(tiles), kThreads, smem, st>>>(in, e, shift, w.table,
+                                                                                          w.start, ok, op, ov);
+  } else {
+    GM_TRY_CUDA(cudaFuncSetAttribute(radix_scatter_kernel<BITS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+    GM_TRY_CUDA(cudaFuncSetAttribute(radix_scatter_kernel<BITS, false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared));
+    radix_scatter_kernel<BITS, false><<<static_cast<unsigned>(tiles), kThreads, smem, st>>>(in, e, shift, w.table,
+                                                                                           w.start, ok, op, ov);
+  }
+  GM_CHECK_LAUNCH("radix_scatter_kernel");
+  return GM_OK;
+}
+
 // Full build: rowptr, col, perm. keys in [0, rows), values < 2^31.
 inline gm_status radix_build(const int64_t* keys, const int64_t* values, int64_t e, int64_t rows, int64_t* rowptr,
                              int32_t* col, int32_t* perm, const RadixWs& w, cudaStream_t st) {
-  const int64_t tiles = ceil_div(e, kTile);
-  const int passes = (key_bits(rows) + kBits - 1) / kBits;
+  const int bits = key_bits(rows);
+  // widest digit (A/B knob GM_RADIX_BITS, 8 or 11)
+  // (C4: 3 passes of 8 bits 1.5 ms of scatter vs 2 passes of 11 bits 2.06 ms:
+  // the 2048-digit tiles leave ~2-entry runs and 8x the ranking work)
+  static const int max_bits = [] {
+    const char* ev = getenv("GM_RADIX_BITS");
+    return ev && atoi(ev) == 11 ? kMaxBits : 8;
+  }();
+  const int passes = (bits + max_bits - 1) / max_bits;
+  const int dbits = (bits + passes - 1) / passes;  // <= 11
   In in{keys, values, nullptr, nullptr, nullptr};
   int cur = 0;
   uint32_t* last_keys = nullptr;
   for (int ps = 0; ps < passes; ++ps) {
-    const int shift = ps * kBits;
-    radix_hist_kernel<<<static_cast<unsigned>(tiles), kThreads, 0, st>>>(in, e, shift, tiles, w.table);
-    GM_CHECK_LAUNCH("radix_hist_kernel");
-    gm_status s = cb::scan32_exclusive(w.table, kBins * tiles, w.partial, st);
-    if (s != GM_OK) return s;
+    const int shift = ps * dbits;
     const bool last = ps == passes - 1;
     uint32_t* ok = w.buf[cur][0];
     uint32_t* op = last ? reinterpret_cast<uint32_t*>(perm) : w.buf[cur][1];
     uint32_t* ov = last ? reinterpret_cast<uint32_t*>(col) : w.buf[cur][2];
-    constexpr size_t stage_bytes = 3 * kTile * sizeof(uint32_t);
-    if (last) {
-      GM_TRY_CUDA(cudaFuncSetAttribute(radix_scatter_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(stage_bytes)));
-      radix_scatter_kernel<true><<<static_cast<unsigned>(tiles), kThreads, stage_bytes, st>>>(in, e, shift, tiles,
-                                                                                             w.table, ok, op, ov);
-    } else {
-      GM_TRY_CUDA(cudaFuncSetAttribute(radix_scatter_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(stage_bytes)));
-      radix_scatter_kernel<false><<<static_cast<unsigned>(tiles), kThreads, stage_bytes, st>>>(in, e, shift, tiles,
-                                                                                              w.table, ok, op, ov);
-    }
-    GM_CHECK_LAUNCH("radix_scatter_kernel");
+    const gm_status s = dbits <= 8 ? radix_pass<8>(in, e, shift, last, w, ok, op, ov, st)
+                                   : radix_pass<11>(in, e, shift, last, w, ok, op, ov, st);
+    if (s != GM_OK) return s;
     in = In{nullptr, nullptr, ok, op, ov};
     last_keys = ok;
     cur ^= 1;
   }
-  rowptr_from_sorted_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div((e + 4) / 4, 256), kNumSMs * 64)), 256,
-                              0, st>>>(last_keys, e, rows, rowptr);
+  rowptr_from_sorted_kernel<<<static_cast<unsigned>(ceil_div((e + 4) / 4, 256)), 256, 0, st>>>(last_keys, e, rows,
+                                                                                              rowptr);
   GM_CHECK_LAUNCH("rowptr_from_sorted_kernel");
   return GM_OK;
 }

@@ -518,7 +518,6 @@ __global__ void __launch_bounds__(256) spmm_light_kernel(const SpmmArgs p) {
         VecT::store_global(orow + slot[j] * V, acc.v[j]);
         if (want_arg) {
           int32_t* arow = p.arg + static_cast<int64_t>(r) * p.f + slot[j] * V;
-#pragma unroll
           store_arg<V>(arow, acc.a[j]);
         }
       }
@@ -646,7 +645,6 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 8 || (SCALED && (MODE >= 2 
         VecT::store_global(out + obase + soff[j], acc.v[j]);
         if (want_arg) {
           int32_t* arow = p.arg + obase + soff[j];
-#pragma unroll
           store_arg<V>(arow, acc.a[j]);
         }
       }
@@ -991,7 +989,6 @@ __global__ void __launch_bounds__(kHeavyThreads) spmm_heavy_kernel(const SpmmArg
       VecT::store_global(orow + (p.slot_base + s) * V, acc.v[m]);
       if (want_arg) {
         int32_t* arow = p.arg + static_cast<int64_t>(r) * p.f + (p.slot_base + s) * V;
-#pragma unroll
         store_arg<V>(arow, acc.a[m]);
       }
     }
@@ -1168,7 +1165,7 @@ __global__ void __launch_bounds__(64) spmm_hub_kernel(const SpmmArgs p) {
   using RawL = typename HL::R;
   // one edge into the running value(s); LEX: seeded blocks break ties on COO id
   auto combine = [&](const RawL raw, const A sc, const int32_t pm, const bool is_first, auto lex_c) {
-    constexpr bool LEX = decltype(lex_c)::value;
+    [[maybe_unused]] constexpr bool LEX = decltype(lex_c)::value;
     T tmp[LE];
     memcpy(tmp, &raw, LB);
 #pragma unroll

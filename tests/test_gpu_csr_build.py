@@ -2,7 +2,9 @@
 restatement (itself pinned to the reference, tests/test_oracle.py), across the
 shapes that select each route of gm_build_compressed:
 
-* the bucketed stable sort (csr_bucket.cuh): many rows, power-law hub rows
+* the LSD radix sort (csr_radix.cuh, default): 1, 2 and 3 passes of up to
+  11-bit digits;
+* the bucketed stable sort (csr_bucket.cuh, GM_CSR_ALGO=bucket): many rows, power-law hub rows
   longer than a whole bucket (single-row buckets), few rows with millions of
   entries, keys confined to a narrow row band, duplicate edges;
 * the scatter + per-row sort fallback (more buckets than fit shared memory).
@@ -42,6 +44,8 @@ def check(keys, values, n_rows):
     (1, 2_000, 4_000_000),      # power-law over few rows: hubs > one bucket (131,072) -> single-row buckets
     (0, 4_000_000, 6_000_000),  # many rows (1,954 row buckets)
     (1, 300_000, 12_000_000),   # many entry-count cuts
+    (1, 4_000_000, 9_000_000),  # 22-bit keys: two 11-bit LSD passes
+    (0, 40_000_000, 1_500_000), # 26-bit keys: three 9-bit passes, mostly empty rows
 ])
 def test_bucketed_build_bit_exact(kind, n, e):
     src, dst = synth(kind, n, n, e, seed=n + e)

@@ -21,5 +21,5 @@ ref = gm.build_compressed(dst, src, bench.N_NODES)
 per = bench.timed_steps(lambda: gm.build_compressed(dst, src, bench.N_NODES), 10, flush)
 v = gm.build_compressed(dst, src, bench.N_NODES)
 same = bool(torch.equal(v.perm, ref.perm) and torch.equal(v.col, ref.col) and torch.equal(v.rowptr, ref.rowptr))
-print(json.dumps({"env": {k: os.environ.get(k) for k in ("GM_CSR_BUCKET", "GM_CSR_FIN_SMEM")},
+print(json.dumps({"env": {k: os.environ.get(k) for k in ("GM_CSR_ALGO", "GM_RADIX_BITS")},
                   "ms": round(statistics.mean(per), 4), "min": round(min(per), 4), "repeatable": same}))
