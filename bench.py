@@ -304,7 +304,8 @@ def single_gpu_secondary(gm, L, lib, g, x, cs, plan, flush_buf, steps, hbm):
                      "frac": mb / mms / 1e6 / hbm, "traffic": traffic_of("spmm_max_traffic.json"),
                      "algorithmic_bytes_per_call": mb,
                      "bytes_model": "gather model + 4 B int32 argmax per output element"}}
-    del mo, ma
+    ma_keep = ma
+    del mo
     # CSR build (build_compressed of the CSC: keys = dst, values = src), a fresh
     # build per step (the reference rebuilds it per EdgeIndex, edge_index.cpp:121-136)
     dst, src = g.dst(), g.src()
@@ -332,6 +333,50 @@ def single_gpu_secondary(gm, L, lib, g, x, cs, plan, flush_buf, steps, hbm):
                      "bytes_model": "two-pass stable counting sort: read dst (8E), read dst+src (16E), "
                                     "write col+perm int32 (8E), write rowptr (8(N+1))"}}
     del ws, col, perm
+    # backward of the two aggregations (§8f-1), same graph, L2 flushed per step:
+    # dw = per-edge dot of the output gradient's destination row with the source
+    # row (message_passing.hpp:156-165, CSC order); max backward = argpos scatter
+    # + gather_rows adjoint as one gather over the source view (aggregate.hpp:295-308)
+    gout = torch.empty_like(x)
+    L.check(lib.gm_synth_features(SEED + 7, 0, N_NODES, F, 1, L.GM_F32, C.c_void_p(gout.data_ptr()),
+                                  C.c_void_p(stream.cuda_stream)))
+    rows = csc.entry_rows()
+    dw = torch.empty(N_EDGES, dtype=torch.float32, device=x.device)
+
+    def dw_step():
+        L.check(lib.gm_edge_dot_csc(L.GM_F32, C.byref(cs), C.byref(plan), C.c_void_p(rows.data_ptr()),
+                                    C.c_void_p(gout.data_ptr()), C.c_void_p(x.data_ptr()), F,
+                                    C.c_void_p(dw.data_ptr()), C.c_void_p(stream.cuda_stream)))
+    dw_step()
+    per = timed_steps(dw_step, max(3, steps // 3), flush_buf)
+    dms = statistics.mean(per)
+    db = N_EDGES * (F * 4 + 16) + N_NODES * (F * 4 + 8)
+    sec["backward_dw"] = {
+        "ms": dms, "gedges_s": N_EDGES / dms / 1e6,
+        "roofline": {"bound": "hbm", "achieved": db / dms / 1e6, "peak": hbm, "unit": "GB/s",
+                     "frac": db / dms / 1e6 / hbm, "algorithmic_bytes_per_call": db,
+                     "bytes_model": "per edge: source row gather 4F + col/row/perm/dw 16; per row: gradient row 4F + rowptr 8"}}
+    del dw
+    view = g.source_view()
+    vplan = view.plan(row_bytes=F * 4)
+    vcs = view.c_struct()
+    dx = torch.empty_like(x)
+
+    def maxbwd_step():
+        L.check(lib.gm_spmm_max_backward(C.byref(vcs), C.byref(vplan), L.GM_F32, C.c_void_p(ma_keep.data_ptr()),
+                                         C.c_void_p(gout.data_ptr()), F, C.c_void_p(dx.data_ptr()),
+                                         C.c_void_p(stream.cuda_stream)))
+    maxbwd_step()
+    per = timed_steps(maxbwd_step, max(3, steps // 3), flush_buf)
+    mbms = statistics.mean(per)
+    mbb = N_EDGES * (F * 4 + 8) + N_NODES * (3 * F * 4 + 8)
+    sec["backward_max"] = {
+        "ms": mbms, "gedges_s": N_EDGES / mbms / 1e6,
+        "roofline": {"bound": "hbm", "achieved": mbb / mbms / 1e6, "peak": hbm, "unit": "GB/s",
+                     "frac": mbb / mbms / 1e6 / hbm, "algorithmic_bytes_per_call": mbb,
+                     "bytes_model": "per source-view entry: destination argmax row 4F + col/eid 8; per row: gradient "
+                                    "row 4F (each winner read once), dx row 4F, argmax 4F counted once, rowptr 8"}}
+    del dx, gout, ma_keep
     sec["segment_matmul_C3"] = bench_segment_matmul(gm, L, x.device)
     sec["segment_matmul_C3_fp32"] = bench_segment_matmul(gm, L, x.device, fp32=True)
     sec["segment_matmul_F1024"] = bench_segment_matmul(gm, L, x.device, f=1024, rows=500_000)

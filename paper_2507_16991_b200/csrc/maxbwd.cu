@@ -16,6 +16,7 @@
 // Traffic per edge: the argmax slice of the destination row (4 B per column),
 // the gradient only where a column matches (sparse), plus col/eid.
 #include <algorithm>
+#include <cmath>
 
 #include "vec.cuh"
 
@@ -131,45 +132,188 @@ __global__ void __launch_bounds__(256) maxbwd_light_kernel(const int64_t* __rest
   }
 }
 
-// Hub rows (deg > the plan's threshold): one warp per (hub row, 32-column
-// chunk), one column per lane, entries walked in order in batches of 32
-// (metadata) x kU (loads in flight).
-template <typename S>
-__global__ void __launch_bounds__(128) maxbwd_hub_kernel(const int64_t* __restrict__ rowptr,
-                                                         const int32_t* __restrict__ col,
-                                                         const int32_t* __restrict__ eid,
-                                                         const int32_t* __restrict__ heavy, int64_t num_heavy,
-                                                         const int32_t* __restrict__ arg, const S* __restrict__ g,
-                                                         int64_t f, S* __restrict__ dx) {
+// fp32 rows of 16-byte multiples (the hot case): the forward flat sweep's
+// schedule over the source view. One warp streams a heavy-free window of
+// consecutive source rows as one contiguous entry range, U entries per batch
+// regardless of row boundaries; (destination, edge id) pairs are prefetched
+// two batches ahead, one per lane, and broadcast by shuffle. Software
+// pipeline: while batch b's gradient slices (16 bytes per lane, loaded only
+// where an argmax matches) are in flight, batch b+1's argmax slices already
+// are too; then b's contributions are added in entry order, so each output
+// element is still one lane's sequential sum. Lanes past the row's last slot
+// re-read it and never store.
+// (same-box C4 A/B, whole backward: 4 entries / 4 CTAs per SM 12.3 ms, 6 / 3
+// 17.4, 8 / 2 15.7; the unpipelined two-phase form 12.2 at 6 / 3 with spills,
+// the previous warp-per-row gather 24.9 + 4.4 ms for hubs)
+#ifndef GM_MAXBWD_MINB
+#define GM_MAXBWD_MINB 4
+#endif
+#ifndef GM_MAXBWD_U
+#define GM_MAXBWD_U 4
+#endif
+template <int U>
+__global__ void __launch_bounds__(256, GM_MAXBWD_MINB) maxbwd_flat_kernel(const int64_t* __restrict__ rowptr,
+                                                          const int32_t* __restrict__ col,
+                                                          const int32_t* __restrict__ eid,
+                                                          const int32_t* __restrict__ windows, int64_t num_windows,
+                                                          const int32_t* __restrict__ arg, const float* __restrict__ g,
+                                                          int64_t f, float* __restrict__ dx) {
+  static_assert(4 * U <= 32, "4 match bits per entry in one word");
   constexpr unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
-  const int64_t chunks = (f + 31) / 32;
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (w >= num_heavy * chunks) return;
-  const int r = heavy[w / chunks];
-  const int64_t c = (w % chunks) * 32 + lane;
-  const bool valid = c < f;
+  if (w >= num_windows) return;
+  const int ra = windows[2 * w], rb = windows[2 * w + 1];
+  const int32_t kbeg = static_cast<int32_t>(rowptr[ra]);
+  const int32_t kend = static_cast<int32_t>(rowptr[rb]);
+  const uint32_t fu = static_cast<uint32_t>(f);
+  const int nsl_all = static_cast<int>(f / 4);
+  for (int sb = 0; sb < nsl_all; sb += 32) {  // column passes of 32 16-byte slots
+    const int nsl = min(32, nsl_all - sb);
+    const bool valid = lane < nsl;
+    const uint32_t soff = static_cast<uint32_t>(sb + min(lane, nsl - 1)) * 4u;
+    int cbase = ra;
+    int32_t rend_l = (cbase + lane < rb) ? static_cast<int32_t>(rowptr[cbase + 1 + lane]) : kend;
+    int row = ra;
+    int32_t row_end = __shfl_sync(FULL, rend_l, 0);
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    auto flush = [&]() {
+      if (valid)
+        __stcs(reinterpret_cast<float4*>(dx + static_cast<uint64_t>(static_cast<uint32_t>(row)) * fu + soff),
+               make_float4(acc[0], acc[1], acc[2], acc[3]));
+      acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
+      ++row;
+      if (row < rb) {
+        if (row - cbase >= 32) {
+          cbase = row;
+          rend_l = (cbase + lane < rb) ? static_cast<int32_t>(rowptr[cbase + 1 + lane]) : kend;
+        }
+        row_end = __shfl_sync(FULL, rend_l, row - cbase);
+      }
+    };
+    // (evict_last for the plan's hot destinations measured 12.3 -> 13.3 ms on C4)
+    auto fetch = [&](int32_t kb, int32_t& c, int32_t& e) {
+      if (lane < U) {
+        const int32_t k = min(kb + lane, kend - 1);
+        c = col[k];
+        e = eid[k];
+      }
+    };
+    int4 av[U];
+#define GM_MB_LOAD_ARG(cbatch)                                                                         \
+  _Pragma("unroll") for (int u = 0; u < U; ++u) {                                                     \
+    const uint32_t v = static_cast<uint32_t>(__shfl_sync(FULL, (cbatch), u));                          \
+    av[u] = __ldcs(reinterpret_cast<const int4*>(arg + static_cast<uint64_t>(v) * fu + soff));       \
+  }
+    if (kend > kbeg) {
+      int32_t c0 = 0, e0 = -2, c1 = 0, e1 = -2;
+      fetch(kbeg, c0, e0);
+      if (kbeg + U < kend) fetch(kbeg + U, c1, e1);
+      GM_MB_LOAD_ARG(c0)
+      for (int32_t k0 = kbeg; k0 < kend; k0 += U) {
+        const int nb = min(U, kend - k0);
+        uint32_t mask = 0;  // 4 match bits per entry
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int32_t eu = __shfl_sync(FULL, e0, u);
+          const uint32_t m = static_cast<uint32_t>(av[u].x == eu) | (static_cast<uint32_t>(av[u].y == eu) << 1) |
+                             (static_cast<uint32_t>(av[u].z == eu) << 2) |
+                             (static_cast<uint32_t>(av[u].w == eu) << 3);
+          mask |= (u < nb ? m : 0u) << (4 * u);
+        }
+        const int32_t cb = c0;
+        c0 = c1;
+        e0 = e1;
+        if (k0 + 2 * U < kend) fetch(k0 + 2 * U, c1, e1);
+        if (k0 + U < kend) {  // next batch's argmax slices, in flight with this batch's gradients
+          GM_MB_LOAD_ARG(c0)
+        }
+        float4 gv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t v = static_cast<uint32_t>(__shfl_sync(FULL, cb, u));
+          if ((mask >> (4 * u)) & 15u)
+            gv[u] = __ldg(reinterpret_cast<const float4*>(g + static_cast<uint64_t>(v) * fu + soff));
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (u < nb) {
+            while (k0 + u >= row_end) flush();
+            const uint32_t m = (mask >> (4 * u)) & 15u;
+            if (m) {
+              if (m & 1u) acc[0] = __fadd_rn(acc[0], gv[u].x);
+              if (m & 2u) acc[1] = __fadd_rn(acc[1], gv[u].y);
+              if (m & 4u) acc[2] = __fadd_rn(acc[2], gv[u].z);
+              if (m & 8u) acc[3] = __fadd_rn(acc[3], gv[u].w);
+            }
+          }
+        }
+      }
+    }
+    while (row < rb) flush();
+  }
+#undef GM_MB_LOAD_ARG
+}
+
+// Hub rows (out-degree > the plan's threshold, up to ~20K entries on C4): one
+// CTA per (hub row, 32-column chunk). Per round its 16 (fp64: 8) warps fetch 16
+// consecutive entries each (lane = column): all argmax loads, then the
+// matching gradient loads, then each entry's contribution — the gradient or
+// an exact +0 — goes to a [256 (128) entries x 32 columns] shared tile. Warp 0 then
+// adds the tile's rows in entry order. Adding +0 never changes a sum that
+// started at +0 (it cannot become -0), so the tile's zeros are exact and each
+// column is one lane's sequential sum in the reference's order, while the
+// loads of 256 entries are in flight at once instead of one warp's batch.
+template <typename S>
+constexpr int hub_warps() { return sizeof(S) == 8 ? 8 : 16; }  // tile <= 48 KB static
+constexpr int kHubPer = 16;                                     // entries per warp per round
+template <typename S>
+__global__ void __launch_bounds__(hub_warps<S>() * 32, 2) maxbwd_hub_tile_kernel(
+    const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col, const int32_t* __restrict__ eid,
+    const int32_t* __restrict__ heavy, int64_t num_heavy, const int32_t* __restrict__ arg, const S* __restrict__ g,
+    int64_t f, S* __restrict__ dx) {
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int kHubRound = hub_warps<S>() * kHubPer;
+  __shared__ S tile[kHubRound][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t chunks = (f + 31) / 32;
+  const int r = heavy[blockIdx.x / chunks];
+  const int64_t cc = (blockIdx.x % chunks) * 32 + lane;
+  const bool valid = cc < f;
+  const int64_t c = valid ? cc : f - 1;  // lanes past f re-read the last column, never store
   const int64_t kb = rowptr[r], ke = rowptr[r + 1];
   S acc = S(0);
-  for (int64_t m0 = kb; m0 < ke; m0 += 32) {
-    const bool has = m0 + lane < ke;
+  for (int64_t base = kb; base < ke; base += kHubRound) {
+    const int64_t m0 = base + w * kHubPer;
+    const bool has = lane < kHubPer && m0 + lane < ke;
     const int32_t mv = has ? col[m0 + lane] : 0;
     const int32_t me = has ? eid[m0 + lane] : -2;
-    const int n = static_cast<int>(ke - m0 < 32 ? ke - m0 : 32);
-    for (int u0 = 0; u0 < n; u0 += kU) {
-      int32_t a[kU], ev[kU], vv[kU];
+    int32_t a[kHubPer];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        vv[u] = __shfl_sync(FULL, mv, u0 + u);
-        ev[u] = __shfl_sync(FULL, me, u0 + u);
-        a[u] = (valid && u0 + u < n) ? __ldg(arg + static_cast<int64_t>(vv[u]) * f + c) : -3;
-      }
-#pragma unroll
-      for (int u = 0; u < kU; ++u)
-        if (a[u] == ev[u]) acc = add_rn(acc, __ldg(g + static_cast<int64_t>(vv[u]) * f + c));
+    for (int u = 0; u < kHubPer; ++u) {
+      const int32_t vv = __shfl_sync(FULL, mv, u);
+      a[u] = m0 + u < ke ? __ldg(arg + static_cast<int64_t>(vv) * f + c) : -3;
     }
+    uint32_t hit = 0;
+#pragma unroll
+    for (int u = 0; u < kHubPer; ++u) hit |= static_cast<uint32_t>(a[u] == __shfl_sync(FULL, me, u)) << u;
+    S gv[kHubPer];
+#pragma unroll
+    for (int u = 0; u < kHubPer; ++u) {
+      const int32_t vv = __shfl_sync(FULL, mv, u);
+      gv[u] = ((hit >> u) & 1u) ? __ldg(g + static_cast<int64_t>(vv) * f + c) : S(0);
+    }
+#pragma unroll
+    for (int u = 0; u < kHubPer; ++u) tile[w * kHubPer + u][lane] = gv[u];
+    __syncthreads();
+    if (w == 0) {
+      const int n = static_cast<int>(ke - base < kHubRound ? ke - base : kHubRound);
+#pragma unroll 8
+      for (int i = 0; i < n; ++i) acc = add_rn(acc, tile[i][lane]);
+    }
+    __syncthreads();
   }
-  if (valid) dx[static_cast<int64_t>(r) * f + c] = acc;
+  if (w == 0 && valid) dx[static_cast<int64_t>(r) * f + c] = acc;
 }
 
 __global__ void widen_kernel(const int32_t* __restrict__ in, int64_t n, int64_t* __restrict__ out) {
@@ -232,8 +376,8 @@ gm_status launch_bwd(const gm_csr* v, const gm_spmm_plan* plan, const int32_t* a
     bool done = false;
     if constexpr (sizeof(S) == 4) {
       if (f % 4 == 0 && al % 16 == 0) {
-        maxbwd_light_kernel<S, 4><<<lgrid, 256, 0, st>>>(v->rowptr, v->col, v->perm, plan->light_windows,
-                                                         plan->num_light_windows, arg, g, f, dx);
+        maxbwd_flat_kernel<GM_MAXBWD_U><<<lgrid, 256, 0, st>>>(v->rowptr, v->col, v->perm, plan->light_windows,
+                                                               plan->num_light_windows, arg, g, f, dx);
         done = true;
       }
     }
@@ -248,9 +392,9 @@ gm_status launch_bwd(const gm_csr* v, const gm_spmm_plan* plan, const int32_t* a
   }
   if (plan->num_heavy > 0) {
     const int64_t warps = plan->num_heavy * ceil_div(f, 32);
-    maxbwd_hub_kernel<S><<<static_cast<unsigned>(ceil_div(warps * 32, 128)), 128, 0, st>>>(
+    maxbwd_hub_tile_kernel<S><<<static_cast<unsigned>(warps), hub_warps<S>() * 32, 0, st>>>(
         v->rowptr, v->col, v->perm, plan->heavy_rows, plan->num_heavy, arg, g, f, dx);
-    GM_CHECK_LAUNCH("maxbwd_hub_kernel");
+    GM_CHECK_LAUNCH("maxbwd_hub_tile_kernel");
   }
   return GM_OK;
 }
