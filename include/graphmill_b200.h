@@ -387,6 +387,45 @@ GM_API gm_status gm_spmm_accumulate(const gm_csr* csr, const gm_spmm_plan* plan,
                                     const int32_t* mean_deg, void* out, int32_t* arg_out,
                                     gm_stream_t stream);
 
+/* Epilogue extras of gm_spmm_ex (either part may be unused):
+ *  - fp32 carry for bf16 sums continued across source blocks (multi-GPU
+ *    overlap): carry_mode GM_CARRY_START starts the rows at 0 and stores fp32
+ *    rows to `carry`; GM_CARRY_CONTINUE seeds each row from `carry` and stores
+ *    it back; GM_CARRY_FINISH seeds from `carry` and stores the row rounded
+ *    (RNE) to `out` — one rounding per row, as on one GPU. bf16 sum/mean only.
+ *  - push: every finished output row is also stored, as `out` holds it, into
+ *    up to GM_MAX_PUSH peer buffers at global row push_row0 + local row (the
+ *    peers' [num_global_rows, f] input of the next layer, mapped into this
+ *    process: CUDA IPC / VMM over NVLink). push_mask[r] bit q selects peer q
+ *    for local row r (NULL: every peer). The caller orders the peers' later
+ *    reads after this call (e.g. a collective on `stream`). push_mask bit j
+ *    refers to push_dst[j]. Sum/mean layers only. */
+#define GM_MAX_PUSH 8
+typedef enum { GM_CARRY_NONE = 0, GM_CARRY_START = 1, GM_CARRY_CONTINUE = 2, GM_CARRY_FINISH = 3 } gm_carry_mode;
+typedef struct gm_spmm_epilogue {
+  float* carry;
+  int32_t carry_mode;
+  int32_t n_push;
+  void* push_dst[GM_MAX_PUSH];
+  int64_t push_row0;
+  const uint32_t* push_mask;
+} gm_spmm_epilogue;
+/* gm_spmm (accumulate = 0) / gm_spmm_accumulate (accumulate = 1: every row
+ * continues from out / arg_out, or from the carry for CONTINUE / FINISH) with
+ * an epilogue (NULL: none). */
+GM_API gm_status gm_spmm_ex(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype dtype, const void* x, int64_t f,
+                            const void* edge_weight, gm_reduce reduce, int32_t accumulate, const int32_t* mean_deg,
+                            const gm_spmm_epilogue* epilogue, void* out, int32_t* arg_out, gm_stream_t stream);
+
+/* Peer memory for the push epilogue: export a device pointer (CUDA IPC handle
+ * of its allocation + the pointer's offset, gm_ipc_handle_bytes() bytes), open
+ * a peer's export (NVLink P2P mapping; *base_out is what gm_ipc_close_handle
+ * takes). */
+GM_API size_t gm_ipc_handle_bytes(void);
+GM_API gm_status gm_ipc_get_handle(const void* dev_ptr, void* handle_out);
+GM_API gm_status gm_ipc_open_handle(const void* handle, void** dev_ptr_out, void** base_out);
+GM_API gm_status gm_ipc_close_handle(void* base);
+
 /* Multi-GPU SpMM over NCCL (north_star: dst-row partition + source exchange).
  * ncclComm_t is NCCL's own handle (struct ncclComm*); the library resolves
  * NCCL at run time (dlopen libnccl.so.2). Hosts without their own NCCL

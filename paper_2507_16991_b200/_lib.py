@@ -60,6 +60,21 @@ class gm_gcn_norm(C.Structure):
                 ("bias", C.c_void_p), ("relu", C.c_int)]
 
 
+GM_MAX_PUSH = 8
+GM_CARRY_NONE, GM_CARRY_START, GM_CARRY_CONTINUE, GM_CARRY_FINISH = 0, 1, 2, 3
+
+
+class gm_spmm_epilogue(C.Structure):
+    _fields_ = [
+        ("carry", C.c_void_p),
+        ("carry_mode", C.c_int32),
+        ("n_push", C.c_int32),
+        ("push_dst", C.c_void_p * GM_MAX_PUSH),
+        ("push_row0", C.c_int64),
+        ("push_mask", C.c_void_p),
+    ]
+
+
 GM_DIST_EXACT, GM_DIST_BLOCKED, GM_DIST_HALO = 0, 1, 2
 
 
@@ -103,6 +118,12 @@ SIGNATURES = {
                           C.POINTER(gm_gcn_norm), C.c_int, _P, _P, _P]),
     "gm_spmm_accumulate": (C.c_int, [C.POINTER(gm_csr), C.POINTER(gm_spmm_plan), C.c_int, _P, _I64, _P,
                                      C.c_int, _P, _P, _P, _P]),
+    "gm_spmm_ex": (C.c_int, [C.POINTER(gm_csr), C.POINTER(gm_spmm_plan), C.c_int, _P, _I64, _P, C.c_int,
+                             C.c_int32, _P, C.POINTER(gm_spmm_epilogue), _P, _P, _P]),
+    "gm_ipc_handle_bytes": (C.c_size_t, []),
+    "gm_ipc_get_handle": (C.c_int, [_P, _P]),
+    "gm_ipc_open_handle": (C.c_int, [_P, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
+    "gm_ipc_close_handle": (C.c_int, [_P]),
     "gm_mark_columns": (C.c_int, [C.POINTER(gm_csr), _P, _P]),
     "gm_gather_rows": (C.c_int, [C.c_int, _P, _I64, _P, _I64, _P, _P]),
     "gm_csr_split_blocks_workspace": (C.c_size_t, [_I64, C.c_int32]),

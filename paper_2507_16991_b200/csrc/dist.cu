@@ -139,8 +139,75 @@ GM_API gm_status gm_nccl_comm_destroy(ncclComm_t comm) {
   return GM_OK;
 }
 
+// ---- peer memory (the push epilogue's targets) -------------------------------
+// A CUDA IPC handle covers a whole allocation; the importer adds the offset of
+// the exported pointer inside it (caching allocators sub-allocate), found with
+// the driver's cuMemGetAddressRange (libcuda is resolved at run time).
+namespace {
+using cuMemGetAddressRange_t = int (*)(unsigned long long*, size_t*, unsigned long long);
+cuMemGetAddressRange_t address_range() {
+  static cuMemGetAddressRange_t fn = [] {
+    void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libcuda.so", RTLD_NOW | RTLD_GLOBAL);
+    return h ? reinterpret_cast<cuMemGetAddressRange_t>(dlsym(h, "cuMemGetAddressRange_v2")) : nullptr;
+  }();
+  return fn;
+}
+}  // namespace
+
+GM_API size_t gm_ipc_handle_bytes(void) { return sizeof(cudaIpcMemHandle_t) + sizeof(int64_t); }
+
+GM_API gm_status gm_ipc_get_handle(const void* dev_ptr, void* handle_out) {
+  GM_REQUIRE(dev_ptr && handle_out, GM_ERR_INVALID_ARGUMENT, "gm_ipc_get_handle: null argument");
+  auto range = address_range();
+  GM_REQUIRE(range, GM_ERR_CUDA, "gm_ipc_get_handle: cuMemGetAddressRange unavailable");
+  unsigned long long base = 0;
+  size_t size = 0;
+  GM_REQUIRE(range(&base, &size, reinterpret_cast<unsigned long long>(dev_ptr)) == 0, GM_ERR_CUDA,
+             "gm_ipc_get_handle: pointer is not device memory");
+  cudaIpcMemHandle_t h;
+  GM_TRY_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  const int64_t off = static_cast<int64_t>(reinterpret_cast<unsigned long long>(dev_ptr) - base);
+  memcpy(handle_out, &h, sizeof(h));
+  memcpy(static_cast<unsigned char*>(handle_out) + sizeof(h), &off, sizeof(off));
+  return GM_OK;
+}
+
+GM_API gm_status gm_ipc_open_handle(const void* handle, void** dev_ptr_out, void** base_out) {
+  GM_REQUIRE(handle && dev_ptr_out && base_out, GM_ERR_INVALID_ARGUMENT, "gm_ipc_open_handle: null argument");
+  cudaIpcMemHandle_t h;
+  int64_t off = 0;
+  memcpy(&h, handle, sizeof(h));
+  memcpy(&off, static_cast<const unsigned char*>(handle) + sizeof(h), sizeof(off));
+  void* base = nullptr;
+  GM_TRY_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  *base_out = base;
+  *dev_ptr_out = static_cast<unsigned char*>(base) + off;
+  return GM_OK;
+}
+
+GM_API gm_status gm_ipc_close_handle(void* base) {
+  GM_REQUIRE(base, GM_ERR_INVALID_ARGUMENT, "gm_ipc_close_handle: null base");
+  GM_TRY_CUDA(cudaIpcCloseMemHandle(base));
+  return GM_OK;
+}
+
+namespace {
+// bf16 sums in the blocked / halo modes carry fp32 rows between the blocks
+size_t carry_bytes(const gm_dist_layout* L, gm_dtype dtype, int64_t f) {
+  if (dtype != GM_BF16 || L->mode == GM_DIST_EXACT || !L->blocks) return 0;
+  return align_up(static_cast<size_t>(L->blocks[0].num_rows) * static_cast<size_t>(f) * sizeof(float), 256);
+}
+size_t exchange_bytes(const gm_dist_layout* L, gm_dtype dtype, int64_t f);
+}  // namespace
+
 GM_API size_t gm_dist_spmm_workspace(const gm_dist_layout* L, gm_dtype dtype, int64_t f) {
   if (!L || f < 0 || L->world < 1) return 0;
+  return exchange_bytes(L, dtype, f) + carry_bytes(L, dtype, f);
+}
+
+namespace {
+size_t exchange_bytes(const gm_dist_layout* L, gm_dtype dtype, int64_t f) {
   const size_t row = static_cast<size_t>(f) * esize(dtype);
   if (L->mode == GM_DIST_EXACT) return align_up(static_cast<size_t>(L->world) * L->shard_rows * row, 256);
   if (L->mode == GM_DIST_BLOCKED)
@@ -153,6 +220,7 @@ GM_API size_t gm_dist_spmm_workspace(const gm_dist_layout* L, gm_dtype dtype, in
   }
   return align_up(static_cast<size_t>(send) * row, 256) + align_up(static_cast<size_t>(recv) * row, 256);
 }
+}  // namespace
 
 GM_API gm_status gm_dist_spmm(const gm_dist_layout* L, gm_dtype dtype, const void* x_shard, int64_t f,
                               gm_reduce reduce, void* out, int32_t* arg_out, void* workspace, size_t workspace_bytes,
@@ -189,6 +257,20 @@ GM_API gm_status gm_dist_spmm(const gm_dist_layout* L, gm_dtype dtype, const voi
   }
 
   const gm_reduce first = reduce == GM_MEAN ? GM_SUM : reduce;
+  // bf16 sum/mean: fp32 running rows in the workspace tail, one rounding at the end
+  gm_spmm_epilogue ep{};
+  const bool carry = carry_bytes(L, dtype, f) > 0 && !maxmin;
+  if (carry) ep.carry = reinterpret_cast<float*>(ws + exchange_bytes(L, dtype, f));
+  auto run_block = [&](int b, const void* xb, gm_reduce k, bool cont, bool last) -> gm_status {
+    if (carry) {
+      ep.carry_mode = !cont ? GM_CARRY_START : last ? GM_CARRY_FINISH : GM_CARRY_CONTINUE;
+      return gm_spmm_ex(&L->blocks[b], &L->plans[b], dtype, xb, f, nullptr, k, cont ? 1 : 0,
+                        k == GM_MEAN ? L->mean_deg : nullptr, &ep, out, nullptr, stream);
+    }
+    if (!cont) return gm_spmm(&L->blocks[b], &L->plans[b], dtype, xb, f, nullptr, nullptr, k, out, arg_out, stream);
+    return gm_spmm_accumulate(&L->blocks[b], &L->plans[b], dtype, xb, f, nullptr, k,
+                              k == GM_MEAN ? L->mean_deg : nullptr, out, arg_out, stream);
+  };
   if (L->mode == GM_DIST_BLOCKED) {
     GM_REQUIRE(L->chunks >= 1 && L->chunk_rows >= 1, GM_ERR_INVALID_ARGUMENT, "gm_dist_spmm: bad chunk layout");
     const size_t chunk_bytes = align_up(static_cast<size_t>(L->world) * L->chunk_rows * row, 256);
@@ -198,14 +280,13 @@ GM_API gm_status gm_dist_spmm(const gm_dist_layout* L, gm_dtype dtype, const voi
                                     ws + c * chunk_bytes, static_cast<size_t>(L->chunk_rows) * row, ncclUint8, comm, cst));
       GM_TRY_CUDA(cudaEventRecord(ev[2 + c], cst));
     }
-    s = gm_spmm(&L->blocks[0], &L->plans[0], dtype, x_shard, f, nullptr, nullptr, first, out, arg_out, stream);
+    s = run_block(0, x_shard, first, false, false);
     if (s != GM_OK) return s;
     for (int c = 0; c < L->chunks; ++c) {
       GM_TRY_CUDA(cudaStreamWaitEvent(st, ev[2 + c], 0));
       const bool last = c == L->chunks - 1;
       const gm_reduce k = (last || reduce != GM_MEAN) ? reduce : GM_SUM;
-      s = gm_spmm_accumulate(&L->blocks[1 + c], &L->plans[1 + c], dtype, ws + c * chunk_bytes, f, nullptr, k,
-                             k == GM_MEAN ? L->mean_deg : nullptr, out, arg_out, stream);
+      s = run_block(1 + c, ws + c * chunk_bytes, k, true, last);
       if (s != GM_OK) return s;
     }
     return GM_OK;
@@ -238,11 +319,10 @@ GM_API gm_status gm_dist_spmm(const gm_dist_layout* L, gm_dtype dtype, const voi
   }
   GM_TRY_NCCL(nccl().group_end());
   GM_TRY_CUDA(cudaEventRecord(ev[1], cst));
-  s = gm_spmm(&L->blocks[0], &L->plans[0], dtype, x_shard, f, nullptr, nullptr, first, out, arg_out, stream);
+  s = run_block(0, x_shard, first, false, false);
   if (s != GM_OK) return s;
   GM_TRY_CUDA(cudaStreamWaitEvent(st, ev[1], 0));
-  return gm_spmm_accumulate(&L->blocks[1], &L->plans[1], dtype, recv_buf, f, nullptr, reduce,
-                            reduce == GM_MEAN ? L->mean_deg : nullptr, out, arg_out, stream);
+  return run_block(1, recv_buf, reduce, true, true);
 }
 
 }  // extern "C"

@@ -295,7 +295,8 @@ static bool narrow_rows_8b() {
 static gm_status spmm_impl(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype dtype,
                            const void* x, int64_t f, const void* edge_weight,
                            const gm_gcn_norm* gcn, gm_reduce reduce, void* out, int32_t* arg_out,
-                           int accum, const int32_t* mean_deg, gm_stream_t stream) {
+                           int accum, const int32_t* mean_deg, gm_stream_t stream,
+                           const gm_spmm_epilogue* ep = nullptr) {
   GM_REQUIRE(csr && plan, GM_ERR_INVALID_ARGUMENT, "gm_spmm: null csr/plan");
   GM_REQUIRE(f >= 0, GM_ERR_INVALID_ARGUMENT, "gm_spmm: negative feature width");
   GM_REQUIRE(!(edge_weight && gcn), GM_ERR_INVALID_ARGUMENT,
@@ -311,12 +312,27 @@ static gm_status spmm_impl(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype
              "gm_spmm: gcn norm needs both degree arrays");
   GM_REQUIRE(!gcn || !(gcn->bias || gcn->relu) || reduce == GM_SUM || reduce == GM_MEAN, GM_ERR_INVALID_ARGUMENT,
              "gm_spmm: the bias/relu epilogue applies to sum/mean");
+  const bool carry = ep && ep->carry_mode != GM_CARRY_NONE;
+  const bool push = ep && ep->n_push > 0;
+  GM_REQUIRE(!carry || (dtype == GM_BF16 && !maxmin && ep->carry && ep->carry_mode <= GM_CARRY_FINISH),
+             GM_ERR_INVALID_ARGUMENT, "gm_spmm_ex: the fp32 carry applies to bf16 sum/mean");
+  GM_REQUIRE(!carry || (ep->carry_mode == GM_CARRY_START) == (accum == 0), GM_ERR_INVALID_ARGUMENT,
+             "gm_spmm_ex: GM_CARRY_START starts the rows (accumulate = 0); CONTINUE/FINISH continue them");
+  GM_REQUIRE(!push || (ep->n_push <= GM_MAX_PUSH && !maxmin && !gcn), GM_ERR_INVALID_ARGUMENT,
+             "gm_spmm_ex: push carries sum/mean layers to <= GM_MAX_PUSH peers (no fused GCN term)");
+  GM_REQUIRE(!(carry && push && ep->carry_mode != GM_CARRY_FINISH), GM_ERR_INVALID_ARGUMENT,
+             "gm_spmm_ex: rows are pushed by the block that finishes them");
   if (csr->num_rows == 0 || f == 0) return GM_OK;
   GM_REQUIRE(x && out, GM_ERR_INVALID_ARGUMENT, "gm_spmm: null x/out");
+  if (push)
+    for (int q = 0; q < ep->n_push; ++q)
+      GM_REQUIRE(ep->push_dst[q] != nullptr, GM_ERR_INVALID_ARGUMENT, "gm_spmm_ex: null push target");
 
   const size_t esz = dtype == GM_F64 ? 8 : dtype == GM_F32 ? 4 : 2;
   const size_t rowbytes = static_cast<size_t>(f) * esz;
-  const uintptr_t align = reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(out);
+  uintptr_t align = reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(out);
+  if (push)
+    for (int q = 0; q < ep->n_push; ++q) align |= reinterpret_cast<uintptr_t>(ep->push_dst[q]);
   int vb = 16;
   while (vb > static_cast<int>(esz) && (rowbytes % vb != 0 || align % vb != 0)) vb >>= 1;
   GM_REQUIRE(rowbytes % vb == 0 && align % vb == 0, GM_ERR_INVALID_ARGUMENT,
@@ -343,6 +359,16 @@ static gm_status spmm_impl(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype
   p.is_min = reduce == GM_MIN;
   p.accum = accum;
   p.mean_deg = mean_deg;
+  if (carry) {
+    p.carry = ep->carry;
+    p.carry_out = ep->carry_mode == GM_CARRY_FINISH;
+  }
+  if (push) {
+    p.n_push = ep->n_push;
+    for (int q = 0; q < ep->n_push; ++q) p.push_dst[q] = ep->push_dst[q];
+    p.push_row0 = ep->push_row0;
+    p.push_mask = ep->push_mask;
+  }
   p.num_rows = csr->num_rows;
   p.f = f;
   p.win_row = plan->win_row;
@@ -391,6 +417,22 @@ GM_API gm_status gm_spmm(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype d
                          const gm_gcn_norm* gcn, gm_reduce reduce, void* out, int32_t* arg_out,
                          gm_stream_t stream) {
   return spmm_impl(csr, plan, dtype, x, f, edge_weight, gcn, reduce, out, arg_out, 0, nullptr, stream);
+}
+
+GM_API gm_status gm_spmm_ex(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype dtype, const void* x, int64_t f,
+                            const void* edge_weight, gm_reduce reduce, int32_t accumulate, const int32_t* mean_deg,
+                            const gm_spmm_epilogue* epilogue, void* out, int32_t* arg_out, gm_stream_t stream) {
+  const bool maxmin = reduce == GM_MAX || reduce == GM_MIN;
+  if (accumulate) {
+    GM_REQUIRE(!maxmin || arg_out, GM_ERR_INVALID_ARGUMENT,
+               "gm_spmm_ex: max/min continuation needs the running arg_out (ties break on COO id)");
+    GM_REQUIRE(reduce != GM_MEAN || mean_deg, GM_ERR_INVALID_ARGUMENT,
+               "gm_spmm_ex: a continued mean needs the full-row degrees");
+    GM_REQUIRE(dtype != GM_BF16 || maxmin || (epilogue && epilogue->carry_mode != GM_CARRY_NONE),
+               GM_ERR_INVALID_ARGUMENT, "gm_spmm_ex: continued bf16 sum/mean needs the fp32 carry");
+  }
+  return spmm_impl(csr, plan, dtype, x, f, edge_weight, nullptr, reduce, out, arg_out, accumulate ? 1 : 0,
+                   accumulate ? mean_deg : nullptr, stream, epilogue);
 }
 
 GM_API gm_status gm_spmm_accumulate(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype dtype,

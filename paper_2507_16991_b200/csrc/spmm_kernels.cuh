@@ -68,7 +68,59 @@ struct SpmmArgs {
   int accum;
   const int32_t* mean_deg;       // MEAN denominators per row (NULL = row length)
   int stream_x;                  // X exceeds the L2 budget: gathers carry eviction policies
+  // epilogue (gm_spmm_ex): fp32 carry of bf16 block sums, push to peer buffers
+  float* carry;                  // non-NULL: bf16 sum/mean rows seed from / store to fp32 rows here
+  int carry_out;                 // 1: this block finishes the rows (store rounded to out)
+  int n_push;
+  void* push_dst[GM_MAX_PUSH];
+  int64_t push_row0;
+  const uint32_t* push_mask;
 };
+
+// Row-slice store of the epilogue: fp32 carry (bf16 blocks that are not the
+// last), else the narrowed vector to out plus one plain store per selected
+// peer (NVLink P2P when the peer buffer is mapped from another GPU).
+// (max/min layers take neither: their paths compile to the plain store.)
+template <typename T, typename VecT, bool EPI = true>
+__device__ __forceinline__ void epi_store(const SpmmArgs& p, T* out, uint64_t elem, int64_t row,
+                                          const typename VecT::A* v) {
+  constexpr int V = VecT::V;
+  if constexpr (!EPI) {
+    VecT::store_global(out + elem, v);
+    return;
+  }
+  if constexpr (sizeof(T) == 2) {
+    if (p.carry != nullptr && !p.carry_out) {
+      float* c = p.carry + elem;
+#pragma unroll
+      for (int e = 0; e < V; ++e) c[e] = v[e];
+      return;
+    }
+  }
+  VecT::store_global(out + elem, v);
+  if (p.n_push) {
+    const typename VecT::R r = VecT::pack(v);
+    const uint32_t m = p.push_mask ? p.push_mask[row] : 0xffffffffu;
+    const uint64_t gelem = elem + static_cast<uint64_t>(p.push_row0) * static_cast<uint64_t>(p.f);
+#pragma unroll
+    for (int q = 0; q < GM_MAX_PUSH; ++q)  // static indices: the targets stay in the parameter bank
+      if (q < p.n_push && ((m >> q) & 1u))
+        *reinterpret_cast<typename VecT::R*>(static_cast<T*>(p.push_dst[q]) + gelem) = r;
+  }
+}
+// Seed V accumulators of a bf16 row slice from the fp32 carry; false: no carry.
+template <typename T, typename A, int V>
+__device__ __forceinline__ bool carry_seed(const SpmmArgs& p, uint64_t elem, A* v) {
+  if constexpr (sizeof(T) == 2) {
+    if (p.carry != nullptr) {
+      const float* c = p.carry + elem;
+#pragma unroll
+      for (int e = 0; e < V; ++e) v[e] = c[e];
+      return true;
+    }
+  }
+  return false;
+}
 
 // L2 eviction-priority policies (createpolicy; PTX ISA "Cache eviction priority hints").
 __device__ __forceinline__ uint64_t policy_evict_last() {
@@ -441,9 +493,12 @@ __global__ void __launch_bounds__(256) spmm_light_kernel(const SpmmArgs p) {
     if (p.accum) {
 #pragma unroll
       for (int j = 0; j < NV; ++j)
-        if (valid[j])
-          seeded = acc.template seed<T, VecT>(j, out + static_cast<int64_t>(r) * p.f + slot[j] * V,
-                                             MAXMIN ? p.arg + static_cast<int64_t>(r) * p.f + slot[j] * V : nullptr);
+        if (valid[j]) {
+          const uint64_t el = static_cast<uint64_t>(r) * p.f + slot[j] * V;
+          if (!MAXMIN && carry_seed<T, A, V>(p, el, acc.v[j])) seeded = true;
+          else
+            seeded = acc.template seed<T, VecT>(j, out + el, MAXMIN ? p.arg + el : nullptr);
+        }
     }
     const bool lex = p.accum != 0;
     const int32_t dd = gcn ? p.gdeg_dst[r] : 0;
@@ -511,17 +566,17 @@ __global__ void __launch_bounds__(256) spmm_light_kernel(const SpmmArgs p) {
           if (valid[j]) layer_epilogue<A>(acc.v[j], V, p, slot[j] * V);
       }
     }
-    T* orow = out + static_cast<int64_t>(r) * p.f;
 #pragma unroll
     for (int j = 0; j < NV; ++j)
       if (valid[j]) {
-        VecT::store_global(orow + slot[j] * V, acc.v[j]);
+        epi_store<T, VecT, !MAXMIN>(p, out, static_cast<uint64_t>(r) * p.f + slot[j] * V, r, acc.v[j]);
         if (want_arg) {
           int32_t* arow = p.arg + static_cast<int64_t>(r) * p.f + slot[j] * V;
           store_arg<V>(arow, acc.a[j]);
         }
       }
   }
+  if (p.n_push) __threadfence_system();
 }
 
 
@@ -620,8 +675,10 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 8 || (SCALED && (MODE >= 2 
       bool have = false;
 #pragma unroll
       for (int j = 0; j < NV; ++j)
-        if (valid[j])
-          have = acc.template seed<T, VecT>(j, out + ob + soff[j], MAXMIN ? p.arg + ob + soff[j] : nullptr);
+        if (valid[j]) {
+          if (!MAXMIN && carry_seed<T, A, V>(p, ob + soff[j], acc.v[j])) have = true;
+          else have = acc.template seed<T, VecT>(j, out + ob + soff[j], MAXMIN ? p.arg + ob + soff[j] : nullptr);
+        }
       first = !have;
     }
   };
@@ -642,7 +699,7 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 8 || (SCALED && (MODE >= 2 
 #pragma unroll
     for (int j = 0; j < NV; ++j)
       if (valid[j]) {
-        VecT::store_global(out + obase + soff[j], acc.v[j]);
+        epi_store<T, VecT, !MAXMIN>(p, out, obase + soff[j], row, acc.v[j]);
         if (want_arg) {
           int32_t* arow = p.arg + obase + soff[j];
           store_arg<V>(arow, acc.a[j]);
@@ -808,6 +865,9 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 8 || (SCALED && (MODE >= 2 
     }
   }
   while (row < rb) flush();
+  // pushed rows must be visible to the peers before the caller's collective
+  // releases their next read
+  if (!MAXMIN && p.n_push) __threadfence_system();
 }
 
 // ---------------------------------------------------------------------------
@@ -908,9 +968,14 @@ __global__ void __launch_bounds__(kHeavyThreads) spmm_heavy_kernel(const SpmmArg
 #pragma unroll
     for (int m = 0; m < MH; ++m) {
       const int s = t + m * kHeavyThreads;
-      if (s < nslots)
-        seeded = acc.template seed<T, VecT>(m, orow0 + (p.slot_base + s) * V,
-                                            MAXMIN ? p.arg + static_cast<int64_t>(r) * p.f + (p.slot_base + s) * V : nullptr);
+      if (s < nslots) {
+        const uint64_t el = static_cast<uint64_t>(r) * p.f + (p.slot_base + s) * V;
+        if (!MAXMIN && carry_seed<T, A, V>(p, el, acc.v[m])) seeded = true;
+        else
+          seeded = acc.template seed<T, VecT>(m, orow0 + (p.slot_base + s) * V,
+                                              MAXMIN ? p.arg + static_cast<int64_t>(r) * p.f + (p.slot_base + s) * V
+                                                     : nullptr);
+      }
     }
   }
   const bool lex = MAXMIN && p.accum != 0;
@@ -981,18 +1046,19 @@ __global__ void __launch_bounds__(kHeavyThreads) spmm_heavy_kernel(const SpmmArg
       if (s < nslots) layer_epilogue<A>(acc.v[m], V, p, (p.slot_base + s) * V);
     }
   }
-  T* orow = static_cast<T*>(p.out) + static_cast<int64_t>(r) * p.f;
 #pragma unroll
   for (int m = 0; m < MH; ++m) {
     const int s = t + m * kHeavyThreads;
     if (s < nslots) {
-      VecT::store_global(orow + (p.slot_base + s) * V, acc.v[m]);
+      epi_store<T, VecT, !MAXMIN>(p, static_cast<T*>(p.out),
+                                  static_cast<uint64_t>(r) * p.f + (p.slot_base + s) * V, r, acc.v[m]);
       if (want_arg) {
         int32_t* arow = p.arg + static_cast<int64_t>(r) * p.f + (p.slot_base + s) * V;
         store_arg<V>(arow, acc.a[m]);
       }
     }
   }
+  if (p.n_push) __threadfence_system();
 }
 
 // ---------------------------------------------------------------------------
@@ -1153,14 +1219,18 @@ __global__ void __launch_bounds__(64) spmm_hub_kernel(const SpmmArgs p) {
     a[i] = -1;
   }
   if (p.accum && lane_valid) {
-    T tmp[LE];
-    memcpy(tmp, orow + e0, LB);
+    if (!MAXMIN && carry_seed<T, A, LE>(p, static_cast<uint64_t>(r) * p.f + e0, v)) {
+      first = false;
+    } else {
+      T tmp[LE];
+      memcpy(tmp, orow + e0, LB);
 #pragma unroll
-    for (int i = 0; i < LE; ++i) {
-      v[i] = widen(tmp[i]);
-      if (MAXMIN) a[i] = p.arg[static_cast<int64_t>(r) * p.f + e0 + i];
+      for (int i = 0; i < LE; ++i) {
+        v[i] = widen(tmp[i]);
+        if (MAXMIN) a[i] = p.arg[static_cast<int64_t>(r) * p.f + e0 + i];
+      }
+      first = MAXMIN ? a[0] == -1 : false;
     }
-    first = MAXMIN ? a[0] == -1 : false;
   }
   using RawL = typename HL::R;
   // one edge into the running value(s); LEX: seeded blocks break ties on COO id
@@ -1242,10 +1312,25 @@ __global__ void __launch_bounds__(64) spmm_hub_kernel(const SpmmArgs p) {
     const int64_t n_valid = p.f - e0;
     layer_epilogue<A>(v, static_cast<int>(n_valid < LE ? n_valid : LE), p, e0);
   }
+  if constexpr (sizeof(T) == 2 && !MAXMIN) {
+    if (p.carry != nullptr && !p.carry_out) {
+#pragma unroll
+      for (int j = 0; j < LE; ++j) p.carry[static_cast<int64_t>(r) * p.f + e0 + j] = v[j];
+      return;
+    }
+  }
   T tmp[LE];
 #pragma unroll
   for (int j = 0; j < LE; ++j) tmp[j] = narrow<T, A>(v[j]);
   memcpy(orow + e0, tmp, LB);
+  if (!MAXMIN && p.n_push) {
+    const uint32_t m = p.push_mask ? p.push_mask[r] : 0xffffffffu;
+    const int64_t ge = (p.push_row0 + r) * p.f + e0;
+#pragma unroll
+    for (int q = 0; q < GM_MAX_PUSH; ++q)
+      if (q < p.n_push && ((m >> q) & 1u)) memcpy(static_cast<T*>(p.push_dst[q]) + ge, tmp, LB);
+    __threadfence_system();
+  }
   if (want_arg) {
 #pragma unroll
     for (int j = 0; j < LE; ++j) p.arg[static_cast<int64_t>(r) * p.f + e0 + j] = a[j];

@@ -128,6 +128,14 @@ struct Vec {
       for (int i = 0; i < V; ++i) out[i] = widen(tmp[i]);
     }
   }
+  __device__ static __forceinline__ R pack(const A* vals) {
+    T tmp[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) tmp[i] = narrow<T, A>(vals[i]);
+    R r;
+    memcpy(&r, tmp, VB);
+    return r;
+  }
   __device__ static __forceinline__ void store_global(T* p, const A* vals) {
     T tmp[V];
 #pragma unroll

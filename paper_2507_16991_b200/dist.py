@@ -91,6 +91,36 @@ class _Done:
         return None
 
 
+def _block_spmm(v, x, f, kind, out, arg, accumulate, mean_deg=None, carry=None, carry_mode=0, what="gm_spmm"):
+    """One source block of a rank's rows: a fresh gm_spmm, a seeded
+    gm_spmm_accumulate, or (bf16 sum/mean) gm_spmm_ex with the fp32 carry."""
+    from .graphmill import _DT, _p, _stream
+    lib = L.lib()
+    cs = v.c_struct()
+    plan = v.plan(f * x.element_size())
+    dt = _DT[x.dtype]
+    md = _p(mean_deg) if (mean_deg is not None and kind == L.GM_MEAN) else None
+    if carry is not None:
+        ep = L.gm_spmm_epilogue()
+        ep.carry = carry.data_ptr()
+        ep.carry_mode = carry_mode
+        L.check(lib.gm_spmm_ex(C.byref(cs), C.byref(plan), dt, _p(x), f, None, kind, 1 if accumulate else 0, md,
+                               C.byref(ep), _p(out), None, _stream()), what)
+    elif accumulate:
+        L.check(lib.gm_spmm_accumulate(C.byref(cs), C.byref(plan), dt, _p(x), f, None, kind, md, _p(out),
+                                       _p(arg) if arg is not None else None, _stream()), what)
+    else:
+        L.check(lib.gm_spmm(C.byref(cs), C.byref(plan), dt, _p(x), f, None, None, kind, _p(out),
+                            _p(arg) if arg is not None else None, _stream()), what)
+
+
+def _carry_buffer(cache, n, f, device):
+    key = ("carry", n, f)
+    if key not in cache:
+        cache[key] = torch.empty(n, f, dtype=torch.float32, device=device)
+    return cache[key]
+
+
 class BlockedSpmm:
     """One rank's exchange-overlapped SpMM over its destination rows.
 
@@ -100,8 +130,9 @@ class BlockedSpmm:
     (default: async NCCL all_gather_into_tensor). Results: MAX/MIN values and
     argmax equal the single-GPU ones bit-for-bit (NaN-free inputs); SUM/MEAN
     continue each row's sum across blocks (fp32-tolerance, one re-association
-    per block boundary). For bit-identical sums use exact mode
-    (allgather_features + one gm_spmm)."""
+    per block boundary). bf16 SUM/MEAN carry the running rows in fp32
+    (gm_spmm_ex GM_CARRY_*) and round once, in the last block, as one GPU does.
+    For bit-identical sums use exact mode (allgather_features + one gm_spmm)."""
 
     def __init__(self, rows, num_src_rows: int, rank: int, world: int, chunks: int = 4,
                  allgather=None, group=None):
@@ -153,8 +184,7 @@ class BlockedSpmm:
         f = x_shard.shape[1]
         n = self.blocks[0].num_rows()
         maxmin = reduce in ("max", "min")
-        if x_shard.dtype == torch.bfloat16 and not maxmin:
-            raise ValueError("BlockedSpmm: bf16 sum/mean rounds between blocks; use exact mode")
+        carry = x_shard.dtype == torch.bfloat16 and not maxmin
         if out is None:
             out = torch.empty(n, f, dtype=x_shard.dtype, device=x_shard.device)
         if maxmin and arg is None:
@@ -163,23 +193,18 @@ class BlockedSpmm:
         # every chunk's exchange is in flight before the local block starts
         works = [self.allgather(bufs[c], x_shard[c * self.cs:(c + 1) * self.cs]) or _Done()
                  for c in range(self.chunks)]
-        lib = L.lib()
-        dt = _DT[x_shard.dtype]
         first_kind = L.GM_SUM if reduce == "mean" else _KIND[reduce]
-        v = self.blocks[0]
-        cs = v.c_struct()
-        rb = f * x_shard.element_size()
-        L.check(lib.gm_spmm(C.byref(cs), C.byref(v.plan(rb)), dt, _p(x_shard), f, None, None, first_kind,
-                            _p(out), _p(arg) if maxmin else None, _stream()), "gm_spmm (local block)")
+        # bf16 sums: fp32 running rows, rounded once in the last block (as one GPU)
+        acc = _carry_buffer(self._bufs, n, f, x_shard.device) if carry else None
+        _block_spmm(self.blocks[0], x_shard, f, first_kind, out, arg if maxmin else None, False,
+                    carry=acc, carry_mode=L.GM_CARRY_START, what="gm_spmm (local block)")
         for c in range(self.chunks):
             works[c].wait()
-            v = self.blocks[1 + c]
             last = c == self.chunks - 1
             kind = _KIND[reduce] if (last or reduce != "mean") else L.GM_SUM
-            cs = v.c_struct()
-            L.check(lib.gm_spmm_accumulate(C.byref(cs), C.byref(v.plan(rb)), dt, _p(bufs[c]), f, None, kind,
-                                           _p(self.mean_deg) if kind == L.GM_MEAN else None, _p(out),
-                                           _p(arg) if maxmin else None, _stream()), "gm_spmm_accumulate")
+            _block_spmm(self.blocks[1 + c], bufs[c], f, kind, out, arg if maxmin else None, True,
+                        mean_deg=self.mean_deg, carry=acc,
+                        carry_mode=L.GM_CARRY_FINISH if last else L.GM_CARRY_CONTINUE, what="gm_spmm (block)")
         return (out, arg) if maxmin else out
 
 
@@ -293,8 +318,7 @@ class HaloSpmm:
         f = x_shard.shape[1]
         n = self.blocks[0].num_rows()
         maxmin = reduce in ("max", "min")
-        if x_shard.dtype == torch.bfloat16 and not maxmin:
-            raise ValueError("HaloSpmm: bf16 sum/mean rounds between blocks; use exact mode")
+        carry = x_shard.dtype == torch.bfloat16 and not maxmin
         if out is None:
             out = torch.empty(n, f, dtype=x_shard.dtype, device=x_shard.device)
         if maxmin and arg is None:
@@ -311,20 +335,109 @@ class HaloSpmm:
                                    _stream()), "gm_gather_rows")
         work = self.alltoall(recv_buf[: self.halo_rows()], send_buf[: self.send_idx.numel()], self.recv_splits,
                              self.send_splits) or _Done()
-        rb = f * x_shard.element_size()
-        v = self.blocks[0]
-        cs = v.c_struct()
         first_kind = L.GM_SUM if reduce == "mean" else _KIND[reduce]
-        L.check(lib.gm_spmm(C.byref(cs), C.byref(v.plan(rb)), dt, _p(x_shard), f, None, None, first_kind,
-                            _p(out), _p(arg) if maxmin else None, _stream()), "gm_spmm (own shard)")
+        acc = _carry_buffer(self._bufs, n, f, x_shard.device) if carry else None
+        _block_spmm(self.blocks[0], x_shard, f, first_kind, out, arg if maxmin else None, False,
+                    carry=acc, carry_mode=L.GM_CARRY_START, what="gm_spmm (own shard)")
         work.wait()
-        v = self.blocks[1]
-        cs = v.c_struct()
-        kind = _KIND[reduce]
-        L.check(lib.gm_spmm_accumulate(C.byref(cs), C.byref(v.plan(rb)), dt, _p(recv_buf), f, None, kind,
-                                       _p(self.mean_deg) if kind == L.GM_MEAN else None, _p(out),
-                                       _p(arg) if maxmin else None, _stream()), "gm_spmm_accumulate (halo)")
+        _block_spmm(self.blocks[1], recv_buf, f, _KIND[reduce], out, arg if maxmin else None, True,
+                    mean_deg=self.mean_deg, carry=acc, carry_mode=L.GM_CARRY_FINISH, what="gm_spmm (halo)")
         return (out, arg) if maxmin else out
+
+
+# ---------------------------------------------------------------------------
+# Push mode: the exchange of layer l+1 fused into the SpMM of layer l. Every
+# rank keeps a replica of the layer input X ([N, F]); the SpMM over its
+# destination rows reads the local replica only and its epilogue stores each
+# finished output row both into its own next-layer replica and, over NVLink
+# P2P, into every peer's replica that references the row (gm_spmm_ex push).
+# No collective moves features: a one-element all_reduce after the kernel
+# orders the peers' next reads. Rows are computed by the single-GPU kernel
+# over the whole local X, so results are bit-identical to one GPU.
+# ---------------------------------------------------------------------------
+def push_masks(rows, num_src_rows: int, r0: int, r1: int, rank: int, world: int, gather=None, group=None):
+    """Per local row v in [r0, r1): bit j set iff the j-th peer (ranks in
+    order, this rank skipped) references source v. gather(t) -> [world, N] stack of every rank's referenced-column
+    bitmap (default: all_gather over `group`). uint32 [r1 - r0] on the device."""
+    from .graphmill import _p, _stream
+    mark = torch.empty(num_src_rows, dtype=torch.uint8, device=rows.rowptr.device)
+    cs = rows.c_struct()
+    L.check(L.lib().gm_mark_columns(C.byref(cs), _p(mark), _stream()), "gm_mark_columns")
+    if gather is None:
+        parts = [torch.empty_like(mark) for _ in range(world)]
+        dist.all_gather(parts, mark, group=group)
+        allm = torch.stack(parts)
+    else:
+        allm = gather(mark)
+    bits = (allm[:, r0:r1].to(torch.int64) != 0).to(torch.int64)
+    # bit j = the j-th peer in rank order without this rank (PushSpmm's push_dst[j])
+    w = torch.tensor([0 if q == rank else 1 << (q if q < rank else q - 1) for q in range(world)],
+                     dtype=torch.int64, device=bits.device).view(world, 1)
+    return (bits * w).sum(0).to(torch.int32).contiguous()
+
+
+def open_peer_buffers(t: torch.Tensor, group=None):
+    """Map every peer's `t` (same shape on every rank) into this process over
+    CUDA IPC (NVLink P2P). Returns [world] device pointers (own rank: t's
+    pointer) and the opened bases to close with close_peer_buffers."""
+    lib = L.lib()
+    nb = lib.gm_ipc_handle_bytes()
+    h = (C.c_ubyte * nb)()
+    L.check(lib.gm_ipc_get_handle(C.c_void_p(t.data_ptr()), h), "gm_ipc_get_handle")
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    handles = [None] * world
+    dist.all_gather_object(handles, bytes(h), group=group)
+    ptrs, bases = [], []
+    for q in range(world):
+        if q == rank:
+            ptrs.append(t.data_ptr())
+            continue
+        buf = (C.c_ubyte * nb).from_buffer_copy(handles[q])
+        p, b = C.c_void_p(), C.c_void_p()
+        L.check(lib.gm_ipc_open_handle(buf, C.byref(p), C.byref(b)), "gm_ipc_open_handle")
+        ptrs.append(p.value)
+        bases.append(b.value)
+    return ptrs, bases
+
+
+def close_peer_buffers(bases):
+    for b in bases:
+        L.check(L.lib().gm_ipc_close_handle(C.c_void_p(b)), "gm_ipc_close_handle")
+
+
+class PushSpmm:
+    """One rank's push-mode SpMM over its destination rows [r0, r1).
+
+    rows: the rank's CSC row slice (global source ids); mask: push_masks(...)
+    or None (push every row to every peer). __call__(x, out_next, peer_ptrs)
+    reads x (this rank's full replica of the layer input), writes the rows to
+    out_next[r0:r1] and pushes them into peer_ptrs[q] ([N, F] replicas of the
+    next layer's input on the other ranks, peer_ptrs[rank] ignored)."""
+
+    def __init__(self, rows, r0: int, r1: int, rank: int, world: int, mask: Optional[torch.Tensor] = None):
+        assert world - 1 <= L.GM_MAX_PUSH, "push mode targets at most GM_MAX_PUSH peers"
+        self.rows, self.r0, self.r1, self.rank, self.world, self.mask = rows, r0, r1, rank, world, mask
+
+    def __call__(self, x: torch.Tensor, out_next: torch.Tensor, peer_ptrs, reduce: str = "sum"):
+        from .graphmill import _DT, _KIND, _p, _stream
+        assert reduce in ("sum", "mean"), "push mode carries sum/mean layers"
+        f = x.shape[1]
+        lib = L.lib()
+        ep = L.gm_spmm_epilogue()
+        n = 0
+        for q in range(self.world):
+            if q != self.rank:
+                ep.push_dst[n] = peer_ptrs[q]
+                n += 1
+        ep.n_push = n
+        ep.push_row0 = self.r0
+        ep.push_mask = self.mask.data_ptr() if self.mask is not None else None
+        cs = self.rows.c_struct()
+        plan = self.rows.plan(f * x.element_size())
+        L.check(lib.gm_spmm_ex(C.byref(cs), C.byref(plan), _DT[x.dtype], _p(x), f, None, _KIND[reduce], 0, None,
+                               C.byref(ep), _p(out_next[self.r0:self.r1]), None, _stream()), "gm_spmm_ex (push)")
+        return out_next
 
 
 # ---------------------------------------------------------------------------

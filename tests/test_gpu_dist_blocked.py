@@ -144,13 +144,20 @@ def test_blocked_f64_sum_and_repeat_calls():
         assert np.allclose(a.cpu().numpy(), ref[r0:r1], rtol=1e-12, atol=1e-12)
 
 
-def test_blocked_rejects_bf16_sum():
+def test_blocked_bf16_max_is_exact():
+    # bf16 max/min never rounds, so the overlap mode is bit-exact in any dtype
+    # (bf16 sums carry fp32 rows: tests/test_gpu_dist_push.py)
     n, e, f = 2000, 20000, 8
     src, dst, x, csc, rp, shards, ranks = _setup(n, e, f, 2, 2, dtype=torch.bfloat16)
-    with pytest.raises(ValueError):
-        ranks[0][2](shards[0], "sum")
-    out, arg = ranks[0][2](shards[0], "max")   # max is exact in any dtype
-    torch.cuda.synchronize()
+    orc = Oracle()
+    rpo, colo, permo = orc.build_compressed(dst, src, n)
+    xb = torch.from_numpy(x).to(torch.bfloat16).float().numpy()
+    want, warg = orc.spmm_max(rpo, colo, permo, xb)
+    for i, (r0, r1, bs) in enumerate(ranks):
+        out, arg = bs(shards[i], "max")
+        torch.cuda.synchronize()
+        assert np.array_equal(out.float().cpu().numpy(), want[r0:r1])
+        assert np.array_equal(arg.cpu().numpy().astype(np.int64), warg[r0:r1])
 
 
 # ---------------------------------------------------------------------------
