@@ -171,14 +171,17 @@ def bench_segment_matmul(gm, L, device, f=128, rows=1_939_743, rank=0, world=1, 
             "bound": "hbm" if ai * hbm / 1e3 < bf16_peak else "tensor"}
 
 
-def workload_config(world: int) -> dict:
+def workload_config(world: int, mode: str = "push") -> dict:
     """The `config` both arms print (same workload, same keys)."""
+    par = f"dst-row partition x{world}"
+    if world > 1:
+        par += (" (each rank builds its CSC rows from its own COO chunk); " + (
+            "push mode: the SpMM epilogue stores finished rows into the referencing peers' next-layer X "
+            "over NVLink P2P, one 1-element all_reduce per step" if mode == "push" else
+            f"{CHUNKS} chunked async NCCL all-gathers of X overlapped with source-blocked aggregation"))
     return {"workload": "ogbn-products-shaped power-law graph (configs[3]), full-graph sum SpMM",
             "nodes": N_NODES, "edges": N_EDGES, "feats": F, "graph": "Chung-Lu alpha=0.5",
-            "seed": hex(SEED),
-            "parallelism": f"dst-row partition x{world}" + (
-                f" + {CHUNKS} chunked async NCCL all-gathers of X overlapped with source-blocked "
-                "aggregation" if world > 1 else ""),
+            "seed": hex(SEED), "parallelism": par, "mode": mode if world > 1 else "single GPU",
             "l2": "GPU arm: L2 flushed between timed steps (256 MB write); X = 980 MB > L2"}
 
 
@@ -384,6 +387,241 @@ def single_gpu_secondary(gm, L, lib, g, x, cs, plan, flush_buf, steps, hbm):
     return sec
 
 
+def main_multi(args, world, rank, local):
+    """N > 1 (one process per GPU): every rank generates only its chunk of the
+    COO edge list and builds its CSC row slice with the distributed
+    build_compressed (dist.build_local_csc: degree all-reduce, nnz cuts, one
+    edge all_to_all, local stable build). Headline step (GM_BENCH_MODE=push,
+    default): the push-mode SpMM — every rank aggregates its destination rows
+    from its replica of X and its epilogue stores each finished row into the
+    peers' next-layer replicas over NVLink P2P (halo masks: only to peers that
+    reference the row); a one-element all_reduce orders the next reads. The
+    output of step s is the input of step s+1 (ping-pong replicas), i.e. the
+    steady state of a multi-layer model. GM_BENCH_MODE=blocked: CHUNKS async
+    all-gathers of X overlapped with source-blocked aggregation. The other
+    modes (exact, blocked, halo, C5-shaped bf16) are secondary lines."""
+    import torch.distributed as dist
+
+    import paper_2507_16991_b200 as gm
+    from paper_2507_16991_b200 import _lib as L
+    from paper_2507_16991_b200 import dist as gd
+
+    device = torch.device("cuda", local)
+    backend = os.environ.get("GM_BENCH_BACKEND", "nccl")  # "gloo": N>1 logic check on one GPU (not a bench)
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=device)
+    else:
+        dist.init_process_group(backend)
+    stream = torch.cuda.current_stream().cuda_stream
+    lib = L.lib()
+    hbm, bf16_peak, peak_kind = peaks()
+
+    def local_graph(n, e, seed):
+        e0, e1 = rank * e // world, (rank + 1) * e // world
+        src = torch.empty(e1 - e0, dtype=torch.int64, device=device)
+        dst = torch.empty(e1 - e0, dtype=torch.int64, device=device)
+        L.check(lib.gm_synth_edges(1, seed, e0, e1 - e0, n, n, src.data_ptr(), dst.data_ptr(), stream))
+        cuts, rows = gd.build_local_csc(src, dst, e0, n, rank, world)
+        return cuts, rows
+
+    def maxed(vals):
+        t = torch.tensor([float(v) for v in vals], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
+
+    def timed(step, steps, warmup, flush_buf):
+        for _ in range(warmup):
+            step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for i in range(steps):
+            flush_buf.zero_()
+            evs[i][0].record()
+            step()
+            evs[i][1].record()
+        torch.cuda.synchronize()
+        dist.barrier()
+        per = [a.elapsed_time(b) for a, b in evs]
+        return maxed([sum(per) / steps])[0], per
+
+    cuts, rows = local_graph(N_NODES, N_EDGES, SEED)
+    r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
+    local_edges = rows.num_entries()
+    x = torch.empty(N_NODES, F, dtype=torch.float32, device=device)  # replica: identical on every rank
+    L.check(lib.gm_synth_features(SEED, 0, N_NODES, F, 0, L.GM_F32, x.data_ptr(), stream))
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    mode = os.environ.get("GM_BENCH_MODE", "push")
+    push_note = None
+    mask = None
+    if mode == "push":
+        try:
+            xb = torch.empty_like(x)
+            ptr_b, bases_b = gd.open_peer_buffers(xb)
+            mask = gd.push_masks(rows, N_NODES, r0, r1, rank, world)
+            op = gd.PushSpmm(rows, r0, r1, rank, world, mask)
+            one = torch.ones(1, device=device)
+
+            def step():
+                # one layer: aggregate this rank's rows of X, push them into every
+                # referencing peer's next-layer input (xb), then order the reads
+                op(x, xb, ptr_b)
+                dist.all_reduce(one)
+        except Exception as exc:  # noqa: BLE001 - no P2P mapping here: the overlap mode is the headline
+            push_note = f"push mode unavailable ({str(exc)[:160]}); blocked mode timed instead"
+            mode = "blocked"
+    s_rows, c_rows = gd.chunk_layout(N_NODES, world, CHUNKS)
+    lo, hi = rank * s_rows, min((rank + 1) * s_rows, N_NODES)
+    x_shard = torch.zeros(CHUNKS * c_rows, F, dtype=torch.float32, device=device)
+    x_shard[: max(0, hi - lo)].copy_(x[lo:hi])
+    blocked = gd.BlockedSpmm(rows, N_NODES, rank, world, CHUNKS)
+    out_local = torch.empty(r1 - r0, F, dtype=torch.float32, device=device)
+    if mode == "blocked":
+        def step():
+            blocked(x_shard, "sum", out=out_local)
+
+    with ClockSampler(local) as clk:
+        ms, per_step = timed(step, args.steps, args.warmup, flush_buf)
+    value = N_EDGES / (ms * 1e-3) / 1e9
+
+    # roofline at N: the slowest rank's local gather-model bytes against its
+    # HBM, plus the exchange each step needs (NVLink 5: 900 GB/s per direction)
+    lb = spmm_bytes(r1 - r0, local_edges, F)
+    if mode == "push":
+        peers_per_row = (torch.bitwise_and(mask.view(-1, 1), torch.tensor([1 << j for j in range(world - 1)],
+                         dtype=torch.int32, device=device)) != 0).sum() if mask is not None else (r1 - r0) * (world - 1)
+        xbytes = int(peers_per_row) * F * 4
+        xkind = "push: rows stored by the SpMM epilogue into referencing peers (NVLink P2P)"
+    else:
+        xbytes = (world - 1) * s_rows * F * 4
+        xkind = "chunked all-gather of X shards (received per rank)"
+    lb_max, xb_max = maxed([lb, xbytes])
+    nvlink = 900.0
+    roof = {"bound": "hbm", "achieved": lb_max / ms / 1e6, "peak": hbm, "unit": "GB/s",
+            "frac": lb_max / ms / 1e6 / hbm, "traffic": None, "peak_kind": peak_kind,
+            "algorithmic_bytes_per_call": lb_max,
+            "unit_of_launch": "the slowest rank's SpMM over its destination rows (gather model)",
+            "exchange": {"mode": xkind, "bytes_per_rank_max": xb_max, "nvlink_gbs": nvlink,
+                         "nvlink_floor_ms": xb_max / nvlink / 1e6, "hbm_floor_ms": lb_max / hbm / 1e6,
+                         "step_floor_ms": max(xb_max / nvlink / 1e6, lb_max / hbm / 1e6)}}
+
+    push_check = None
+    if mode == "push":
+        # end-to-end numerics at N: the rows this rank reads next (its own +
+        # every source it references) must equal the exact (all-gather +
+        # single-GPU kernel) output of their owners, bit for bit
+        s_rows_ = -(-N_NODES // world)
+        sh = gd.Shard(rank, world, r0, r1, s_rows_)
+        x_full = torch.empty(s_rows_ * world, F, dtype=torch.float32, device=device)
+        gd.allgather_features(x_shard[:s_rows_], sh, out=x_full)
+        ex = torch.empty(r1 - r0, F, dtype=torch.float32, device=device)
+        cs_ = rows.c_struct()
+        L.check(lib.gm_spmm(C.byref(cs_), C.byref(rows.plan(F * 4)), L.GM_F32, C.c_void_p(x_full.data_ptr()), F, None,
+                            None, L.GM_SUM, C.c_void_p(ex.data_ptr()), None, C.c_void_p(stream)))
+        rmax = int(maxed([r1 - r0])[0])
+        pad = torch.zeros(rmax, F, dtype=torch.float32, device=device)
+        pad[: r1 - r0].copy_(ex)
+        allx = torch.empty(world * rmax, F, dtype=torch.float32, device=device)
+        dist.all_gather_into_tensor(allx, pad)
+        full = torch.cat([allx[q * rmax:q * rmax + int(cuts[q + 1] - cuts[q])] for q in range(world)])
+        mark = torch.empty(N_NODES, dtype=torch.uint8, device=device)
+        L.check(lib.gm_mark_columns(C.byref(cs_), C.c_void_p(mark.data_ptr()), C.c_void_p(stream)))
+        need = mark != 0
+        need[r0:r1] = True
+        bad = int(maxed([float((xb[need] != full[need]).any(dim=1).sum())])[0])
+        push_check = {"rows_checked_per_rank": int(need.sum()), "mismatched_rows_max_over_ranks": bad,
+                      "reference": "exact mode (all-gather + single-GPU gm_spmm)"}
+        del x_full, allx, full
+        gd.close_peer_buffers(bases_b)
+    secondary = None
+    if not args.no_secondary:
+        try:
+            secondary = multi_secondary(args, gm, L, gd, dist, lib, device, rank, world, rows, cuts, x, x_shard,
+                                        blocked, out_local, flush_buf, timed, maxed, local_graph, mode)
+        except Exception as exc:  # noqa: BLE001 - reported, never substituted for the headline
+            secondary = {"error": str(exc)[:300]}
+    plan = rows.plan(F * 4)
+    launches = 1 + (1 if plan.num_heavy > 0 else 0)
+    if mode == "blocked":
+        launches = sum(1 + (1 if v.plan(F * 4).num_heavy > 0 else 0) for v in blocked.blocks)
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": "GEdges/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": dict(workload_config(world, mode), **({"note": push_note} if push_note else {})),
+            "push_numerics": push_check,
+            "roofline": roof, "cpu_baseline": None, "e2e": None, "gpu_launches": launches * args.steps,
+            "clocks": clk.summary(), "secondary": secondary,
+            "per_step_ms": {"min": min(per_step), "median": statistics.median(per_step), "max": max(per_step)},
+        }))
+    dist.destroy_process_group()
+
+
+def multi_secondary(args, gm, L, gd, dist, lib, device, rank, world, rows, cuts, x, x_shard, blocked, out_local,
+                    flush_buf, timed, maxed, local_graph, mode):
+    """Secondary lines at N > 1, each timed like the headline (max over ranks)."""
+    sec = {}
+    steps = max(3, args.steps // 3)
+    r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
+    stream = torch.cuda.current_stream().cuda_stream
+    s_rows = -(-N_NODES // world)
+    sh = gd.Shard(rank, world, r0, r1, s_rows)
+    cs = rows.c_struct()
+    plan = rows.plan(F * 4)
+    x_full = torch.empty(s_rows * world, F, dtype=torch.float32, device=device)
+
+    def step_exact():
+        gd.allgather_features(x_shard[:s_rows], sh, out=x_full)
+        L.check(lib.gm_spmm(C.byref(cs), C.byref(plan), L.GM_F32, C.c_void_p(x_full.data_ptr()), F, None, None,
+                            L.GM_SUM, C.c_void_p(out_local.data_ptr()), None, C.c_void_p(stream)))
+    ms, _ = timed(step_exact, steps, 2, flush_buf)
+    sec["exact_mode_spmm"] = {"ms": ms, "gedges_s": N_EDGES / ms / 1e6, "numerics": "bit-identical to 1 GPU"}
+    exact = out_local.clone()
+    if mode != "blocked":
+        ms, _ = timed(lambda: blocked(x_shard, "sum", out=out_local), steps, 2, flush_buf)
+        sec["blocked_mode_spmm"] = {"ms": ms, "gedges_s": N_EDGES / ms / 1e6, "chunks": CHUNKS,
+                                    "numerics": "sums continued across 1+CHUNKS source blocks (fp32 tolerance)"}
+    blocked(x_shard, "sum", out=out_local)
+    torch.cuda.synchronize()
+    d, m = maxed([float((out_local - exact).abs().max()), float(exact.abs().max())])
+    sec["blocked_vs_exact_max_abs_diff"] = d
+    sec["exact_max_abs"] = m
+    need = gd.halo_need(rows, N_NODES, rank, world)
+    halo = gd.HaloSpmm(rows, N_NODES, rank, world, need, gd.exchange_need_lists(need))
+    xs = x_shard[:s_rows]
+    ms, _ = timed(lambda: halo(xs, "sum", out=out_local), steps, 2, flush_buf)
+    hr = maxed([float(halo.halo_rows())])[0]
+    sec["halo_mode_spmm"] = {"ms": ms, "gedges_s": N_EDGES / ms / 1e6, "max_halo_rows": int(hr),
+                             "halo_frac_of_remote_rows": hr / (N_NODES - s_rows)}
+    sec["block_nnz"] = blocked.block_nnz()
+    # C5-shaped (ogbn-papers100M: F = 128 bf16, Chung-Lu alpha 0.5) at 1/16 of its size per the
+    # whole job, blocked mode with the fp32 carry (bf16 sums rounded once per row)
+    n5, e5, f5 = 111_059_956 // 16, 1_615_685_872 // 16, 128
+    cuts5, rows5 = local_graph(n5, e5, SEED + 5)
+    a5, b5 = int(cuts5[rank]), int(cuts5[rank + 1])
+    s5, c5 = gd.chunk_layout(n5, world, CHUNKS)
+    x5 = torch.empty(min(s5, n5 - rank * s5), f5, dtype=torch.bfloat16, device=device)
+    L.check(lib.gm_synth_features(SEED + 5, rank * s5, x5.shape[0], f5, 0, L.GM_BF16, x5.data_ptr(), stream))
+    xs5 = torch.zeros(CHUNKS * c5, f5, dtype=torch.bfloat16, device=device)
+    xs5[: x5.shape[0]].copy_(x5)
+    del x5
+    blk5 = gd.BlockedSpmm(rows5, n5, rank, world, CHUNKS)
+    o5 = torch.empty(b5 - a5, f5, dtype=torch.bfloat16, device=device)
+    ms, _ = timed(lambda: blk5(xs5, "sum", out=o5), steps, 2, flush_buf)
+    hbm = peaks()[0]
+    lb5 = maxed([spmm_bytes(b5 - a5, rows5.num_entries(), f5, esz=2)])[0]
+    sec["c5_shape_bf16_blocked"] = {
+        "nodes": n5, "edges": e5, "feats": f5, "ms": ms, "gedges_s": e5 / ms / 1e6,
+        "roofline": {"bound": "hbm", "achieved": lb5 / ms / 1e6, "peak": hbm, "frac": lb5 / ms / 1e6 / hbm},
+        "numerics": "bf16 sums carried in fp32 across the 1+CHUNKS blocks, one rounding per row"}
+    del blk5, xs5, rows5
+    sec["segment_matmul_C3"] = bench_segment_matmul(gm, L, device, rank=rank, world=world, dist=dist)
+    sec["segment_matmul_F1024"] = bench_segment_matmul(gm, L, device, f=1024, rows=500_000, rank=rank, world=world,
+                                                       dist=dist)
+    return sec
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -406,107 +644,60 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
-    device = torch.device("cuda", local)
-    dist = None
     if world > 1:
-        import torch.distributed as dist
-        backend = os.environ.get("GM_BENCH_BACKEND", "nccl")  # "gloo": N>1 logic check on one GPU (not a bench)
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=device)
-        else:
-            dist.init_process_group(backend)
+        main_multi(args, world, rank, local)
+        return
+    device = torch.device("cuda", local)
     stream = torch.cuda.current_stream().cuda_stream
     lib = L.lib()
 
     g, x = make_graph(gm, L, N_NODES, N_EDGES, F, device, stream)
     csc = g.to_csc()
     torch.cuda.synchronize()
-
-    # ---- partition (N > 1): nnz-balanced dst rows, equal-row X shards ----------
-    # The timed step at N > 1 is the exchange-overlapped path (BlockedSpmm):
-    # the own-shard block aggregates while the CHUNKS async NCCL all-gathers
-    # of X are in flight, then each chunk's block continues the rows' sums as
-    # it lands. "exact" (one all-gather, then one bit-identical gm_spmm) is
-    # timed beside it as a secondary line.
-    from paper_2507_16991_b200.dist import BlockedSpmm, allgather_features, chunk_layout, make_shard
-    rowptr_h = csc.rowptr.cpu().numpy()
-    sh = make_shard(rowptr_h, N_NODES, rank, world)
-    r0, r1 = sh.row_begin, sh.row_end
-    local_edges = int(rowptr_h[r1] - rowptr_h[r0])
-    local_csr = csc if world == 1 else csc.row_slice(r0, r1, local_edges)
     out = torch.empty(N_NODES, F, dtype=torch.float32, device=device)
-    x_full = x
-    plan = local_csr.plan()
-    cs = local_csr.c_struct()
-    if world > 1:
-        x_full = torch.zeros(sh.shard_rows * world, F, dtype=torch.float32, device=device)
-        s_rows, c_rows = chunk_layout(N_NODES, world, CHUNKS)
-        lo, hi = rank * s_rows, min((rank + 1) * s_rows, N_NODES)
-        x_shard = torch.zeros(CHUNKS * c_rows, F, dtype=torch.float32, device=device)
-        x_shard[: max(0, hi - lo)].copy_(x[lo:hi])
-        blocked = BlockedSpmm(local_csr, N_NODES, rank, world, CHUNKS)
-        out_local = out[r0:r1]
-
-    def step_exact():
-        if world > 1:
-            allgather_features(x_shard[: sh.shard_rows], sh, out=x_full)
-        L.check(lib.gm_spmm(C.byref(cs), C.byref(plan), L.GM_F32, C.c_void_p(x_full.data_ptr()), F, None,
-                            None, L.GM_SUM, C.c_void_p(out[r0:].data_ptr()), None,
-                            C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    plan = csc.plan()
+    cs = csc.c_struct()
 
     def step():
-        if world > 1:
-            blocked(x_shard, "sum", out=out_local)
-        else:
-            step_exact()
+        L.check(lib.gm_spmm(C.byref(cs), C.byref(plan), L.GM_F32, C.c_void_p(x.data_ptr()), F, None,
+                            None, L.GM_SUM, C.c_void_p(out.data_ptr()), None,
+                            C.c_void_p(torch.cuda.current_stream().cuda_stream)))
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     # L2 (126 MB) is flushed between timed steps by a 256 MB write outside the
     # events, so no step sees rows a previous step left resident.
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=device)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
         for i in range(args.steps):
             flush_buf.zero_()
             evs[i][0].record()
             step()
             evs[i][1].record()
         torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
     per_step = [a.elapsed_time(b) for a, b in evs]
-    total_ms = sum(per_step)
-    if dist:
-        t = torch.tensor([total_ms], device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    ms = total_ms / args.steps
+    ms = sum(per_step) / args.steps
     value = N_EDGES / (ms * 1e-3) / 1e9
 
     hbm, bf16_peak, peak_kind = peaks()
     # roofline of the dominant launch (one gm_spmm call = light + concurrent hub kernel)
-    call_ms = statistics.mean(per_step) if world == 1 else None
+    call_ms = statistics.mean(per_step)
     roof = None
-    if world == 1:
-        b = spmm_bytes(N_NODES, N_EDGES, F)
-        ach = b / (call_ms * 1e-3) / 1e9
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", "spmm_traffic.json")
-        if os.path.exists(tp):
-            try:
-                traffic = json.load(open(tp)).get("dram_bytes_per_call")
-            except Exception:
-                traffic = None
-        roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                "traffic": traffic, "peak_kind": peak_kind, "algorithmic_bytes_per_call": b,
-                "unit_of_launch": "one gm_spmm call (warp-window kernel + concurrent hub-row kernel)"}
+    b = spmm_bytes(N_NODES, N_EDGES, F)
+    ach = b / (call_ms * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "spmm_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_call")
+        except Exception:
+            traffic = None
+    roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+            "traffic": traffic, "peak_kind": peak_kind, "algorithmic_bytes_per_call": b,
+            "unit_of_launch": "one gm_spmm call (warp-window kernel + concurrent hub-row kernel)"}
 
     # ---- e2e through the public C-ABI with host buffers (N = 1) -----------------
     # Every step copies its input X (pinned host -> device), runs gm_spmm and
@@ -515,147 +706,88 @@ def main():
     # of step i-1 overlap the SpMM of step i (PCIe is full duplex). The serial
     # (unpipelined) figure is reported beside it.
     e2e = None
-    if world == 1:
-        xh = torch.empty(N_NODES, F, dtype=torch.float32).pin_memory()
-        ohs = [torch.empty(N_NODES, F, dtype=torch.float32).pin_memory() for _ in range(2)]
-        xh.copy_(x.cpu())
-        xds = [torch.empty_like(x) for _ in range(2)]
-        outs = [torch.empty_like(x) for _ in range(2)]
-        s_in, s_cmp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
-        e2e_steps = max(4, min(args.steps, 10))
+    xh = torch.empty(N_NODES, F, dtype=torch.float32).pin_memory()
+    ohs = [torch.empty(N_NODES, F, dtype=torch.float32).pin_memory() for _ in range(2)]
+    xh.copy_(x.cpu())
+    xds = [torch.empty_like(x) for _ in range(2)]
+    outs = [torch.empty_like(x) for _ in range(2)]
+    s_in, s_cmp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    e2e_steps = max(4, min(args.steps, 10))
 
-        def spmm_on(xd, od, stream):
-            L.check(lib.gm_spmm(C.byref(cs), C.byref(plan), L.GM_F32, C.c_void_p(xd.data_ptr()), F, None,
-                                None, L.GM_SUM, C.c_void_p(od.data_ptr()), None, C.c_void_p(stream.cuda_stream)))
+    def spmm_on(xd, od, stream):
+        L.check(lib.gm_spmm(C.byref(cs), C.byref(plan), L.GM_F32, C.c_void_p(xd.data_ptr()), F, None,
+                            None, L.GM_SUM, C.c_void_p(od.data_ptr()), None, C.c_void_p(stream.cuda_stream)))
 
-        def run_pipelined(steps):
-            h2d = [torch.cuda.Event() for _ in range(2)]
-            cmp = [torch.cuda.Event() for _ in range(2)]
-            d2h = [torch.cuda.Event() for _ in range(2)]
-            for i in range(steps):
-                b = i % 2
-                if i >= 2:
-                    s_in.wait_event(cmp[b])     # xds[b] free again
-                with torch.cuda.stream(s_in):
-                    xds[b].copy_(xh, non_blocking=True)
-                    h2d[b].record(s_in)
-                s_cmp.wait_event(h2d[b])
-                if i >= 2:
-                    s_cmp.wait_event(d2h[b])    # outs[b] read back already
-                spmm_on(xds[b], outs[b], s_cmp)
-                cmp[b].record(s_cmp)
-                s_out.wait_event(cmp[b])
-                with torch.cuda.stream(s_out):
-                    ohs[b].copy_(outs[b], non_blocking=True)
-                    d2h[b].record(s_out)
+    def run_pipelined(steps):
+        h2d = [torch.cuda.Event() for _ in range(2)]
+        cmp = [torch.cuda.Event() for _ in range(2)]
+        d2h = [torch.cuda.Event() for _ in range(2)]
+        for i in range(steps):
+            b = i % 2
+            if i >= 2:
+                s_in.wait_event(cmp[b])     # xds[b] free again
+            with torch.cuda.stream(s_in):
+                xds[b].copy_(xh, non_blocking=True)
+                h2d[b].record(s_in)
+            s_cmp.wait_event(h2d[b])
+            if i >= 2:
+                s_cmp.wait_event(d2h[b])    # outs[b] read back already
+            spmm_on(xds[b], outs[b], s_cmp)
+            cmp[b].record(s_cmp)
+            s_out.wait_event(cmp[b])
+            with torch.cuda.stream(s_out):
+                ohs[b].copy_(outs[b], non_blocking=True)
+                d2h[b].record(s_out)
 
-        run_pipelined(2)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        a = torch.cuda.Event(enable_timing=True)
-        bev = torch.cuda.Event(enable_timing=True)
-        a.record(s_in)
-        run_pipelined(e2e_steps)
-        s_in.wait_stream(s_out)
-        bev.record(s_in)
-        torch.cuda.synchronize()
-        ems = a.elapsed_time(bev) / e2e_steps
-        wall_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
+    run_pipelined(2)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    a = torch.cuda.Event(enable_timing=True)
+    bev = torch.cuda.Event(enable_timing=True)
+    a.record(s_in)
+    run_pipelined(e2e_steps)
+    s_in.wait_stream(s_out)
+    bev.record(s_in)
+    torch.cuda.synchronize()
+    ems = a.elapsed_time(bev) / e2e_steps
+    wall_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
 
-        # serial reference point: copy in, aggregate, copy out, one step at a time
-        a2, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        cur = torch.cuda.current_stream()
-        a2.record()
-        for _ in range(3):
-            xds[0].copy_(xh, non_blocking=True)
-            spmm_on(xds[0], outs[0], cur)
-            ohs[0].copy_(outs[0], non_blocking=True)
-        b2.record()
-        torch.cuda.synchronize()
-        sms = a2.elapsed_time(b2) / 3
-        assert torch.equal(ohs[0], ohs[1]), "pipelined and serial e2e outputs differ"
-        e2e = {"value": N_EDGES / (ems * 1e-3) / 1e9, "unit": "GEdges/s",
-               "h2d_bytes_per_step": N_NODES * F * 4, "d2h_bytes_per_step": N_NODES * F * 4,
-               "ms_per_step": ems, "wall_ms_per_step": wall_ms, "mode": "3-stream pipelined across steps",
-               "serial_value": N_EDGES / (sms * 1e-3) / 1e9, "serial_ms_per_step": sms}
+    # serial reference point: copy in, aggregate, copy out, one step at a time
+    a2, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    cur = torch.cuda.current_stream()
+    a2.record()
+    for _ in range(3):
+        xds[0].copy_(xh, non_blocking=True)
+        spmm_on(xds[0], outs[0], cur)
+        ohs[0].copy_(outs[0], non_blocking=True)
+    b2.record()
+    torch.cuda.synchronize()
+    sms = a2.elapsed_time(b2) / 3
+    assert torch.equal(ohs[0], ohs[1]), "pipelined and serial e2e outputs differ"
+    e2e = {"value": N_EDGES / (ems * 1e-3) / 1e9, "unit": "GEdges/s",
+           "h2d_bytes_per_step": N_NODES * F * 4, "d2h_bytes_per_step": N_NODES * F * 4,
+           "ms_per_step": ems, "wall_ms_per_step": wall_ms, "mode": "3-stream pipelined across steps",
+           "serial_value": N_EDGES / (sms * 1e-3) / 1e9, "serial_ms_per_step": sms}
 
     secondary = None
-
-    def multi_gpu_secondary():
-        # exact mode: one all-gather, then one bit-identical gm_spmm per rank
-        for _ in range(2):
-            step_exact()
-        torch.cuda.synchronize()
-        dist.barrier()
-        a, bev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for _ in range(5):
-            step_exact()
-        bev.record()
-        torch.cuda.synchronize()
-        t = torch.tensor([a.elapsed_time(bev) / 5], device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        exact_ms = float(t.item())
-        # numerics check at N > 1: overlap-mode rows vs the exact (1-GPU-identical) rows
-        blk_out = torch.empty_like(out_local)
-        blocked(x_shard, "sum", out=blk_out)
-        torch.cuda.synchronize()
-        diff = (blk_out - out_local).abs().max()
-        ref_mag = out_local.abs().max()
-        chk = torch.stack([diff, ref_mag])
-        dist.all_reduce(chk, op=dist.ReduceOp.MAX)
-        # halo-only exchange: one all_to_all of the referenced remote rows
-        from paper_2507_16991_b200.dist import HaloSpmm, exchange_need_lists, halo_need
-        need = halo_need(local_csr, N_NODES, rank, world)
-        halo = HaloSpmm(local_csr, N_NODES, rank, world, need, exchange_need_lists(need))
-        xs = x_shard[: sh.shard_rows]
-        for _ in range(2):
-            halo(xs, "sum", out=out_local)
-        torch.cuda.synchronize()
-        dist.barrier()
-        a.record()
-        for _ in range(5):
-            halo(xs, "sum", out=out_local)
-        bev.record()
-        torch.cuda.synchronize()
-        t = torch.tensor([a.elapsed_time(bev) / 5, float(halo.halo_rows())], device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return {"exact_mode_spmm": {"ms": exact_ms, "gedges_s": N_EDGES / exact_ms / 1e6,
-                                         "numerics": "bit-identical to 1 GPU"},
-                     "halo_mode_spmm": {"ms": float(t[0]), "gedges_s": N_EDGES / float(t[0]) / 1e6,
-                                        "max_halo_rows": int(t[1]), "halo_frac_of_remote_rows":
-                                        float(t[1]) / (N_NODES - sh.shard_rows)},
-                     "overlap_mode_numerics": "sum continued across 1+CHUNKS source blocks (fp32 tolerance)",
-                "overlap_vs_exact_max_abs_diff": float(chk[0]), "exact_max_abs": float(chk[1]),
-                     "block_nnz": blocked.block_nnz(),
-                     "segment_matmul_C3": bench_segment_matmul(gm, L, device, rank=rank, world=world, dist=dist),
-                     "segment_matmul_F1024": bench_segment_matmul(gm, L, device, f=1024, rows=500_000, rank=rank,
-                                                                  world=world, dist=dist)}
-    if world > 1 and not args.no_secondary:
-        try:  # reported, never substituted for the headline
-            secondary = multi_gpu_secondary()
-        except Exception as exc:  # noqa: BLE001
-            secondary = {"error": str(exc)[:300]}
-    if world == 1 and not args.no_secondary:
+    if not args.no_secondary:
         secondary = single_gpu_secondary(gm, L, lib, g, x, cs, plan, flush_buf, args.steps, hbm)
 
     cpu = None
-    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
         try:
             cpu = cpu_baseline_line(g, x)
         except Exception as exc:
             cpu = {"error": str(exc)[:200]}
 
     launches_per_step = 1 + (1 if plan.num_heavy > 0 else 0)
-    if world > 1:
-        launches_per_step = sum(1 + (1 if v.plan().num_heavy > 0 else 0) for v in blocked.blocks)
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "GEdges/s", "n_gpus": world, "steps": args.steps,
+            "metric": METRIC, "value": value, "unit": "GEdges/s", "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": workload_config(world),
+            "config": workload_config(1),
             "plan": {"l2_hot_mb": int(plan.l2_hot_bytes >> 20), "heavy_rows": int(plan.num_heavy)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
@@ -663,8 +795,6 @@ def main():
             "per_step_ms": {"min": min(per_step), "median": statistics.median(per_step), "max": max(per_step)},
         }
         print(json.dumps(line))
-    if dist:
-        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -56,6 +56,96 @@ def allgather_features(x_shard: torch.Tensor, shard: Shard, group=None, out=None
 
 
 # ---------------------------------------------------------------------------
+# Distributed build_compressed: every rank holds one contiguous chunk of the
+# COO edge list (edges [first_eid, first_eid + len), e.g. its file shard) and
+# ends with the CSC row slice of its destination rows — global source ids in
+# col, global COO positions in perm — without any rank holding the whole graph:
+#   1. in-degrees of the local chunk (gm_degree), summed over ranks;
+#   2. nnz-balanced row cuts from the global degrees;
+#   3. each edge routed to the rank owning its destination (a stable grouping
+#      by owner = gm_build_compressed over owner ids), one all_to_all;
+#   4. the received edges (from rank q: q's chunk, ascending COO position; in q
+#      order: ascending overall) compressed locally, perm mapped back to the
+#      global positions. Stable at every step, so the slice is bit-identical to
+#      the single-GPU CSC's rows [r0, r1).
+# The phases are separate functions so one process can drive virtual ranks.
+# ---------------------------------------------------------------------------
+def local_degrees(dst: torch.Tensor, num_nodes: int) -> torch.Tensor:
+    from .graphmill import _p, _stream
+    deg = torch.empty(num_nodes, dtype=torch.int32, device=dst.device)
+    L.check(L.lib().gm_degree(_p(dst), dst.numel(), num_nodes, _p(deg), _stream()), "gm_degree")
+    return deg
+
+
+def cuts_from_degrees(deg: torch.Tensor, world: int) -> np.ndarray:
+    rowptr = np.zeros(deg.numel() + 1, np.int64)
+    np.cumsum(deg.cpu().numpy().astype(np.int64), out=rowptr[1:])
+    return partition_rows_by_nnz(rowptr, world)
+
+
+def route_edges(src: torch.Tensor, dst: torch.Tensor, first_eid: int, cuts: np.ndarray):
+    """(src, dst, eid) of the local chunk grouped stably by owner rank, and the
+    per-owner counts (host list)."""
+    from .graphmill import build_compressed
+    world = len(cuts) - 1
+    dev = dst.device
+    owner = torch.searchsorted(torch.from_numpy(np.ascontiguousarray(cuts[1:])).to(dev), dst, right=True)
+    pos = torch.arange(dst.numel(), dtype=torch.int64, device=dev)
+    grp = build_compressed(owner, pos, world)  # stable grouping: perm = positions in owner order
+    order = grp.perm.to(torch.int64)
+    counts = (grp.rowptr[1:] - grp.rowptr[:-1]).cpu().tolist()
+    return src[order], dst[order], order + first_eid, counts
+
+
+def local_csc_from_routed(src: torch.Tensor, dst: torch.Tensor, eid: torch.Tensor, r0: int, r1: int,
+                          num_nodes: int):
+    """CSC row slice of rows [r0, r1) from the edges routed to this rank (in
+    ascending COO position): rowptr rebased to 0, global col / perm."""
+    from .graphmill import CsrView, build_compressed
+    loc = build_compressed(dst - r0, src, r1 - r0, num_nodes)
+    perm = eid[loc.perm.to(torch.int64)].to(torch.int32)
+    return CsrView(loc.rowptr, loc.col, perm, num_nodes, dst.numel())
+
+
+def _alltoall_rows(tensors, send_counts, group=None):
+    """all_to_all_single of several same-length int64 tensors with one split
+    plan (gloo: through host memory)."""
+    world = dist.get_world_size(group)
+    dev = tensors[0].device
+    cpu = dist.get_backend(group) == "gloo"
+    sc = torch.tensor(send_counts, dtype=torch.int64, device="cpu" if cpu else dev)
+    rc = torch.empty_like(sc)
+    dist.all_to_all_single(rc, sc, group=group)
+    recv_counts = rc.cpu().tolist()
+    outs = []
+    for t in tensors:
+        inp = t.cpu() if cpu else t
+        out = torch.empty(sum(recv_counts), dtype=t.dtype, device=inp.device)
+        dist.all_to_all_single(out, inp, output_split_sizes=recv_counts, input_split_sizes=list(send_counts),
+                               group=group)
+        outs.append(out.to(dev))
+    return outs
+
+
+def build_local_csc(src: torch.Tensor, dst: torch.Tensor, first_eid: int, num_nodes: int, rank: int,
+                    world: int, group=None):
+    """Distributed build_compressed over torch.distributed (see above).
+    Returns (cuts, CsrView of this rank's rows)."""
+    deg = local_degrees(dst, num_nodes)
+    if dist.get_backend(group) == "gloo":
+        d = deg.cpu()
+        dist.all_reduce(d, group=group)
+        deg = d.to(deg.device)
+    else:
+        dist.all_reduce(deg, group=group)
+    cuts = cuts_from_degrees(deg, world)
+    s, d, e, counts = route_edges(src, dst, first_eid, cuts)
+    rs, rd, re = _alltoall_rows([s, d, e], counts, group)
+    del s, d, e
+    return cuts, local_csc_from_routed(rs, rd, re, int(cuts[rank]), int(cuts[rank + 1]), num_nodes)
+
+
+# ---------------------------------------------------------------------------
 # Exchange-overlapped aggregation (SURVEY.md §8e): the rank's rows are split
 # by source into block 0 (sources in its own X shard: runs at once, while the
 # exchange is in flight) and blocks 1..G (sources delivered by exchange chunk
