@@ -243,7 +243,10 @@ __device__ __forceinline__ void split3x2(float a, float b, uint32_t& hw, uint32_
 // hi*lo + lo*hi + mid*mid against the matching W pieces (K-major [G*N, 3*Kp]).
 // CVT = 1: the same converter path with a single piece (fp32 x rounded to bf16
 // in the kernel, bf16 W): x is read once as fp32 instead of a separate cast pass.
-template <int KBLK, int CVT>
+// SPLITACC: the split-accumulator variant (P.acc_sets > 0) is its own
+// instantiation, so the single-accumulator epilogue carries none of its
+// registers (the shared form spilled 120 B per thread).
+template <int KBLK, int CVT, bool SPLITACC = false>
 __global__ void __launch_bounds__(CVT > 0 ? kThreads + 32 * kCvtWarps : kThreads, 1)
 segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ CUtensorMap map_a,
                       const __grid_constant__ CUtensorMap map_b, const __grid_constant__ CUtensorMap map_c,
@@ -416,7 +419,7 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
           constexpr int kPa[6] = {0, 0, 1, 0, 2, 1};
           constexpr int kPb[6] = {0, 1, 0, 2, 0, 1};
           constexpr int kPairs = CVT == 3 ? 6 : 1;
-          if (CVT == 3 && P.acc_sets > 0) {
+          if (SPLITACC && CVT == 3 && P.acc_sets > 0) {
             // set kb % R: columns [2 set, 2 set + 1) * bn hold (hi*hi, corrections)
             const int set = kb % P.acc_sets;
             const bool first_use = kb < P.acc_sets;
@@ -444,7 +447,7 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
                                                : smem_u32(b_buf + static_cast<size_t>(s) * b_kblock_bytes);
           uint32_t d = tmem_d;
           bool fresh = kb == 0;
-          if (CVT == 0 && P.acc_sets > 0) {
+          if (SPLITACC && CVT == 0 && P.acc_sets > 0) {
             // staged fp32 split: k-blocks of segment 0 (hi*hi) -> main sets,
             // segments 1..5 (corrections) -> correction sets
             const int segb = P.a_seg_k / KBLK;
@@ -516,7 +519,7 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
       // split accumulators: (sum of the hi*hi sets) + (sum of the correction sets), fp32 RN
       auto load_cols = [&](uint32_t col, uint32_t* v, auto width_c) {
         constexpr int W = decltype(width_c)::value;
-        if (CVT == 1 || P.acc_sets == 0) {
+        if (!SPLITACC || CVT == 1 || P.acc_sets == 0) {
           tmem_ld32<W>(tbase + col, v);
           tmem_wait_ld();
           return;
@@ -548,7 +551,7 @@ segment_matmul_kernel(const __grid_constant__ Params P, const __grid_constant__ 
       };
       if (full_tile) {
         for (int c = c_lo; c < c_hi; c += chunk_cols) {
-          if ((CVT == 3 || (CVT == 0 && out_f32)) && P.acc_sets > 0) {
+          if (SPLITACC && (CVT == 3 || (CVT == 0 && out_f32)) && P.acc_sets > 0) {
             // split accumulators: summed and staged 16 columns at a time
             if (lane == 0 && nstore >= 1) bulk_wait_read<0>();  // the previous store has read the box
             __syncwarp();
@@ -971,7 +974,12 @@ static gm_status segment_matmul_impl(const void* x, const int64_t* ptr_host, int
   // fp32-accurate split: separate hi*hi / correction accumulators, spread over
   // as many k-block sets as TMEM's 512 columns hold (two buffered tiles)
   P.acc_sets = 0;
-  if ((a_f32 && a_pieces == 3) || (a_seg_k > 0 && out_dtype == GM_F32)) {
+  // only where K is long enough for the mixed accumulator to cost accuracy
+  // (K=1433: norm error 1.6e-5 with one accumulator, 2.7e-7 split; K=128 stays
+  // inside the 1e-5 bar with one, and the split epilogue costs C3 0.35 -> 0.46 ms)
+  static const int64_t acc_min_k = [] { const char* e = getenv("GM_GEMM_ACC_MIN_K"); return e ? atoll(e) : 512; }();
+  const int64_t logical_k = a_f32 ? k_in : a_seg_k;
+  if (((a_f32 && a_pieces == 3) || (a_seg_k > 0 && out_dtype == GM_F32)) && logical_k >= acc_min_k) {
     static const int sets_env = [] { const char* e = getenv("GM_GEMM_ACC_SETS"); return e ? atoi(e) : 4; }();
     int sets = std::max(0, std::min(sets_env, 512 / (4 * P.bn)));
     sets = std::min(sets, a_f32 ? P.k_blocks : static_cast<int>(a_seg_k / kblk));
@@ -1069,9 +1077,13 @@ static gm_status segment_matmul_impl(const void* x, const int64_t* ptr_host, int
   }
 
   // per call: the attribute is per device, and a process may drive several
-  auto kern = a_f32 ? (a_pieces == 3 ? (kblk == 64 ? segment_matmul_kernel<64, 3> : segment_matmul_kernel<32, 3>)
+  const bool split = P.acc_sets > 0;
+  auto kern = a_f32 ? (a_pieces == 3 ? (split ? (kblk == 64 ? segment_matmul_kernel<64, 3, true>
+                                                            : segment_matmul_kernel<32, 3, true>)
+                                              : (kblk == 64 ? segment_matmul_kernel<64, 3> : segment_matmul_kernel<32, 3>))
                                       : (kblk == 64 ? segment_matmul_kernel<64, 1> : segment_matmul_kernel<32, 1>))
-                    : (kblk == 64 ? segment_matmul_kernel<64, 0> : segment_matmul_kernel<32, 0>);
+                    : (split ? (kblk == 64 ? segment_matmul_kernel<64, 0, true> : segment_matmul_kernel<32, 0, true>)
+                             : (kblk == 64 ? segment_matmul_kernel<64, 0> : segment_matmul_kernel<32, 0>));
   GM_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   const unsigned grid = static_cast<unsigned>(std::min<int32_t>(tiles, kNumSMs));
   kern<<<grid, a_f32 ? kThreads + 32 * kCvtWarps : kThreads, smem, st>>>(P, map_a, map_b, map_c, G);
