@@ -358,6 +358,7 @@ def single_gpu_secondary(gm, L, lib, g, x, cs, plan, flush_buf, steps, hbm):
         "ms": dms, "gedges_s": N_EDGES / dms / 1e6,
         "roofline": {"bound": "hbm", "achieved": db / dms / 1e6, "peak": hbm, "unit": "GB/s",
                      "frac": db / dms / 1e6 / hbm, "algorithmic_bytes_per_call": db,
+                     "traffic": traffic_of("backward_dw_traffic.json"),
                      "bytes_model": "per edge: source row gather 4F + col/row/perm/dw 16; per row: gradient row 4F + rowptr 8"}}
     del dw
     view = g.source_view()
@@ -377,6 +378,7 @@ def single_gpu_secondary(gm, L, lib, g, x, cs, plan, flush_buf, steps, hbm):
         "ms": mbms, "gedges_s": N_EDGES / mbms / 1e6,
         "roofline": {"bound": "hbm", "achieved": mbb / mbms / 1e6, "peak": hbm, "unit": "GB/s",
                      "frac": mbb / mbms / 1e6 / hbm, "algorithmic_bytes_per_call": mbb,
+                     "traffic": traffic_of("backward_max_traffic.json"),
                      "bytes_model": "per source-view entry: destination argmax row 4F + col/eid 8; per row: gradient "
                                     "row 4F (each winner read once), dx row 4F, argmax 4F counted once, rowptr 8"}}
     del dx, gout, ma_keep

@@ -459,8 +459,15 @@ def push_masks(rows, num_src_rows: int, r0: int, r1: int, rank: int, world: int,
         allm = torch.stack(parts)
     else:
         allm = gather(mark)
+    return masks_from_bitmaps(allm, r0, r1, rank)
+
+
+def masks_from_bitmaps(allm: torch.Tensor, r0: int, r1: int, rank: int) -> torch.Tensor:
+    """allm [world, N]: every rank's referenced-source bitmap. Per row of
+    [r0, r1): bit j = the j-th peer in rank order without `rank` (PushSpmm's
+    push_dst[j]) references it."""
+    world = allm.shape[0]
     bits = (allm[:, r0:r1].to(torch.int64) != 0).to(torch.int64)
-    # bit j = the j-th peer in rank order without this rank (PushSpmm's push_dst[j])
     w = torch.tensor([0 if q == rank else 1 << (q if q < rank else q - 1) for q in range(world)],
                      dtype=torch.int64, device=bits.device).view(world, 1)
     return (bits * w).sum(0).to(torch.int32).contiguous()

@@ -185,3 +185,75 @@ def test_halo_protocol_addresses_every_referenced_source(world):
         p.join(timeout=60)
         assert p.exitcode == 0
     assert all(ok for _, ok in res)
+
+
+def _build_worker(rank, world, port, n, e, q):
+    """Distributed build_compressed protocol on gloo (dist.build_local_csc's
+    collectives and ordering argument): degree all-reduce, the real nnz
+    partitioner, owner routing through dist._alltoall_rows (gloo path), then
+    the local stable build — the oracle's counting sort stands in for the
+    device kernels (stable grouping by owner, local compress)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.oracle import Oracle
+        from paper_2507_16991_b200 import _lib as L
+        from paper_2507_16991_b200.dist import _alltoall_rows, partition_rows_by_nnz
+        lib = L.lib()
+        e0, e1 = rank * e // world, (rank + 1) * e // world
+        src = np.zeros(e1 - e0, np.int64)
+        dst = np.zeros(e1 - e0, np.int64)
+        lib.gm_synth_edges_host(1, 5, e0, e1 - e0, n, n, src.ctypes.data, dst.ctypes.data)
+        deg = torch.from_numpy(np.bincount(dst, minlength=n).astype(np.int32))
+        dist.all_reduce(deg)
+        rp = np.zeros(n + 1, np.int64)
+        np.cumsum(deg.numpy().astype(np.int64), out=rp[1:])
+        cuts = partition_rows_by_nnz(rp, world)
+        owner = np.searchsorted(cuts[1:], dst, side="right")
+        order = np.argsort(owner, kind="stable")
+        counts = np.bincount(owner, minlength=world).tolist()
+        rs, rd, re = _alltoall_rows([torch.from_numpy(src[order]), torch.from_numpy(dst[order]),
+                                     torch.from_numpy(order + e0)], counts)
+        r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
+        lrp, lcol, lperm = Oracle().build_compressed(rd.numpy() - r0, rs.numpy(), r1 - r0)
+        q.put((rank, r0, r1, lrp, lcol, re.numpy()[lperm]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_build_protocol_matches_global_csc(world):
+    n, e = 3000, 60000
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_build_worker, args=(r, world, port, n, e, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    from oracle.oracle import Oracle
+    from paper_2507_16991_b200 import _lib as L
+    src = np.zeros(e, np.int64)
+    dst = np.zeros(e, np.int64)
+    L.lib().gm_synth_edges_host(1, 5, 0, e, n, n, src.ctypes.data, dst.ctypes.data)
+    rp, col, perm = Oracle().build_compressed(dst, src, n)
+    covered = 0
+    for rank, r0, r1, lrp, lcol, lperm in sorted(res, key=lambda t: t[0]):
+        assert np.array_equal(lrp, rp[r0:r1 + 1] - rp[r0])
+        assert np.array_equal(lcol, col[rp[r0]:rp[r1]])
+        assert np.array_equal(lperm, perm[rp[r0]:rp[r1]])
+        covered += r1 - r0
+    assert covered == n
+
+
+def test_push_mask_bits_name_the_peer_slots():
+    from paper_2507_16991_b200.dist import masks_from_bitmaps
+    allm = torch.tensor([[1, 0, 1, 1], [0, 1, 1, 0], [1, 1, 0, 1]], dtype=torch.uint8)  # 3 ranks, 4 rows
+    # rank 1 owns rows [1, 3); its peers in push_dst order are ranks 0, 2 -> bits 0, 1
+    m = masks_from_bitmaps(allm, 1, 3, 1)
+    assert m.tolist() == [0b10, 0b01]
+    # rank 0 owns rows [0, 2); peers 1, 2 -> bits 0, 1
+    assert masks_from_bitmaps(allm, 0, 2, 0).tolist() == [0b10, 0b11]
