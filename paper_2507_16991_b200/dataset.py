@@ -29,7 +29,9 @@ from .graphmill import EdgeIndex, _p, _stream
 
 FORMAT = "graphmill.dataset"   # dataset_io.hpp:22
 VERSION = 1                    # dataset_io.hpp:23
-_DTYPES = {"float32": (torch.float32, "f32"), "float64": (torch.float64, "f64")}
+# dtype -> (torch dtype, file token): dataset_io.hpp:44-50; int64 columns are
+# 8-byte elements (dataset_io.cpp:289-291 sizes every non-f32 dtype as 8 bytes)
+_DTYPES = {"float32": (torch.float32, "f32"), "float64": (torch.float64, "f64"), "int64": (torch.int64, "i64")}
 STAGING_BYTES = 64 << 20
 
 
@@ -61,7 +63,7 @@ def read_manifest(path_dir: str) -> dict:
     if j.get("version") != VERSION:
         raise RuntimeError(f"dataset: unsupported version in {path}")
     for n in j["node_types"]:
-        if n["dtype"] not in _DTYPES and n["dtype"] != "int64":
+        if n["dtype"] not in _DTYPES:
             raise ValueError(f"unknown dtype: {n['dtype']}")
         if n["count"] < 0 or n["feature_width"] < 0:
             raise RuntimeError(f"dataset: negative extent for node type {n['name']}")

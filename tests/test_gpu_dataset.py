@@ -109,3 +109,24 @@ def test_manifest_validation_messages(tmp_path):
         ds.read_manifest(str(tmp_path))
     man = ds.read_manifest(os.path.join(GOLD, "dataset_f64"))
     assert [n["name"] for n in man["node_types"]] == ["author", "paper"]
+
+
+@pytest.mark.gpu
+def test_int64_feature_column(tmp_path):
+    """An int64 node feature column (dtype "int64", file token i64, 8-byte
+    elements: dataset_io.hpp:44-50, dataset_io.cpp:289-305) loads as int64."""
+    rng = np.random.default_rng(11)
+    n, f, e = 1000, 3, 5000
+    d = tmp_path / "i64"
+    d.mkdir()
+    x = rng.integers(-(1 << 40), 1 << 40, size=(n, f)).astype(np.int64)
+    x.tofile(d / "node_v.i64.bin")
+    pairs = rng.integers(0, n, size=(e, 2)).astype(np.uint64)
+    pairs.tofile(d / "edge_v__r__v.u64.bin")
+    json.dump({"format": "graphmill.dataset", "version": 1,
+               "node_types": [{"name": "v", "count": n, "feature_width": f, "dtype": "int64", "has_time": False}],
+               "edge_types": [{"src": "v", "rel": "r", "dst": "v", "edge_count": e, "has_time": False}]},
+              open(d / "manifest.json", "w"))
+    got = ds.load_dataset(str(d))
+    assert got.features["v"].dtype == torch.int64
+    assert np.array_equal(got.features["v"].cpu().numpy(), x)
