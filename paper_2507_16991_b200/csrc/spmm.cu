@@ -322,6 +322,8 @@ static gm_status spmm_impl(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype
              "gm_spmm_ex: push carries sum/mean layers to <= GM_MAX_PUSH peers (no fused GCN term)");
   GM_REQUIRE(!(carry && push && ep->carry_mode != GM_CARRY_FINISH), GM_ERR_INVALID_ARGUMENT,
              "gm_spmm_ex: rows are pushed by the block that finishes them");
+  GM_REQUIRE(!(carry || push) || !edge_weight, GM_ERR_INVALID_ARGUMENT,
+             "gm_spmm_ex: the carry / push epilogue takes unweighted sum/mean layers");
   if (csr->num_rows == 0 || f == 0) return GM_OK;
   GM_REQUIRE(x && out, GM_ERR_INVALID_ARGUMENT, "gm_spmm: null x/out");
   if (push)

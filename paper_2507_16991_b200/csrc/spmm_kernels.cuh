@@ -80,12 +80,19 @@ struct SpmmArgs {
 // Row-slice store of the epilogue: fp32 carry (bf16 blocks that are not the
 // last), else the narrowed vector to out plus one plain store per selected
 // peer (NVLink P2P when the peer buffer is mapped from another GPU).
-// (max/min layers take neither: their paths compile to the plain store.)
+// EPI = false compiles to the plain store: the flat kernel instantiates the
+// epilogue separately (launched only when the call asks for it) — inlined
+// into every row flush of the hot instantiations it cost the C5 bf16 sweep
+// 76 -> 87 ms, and as a non-inlined call 4.2 -> 4.9 ms on C4.
 template <typename T, typename VecT, bool EPI = true>
 __device__ __forceinline__ void epi_store(const SpmmArgs& p, T* out, uint64_t elem, int64_t row,
                                           const typename VecT::A* v) {
   constexpr int V = VecT::V;
+#ifdef GM_NO_EPI  // A/B builds only: every path takes the plain store
+  if constexpr (true) {
+#else
   if constexpr (!EPI) {
+#endif
     VecT::store_global(out + elem, v);
     return;
   }
@@ -610,7 +617,7 @@ constexpr int kFlatGather = GM_FLAT_GATHER_V;
 #ifndef GM_FLAT_MAX_U
 #define GM_FLAT_MAX_U 6  // edges per batch of the 16-byte one-vector max/min path
 #endif
-template <typename T, int VB, int NV, int U, int MODE, bool SCALED, bool ACC, int LM>
+template <typename T, int VB, int NV, int U, int MODE, bool SCALED, bool ACC, int LM, bool EPI = false>
 __global__ void __launch_bounds__(256, (sizeof(T) == 8 || (SCALED && (MODE >= 2 || NV > 1 || VB <= 8))) ? 3 : 4) spmm_flat_kernel(const SpmmArgs p) {
   constexpr bool MAXMIN = MODE >= 2;
   constexpr bool IS_MIN = MODE == 3;
@@ -699,7 +706,7 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 8 || (SCALED && (MODE >= 2 
 #pragma unroll
     for (int j = 0; j < NV; ++j)
       if (valid[j]) {
-        epi_store<T, VecT, !MAXMIN>(p, out, obase + soff[j], row, acc.v[j]);
+        epi_store<T, VecT, EPI && !MAXMIN>(p, out, obase + soff[j], row, acc.v[j]);
         if (want_arg) {
           int32_t* arow = p.arg + obase + soff[j];
           store_arg<V>(arow, acc.a[j]);
@@ -867,7 +874,7 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 8 || (SCALED && (MODE >= 2 
   while (row < rb) flush();
   // pushed rows must be visible to the peers before the caller's collective
   // releases their next read
-  if (!MAXMIN && p.n_push) __threadfence_system();
+  if (EPI && !MAXMIN && p.n_push) __threadfence_system();
 }
 
 // ---------------------------------------------------------------------------
@@ -1366,6 +1373,7 @@ gm_status launch_flat(const SpmmArgs& p0, int64_t ns, cudaStream_t st) {
   // streaming gathers unless X is small enough to live in L2; hot rows keep
   // an evict_last policy on the plain (unscaled, fresh) path when hinted
   const int lm = p0.stream_x == 0 ? 0 : (p0.src_class != nullptr && !p0.accum) ? 2 : 1;
+  const bool epi = p0.carry != nullptr || p0.n_push > 0;
   for (int64_t base = 0; base < ns; base += chunk) {
     SpmmArgs p = p0;
     p.slot_base = base;
@@ -1384,6 +1392,13 @@ gm_status launch_flat(const SpmmArgs& p0, int64_t ns, cudaStream_t st) {
   } while (0)
 #define GM_FLAT_K(NV_, U_, M_)                                                                     \
   do {                                                                                             \
+    if constexpr (M_ < 2) {                                                                        \
+      if (epi) {  /* carry / push epilogue: unscaled sum/mean, own instantiations */               \
+        if (p.accum) spmm_flat_kernel<T, VB, NV_, U_, M_, false, true, 1, true><<<grid, 256, 0, st>>>(p); \
+        else spmm_flat_kernel<T, VB, NV_, U_, M_, false, false, 1, true><<<grid, 256, 0, st>>>(p);        \
+        break;                                                                                     \
+      }                                                                                            \
+    }                                                                                              \
     if (lm == 2) {                                                                                 \
       if (scaled) spmm_flat_kernel<T, VB, NV_, U_, M_, true, false, 2><<<grid, 256, 0, st>>>(p);     \
       else spmm_flat_kernel<T, VB, NV_, U_, M_, false, false, 2><<<grid, 256, 0, st>>>(p);           \
