@@ -12,6 +12,7 @@
 //   aggregate (edge rows by index)                      aggregate.hpp:154-215
 //   grouped_matmul (bf16 and fp32, per-group tensors)   hetero.hpp:134-157
 //   DistSpmm (dst-row partition over an ncclComm_t)
+//   PushSpmm (exchange fused into the SpMM epilogue)
 // Data lives on the device (DeviceMatrix / DeviceArray); std::invalid_argument,
 // std::out_of_range and std::logic_error carry the reference's message shapes.
 #pragma once
@@ -575,6 +576,53 @@ class DistSpmm {
   gm_spmm_plan plan_{};
   cudaStream_t comm_stream_ = nullptr;
   DeviceArray<unsigned char> ws_;
+};
+
+// One rank of push mode (gm_spmm_ex push epilogue): the SpMM over rows
+// [r0, r1) of `csc` (global source ids) reads this rank's replica of the layer
+// input and stores every finished row into out_next (its rows r0..r1) and into
+// each peer's replica of the next layer's input — device pointers mapped into
+// this process, e.g. by gm_ipc_open_handle over NVLink. mask (optional, one
+// word per local row): bit j = push to peers[j]. The caller orders the peers'
+// reads after the call (a collective on the stream). Sum/mean layers.
+class PushSpmm {
+ public:
+  PushSpmm(const CsrView& csc, Index r0, Index r1, std::vector<void*> peers,
+           const DeviceArray<std::uint32_t>* mask = nullptr)
+      : csc_(csc), r0_(r0), r1_(r1), peers_(std::move(peers)), mask_(mask) {
+    if (r0 < 0 || r1 < r0 || r1 > csc.num_rows()) throw std::invalid_argument("PushSpmm: bad row range");
+    if (peers_.size() > GM_MAX_PUSH) throw std::invalid_argument("PushSpmm: at most GM_MAX_PUSH peers");
+    const std::vector<Index> rp = csc.rowptr.to_host();
+    slice_ = gm_csr{r1 - r0, csc.num_cols, rp[static_cast<std::size_t>(r1)] - rp[static_cast<std::size_t>(r0)],
+                    csc.rowptr.data() + r0, csc.col.data(), csc.perm.data()};
+    const std::size_t bytes = gm_spmm_plan_bytes(slice_.num_rows, slice_.num_cols, slice_.nnz);
+    plan_buf_ = DeviceArray<unsigned char>(bytes ? bytes : 1);
+    detail::check(gm_spmm_plan_build(&slice_, plan_buf_.data(), bytes, &plan_, stream()));
+  }
+
+  template <class S>
+  void operator()(const DeviceMatrix<S>& x, DeviceMatrix<S>& out_next, AggKind kind) const {
+    if (kind != AggKind::sum && kind != AggKind::mean) throw std::invalid_argument("PushSpmm: sum or mean");
+    if (x.rows() != csc_.num_cols || out_next.rows() != x.rows() || out_next.cols() != x.cols())
+      throw std::invalid_argument("PushSpmm: x / out_next must be [num_nodes, F] replicas");
+    gm_spmm_epilogue ep{};
+    ep.n_push = static_cast<std::int32_t>(peers_.size());
+    for (std::size_t q = 0; q < peers_.size(); ++q) ep.push_dst[q] = peers_[q];
+    ep.push_row0 = r0_;
+    ep.push_mask = mask_ ? mask_->data() : nullptr;
+    detail::check(gm_spmm_ex(&slice_, &plan_, detail::dtype_of<S>(), x.data(), x.cols(), nullptr,
+                             kind == AggKind::sum ? GM_SUM : GM_MEAN, 0, nullptr, &ep,
+                             out_next.data() + r0_ * x.cols(), nullptr, stream()));
+  }
+
+ private:
+  CsrView csc_;
+  Index r0_, r1_;
+  std::vector<void*> peers_;
+  const DeviceArray<std::uint32_t>* mask_;
+  gm_csr slice_{};
+  gm_spmm_plan plan_{};
+  DeviceArray<unsigned char> plan_buf_;
 };
 
 }  // namespace b200

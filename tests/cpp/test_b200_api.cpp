@@ -381,3 +381,27 @@ TEST_CASE("DistSpmm over a 1-rank NCCL communicator equals the single-GPU spmm")
   }
   CHECK(gm_nccl_comm_destroy(comm) == GM_OK);
 }
+
+TEST_CASE("PushSpmm: two virtual ranks push their rows into each other's next-layer replica") {
+  Stream s = test_stream(91);
+  const Index n = 4000;
+  std::vector<Index> src(60000), dst(60000);
+  for (std::size_t i = 0; i < src.size(); ++i) {
+    src[i] = static_cast<Index>(s.next_below(n));
+    dst[i] = static_cast<Index>(s.next_below(n));
+  }
+  EdgeIndex e(src, dst, n, n);
+  const auto xh = random_values(static_cast<std::size_t>(n) * 8, 92);
+  auto x0 = DeviceMatrix<float>::from_host(n, 8, std::vector<float>(xh.begin(), xh.end()));
+  auto x1 = DeviceMatrix<float>::from_host(n, 8, std::vector<float>(xh.begin(), xh.end()));
+  DeviceMatrix<float> b0(n, 8), b1(n, 8);
+  const Index cut = 1700;
+  PushSpmm rank0(e.to_csc(), 0, cut, {b1.data()});
+  PushSpmm rank1(e.to_csc(), cut, n, {b0.data()});
+  rank0(x0, b0, AggKind::mean);
+  rank1(x1, b1, AggKind::mean);
+  const auto want = neighbor_aggregate(e, x0, AggKind::mean).to_host();
+  CHECK(b0.to_host() == want);
+  CHECK(b1.to_host() == want);
+  CHECK_THROWS_AS(rank0(x0, b0, AggKind::max), std::invalid_argument);
+}
