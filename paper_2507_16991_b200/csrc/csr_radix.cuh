@@ -326,33 +326,42 @@ __global__ void __launch_bounds__(kThreads, GM_RADIX_MINB) radix_scatter_kernel(
 }
 
 // rowptr from the sorted keys: rowptr[r] = first slot with key >= r. Thread q
-// owns slots [4q, 4q+4): one 16-byte load plus the previous key; the row
-// starts inside the range (usually zero or one) are written directly.
+// owns slots [16q, 16q+16): four 16-byte loads (all in flight) plus the
+// previous key; the row starts inside the range (usually none or one) are
+// written directly.
+constexpr int kRowptrPer = 16;
 __global__ void rowptr_from_sorted_kernel(const uint32_t* __restrict__ key, int64_t e, int64_t rows,
                                           int64_t* __restrict__ rowptr) {
-  const int64_t quads = (e + 4) / 4;  // slots 0..e (slot e closes the last rows)
+  const int64_t groups = (e + kRowptrPer) / kRowptrPer;  // slots 0..e (slot e closes the last rows)
   const bool aligned = (reinterpret_cast<uintptr_t>(key) & 15) == 0;
-  for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < quads;
+  for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < groups;
        q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t k0 = q * 4;
-    int64_t kk[5];
-    kk[0] = k0 == 0 ? -1 : static_cast<int64_t>(__ldg(key + k0 - 1));
-    if (k0 + 4 <= e && aligned) {
-      const uint4 v = __ldg(reinterpret_cast<const uint4*>(key + k0));
-      kk[1] = v.x;
-      kk[2] = v.y;
-      kk[3] = v.z;
-      kk[4] = v.w;
+    const int64_t k0 = q * kRowptrPer;
+    uint32_t kk[kRowptrPer];
+    const int64_t prev = k0 == 0 ? -1 : static_cast<int64_t>(__ldg(key + k0 - 1));
+    if (k0 + kRowptrPer <= e && aligned) {
+#pragma unroll
+      for (int j = 0; j < kRowptrPer / 4; ++j) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(key + k0) + j);
+        kk[4 * j] = v.x;
+        kk[4 * j + 1] = v.y;
+        kk[4 * j + 2] = v.z;
+        kk[4 * j + 3] = v.w;
+      }
+      if (static_cast<int64_t>(kk[kRowptrPer - 1]) == prev) continue;  // no row starts in this range
     } else {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) kk[j + 1] = k0 + j < e ? static_cast<int64_t>(__ldg(key + k0 + j)) : rows;
+      for (int j = 0; j < kRowptrPer; ++j)
+        kk[j] = k0 + j < e ? __ldg(key + k0 + j) : static_cast<uint32_t>(rows);
     }
-    if (kk[4] == kk[0] && k0 + 4 <= e) continue;  // no row starts in this quad
+    int64_t before = prev;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < kRowptrPer; ++j) {
       const int64_t k = k0 + j;
       if (k > e) break;
-      for (int64_t r = kk[j] + 1; r <= kk[j + 1]; ++r) rowptr[r] = k;  // rows (prev, key[k]] start at k
+      const int64_t cur = static_cast<int64_t>(kk[j]);
+      for (int64_t r = before + 1; r <= cur; ++r) rowptr[r] = k;  // rows (prev, key[k]] start at k
+      before = cur;
     }
   }
 }
@@ -459,8 +468,8 @@ inline gm_status radix_build(const int64_t* keys, const int64_t* values, int64_t
     last_keys = ok;
     cur ^= 1;
   }
-  rowptr_from_sorted_kernel<<<static_cast<unsigned>(ceil_div((e + 4) / 4, 256)), 256, 0, st>>>(last_keys, e, rows,
-                                                                                              rowptr);
+  rowptr_from_sorted_kernel<<<static_cast<unsigned>(ceil_div((e + kRowptrPer) / kRowptrPer, 256)), 256, 0, st>>>(
+      last_keys, e, rows, rowptr);
   GM_CHECK_LAUNCH("rowptr_from_sorted_kernel");
   return GM_OK;
 }
