@@ -42,3 +42,29 @@ def test_local_csc_equals_global_rows(world, n, e, kind):
         k0, k1 = int(rp[r0]), int(rp[r1])
         assert torch.equal(loc.col, csc.col[k0:k1]), r
         assert torch.equal(loc.perm, csc.perm[k0:k1]), r
+
+
+def test_more_ranks_than_rows_and_empty_chunks():
+    # 8 ranks over 5 rows and 7 edges: most ranks own no rows, some chunks are empty
+    n, world = 5, 8
+    src = torch.tensor([0, 4, 2, 2, 1, 3, 0], dtype=torch.int64, device="cuda")
+    dst = torch.tensor([1, 1, 4, 0, 1, 3, 3], dtype=torch.int64, device="cuda")
+    e = src.numel()
+    csc = gm.EdgeIndex(src, dst, n, n).to_csc()
+    rp = csc.rowptr.cpu().numpy()
+    chunks = [(q * e // world, (q + 1) * e // world) for q in range(world)]
+    deg = sum(local_degrees(dst[a:b], n) for a, b in chunks)
+    cuts = cuts_from_degrees(deg, world)
+    routed = [route_edges(src[a:b], dst[a:b], a, cuts) for a, b in chunks]
+    offs = [np.concatenate([[0], np.cumsum(r[3])]) for r in routed]
+    total = 0
+    for r in range(world):
+        r0, r1 = int(cuts[r]), int(cuts[r + 1])
+        parts = [[routed[q][i][offs[q][r]:offs[q][r + 1]] for q in range(world)] for i in range(3)]
+        s, d, eid = (torch.cat(p) for p in parts)
+        loc = local_csc_from_routed(s, d, eid, r0, r1, n)
+        k0, k1 = int(rp[r0]), int(rp[r1])
+        assert torch.equal(loc.rowptr, csc.rowptr[r0:r1 + 1] - csc.rowptr[r0])
+        assert torch.equal(loc.col, csc.col[k0:k1]) and torch.equal(loc.perm, csc.perm[k0:k1])
+        total += loc.num_entries()
+    assert total == e
