@@ -151,6 +151,15 @@ __global__ void __launch_bounds__(256) maxbwd_light_kernel(const int64_t* __rest
 #ifndef GM_MAXBWD_U
 #define GM_MAXBWD_U 4
 #endif
+// staged variant (default): entries per batch and warps per CTA. Same-box C4
+// A/B (whole backward, ms): U/W 8/8 14.4, 4/16 10.4, 2/16 8.9, 2/8 8.2, 2/4
+// 7.8, 2/2 7.6, 3/2 7.6; the register-pipelined sweep 12.1.
+#ifndef GM_MAXBWD_SU
+#define GM_MAXBWD_SU 3
+#endif
+#ifndef GM_MAXBWD_SW
+#define GM_MAXBWD_SW 2
+#endif
 template <int U>
 __global__ void __launch_bounds__(256, GM_MAXBWD_MINB) maxbwd_flat_kernel(const int64_t* __restrict__ rowptr,
                                                           const int32_t* __restrict__ col,
@@ -253,6 +262,151 @@ __global__ void __launch_bounds__(256, GM_MAXBWD_MINB) maxbwd_flat_kernel(const 
     while (row < rb) flush();
   }
 #undef GM_MB_LOAD_ARG
+}
+
+// Staged variant (the default; GM_MAXBWD_STAGED=0 selects the register sweep
+// above): the same window sweep, but the argmax
+// and gradient slices go through a per-warp shared-memory ring with 16-byte
+// cp.async instead of registers, so kStageD batches of U entries are in
+// flight per warp without register pressure. Per iteration: issue the argmax
+// slices of batch i+2; when batch i+1's have landed, form its match masks and
+// issue its gradient slices (zero-filled where no column of the slice
+// matches); when batch i's gradients have landed, add them in entry order.
+constexpr int kStageD = 3;
+template <int U, int WARPS>
+__global__ void __launch_bounds__(32 * WARPS, 1) maxbwd_staged_kernel(
+    const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col, const int32_t* __restrict__ eid,
+    const int32_t* __restrict__ windows, int64_t num_windows, const int32_t* __restrict__ arg,
+    const float* __restrict__ g, int64_t f, float* __restrict__ dx) {
+  static_assert(4 * U <= 32, "4 match bits per entry in one word");
+  constexpr unsigned FULL = 0xffffffffu;
+  extern __shared__ __align__(16) unsigned char mb_smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  // per warp: kStageD stages of {arg[U][32] int4, grad[U][32] float4}
+  int4* sarg = reinterpret_cast<int4*>(mb_smem) + static_cast<size_t>(wib) * kStageD * 2 * U * 32;
+  const int64_t w = static_cast<int64_t>(blockIdx.x) * WARPS + wib;
+  if (w >= num_windows) return;
+  const int ra = windows[2 * w], rb = windows[2 * w + 1];
+  const int32_t kbeg = static_cast<int32_t>(rowptr[ra]);
+  const int32_t kend = static_cast<int32_t>(rowptr[rb]);
+  const uint32_t fu = static_cast<uint32_t>(f);
+  const int nsl_all = static_cast<int>(f / 4);
+  auto st_arg = [&](int b) { return sarg + static_cast<size_t>(b % kStageD) * 2 * U * 32; };
+  auto st_grad = [&](int b) { return reinterpret_cast<float4*>(st_arg(b) + U * 32); };
+  for (int sb = 0; sb < nsl_all; sb += 32) {  // column passes of 32 16-byte slots
+    const int nsl = min(32, nsl_all - sb);
+    const bool valid = lane < nsl;
+    const uint32_t soff = static_cast<uint32_t>(sb + min(lane, nsl - 1)) * 4u;
+    int cbase = ra;
+    int32_t rend_l = (cbase + lane < rb) ? static_cast<int32_t>(rowptr[cbase + 1 + lane]) : kend;
+    int row = ra;
+    int32_t row_end = __shfl_sync(FULL, rend_l, 0);
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    auto flush = [&]() {
+      if (valid)
+        __stcs(reinterpret_cast<float4*>(dx + static_cast<uint64_t>(static_cast<uint32_t>(row)) * fu + soff),
+               make_float4(acc[0], acc[1], acc[2], acc[3]));
+      acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
+      ++row;
+      if (row < rb) {
+        if (row - cbase >= 32) {
+          cbase = row;
+          rend_l = (cbase + lane < rb) ? static_cast<int32_t>(rowptr[cbase + 1 + lane]) : kend;
+        }
+        row_end = __shfl_sync(FULL, rend_l, row - cbase);
+      }
+    };
+    const int nb = (kend - kbeg + U - 1) / U;  // batches of this window
+    // per-lane metadata of a batch: lane u < U holds entry u's (destination, edge id)
+    auto meta = [&](int b, int32_t& c, int32_t& e) {
+      c = 0;
+      e = -2;
+      if (lane < U && b < nb) {
+        const int32_t k = min(kbeg + b * U + lane, kend - 1);
+        c = col[k];
+        e = (kbeg + b * U + lane < kend) ? eid[k] : -2;
+      }
+    };
+    // plain 16-byte cp.async (an evict_last hint for the plan's hot
+    // destinations measured 7.6 -> 8.1 ms, evict_first for the rest slower still)
+    auto cp16 = [&](uint32_t sa, const void* src, uint32_t nbytes) {
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(src), "r"(nbytes) : "memory");
+    };
+    auto issue_arg = [&](int b, int32_t c) {
+      if (b < nb) {
+        int4* dst = st_arg(b);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t v = static_cast<uint32_t>(__shfl_sync(FULL, c, u));
+          const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(dst + u * 32 + lane));
+          cp16(sa, arg + static_cast<uint64_t>(v) * fu + soff, 16u);
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    // match masks of batch b (its argmax slices in smem) and its gradient issue
+    auto masks_and_grad = [&](int b, int32_t c, int32_t e) -> uint32_t {
+      uint32_t mask = 0;
+      if (b < nb) {
+        const int4* sa = st_arg(b);
+        float4* dst = st_grad(b);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int32_t eu = __shfl_sync(FULL, e, u);
+          const uint32_t v = static_cast<uint32_t>(__shfl_sync(FULL, c, u));
+          const int4 a4 = sa[u * 32 + lane];
+          const uint32_t m = static_cast<uint32_t>(a4.x == eu) | (static_cast<uint32_t>(a4.y == eu) << 1) |
+                             (static_cast<uint32_t>(a4.z == eu) << 2) | (static_cast<uint32_t>(a4.w == eu) << 3);
+          mask |= m << (4 * u);
+          const uint32_t gd = static_cast<uint32_t>(__cvta_generic_to_shared(dst + u * 32 + lane));
+          // zero-fill (no read) where no column of the slice matches
+          cp16(gd, g + static_cast<uint64_t>(v) * fu + soff, m ? 16u : 0u);
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      return mask;
+    };
+    int32_t c0, e0, c1, e1, c2, e2;
+    meta(0, c0, e0);
+    meta(1, c1, e1);
+    issue_arg(0, c0);                 // A0
+    issue_arg(1, c1);                 // A1
+    asm volatile("cp.async.wait_group 1;" ::: "memory");  // A0 landed
+    __syncwarp();
+    uint32_t mask_cur = masks_and_grad(0, c0, e0);  // G0
+    for (int b = 0; b < nb; ++b) {
+      meta(b + 2, c2, e2);
+      issue_arg(b + 2, c2);                                 // A(b+2)
+      asm volatile("cp.async.wait_group 2;" ::: "memory");  // A(b+1) landed (G(b), A(b+2) may fly)
+      __syncwarp();
+      const uint32_t mask_next = masks_and_grad(b + 1, c1, e1);  // G(b+1)
+      asm volatile("cp.async.wait_group 2;" ::: "memory");  // G(b) landed
+      __syncwarp();
+      const float4* sg = st_grad(b);
+      const int32_t k0 = kbeg + b * U;
+      const int n_e = min(U, kend - k0);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (u < n_e) {
+          while (k0 + u >= row_end) flush();
+          const uint32_t m = (mask_cur >> (4 * u)) & 15u;
+          if (m) {
+            const float4 gv = sg[u * 32 + lane];
+            if (m & 1u) acc[0] = __fadd_rn(acc[0], gv.x);
+            if (m & 2u) acc[1] = __fadd_rn(acc[1], gv.y);
+            if (m & 4u) acc[2] = __fadd_rn(acc[2], gv.z);
+            if (m & 8u) acc[3] = __fadd_rn(acc[3], gv.w);
+          }
+        }
+      }
+      __syncwarp();  // stage b is reused by A(b+3)
+      mask_cur = mask_next;
+      c1 = c2;
+      e1 = e2;
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    while (row < rb) flush();
+  }
 }
 
 // Hub rows (out-degree > the plan's threshold, up to ~20K entries on C4): one
@@ -376,8 +530,20 @@ gm_status launch_bwd(const gm_csr* v, const gm_spmm_plan* plan, const int32_t* a
     bool done = false;
     if constexpr (sizeof(S) == 4) {
       if (f % 4 == 0 && al % 16 == 0) {
-        maxbwd_flat_kernel<GM_MAXBWD_U><<<lgrid, 256, 0, st>>>(v->rowptr, v->col, v->perm, plan->light_windows,
-                                                               plan->num_light_windows, arg, g, f, dx);
+        // staged ring (default) vs the register-pipelined sweep (GM_MAXBWD_STAGED=0)
+        static const bool staged = [] { const char* ev = getenv("GM_MAXBWD_STAGED"); return !(ev && ev[0] == '0'); }();
+        if (staged) {
+          constexpr int kU = GM_MAXBWD_SU, kW = GM_MAXBWD_SW;
+          const size_t smem = sizeof(int4) * kStageD * 2 * kU * 32 * kW;
+          GM_TRY_CUDA(cudaFuncSetAttribute(maxbwd_staged_kernel<kU, kW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem)));
+          maxbwd_staged_kernel<kU, kW><<<static_cast<unsigned>(ceil_div(plan->num_light_windows, kW)), 32 * kW, smem,
+                                         st>>>(v->rowptr, v->col, v->perm, plan->light_windows,
+                                               plan->num_light_windows, arg, g, f, dx);
+        } else {
+          maxbwd_flat_kernel<GM_MAXBWD_U><<<lgrid, 256, 0, st>>>(v->rowptr, v->col, v->perm, plan->light_windows,
+                                                                 plan->num_light_windows, arg, g, f, dx);
+        }
         done = true;
       }
     }
