@@ -25,7 +25,10 @@ namespace gm {
 namespace rx {
 
 constexpr int kMaxBits = 11;
-constexpr int kWarps = 8;
+#ifndef GM_RADIX_WARPS  // warps per tile (A/B: 4 warps x 8 / 16 rounds 2.48 / 2.05 ms, 2 x 16 2.58; 8 x 8 1.95)
+#define GM_RADIX_WARPS 8
+#endif
+constexpr int kWarps = GM_RADIX_WARPS;
 constexpr int kThreads = 32 * kWarps;
 // Entries per lane per tile and the scatter's CTAs per SM (same-box A/B on
 // C4, whole build: 16 rounds / 2 CTAs 2.06 ms, 12 / 2 2.09, 8 / 3 2.02,
