@@ -2,7 +2,7 @@
 # launch list of the bench command, --set full captures of the top kernels.
 set -x
 O=gpurun_out
-R=r02z
+R=r02f
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/${R}_gputest.log 2>&1; echo "pytest rc=$?" >> $O/${R}_gputest.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/${R}_smoke.log 2>&1
 timeout 900 python bench.py > $O/${R}_bench.json 2> $O/${R}_bench.err
