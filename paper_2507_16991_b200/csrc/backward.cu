@@ -179,7 +179,10 @@ constexpr int kDotV4Warps = 4;
 #ifndef GM_DOT_BUFS
 #define GM_DOT_BUFS 2
 #endif
-constexpr int kDotBufs = GM_DOT_BUFS;  // staged units per warp (3 and 4 measured slower: fewer resident warps)
+constexpr int kDotBufs = GM_DOT_BUFS;
+#ifndef GM_DOT_SLICE_U
+#define GM_DOT_SLICE_U 8  // entries per sub-batch of the column-slice dw kernel
+#endif  // staged units per warp (3 and 4 measured slower: fewer resident warps)
 // stage unit u = (batch u / nc, column chunk u % nc) of this warp into buffer u % kDotBufs
 // 16-byte cp.async; hot source rows (the plan's classes) carry an evict_last
 // policy so power-law hub rows stay in L2 across the sweep, the rest default
@@ -290,6 +293,109 @@ __global__ void __launch_bounds__(kDotV4Warps * 32) edge_dot_csc_v4_kernel(
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
+// Column-slice form (the default for fp32 rows of 16-byte multiples): the forward sweep's gather
+// pattern — lanes own 16-byte column slices, so an entry's source row is one
+// coalesced 400-byte read across the warp — with the products transposed
+// through shared memory for the reference's sequential chain. Per sub-batch
+// of U entries: all U source-row slices are in flight; lane l forms the
+// exact products g[v][j] * x[u][j] of its slice (the destination row's slice
+// stays in registers across a row's run of entries) and stores them to row t
+// of a [U][F+pad] tile; then lane t < U adds row t's products in j order —
+// the same mul-then-add chain, bit-identical.
+#ifndef GM_DOT_SLICE_MINB
+#define GM_DOT_SLICE_MINB 4
+#endif
+#ifndef GM_DOT_SLICE_COLD
+#define GM_DOT_SLICE_COLD 1  // cold source rows: 1 evict_first (as the forward sweep), 0 default priority
+#endif
+template <int U>
+__global__ void __launch_bounds__(256, GM_DOT_SLICE_MINB) edge_dot_slice_kernel(
+    const int32_t* __restrict__ rows, const int32_t* __restrict__ col, const int32_t* __restrict__ perm, int64_t k0,
+    int64_t e, int64_t per_warp, const float* __restrict__ a, const float* __restrict__ b, int64_t f, int stride,
+    float* __restrict__ out, const uint8_t* __restrict__ src_class, int hot_limit) {
+  constexpr unsigned FULL = 0xffffffffu;
+  // the forward sweep's L2 residency scheme for the gathered source rows:
+  // the plan's hot rows evict_last, the rest streamed
+  uint64_t pol_hot;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_hot));
+  extern __shared__ __align__(16) unsigned char dot_smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  float* tile = reinterpret_cast<float*>(dot_smem) + static_cast<size_t>(wib) * U * stride;
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t kb = w * per_warp;
+  if (kb >= e) return;
+  const int64_t ke = min(e, kb + per_warp);
+  const uint32_t fu = static_cast<uint32_t>(f);
+  const int nsl_all = static_cast<int>(f / 4);
+  int32_t vcur = -1;
+  float4 gcur = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t t0 = kb; t0 < ke; t0 += U) {
+    const int n_e = static_cast<int>(min(static_cast<int64_t>(U), ke - t0));
+    int32_t c = 0, r = 0, pm = 0;
+    bool hot = false;
+    if (lane < n_e) {
+      c = col[k0 + t0 + lane];
+      r = rows[k0 + t0 + lane];
+      pm = perm[k0 + t0 + lane];
+      hot = src_class && src_class[k0 + t0 + lane] < hot_limit;
+    }
+    const uint32_t hmask = __ballot_sync(FULL, hot);
+    float acc = 0.f;
+    for (int sb = 0; sb < nsl_all; sb += 32) {  // column passes of 32 16-byte slots
+      const int nsl = min(32, nsl_all - sb);
+      const uint32_t soff = static_cast<uint32_t>(sb + min(lane, nsl - 1)) * 4u;
+      float4 xv[U];
+#pragma unroll
+      for (int t = 0; t < U; ++t) {
+        const uint32_t u = static_cast<uint32_t>(__shfl_sync(FULL, c, t));
+        const float4* src = reinterpret_cast<const float4*>(b + static_cast<uint64_t>(u) * fu + soff);
+        const int ht = static_cast<int>((hmask >> t) & 1u);
+#if GM_DOT_SLICE_COLD
+        asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+            "@q ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %6;\n\t"
+            "@!q ld.global.cs.nc.v4.f32 {%0,%1,%2,%3}, [%4];\n\t}"
+            : "=f"(xv[t].x), "=f"(xv[t].y), "=f"(xv[t].z), "=f"(xv[t].w)
+            : "l"(src), "r"(ht), "l"(pol_hot));
+#else
+        asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+            "@q ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %6;\n\t"
+            "@!q ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];\n\t}"
+            : "=f"(xv[t].x), "=f"(xv[t].y), "=f"(xv[t].z), "=f"(xv[t].w)
+            : "l"(src), "r"(ht), "l"(pol_hot));
+#endif
+      }
+      if (nsl_all > 32) vcur = -1;  // the cached destination slice is per column pass
+#pragma unroll
+      for (int t = 0; t < U; ++t) {
+        const int32_t v = __shfl_sync(FULL, r, t);
+        if (t < n_e) {
+          if (v != vcur) {
+            gcur = __ldg(reinterpret_cast<const float4*>(a + static_cast<uint64_t>(static_cast<uint32_t>(v)) * fu + soff));
+            vcur = v;
+          }
+          if (lane < nsl)
+            *reinterpret_cast<float4*>(tile + t * stride + (soff - sb * 4)) =
+                make_float4(__fmul_rn(gcur.x, xv[t].x), __fmul_rn(gcur.y, xv[t].y), __fmul_rn(gcur.z, xv[t].z),
+                            __fmul_rn(gcur.w, xv[t].w));
+        }
+      }
+      __syncwarp();
+      if (lane < n_e) {
+        const float4* pr = reinterpret_cast<const float4*>(tile + lane * stride);
+        for (int q = 0; q < nsl; ++q) {
+          const float4 p4 = pr[q];
+          acc = __fadd_rn(acc, p4.x);
+          acc = __fadd_rn(acc, p4.y);
+          acc = __fadd_rn(acc, p4.z);
+          acc = __fadd_rn(acc, p4.w);
+        }
+      }
+      __syncwarp();
+    }
+    if (lane < n_e) out[pm] = acc;
+  }
+}
+
 __global__ void entry_rows_kernel(const int64_t* __restrict__ rowptr, int64_t rows, int32_t* __restrict__ out) {
   // one warp per row: the row id for each of its entries (positions relative to rowptr[0])
   const int lane = threadIdx.x & 31;
@@ -347,6 +453,36 @@ GM_API gm_status gm_edge_dot_csc(gm_dtype dtype, const gm_csr* csc, const gm_spm
   GM_TRY_CUDA(cudaStreamSynchronize(st));
   // entry_rows is indexed from the view's first entry: pass it pre-offset by -k0
   static const bool v4_env = [] { const char* ev = getenv("GM_EDGE_DOT_V4"); return !(ev && ev[0] == '0'); }();
+  // column-slice kernel (default; GM_EDGE_DOT_SLICE=0 selects the row-staged v4
+  // kernel): same-box C4 6.56 vs 7.57 ms, sub-batches of 4/6/8/16 entries
+  // 8.13/6.77/6.56/7.26 ms, 64-512 entries per warp alike, 80 registers 7.0 ms
+  static const bool slice_env = [] { const char* ev = getenv("GM_EDGE_DOT_SLICE"); return !(ev && ev[0] == '0'); }();
+  if (dtype == GM_F32 && slice_env && f % 4 == 0 &&
+      ((reinterpret_cast<uintptr_t>(a_by_dst) | reinterpret_cast<uintptr_t>(b_by_src)) & 15) == 0) {
+    constexpr int kU = GM_DOT_SLICE_U;
+    // tile row stride: one column pass (<= 128 floats) + 4, an odd number of
+    // 16-byte units (conflict-free float4 reads of 8 consecutive rows)
+    int stride = static_cast<int>(std::min<int64_t>(f, 128));
+    if ((stride / 4) % 2 == 0) stride += 4;
+    const size_t smem = sizeof(float) * kU * stride * 8;
+    GM_TRY_CUDA(cudaFuncSetAttribute(edge_dot_slice_kernel<kU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+    static const int64_t per_warp = [] { const char* ev = getenv("GM_EDGE_DOT_PER_WARP"); return ev ? atoll(ev) : 256; }();
+    const int64_t warps = ceil_div(csc->nnz, per_warp);
+    // L2 residency of hot source rows: the same budget rule as gm_spmm
+    const uint8_t* cls = nullptr;
+    int limit = 0;
+    if (plan && plan->src_class && plan->l2_hot_bytes > 0) {
+      const double hot_rows = static_cast<double>(plan->l2_hot_bytes) / static_cast<double>(f * 4);
+      limit = static_cast<int>(std::floor(4.0 * std::log2(1.0 + hot_rows)));
+      if (plan->hot_edge_frac[std::min(limit, GM_PLAN_CLASSES - 1)] >= 0.15) cls = plan->src_class;
+    }
+    edge_dot_slice_kernel<kU><<<static_cast<unsigned>(ceil_div(warps, 8)), 256, smem, st>>>(
+        entry_rows - k0, csc->col, csc->perm, k0, csc->nnz, per_warp, static_cast<const float*>(a_by_dst),
+        static_cast<const float*>(b_by_src), f, stride, static_cast<float*>(out), cls, limit);
+    GM_CHECK_LAUNCH("edge_dot_slice_kernel");
+    return GM_OK;
+  }
   if (dtype == GM_F32 && v4_env && f % 4 == 0 &&
       ((reinterpret_cast<uintptr_t>(a_by_dst) | reinterpret_cast<uintptr_t>(b_by_src)) & 15) == 0) {
     // column chunk per staged unit (GM_EDGE_DOT_CHUNK: 16 / 32 / 64 / 128 floats)

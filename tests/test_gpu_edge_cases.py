@@ -82,3 +82,40 @@ def test_build_compressed_single_row_and_all_in_one_row():
     assert rp.tolist() == [0, 5000]
     assert np.array_equal(perm.numpy(), np.arange(5000))          # stable: COO order kept
     assert np.array_equal(col.numpy(), np.arange(5000)[::-1])
+
+
+@pytest.mark.parametrize("slice_kernel", ["1", "0"])
+def test_edge_dot_on_a_row_slice(slice_kernel, monkeypatch):
+    """gm_edge_dot_csc over a CSC row slice (rowptr[0] != 0, as a multi-GPU rank
+    holds it) writes exactly the slice's entries, equal to the full call's."""
+    import ctypes as C
+    import subprocess
+    import sys
+    code = f"""
+import ctypes as C, torch, numpy as np, sys
+sys.path.insert(0, {repr(str(__import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__)))))})
+import paper_2507_16991_b200 as gm
+from paper_2507_16991_b200 import _lib as L
+n, e, f = 3000, 90000, 20
+s = torch.empty(e, dtype=torch.int64, device='cuda'); d = torch.empty_like(s)
+L.check(L.lib().gm_synth_edges(1, 5, 0, e, n, n, s.data_ptr(), d.data_ptr(), None))
+g = gm.EdgeIndex(s, d, n, n); csc = g.to_csc()
+x = torch.randn(n, f, device='cuda'); go = torch.randn(n, f, device='cuda')
+def run(view, rows, a):  # a: the gradient rows of the view's destinations (local row ids)
+    out = torch.full((e,), float('nan'), device='cuda')
+    cs = view.c_struct()
+    L.check(L.lib().gm_edge_dot_csc(L.GM_F32, C.byref(cs), C.byref(csc.plan()), rows.data_ptr(), a.data_ptr(), x.data_ptr(), f, out.data_ptr(), None))
+    torch.cuda.synchronize(); return out
+full = run(csc, csc.entry_rows(), go)
+rp = csc.rowptr.cpu().numpy(); r0, r1 = 1000, 2200
+view = csc.row_slice(r0, r1, int(rp[r1] - rp[r0]))
+part = run(view, view.entry_rows(), go[r0:])
+sel = csc.perm[int(rp[r0]):int(rp[r1])].long()
+assert torch.equal(part[sel], full[sel])
+mask = torch.ones(e, dtype=torch.bool, device='cuda'); mask[sel] = False
+assert bool(torch.isnan(part[mask]).all())
+print('ok')
+"""
+    env = dict(__import__('os').environ, GM_EDGE_DOT_SLICE=slice_kernel)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
