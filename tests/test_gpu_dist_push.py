@@ -47,7 +47,8 @@ def _ranks(g, n, world):
 
 @pytest.mark.parametrize("world", [2, 3, 4])
 @pytest.mark.parametrize("dtype,f,reduce", [(torch.float32, 100, "sum"), (torch.float32, 33, "mean"),
-                                             (torch.bfloat16, 128, "sum"), (torch.bfloat16, 64, "mean")])
+                                             (torch.bfloat16, 128, "sum"), (torch.bfloat16, 64, "mean"),
+                                             (torch.float32, 8, "sum"), (torch.float32, 602, "mean")])
 @pytest.mark.parametrize("halo", [False, True])
 def test_push_two_layers_bit_identical(world, dtype, f, reduce, halo):
     n, e = 20000, 900_000   # power-law: hub rows take the hub kernel's push path too
