@@ -46,6 +46,9 @@ def check(keys, values, n_rows):
     (1, 300_000, 12_000_000),   # many entry-count cuts
     (1, 4_000_000, 9_000_000),  # 22-bit keys: two 11-bit LSD passes
     (0, 40_000_000, 1_500_000), # 26-bit keys: three 9-bit passes, mostly empty rows
+    (0, 1000, 5001),            # odd edge counts: the TMA scatter's tail element
+    (1, 70_000, 1_234_567),
+    (0, 9, 1),
 ])
 def test_bucketed_build_bit_exact(kind, n, e):
     src, dst = synth(kind, n, n, e, seed=n + e)
