@@ -399,7 +399,8 @@ GM_API gm_status gm_spmm_accumulate(const gm_csr* csr, const gm_spmm_plan* plan,
  *    process: CUDA IPC / VMM over NVLink). push_mask[r] bit q selects peer q
  *    for local row r (NULL: every peer). The caller orders the peers' later
  *    reads after this call (e.g. a collective on `stream`). push_mask bit j
- *    refers to push_dst[j]. Unweighted sum/mean layers only. */
+ *    refers to push_dst[j]. Unweighted layers (sum / mean / max / min: the
+ *    values are pushed, arg_out stays local). */
 #define GM_MAX_PUSH 8
 typedef enum { GM_CARRY_NONE = 0, GM_CARRY_START = 1, GM_CARRY_CONTINUE = 2, GM_CARRY_FINISH = 3 } gm_carry_mode;
 typedef struct gm_spmm_epilogue {

@@ -584,7 +584,8 @@ class DistSpmm {
 // each peer's replica of the next layer's input — device pointers mapped into
 // this process, e.g. by gm_ipc_open_handle over NVLink. mask (optional, one
 // word per local row): bit j = push to peers[j]. The caller orders the peers'
-// reads after the call (a collective on the stream). Sum/mean layers.
+// reads after the call (a collective on the stream). Any unweighted
+// aggregation; max/min also write this rank's argmax (local rows).
 class PushSpmm {
  public:
   PushSpmm(const CsrView& csc, Index r0, Index r1, std::vector<void*> peers,
@@ -601,8 +602,10 @@ class PushSpmm {
   }
 
   template <class S>
-  void operator()(const DeviceMatrix<S>& x, DeviceMatrix<S>& out_next, AggKind kind) const {
-    if (kind != AggKind::sum && kind != AggKind::mean) throw std::invalid_argument("PushSpmm: sum or mean");
+  void operator()(const DeviceMatrix<S>& x, DeviceMatrix<S>& out_next, AggKind kind,
+                  DeviceArray<std::int32_t>* argmax = nullptr) const {
+    const bool mm = kind == AggKind::max || kind == AggKind::min;
+    if (mm && !argmax) throw std::invalid_argument("PushSpmm: max/min need the argmax of this rank's rows");
     if (x.rows() != csc_.num_cols || out_next.rows() != x.rows() || out_next.cols() != x.cols())
       throw std::invalid_argument("PushSpmm: x / out_next must be [num_nodes, F] replicas");
     gm_spmm_epilogue ep{};
@@ -610,9 +613,11 @@ class PushSpmm {
     for (std::size_t q = 0; q < peers_.size(); ++q) ep.push_dst[q] = peers_[q];
     ep.push_row0 = r0_;
     ep.push_mask = mask_ ? mask_->data() : nullptr;
-    detail::check(gm_spmm_ex(&slice_, &plan_, detail::dtype_of<S>(), x.data(), x.cols(), nullptr,
-                             kind == AggKind::sum ? GM_SUM : GM_MEAN, 0, nullptr, &ep,
-                             out_next.data() + r0_ * x.cols(), nullptr, stream()));
+    if (mm) *argmax = DeviceArray<std::int32_t>(static_cast<std::size_t>((r1_ - r0_) * x.cols()));
+    const gm_reduce r = kind == AggKind::sum ? GM_SUM : kind == AggKind::mean ? GM_MEAN
+                        : kind == AggKind::max ? GM_MAX : GM_MIN;
+    detail::check(gm_spmm_ex(&slice_, &plan_, detail::dtype_of<S>(), x.data(), x.cols(), nullptr, r, 0, nullptr, &ep,
+                             out_next.data() + r0_ * x.cols(), mm ? argmax->data() : nullptr, stream()));
   }
 
  private:

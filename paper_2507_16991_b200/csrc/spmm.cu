@@ -318,12 +318,12 @@ static gm_status spmm_impl(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype
              GM_ERR_INVALID_ARGUMENT, "gm_spmm_ex: the fp32 carry applies to bf16 sum/mean");
   GM_REQUIRE(!carry || (ep->carry_mode == GM_CARRY_START) == (accum == 0), GM_ERR_INVALID_ARGUMENT,
              "gm_spmm_ex: GM_CARRY_START starts the rows (accumulate = 0); CONTINUE/FINISH continue them");
-  GM_REQUIRE(!push || (ep->n_push <= GM_MAX_PUSH && !maxmin && !gcn), GM_ERR_INVALID_ARGUMENT,
-             "gm_spmm_ex: push carries sum/mean layers to <= GM_MAX_PUSH peers (no fused GCN term)");
+  GM_REQUIRE(!push || (ep->n_push <= GM_MAX_PUSH && !gcn), GM_ERR_INVALID_ARGUMENT,
+             "gm_spmm_ex: push targets <= GM_MAX_PUSH peers (no fused GCN term)");
   GM_REQUIRE(!(carry && push && ep->carry_mode != GM_CARRY_FINISH), GM_ERR_INVALID_ARGUMENT,
              "gm_spmm_ex: rows are pushed by the block that finishes them");
   GM_REQUIRE(!(carry || push) || !edge_weight, GM_ERR_INVALID_ARGUMENT,
-             "gm_spmm_ex: the carry / push epilogue takes unweighted sum/mean layers");
+             "gm_spmm_ex: the carry / push epilogue takes unweighted layers");
   if (csr->num_rows == 0 || f == 0) return GM_OK;
   GM_REQUIRE(x && out, GM_ERR_INVALID_ARGUMENT, "gm_spmm: null x/out");
   if (push)

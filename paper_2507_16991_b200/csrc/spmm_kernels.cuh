@@ -576,7 +576,7 @@ __global__ void __launch_bounds__(256) spmm_light_kernel(const SpmmArgs p) {
 #pragma unroll
     for (int j = 0; j < NV; ++j)
       if (valid[j]) {
-        epi_store<T, VecT, !MAXMIN>(p, out, static_cast<uint64_t>(r) * p.f + slot[j] * V, r, acc.v[j]);
+        epi_store<T, VecT, true>(p, out, static_cast<uint64_t>(r) * p.f + slot[j] * V, r, acc.v[j]);
         if (want_arg) {
           int32_t* arow = p.arg + static_cast<int64_t>(r) * p.f + slot[j] * V;
           store_arg<V>(arow, acc.a[j]);
@@ -706,7 +706,7 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 8 || (SCALED && (MODE >= 2 
 #pragma unroll
     for (int j = 0; j < NV; ++j)
       if (valid[j]) {
-        epi_store<T, VecT, EPI && !MAXMIN>(p, out, obase + soff[j], row, acc.v[j]);
+        epi_store<T, VecT, EPI>(p, out, obase + soff[j], row, acc.v[j]);
         if (want_arg) {
           int32_t* arow = p.arg + obase + soff[j];
           store_arg<V>(arow, acc.a[j]);
@@ -874,7 +874,7 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 8 || (SCALED && (MODE >= 2 
   while (row < rb) flush();
   // pushed rows must be visible to the peers before the caller's collective
   // releases their next read
-  if (EPI && !MAXMIN && p.n_push) __threadfence_system();
+  if (EPI && p.n_push) __threadfence_system();
 }
 
 // ---------------------------------------------------------------------------
@@ -1057,7 +1057,7 @@ __global__ void __launch_bounds__(kHeavyThreads) spmm_heavy_kernel(const SpmmArg
   for (int m = 0; m < MH; ++m) {
     const int s = t + m * kHeavyThreads;
     if (s < nslots) {
-      epi_store<T, VecT, !MAXMIN>(p, static_cast<T*>(p.out),
+      epi_store<T, VecT, true>(p, static_cast<T*>(p.out),
                                   static_cast<uint64_t>(r) * p.f + (p.slot_base + s) * V, r, acc.v[m]);
       if (want_arg) {
         int32_t* arow = p.arg + static_cast<int64_t>(r) * p.f + (p.slot_base + s) * V;
@@ -1330,7 +1330,7 @@ __global__ void __launch_bounds__(64) spmm_hub_kernel(const SpmmArgs p) {
 #pragma unroll
   for (int j = 0; j < LE; ++j) tmp[j] = narrow<T, A>(v[j]);
   memcpy(orow + e0, tmp, LB);
-  if (!MAXMIN && p.n_push) {
+  if (p.n_push) {
     const uint32_t m = p.push_mask ? p.push_mask[r] : 0xffffffffu;
     const int64_t ge = (p.push_row0 + r) * p.f + e0;
 #pragma unroll
@@ -1392,12 +1392,10 @@ gm_status launch_flat(const SpmmArgs& p0, int64_t ns, cudaStream_t st) {
   } while (0)
 #define GM_FLAT_K(NV_, U_, M_)                                                                     \
   do {                                                                                             \
-    if constexpr (M_ < 2) {                                                                        \
-      if (epi) {  /* carry / push epilogue: unscaled sum/mean, own instantiations */               \
-        if (p.accum) spmm_flat_kernel<T, VB, NV_, U_, M_, false, true, 1, true><<<grid, 256, 0, st>>>(p); \
-        else spmm_flat_kernel<T, VB, NV_, U_, M_, false, false, 1, true><<<grid, 256, 0, st>>>(p);        \
-        break;                                                                                     \
-      }                                                                                            \
+    if (epi) {  /* carry / push epilogue: unweighted layers, own instantiations */                  \
+      if (p.accum) spmm_flat_kernel<T, VB, NV_, U_, M_, false, true, 1, true><<<grid, 256, 0, st>>>(p);   \
+      else spmm_flat_kernel<T, VB, NV_, U_, M_, false, false, 1, true><<<grid, 256, 0, st>>>(p);          \
+      break;                                                                                       \
     }                                                                                              \
     if (lm == 2) {                                                                                 \
       if (scaled) spmm_flat_kernel<T, VB, NV_, U_, M_, true, false, 2><<<grid, 256, 0, st>>>(p);     \

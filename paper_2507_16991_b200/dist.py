@@ -516,10 +516,15 @@ class PushSpmm:
         assert world - 1 <= L.GM_MAX_PUSH, "push mode targets at most GM_MAX_PUSH peers"
         self.rows, self.r0, self.r1, self.rank, self.world, self.mask = rows, r0, r1, rank, world, mask
 
-    def __call__(self, x: torch.Tensor, out_next: torch.Tensor, peer_ptrs, reduce: str = "sum"):
+    def __call__(self, x: torch.Tensor, out_next: torch.Tensor, peer_ptrs, reduce: str = "sum",
+                 arg: Optional[torch.Tensor] = None):
+        """max/min: the values are pushed; the argmax of this rank's rows goes
+        to `arg` ([r1 - r0, F] int32, allocated when None) and is returned."""
         from .graphmill import _DT, _KIND, _p, _stream
-        assert reduce in ("sum", "mean"), "push mode carries sum/mean layers"
+        maxmin = reduce in ("max", "min")
         f = x.shape[1]
+        if maxmin and arg is None:
+            arg = torch.empty(self.r1 - self.r0, f, dtype=torch.int32, device=x.device)
         lib = L.lib()
         ep = L.gm_spmm_epilogue()
         n = 0
@@ -533,8 +538,9 @@ class PushSpmm:
         cs = self.rows.c_struct()
         plan = self.rows.plan(f * x.element_size())
         L.check(lib.gm_spmm_ex(C.byref(cs), C.byref(plan), _DT[x.dtype], _p(x), f, None, _KIND[reduce], 0, None,
-                               C.byref(ep), _p(out_next[self.r0:self.r1]), None, _stream()), "gm_spmm_ex (push)")
-        return out_next
+                               C.byref(ep), _p(out_next[self.r0:self.r1]), _p(arg) if maxmin else None, _stream()),
+                "gm_spmm_ex (push)")
+        return (out_next, arg) if maxmin else out_next
 
 
 # ---------------------------------------------------------------------------

@@ -403,5 +403,15 @@ TEST_CASE("PushSpmm: two virtual ranks push their rows into each other's next-la
   const auto want = neighbor_aggregate(e, x0, AggKind::mean).to_host();
   CHECK(b0.to_host() == want);
   CHECK(b1.to_host() == want);
-  CHECK_THROWS_AS(rank0(x0, b0, AggKind::max), std::invalid_argument);
+  CHECK_THROWS_AS(rank0(x0, b0, AggKind::max), std::invalid_argument);  // max needs the argmax buffer
+  DeviceArray<std::int32_t> arg0, arg1, want_arg;
+  rank0(x0, b0, AggKind::max, &arg0);
+  rank1(x1, b1, AggKind::max, &arg1);
+  const auto want_max = neighbor_aggregate(e, x0, AggKind::max, &want_arg).to_host();
+  CHECK(b0.to_host() == want_max);
+  CHECK(b1.to_host() == want_max);
+  auto wa = want_arg.to_host();
+  auto a0 = arg0.to_host(), a1 = arg1.to_host();
+  a0.insert(a0.end(), a1.begin(), a1.end());
+  CHECK(a0 == wa);
 }

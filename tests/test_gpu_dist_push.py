@@ -48,7 +48,8 @@ def _ranks(g, n, world):
 @pytest.mark.parametrize("world", [2, 3, 4])
 @pytest.mark.parametrize("dtype,f,reduce", [(torch.float32, 100, "sum"), (torch.float32, 33, "mean"),
                                              (torch.bfloat16, 128, "sum"), (torch.bfloat16, 64, "mean"),
-                                             (torch.float32, 8, "sum"), (torch.float32, 602, "mean")])
+                                             (torch.float32, 8, "sum"), (torch.float32, 602, "mean"),
+                                             (torch.float32, 100, "max"), (torch.bfloat16, 128, "min")])
 @pytest.mark.parametrize("halo", [False, True])
 def test_push_two_layers_bit_identical(world, dtype, f, reduce, halo):
     n, e = 20000, 900_000   # power-law: hub rows take the hub kernel's push path too
@@ -66,11 +67,20 @@ def test_push_two_layers_bit_identical(world, dtype, f, reduce, halo):
     A = [x.clone() for _ in range(world)]
     B = [torch.full_like(x, float("nan")) for _ in range(world)]
     ops = [PushSpmm(v, r0, r1, r, world, masks[r]) for r, (r0, r1, v) in enumerate(ranks)]
-    want1 = gm.spmm(g, x, None, reduce)
-    want2 = gm.spmm(g, want1, None, reduce)
-    for src_bufs, dst_bufs, want in ((A, B, want1), (B, A, want2)):
+    maxmin = reduce in ("max", "min")
+    if maxmin:
+        want1, warg1 = gm.neighbor_aggregate(g, x, reduce, return_argmax=True)
+        want2, warg2 = gm.neighbor_aggregate(g, want1, reduce, return_argmax=True)
+    else:
+        want1 = gm.spmm(g, x, None, reduce)
+        want2 = gm.spmm(g, want1, None, reduce)
+        warg1 = warg2 = None
+    for src_bufs, dst_bufs, want, warg in ((A, B, want1, warg1), (B, A, want2, warg2)):
         for r in range(world):
-            ops[r](src_bufs[r], dst_bufs[r], [t.data_ptr() for t in dst_bufs], reduce)
+            res = ops[r](src_bufs[r], dst_bufs[r], [t.data_ptr() for t in dst_bufs], reduce)
+            if maxmin:
+                r0, r1 = ranks[r][0], ranks[r][1]
+                assert torch.equal(res[1], warg[r0:r1]), ("argmax", r)
         torch.cuda.synchronize()
         for q, (r0, r1, v) in enumerate(ranks):
             got = dst_bufs[q]
@@ -92,9 +102,6 @@ def test_push_validation():
     n, e, f = 2000, 20000, 8
     src, dst, g, x = _graph(n, e, f, torch.float32)
     (r0, r1, v), = _ranks(g, n, 1)
-    op = PushSpmm(v, r0, r1, 0, 1)
-    with pytest.raises(AssertionError):
-        op(x, torch.empty_like(x), [x.data_ptr()], "max")
     ep = L.gm_spmm_epilogue()
     ep.n_push = L.GM_MAX_PUSH + 1
     cs = v.c_struct()
