@@ -555,7 +555,7 @@ def main_multi(args, world, rank, local):
             "push_numerics": push_check,
             "roofline": roof, "cpu_baseline": None, "e2e": None, "gpu_launches": launches * args.steps,
             "clocks": clk.summary(), "secondary": secondary,
-            "per_step_ms": {"min": min(per_step), "median": statistics.median(per_step), "max": max(per_step)},
+            "per_step_ms": {"min": min(per_step), "median": statistics.median(per_step), "max": max(per_step), "mean": statistics.mean(per_step), "std": statistics.pstdev(per_step)},
         }))
     dist.destroy_process_group()
 
@@ -794,7 +794,7 @@ def main():
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(), "secondary": secondary,
-            "per_step_ms": {"min": min(per_step), "median": statistics.median(per_step), "max": max(per_step)},
+            "per_step_ms": {"min": min(per_step), "median": statistics.median(per_step), "max": max(per_step), "mean": statistics.mean(per_step), "std": statistics.pstdev(per_step)},
         }
         print(json.dumps(line))
 
