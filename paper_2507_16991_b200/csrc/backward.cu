@@ -7,6 +7,7 @@
 // reference's order (sequential in j), so results are bit-identical.
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 
 #include "vec.cuh"
 
@@ -396,6 +397,144 @@ __global__ void __launch_bounds__(256, GM_DOT_SLICE_MINB) edge_dot_slice_kernel(
   }
 }
 
+// Staged column-slice form: the slice kernel's coalesced gathers, but issued as
+// 16-byte cp.async into an S-stage shared-memory ring per warp instead of
+// registers, so S-1 sub-batches of U source rows stay in flight while the
+// lanes form products and run the chains of the oldest one (no register cost
+// for the in-flight data). The destination row's slice is staged beside the
+// source rows, once per run of equal destinations within a sub-batch (the
+// first entry of each run copies it; the others read that slot). Products are
+// written in place over the source slices; lane t < U then adds row t in j
+// order — the reference's mul-then-add chain, bit-identical. Rows of <= 128
+// floats (one column pass); each warp walks one contiguous entry range.
+template <int U, int S>
+__global__ void __launch_bounds__(128) edge_dot_staged_kernel(
+    const int32_t* __restrict__ rows, const int32_t* __restrict__ col, const int32_t* __restrict__ perm, int64_t k0,
+    int64_t e, int64_t per_warp, const float* __restrict__ a, const float* __restrict__ b, int64_t f, int stride,
+    float* __restrict__ out, const uint8_t* __restrict__ src_class, int hot_limit, int cold_mode) {
+  constexpr unsigned FULL = 0xffffffffu;
+  uint64_t pol_hot, pol_cold;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_hot));
+  if (cold_mode == 1)
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_cold));
+  else
+    asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_cold));
+  extern __shared__ __align__(16) unsigned char dot_smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  // per warp: S stages of {x tile [U][stride] float4, g tile [U][stride] float4}, then S x U perms + S lead masks
+  const size_t stage_f4 = static_cast<size_t>(2) * U * stride;
+  float4* ring = reinterpret_cast<float4*>(dot_smem) + static_cast<size_t>(wib) * S * stage_f4;
+  int32_t* mperm = reinterpret_cast<int32_t*>(reinterpret_cast<float4*>(dot_smem) + (blockDim.x >> 5) * S * stage_f4) +
+                   static_cast<size_t>(wib) * S * (U + 1);
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t kb = w * per_warp;
+  if (kb >= e) return;
+  const int64_t ke = min(e, kb + per_warp);
+  const uint32_t fu = static_cast<uint32_t>(f);
+  const int nsl = static_cast<int>(f / 4);
+  const uint32_t soff = static_cast<uint32_t>(min(lane, nsl - 1)) * 4u;
+  const int nb = static_cast<int>((ke - kb + U - 1) / U);
+  // metadata of the next sub-batch to issue, loaded one issue ahead (its
+  // latency hides behind a whole wait + compute step)
+  int32_t c_n = 0, r_n = -1, pm_n = 0;
+  bool hot_n = false;
+  auto load_meta = [&](int bt) {
+    c_n = 0;
+    r_n = -1;
+    pm_n = 0;
+    hot_n = false;
+    const int64_t t0 = kb + static_cast<int64_t>(bt) * U;
+    if (bt < nb && t0 + lane < ke && lane < U) {
+      c_n = col[k0 + t0 + lane];
+      r_n = rows[k0 + t0 + lane];
+      pm_n = perm[k0 + t0 + lane];
+      hot_n = src_class && src_class[k0 + t0 + lane] < hot_limit;
+    }
+  };
+  auto issue = [&](int bt) {
+    if (bt < nb) {
+      const int s = bt % S;
+      float4* xs = ring + s * stage_f4;
+      float4* gs = xs + U * stride;
+      const int64_t t0 = kb + static_cast<int64_t>(bt) * U;
+      const int n_e = static_cast<int>(min(static_cast<int64_t>(U), ke - t0));
+      const int32_t c = c_n, r = r_n, pm = pm_n;
+      const bool hot = hot_n;
+      load_meta(bt + 1);
+      const int32_t rprev = __shfl_up_sync(FULL, r, 1);
+      const uint32_t lead = __ballot_sync(FULL, lane < n_e && (lane == 0 || r != rprev));
+      const uint32_t hmask = __ballot_sync(FULL, hot);
+      if (lane < U) mperm[s * (U + 1) + lane] = pm;
+      if (lane == 0) mperm[s * (U + 1) + U] = static_cast<int32_t>(lead);
+#pragma unroll
+      for (int t = 0; t < U; ++t) {
+        const uint32_t u = static_cast<uint32_t>(__shfl_sync(FULL, c, t));
+        const uint32_t v = static_cast<uint32_t>(__shfl_sync(FULL, r, t));
+        if (t < n_e && lane < nsl) {
+          const uint32_t sx = static_cast<uint32_t>(__cvta_generic_to_shared(xs + t * stride + lane));
+          const float* src = b + static_cast<uint64_t>(u) * fu + soff;
+          if (cold_mode == 2) {
+            cp_async_16_hint(sx, src, (hmask >> t) & 1u, pol_hot);
+          } else {
+            const uint64_t pol = ((hmask >> t) & 1u) ? pol_hot : pol_cold;
+            asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(sx), "l"(src), "l"(pol)
+                         : "memory");
+          }
+          if ((lead >> t) & 1u) {
+            const uint32_t sg = static_cast<uint32_t>(__cvta_generic_to_shared(gs + t * stride + lane));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sg),
+                         "l"(a + static_cast<uint64_t>(v) * fu + soff)
+                         : "memory");
+          }
+        }
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  load_meta(0);
+#pragma unroll
+  for (int p = 0; p < S - 1; ++p) issue(p);
+  for (int bt = 0; bt < nb; ++bt) {
+    issue(bt + S - 1);
+    asm volatile("cp.async.wait_group %0;" ::"n"(S - 1) : "memory");
+    __syncwarp();
+    const int s = bt % S;
+    float4* xs = ring + s * stage_f4;
+    const float4* gs = xs + U * stride;
+    const int64_t t0 = kb + static_cast<int64_t>(bt) * U;
+    const int n_e = static_cast<int>(min(static_cast<int64_t>(U), ke - t0));
+    const uint32_t lead = static_cast<uint32_t>(mperm[s * (U + 1) + U]);
+    if (lane < nsl) {
+#pragma unroll
+      for (int t = 0; t < U; ++t) {
+        if (t < n_e) {
+          const int lt = 31 - __clz(lead & ((2u << t) - 1u));
+          const float4 xv = xs[t * stride + lane];
+          const float4 gv = gs[lt * stride + lane];
+          xs[t * stride + lane] = make_float4(__fmul_rn(gv.x, xv.x), __fmul_rn(gv.y, xv.y), __fmul_rn(gv.z, xv.z),
+                                              __fmul_rn(gv.w, xv.w));
+        }
+      }
+    }
+    __syncwarp();
+    if (lane < n_e) {
+      const float4* pr = xs + lane * stride;
+      float acc = 0.f;
+#pragma unroll 4
+      for (int q = 0; q < nsl; ++q) {
+        const float4 p4 = pr[q];
+        acc = __fadd_rn(acc, p4.x);
+        acc = __fadd_rn(acc, p4.y);
+        acc = __fadd_rn(acc, p4.z);
+        acc = __fadd_rn(acc, p4.w);
+      }
+      out[mperm[s * (U + 1) + lane]] = acc;
+    }
+    __syncwarp();  // stage s is refilled by the issue of sub-batch bt + S
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
 __global__ void entry_rows_kernel(const int64_t* __restrict__ rowptr, int64_t rows, int32_t* __restrict__ out) {
   // one warp per row: the row id for each of its entries (positions relative to rowptr[0])
   const int lane = threadIdx.x & 31;
@@ -457,6 +596,57 @@ GM_API gm_status gm_edge_dot_csc(gm_dtype dtype, const gm_csr* csc, const gm_spm
   // kernel): same-box C4 6.56 vs 7.57 ms, sub-batches of 4/6/8/16 entries
   // 8.13/6.77/6.56/7.26 ms, 64-512 entries per warp alike, 80 registers 7.0 ms
   static const bool slice_env = [] { const char* ev = getenv("GM_EDGE_DOT_SLICE"); return !(ev && ev[0] == '0'); }();
+  // staged column-slice kernel, an A/B variant (GM_DOT_STAGED=U,S selects the ring
+  // shape, unset/0 keeps the slice kernel): bit-identical but 14.2-14.6 ms on C4
+  // for every ring shape (8,3 / 8,4 / 4,4 / 4,6 / 16,2 / 16,3) vs 6.55 — at 8-16
+  // resident warps per SM (ring-limited) the chains run on U lanes and the warp
+  // issues ~780 instructions per sub-batch (6.0G in all, 35% issue active)
+  static const int staged_cfg = [] {
+    const char* ev = getenv("GM_DOT_STAGED");
+    if (!ev) return 0;
+    if (ev[0] == '0') return 0;
+    return atoi(ev) * 10 + (strchr(ev, ',') ? atoi(strchr(ev, ',') + 1) : 3);
+  }();
+  if (dtype == GM_F32 && staged_cfg && f % 4 == 0 && f <= 128 &&
+      ((reinterpret_cast<uintptr_t>(a_by_dst) | reinterpret_cast<uintptr_t>(b_by_src)) & 15) == 0) {
+    const int nsl = static_cast<int>(f / 4);
+    const int stride = nsl | 1;  // odd 16-byte units: conflict-free float4 reads of consecutive rows
+    const uint8_t* cls = nullptr;
+    int limit = 0;
+    if (plan && plan->src_class && plan->l2_hot_bytes > 0) {
+      const double hot_rows = static_cast<double>(plan->l2_hot_bytes) / static_cast<double>(f * 4);
+      limit = static_cast<int>(std::floor(4.0 * std::log2(1.0 + hot_rows)));
+      if (plan->hot_edge_frac[std::min(limit, GM_PLAN_CLASSES - 1)] >= 0.15) cls = plan->src_class;
+    }
+    // cold source rows: 2 plain cp.async (hot rows alone carry the evict_last hint), 1 evict_first, 0 evict_normal hint
+    static const int cold_first = [] { const char* ev = getenv("GM_DOT_STAGED_COLD"); return ev ? atoi(ev) : 2; }();
+    static const int64_t pw_env = [] { const char* ev = getenv("GM_DOT_STAGED_PER_WARP"); return ev ? atoll(ev) : 0; }();
+    auto launch = [&](auto kern, int U, int S) -> gm_status {
+      const size_t smem = static_cast<size_t>(4) * (static_cast<size_t>(S) * 2 * U * stride * 16 + S * (U + 1) * 4);
+      GM_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      int per_sm = 0;
+      GM_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
+      int dev = 0, sms = kNumSMs;
+      if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const int64_t resident = static_cast<int64_t>(std::max(per_sm, 1)) * sms * 4;
+      int64_t per_warp = pw_env > 0 ? pw_env : ceil_div(csc->nnz, resident);
+      per_warp = std::max<int64_t>(ceil_div(per_warp, U) * U, U);
+      const int64_t warps = ceil_div(csc->nnz, per_warp);
+      kern<<<static_cast<unsigned>(ceil_div(warps, 4)), 128, smem, st>>>(
+          entry_rows - k0, csc->col, csc->perm, k0, csc->nnz, per_warp, static_cast<const float*>(a_by_dst),
+          static_cast<const float*>(b_by_src), f, stride, static_cast<float*>(out), cls, limit, cold_first);
+      GM_CHECK_LAUNCH("edge_dot_staged_kernel");
+      return GM_OK;
+    };
+    switch (staged_cfg) {
+      case 44: return launch(edge_dot_staged_kernel<4, 4>, 4, 4);
+      case 46: return launch(edge_dot_staged_kernel<4, 6>, 4, 6);
+      case 84: return launch(edge_dot_staged_kernel<8, 4>, 8, 4);
+      case 162: return launch(edge_dot_staged_kernel<16, 2>, 16, 2);
+      case 163: return launch(edge_dot_staged_kernel<16, 3>, 16, 3);
+      default: return launch(edge_dot_staged_kernel<8, 3>, 8, 3);
+    }
+  }
   if (dtype == GM_F32 && slice_env && f % 4 == 0 &&
       ((reinterpret_cast<uintptr_t>(a_by_dst) | reinterpret_cast<uintptr_t>(b_by_src)) & 15) == 0) {
     constexpr int kU = GM_DOT_SLICE_U;
