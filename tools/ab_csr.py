@@ -21,5 +21,9 @@ ref = gm.build_compressed(dst, src, bench.N_NODES)
 per = bench.timed_steps(lambda: gm.build_compressed(dst, src, bench.N_NODES), 10, flush)
 v = gm.build_compressed(dst, src, bench.N_NODES)
 same = bool(torch.equal(v.perm, ref.perm) and torch.equal(v.col, ref.col) and torch.equal(v.rowptr, ref.rowptr))
-print(json.dumps({"env": {k: os.environ.get(k) for k in ("GM_CSR_ALGO", "GM_RADIX_BITS")},
+def h(t):
+    t = t.to(torch.int64)
+    return int((t * torch.arange(1, t.numel() + 1, device=t.device, dtype=torch.int64) % 1000003).sum().item())
+print(json.dumps({"env": {k: os.environ.get(k) for k in ("GM_CSR_ALGO", "GM_RADIX_BITS", "GM_CSR_ONESWEEP")},
+                  "hash": [h(v.rowptr), h(v.col), h(v.perm)],
                   "ms": round(statistics.mean(per), 4), "min": round(min(per), 4), "repeatable": same}))
