@@ -388,7 +388,25 @@ static gm_status spmm_impl(const gm_csr* csr, const gm_spmm_plan* plan, gm_dtype
   static const int stream_env = [] { const char* e = getenv("GM_STREAM_X"); return e ? atoi(e) : -1; }();
   p.stream_x = stream_env >= 0 ? stream_env
                                : static_cast<double>(csr->num_cols) * static_cast<double>(rowbytes) > 64.0 * (1 << 20);
-  if (plan->src_class && plan->l2_hot_bytes > 0) {
+  // L2 column blocking, an A/B variant (GM_L2_BLOCK_MB = budget in MB; unset/0
+  // disables): when X is far larger than L2 but its rows are re-read many times
+  // (E >= 16 x source rows) and a column block of >= 128 bytes per row fits the
+  // budget, the columns are processed block by block so each block's gathers
+  // can hit L2 after the first touch. Bit-identical, but on Reddit-shaped C2
+  // (233k rows of 2408 bytes, 492 reads per row) mean 53.7 -> 84-128 ms and max
+  // 64 -> 165-259 ms for budgets of 32-96 MB: a 256-byte block still misses L2
+  // on 45% of its sectors (9.5 GB of DRAM per block) while every block repeats
+  // the per-edge metadata and issue work of the sweep (profiles/r02l2b_*)
+  static const double blk_mb = [] { const char* e = getenv("GM_L2_BLOCK_MB"); return e ? atof(e) : 0.0; }();
+  if (blk_mb > 0 && p.stream_x && stream_env < 0 && csr->num_cols > 0 && csr->nnz >= 16 * csr->num_cols &&
+      gcn == nullptr) {
+    const int64_t fit = static_cast<int64_t>(blk_mb * (1 << 20) / static_cast<double>(csr->num_cols)) / vb;
+    if (fit * vb >= 128 && fit < ns) {
+      p.l2_block_slots = fit >= 32 ? fit / 32 * 32 : fit;
+      p.stream_x = 0;  // block rows are meant to stay: default-priority gathers
+    }
+  }
+  if (p.l2_block_slots == 0 && plan->src_class && plan->l2_hot_bytes > 0) {
     // rows that fit the budget: rank < hot_rows  <=>  class < floor(4*log2(1 + hot_rows))
     const double hot_rows = static_cast<double>(plan->l2_hot_bytes) / static_cast<double>(rowbytes);
     const int limit = static_cast<int>(std::floor(4.0 * std::log2(1.0 + hot_rows)));

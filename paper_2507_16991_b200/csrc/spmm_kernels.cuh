@@ -52,6 +52,9 @@ struct SpmmArgs {
   int64_t f;                 // elements per row
   int64_t slot_base;         // first VB-byte slot of this column chunk
   int64_t slot_end;          // one past the last slot of this chunk
+  int64_t l2_block_slots;    // > 0: process the columns in blocks of this many slots, one after
+                             // another (hub and flat kernels of a block together), so the
+                             // gathered column block of X stays L2-resident across its reuse
   const int32_t* win_row;
   int64_t num_windows;
   int64_t heavy_thr;
@@ -1374,7 +1377,7 @@ gm_status launch_flat(const SpmmArgs& p0, int64_t ns, cudaStream_t st) {
   // an evict_last policy on the plain (unscaled, fresh) path when hinted
   const int lm = p0.stream_x == 0 ? 0 : (p0.src_class != nullptr && !p0.accum) ? 2 : 1;
   const bool epi = p0.carry != nullptr || p0.n_push > 0;
-  for (int64_t base = 0; base < ns; base += chunk) {
+  for (int64_t base = p0.slot_base; base < ns; base += chunk) {
     SpmmArgs p = p0;
     p.slot_base = base;
     p.slot_end = std::min<int64_t>(ns, base + chunk);
@@ -1443,7 +1446,7 @@ gm_status launch_light(const SpmmArgs& p0, int64_t ns, cudaStream_t st) {
   if (p0.gdeg_src == nullptr && ns > 8 && p0.flat_ok)
     return launch_flat<T, VB, MAXMIN>(p0, ns, st);
   // chunk columns so a lane holds <= 8 vectors; pick LPR/NV per chunk
-  for (int64_t base = 0; base < ns; base += 256) {
+  for (int64_t base = p0.slot_base; base < ns; base += 256) {
     SpmmArgs p = p0;
     p.slot_base = base;
     p.slot_end = std::min<int64_t>(ns, base + 256);
@@ -1480,7 +1483,7 @@ template <typename T, int VB, bool MAXMIN>
 gm_status launch_heavy(const SpmmArgs& p0, int64_t num_heavy, int64_t ns, cudaStream_t st) {
   using A = typename AccOf<T>::type;
   constexpr int64_t kChunk = 4 * kHeavyThreads;  // slots per column chunk (MH <= 4)
-  for (int64_t base = 0; base < ns; base += kChunk) {
+  for (int64_t base = p0.slot_base; base < ns; base += kChunk) {
     SpmmArgs p = p0;
     p.slot_base = base;
     p.slot_end = std::min<int64_t>(ns, base + kChunk);
@@ -1536,7 +1539,9 @@ inline bool hub_v1() {
 template <typename T, int VB, bool MAXMIN>
 gm_status launch_hubs(const SpmmArgs& p, int64_t num_heavy, int64_t ns, cudaStream_t st) {
   static const bool wide_v1 = [] { const char* e = getenv("GM_HUB_WIDE_V1"); return !e || atoi(e) != 0; }();
-  if (hub_v1() || (wide_v1 && p.f * static_cast<int64_t>(sizeof(T)) >= kWideRowBytes))
+  // column blocks (p.slot_base > 0 or a partial range) need the slot-ranged kernel
+  const bool ranged = p.slot_base > 0 || ns < p.f * static_cast<int64_t>(sizeof(T)) / VB;
+  if (hub_v1() || ranged || (wide_v1 && p.f * static_cast<int64_t>(sizeof(T)) >= kWideRowBytes))
     return launch_heavy<T, VB, MAXMIN>(p, num_heavy, ns, st);
   return launch_hub<T, VB, MAXMIN>(p, num_heavy, st);
 }
@@ -1544,6 +1549,18 @@ gm_status launch_hubs(const SpmmArgs& p, int64_t num_heavy, int64_t ns, cudaStre
 template <typename T, int VB>
 gm_status dispatch_vb(const SpmmArgs& p, bool maxmin, bool use_heavy, int64_t num_heavy,
                              int64_t ns, cudaStream_t st) {
+  if (p.l2_block_slots > 0 && p.l2_block_slots < ns) {
+    // L2 column blocking: one column block after another, each complete
+    // (every column's accumulation order is unchanged: results are identical)
+    for (int64_t b0 = 0; b0 < ns; b0 += p.l2_block_slots) {
+      SpmmArgs pb = p;
+      pb.slot_base = b0;
+      pb.l2_block_slots = 0;
+      const gm_status s = dispatch_vb<T, VB>(pb, maxmin, use_heavy, num_heavy, std::min(ns, b0 + p.l2_block_slots), st);
+      if (s != GM_OK) return s;
+    }
+    return GM_OK;
+  }
   if constexpr (VB >= 4) {
   if (use_heavy) {
     // profiling only (GM_PROF_SKIP=1: no hub kernel, 2: no light kernel) — results are incomplete

@@ -76,6 +76,10 @@ def spmm_line(name, kind, n, e, f, dtype, reduce):
     r = {"config": name, "reduce": reduce, "dtype": str(dtype).split(".")[-1], "nodes": n, "edges": e, "feats": f,
          "ms": ms, "gedges_s": e / ms / 1e6, "algo_gbs": byts / ms / 1e6, "frac_hbm": byts / ms / 1e6 / HBM,
          "csc_build_ms": build_ms, "heavy_rows": int(csc.plan().num_heavy)}
+    if os.environ.get("GM_AB_HASH"):  # bit hash of the output (same-box A/B of layout knobs)
+        o = gm.neighbor_aggregate(g, x, reduce, return_argmax=True)[0] if reduce in ("max", "min") else gm.spmm(g, x, None, reduce)
+        b = o.contiguous().view(torch.int32 if o.element_size() == 4 else torch.int16).to(torch.int64).flatten()
+        r["out_hash"] = int((b * torch.arange(1, b.numel() + 1, device=b.device, dtype=torch.int64) % 1000003).sum().item())
     print(json.dumps(r), flush=True)
     del g, x, csc
     torch.cuda.empty_cache()
@@ -208,6 +212,8 @@ if __name__ == "__main__":
         spmm_line("C4 ogbn-products", 1, 2_449_029, 61_859_140, 100, torch.float32, "max")
     if "C2" in which:
         spmm_line("C2 reddit", 1, 232_965, 114_615_892, 602, torch.float32, "mean")
+    if "C2X" in which:
+        spmm_line("C2 reddit", 1, 232_965, 114_615_892, 602, torch.float32, "max")
     if "C4B" in which:
         products_backward()
     if "C3L" in which:
