@@ -217,6 +217,9 @@ constexpr size_t scatter_smem_bytes() {
 
 // LAST: write perm / col (int32) and the sorted keys (for rowptr) instead of
 // the next pass's triples.
+#ifndef GM_RADIX_STCS  // intermediate passes: streaming (evict-first) stores of the next pass's triples
+#define GM_RADIX_STCS 1
+#endif
 #ifndef GM_RADIX_MINB
 #define GM_RADIX_MINB 4
 #endif
@@ -385,9 +388,15 @@ __global__ void __launch_bounds__(kThreads, GM_RADIX_MINB) radix_scatter_kernel(
       opos[o] = spos[s];  // perm
       oval[o] = sval[s];  // col
     } else {
+#if GM_RADIX_STCS
       __stcs(okey + o, key);
       __stcs(opos + o, spos[s]);
       __stcs(oval + o, sval[s]);
+#else
+      okey[o] = key;
+      opos[o] = spos[s];
+      oval[o] = sval[s];
+#endif
     }
   }
 }
