@@ -41,6 +41,17 @@ def _stream():
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+def _same_device(where: str, device, *tensors) -> None:
+    """Every kernel argument must live in the device memory of the index (or
+    of the first operand): a host tensor here would reach the kernels as a host
+    pointer. The reference has no devices; this is the mirror's own check."""
+    if device is None or device.type != "cuda":
+        raise ValueError(f"{where}: CUDA tensors required (got {device})")
+    for t in tensors:
+        if t is not None and t.device != device:
+            raise ValueError(f"{where}: all tensors must be on {device} (got {t.device})")
+
+
 def _dev_index(a, device) -> torch.Tensor:
     if isinstance(a, torch.Tensor):
         return a.to(device=device, dtype=torch.int64).contiguous()
@@ -364,6 +375,7 @@ def _run_spmm(grouping: CsrView, x: torch.Tensor, kind: str, w_csr: Optional[tor
               out: Optional[torch.Tensor] = None):
     if x.dtype not in _DT:
         raise ValueError(f"spmm: unsupported dtype {x.dtype}")
+    _same_device("spmm", grouping.rowptr.device, x, out, w_csr)
     x = x.contiguous()
     f = x.shape[1] if x.dim() == 2 else 1
     rows = grouping.num_rows() if num_rows is None else num_rows
@@ -400,6 +412,7 @@ def spmm(e: EdgeIndex, x: torch.Tensor, edge_weight: Optional[torch.Tensor], red
         raise ValueError("spmm: feature rows != num_src_nodes")
     if edge_weight is not None and edge_weight.numel() != e.num_edges():
         raise ValueError("spmm: edge weight length != num_edges")
+    _same_device("spmm", e.src().device, x, edge_weight)
     w_csr = None
     if edge_weight is not None:
         # Undirected + weights: the reference sweeps COO (message_passing.hpp:51-59),
@@ -427,6 +440,7 @@ def spmm_backward(e: EdgeIndex, x: torch.Tensor, edge_weight: Optional[torch.Ten
         raise ValueError("spmm_backward: grad_out must be [num_dst_nodes, F]")
     if edge_weight is not None and edge_weight.numel() != e.num_edges():
         raise ValueError("spmm: edge weight length != num_edges")
+    _same_device("spmm_backward", e.src().device, x, grad_out, edge_weight)
     lib = L.lib()
     g = grad_out.to(x.dtype).contiguous()
     f = g.shape[1]
@@ -469,6 +483,7 @@ def neighbor_aggregate(e: EdgeIndex, x: torch.Tensor, kind: str,
         raise ValueError(f"unknown aggregation kind: {kind}")
     if x.shape[0] != e.num_src_nodes():
         raise ValueError("propagate: h_src rows != num_src_nodes")
+    _same_device("neighbor_aggregate", e.src().device, x, edge_weight)
     # Undirected indices: sum/mean follow the reference's CSR order
     # (A = A^T, message_passing.hpp:47-85). max/min use the exact destination
     # grouping: the reference's dst_grouped_order would gather e.src()[perm]
@@ -499,6 +514,7 @@ def neighbor_aggregate_backward(e: EdgeIndex, kind: str, grad_out: torch.Tensor,
         raise ValueError("neighbor_aggregate_backward: grad_out must be [num_dst_nodes, F]")
     if tuple(argmax.shape) != tuple(grad_out.shape) or argmax.dtype != torch.int32:
         raise ValueError("neighbor_aggregate_backward: argmax must be int32 like grad_out")
+    _same_device("neighbor_aggregate_backward", e.src().device, grad_out, argmax)
     g = grad_out.contiguous()
     f = g.shape[1]
     view = e.source_view()
@@ -542,6 +558,7 @@ def gather_rows(src: torch.Tensor, index, name: str = "gather_rows:") -> torch.T
     tensor.hpp:489-495 (std::out_of_range naming the first bad position)."""
     if src.dim() < 1:
         raise ValueError("gather_rows: rank >= 1 required")
+    _same_device("gather_rows", src.device)
     n = src.shape[0]
     idx = index if isinstance(index, torch.Tensor) else torch.as_tensor(index)
     idx = idx.to(device=src.device)
@@ -581,6 +598,7 @@ def propagate(e: EdgeIndex, h_src: torch.Tensor, h_dst: torch.Tensor, edge_attr:
         raise ValueError("propagate: h_dst rows != num_dst_nodes")
     if edge_attr is not None and edge_attr.shape[0] != e.num_edges():
         raise ValueError("propagate: edge_attr rows != num_edges")
+    _same_device("propagate", e.src().device, h_src, h_dst, edge_attr)
     if path == SEGMENT_FUSED and callback is not None:
         raise ValueError("propagate: edge callbacks require the edge_materialize path")
     if path not in (EDGE_MATERIALIZE, SEGMENT_FUSED):
@@ -662,6 +680,7 @@ def gcn_layer(e: EdgeIndex, h: torch.Tensor, weight: torch.Tensor, bias: torch.T
         raise ValueError("matmul: inner dimension mismatch")
     if h.dtype not in (torch.float32, torch.bfloat16):
         raise ValueError("gcn_layer: f32 or bf16 features")
+    _same_device("gcn_layer", e.src().device, h, weight, bias)
     w = weight.to(h.dtype).unsqueeze(0)
     xw = segment_matmul(h, [0, h.shape[0]], w, out_dtype=h.dtype)
     return gcn_aggregate(e, xw, bias=bias, relu=relu)
@@ -682,6 +701,7 @@ def aggregate(values: torch.Tensor, index: torch.Tensor, num_groups: int, kind: 
     visited in ascending position, exactly the reference's scatter order."""
     if kind not in _KIND:
         raise ValueError(f"unknown aggregation kind: {kind}")
+    _same_device("aggregate", values.device)
     index = index.to(device=values.device, dtype=torch.int64).contiguous()
     if values.shape[0] != index.numel():
         raise ValueError("aggregate: values rows != index length")
@@ -714,6 +734,7 @@ def segment_matmul(x: torch.Tensor, ptr: Sequence[int], weights: torch.Tensor,
         raise ValueError(f"grouped_matmul: group count mismatch ({len(ptr) - 1} inputs, {groups} weight slabs)")
     if x.dim() != 2 or x.shape[1] != k:
         raise ValueError("grouped_matmul: inner dimension mismatch")
+    _same_device("grouped_matmul", x.device, weights)
     ptr = [int(p) for p in (ptr.tolist() if isinstance(ptr, torch.Tensor) else ptr)]
     if ptr[0] != 0 or any(b < a for a, b in zip(ptr, ptr[1:])):
         raise ValueError("grouped_matmul: segment offsets must start at 0 and be non-decreasing")
@@ -785,6 +806,7 @@ def grouped_matmul(inputs: Sequence[torch.Tensor], weights: torch.Tensor,
     for g, h in enumerate(inputs):
         if h.dim() != 2 or h.shape[1] != k:
             raise ValueError(f"grouped_matmul: group {g} inner dimension mismatch")
+    _same_device("grouped_matmul", weights.device, *inputs, *(out or []))
     dev = weights.device
     x32 = all(h.dtype == torch.float32 for h in inputs)
     if x32 and weights.dtype == torch.float32 and out_dtype in (None, torch.float32):

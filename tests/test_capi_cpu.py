@@ -125,3 +125,21 @@ def test_partition_rows_by_nnz():
         for p in range(1, parts):
             target = -(-rowptr[-1] * p // parts)
             assert cuts[p] == min(np.searchsorted(rowptr, target, "left"), deg.size) or cuts[p] == cuts[p - 1]
+
+
+def test_host_tensors_rejected_before_any_kernel_call():
+    """The Python mirror refuses host tensors (they would reach the kernels as
+    host pointers) with a ValueError, before the library is called."""
+    import pytest
+    import torch
+    import paper_2507_16991_b200 as gm
+    x = torch.zeros(4, 8)
+    w = torch.zeros(1, 8, 8)
+    with pytest.raises(ValueError, match="CUDA tensors required"):
+        gm.segment_matmul(x, [0, 4], w)
+    with pytest.raises(ValueError, match="CUDA tensors required"):
+        gm.grouped_matmul([x], w)
+    with pytest.raises(ValueError, match="CUDA tensors required"):
+        gm.gather_rows(x, torch.tensor([0, 1]))
+    with pytest.raises(ValueError, match="CUDA tensors required"):
+        gm.aggregate(x, torch.tensor([0, 1, 1, 0]), 2, "sum")

@@ -119,3 +119,21 @@ print('ok')
     env = dict(__import__('os').environ, GM_EDGE_DOT_SLICE=slice_kernel)
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_host_operands_rejected_on_a_device_index():
+    """A host tensor beside a device index fails loudly (ValueError) instead of
+    reaching a kernel as a host pointer."""
+    src = torch.tensor([0, 1, 2], device="cuda")
+    dst = torch.tensor([1, 2, 0], device="cuda")
+    g = gm.EdgeIndex(src, dst, 3, 3)
+    xh = torch.ones(3, 4)
+    with pytest.raises(ValueError, match="must be on cuda"):
+        gm.spmm(g, xh, None, "sum")
+    with pytest.raises(ValueError, match="must be on cuda"):
+        gm.neighbor_aggregate(g, xh, "max", return_argmax=True)
+    xd = torch.ones(3, 4, device="cuda")
+    with pytest.raises(ValueError, match="must be on cuda"):
+        gm.spmm_backward(g, xd, None, "sum", torch.ones(3, 4))
+    with pytest.raises(ValueError, match="must be on cuda"):
+        gm.gcn_layer(g, xd, torch.ones(4, 4), torch.zeros(4, device="cuda"))
