@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(32 * kColWarps) radix_colscan_kernel(int32_t* 
   const int64_t per = (rows + kColWarps - 1) / kColWarps;
   const int64_t t0 = min(rows, static_cast<int64_t>(w) * per), t1 = min(rows, t0 + per);
   int32_t s = 0;
+#pragma unroll 8
   for (int64_t t = t0; t < t1; ++t) s += table[t * bins + d];
   psum[w][lane] = s;
   __syncthreads();
@@ -162,7 +163,19 @@ __global__ void __launch_bounds__(32 * kColWarps) radix_colscan_kernel(int32_t* 
     all += c;
   }
   int32_t run = before;
-  for (int64_t t = t0; t < t1; ++t) {
+  // the rows' counts in flight 8 at a time (the column walk was latency-bound)
+  int64_t t = t0;
+  for (; t + 8 <= t1; t += 8) {
+    int32_t c[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c[i] = table[(t + i) * bins + d];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      table[(t + i) * bins + d] = run;
+      run += c[i];
+    }
+  }
+  for (; t < t1; ++t) {
     const int32_t c = table[t * bins + d];
     table[t * bins + d] = run;
     run += c;
