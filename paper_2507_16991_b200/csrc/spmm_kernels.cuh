@@ -1083,7 +1083,10 @@ __global__ void __launch_bounds__(kHeavyThreads) spmm_heavy_kernel(const SpmmArg
 // its `full` barrier, slots handed back through `empty`.
 // ---------------------------------------------------------------------------
 constexpr int kHubStage = 32;
-constexpr int kHubRing = 16;
+#ifndef GM_HUB_RING
+#define GM_HUB_RING 16
+#endif
+constexpr int kHubRing = GM_HUB_RING;
 constexpr int kHubMeta = 2 * kHubRing;
 
 template <typename T>
