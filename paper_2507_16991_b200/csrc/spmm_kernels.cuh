@@ -891,6 +891,19 @@ inline int flat_max_nv() {
   static const int nv = [] { const char* e = getenv("GM_FLAT_MAX_NV"); return e ? atoi(e) : 4; }();
   return nv;
 }
+// threads per flat CTA (GM_FLAT_THREADS, multiple of 32, <= 256): 4-warp CTAs
+// (8 per SM at 64 registers) lose only 4 warps per SM to a concurrent hub CTA
+// and finish the sweep with a finer tail. C4 sum, same box: 256 / 224 / 192 /
+// 160 / 128 / 96 threads 4.31 / 4.32 / 4.30 / 4.28 / 4.24 / 4.24 ms; the flat
+// kernel alone 4.15 -> 4.09 ms at 128
+inline int flat_threads() {
+  static const int t = [] {
+    const char* e = getenv("GM_FLAT_THREADS");
+    const int v = e ? atoi(e) : 128;
+    return (v >= 32 && v <= 256 && v % 32 == 0) ? v : 128;
+  }();
+  return t;
+}
 constexpr int kRing = 4;
 
 __device__ __forceinline__ void cp_async(void* smem, const void* gmem, int bytes) {
@@ -1386,29 +1399,30 @@ gm_status launch_flat(const SpmmArgs& p0, int64_t ns, cudaStream_t st) {
     p.slot_end = std::min<int64_t>(ns, base + chunk);
     const int64_t slots = p.slot_end - base;
     const int nv = slots <= 32 ? 1 : slots <= 64 ? 2 : slots <= 128 ? 4 : 8;
-    const unsigned grid = static_cast<unsigned>(ceil_div(p.num_light_windows * 32, 256));
+    const int tpb = flat_threads();
+    const unsigned grid = static_cast<unsigned>(ceil_div(p.num_light_windows * 32, tpb));
     if (grid == 0) continue;
 #define GM_FLAT_H(NV_, U_, M_, H_)                                                               \
   do {                                                                                           \
     if (p.accum) {                                                                               \
-      if (scaled) spmm_flat_kernel<T, VB, NV_, U_, M_, true, true, H_><<<grid, 256, 0, st>>>(p);    \
-      else spmm_flat_kernel<T, VB, NV_, U_, M_, false, true, H_><<<grid, 256, 0, st>>>(p);          \
-    } else if (scaled) spmm_flat_kernel<T, VB, NV_, U_, M_, true, false, H_><<<grid, 256, 0, st>>>(p); \
-    else spmm_flat_kernel<T, VB, NV_, U_, M_, false, false, H_><<<grid, 256, 0, st>>>(p);           \
+      if (scaled) spmm_flat_kernel<T, VB, NV_, U_, M_, true, true, H_><<<grid, tpb, 0, st>>>(p);    \
+      else spmm_flat_kernel<T, VB, NV_, U_, M_, false, true, H_><<<grid, tpb, 0, st>>>(p);          \
+    } else if (scaled) spmm_flat_kernel<T, VB, NV_, U_, M_, true, false, H_><<<grid, tpb, 0, st>>>(p); \
+    else spmm_flat_kernel<T, VB, NV_, U_, M_, false, false, H_><<<grid, tpb, 0, st>>>(p);           \
   } while (0)
 #define GM_FLAT_K(NV_, U_, M_)                                                                     \
   do {                                                                                             \
     if (epi) {  /* carry / push epilogue: unweighted layers, own instantiations */                  \
-      if (p.accum) spmm_flat_kernel<T, VB, NV_, U_, M_, false, true, 1, true><<<grid, 256, 0, st>>>(p);   \
-      else spmm_flat_kernel<T, VB, NV_, U_, M_, false, false, 1, true><<<grid, 256, 0, st>>>(p);          \
+      if (p.accum) spmm_flat_kernel<T, VB, NV_, U_, M_, false, true, 1, true><<<grid, tpb, 0, st>>>(p);   \
+      else spmm_flat_kernel<T, VB, NV_, U_, M_, false, false, 1, true><<<grid, tpb, 0, st>>>(p);          \
       break;                                                                                       \
     }                                                                                              \
     if (lm == 2) {                                                                                 \
-      if (scaled) spmm_flat_kernel<T, VB, NV_, U_, M_, true, false, 2><<<grid, 256, 0, st>>>(p);     \
-      else spmm_flat_kernel<T, VB, NV_, U_, M_, false, false, 2><<<grid, 256, 0, st>>>(p);           \
+      if (scaled) spmm_flat_kernel<T, VB, NV_, U_, M_, true, false, 2><<<grid, tpb, 0, st>>>(p);     \
+      else spmm_flat_kernel<T, VB, NV_, U_, M_, false, false, 2><<<grid, tpb, 0, st>>>(p);           \
     }                                                                                              \
     else if (lm == 1) GM_FLAT_H(NV_, U_, M_, 1);                                                   \
-    else if (!scaled && !p.accum) spmm_flat_kernel<T, VB, NV_, U_, M_, false, false, 0><<<grid, 256, 0, st>>>(p); \
+    else if (!scaled && !p.accum) spmm_flat_kernel<T, VB, NV_, U_, M_, false, false, 0><<<grid, tpb, 0, st>>>(p); \
     else GM_FLAT_H(NV_, U_, M_, 1);                                                                \
   } while (0)
 #define GM_FLAT(NV_, U_)                          \

@@ -78,8 +78,13 @@ def spmm_line(name, kind, n, e, f, dtype, reduce):
          "csc_build_ms": build_ms, "heavy_rows": int(csc.plan().num_heavy)}
     if os.environ.get("GM_AB_HASH"):  # bit hash of the output (same-box A/B of layout knobs)
         o = gm.neighbor_aggregate(g, x, reduce, return_argmax=True)[0] if reduce in ("max", "min") else gm.spmm(g, x, None, reduce)
-        b = o.contiguous().view(torch.int32 if o.element_size() == 4 else torch.int16).to(torch.int64).flatten()
-        r["out_hash"] = int((b * torch.arange(1, b.numel() + 1, device=b.device, dtype=torch.int64) % 1000003).sum().item())
+        bits = o.contiguous().view(torch.int32 if o.element_size() == 4 else torch.int16).flatten()
+        acc, step = 0, 1 << 26  # chunked: a C5 output is 14 G elements
+        for c0 in range(0, bits.numel(), step):
+            b = bits[c0:c0 + step].to(torch.int64)
+            idx = torch.arange(c0 + 1, c0 + 1 + b.numel(), device=b.device, dtype=torch.int64)
+            acc += int((b * idx % 1000003).sum().item())
+        r["out_hash"] = acc
     print(json.dumps(r), flush=True)
     del g, x, csc
     torch.cuda.empty_cache()
