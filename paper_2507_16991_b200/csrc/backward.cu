@@ -654,7 +654,13 @@ GM_API gm_status gm_edge_dot_csc(gm_dtype dtype, const gm_csr* csc, const gm_spm
     // 16-byte units (conflict-free float4 reads of 8 consecutive rows)
     int stride = static_cast<int>(std::min<int64_t>(f, 128));
     if ((stride / 4) % 2 == 0) stride += 4;
-    const size_t smem = sizeof(float) * kU * stride * 8;
+    // warps per CTA (GM_EDGE_DOT_WARPS: 8, 4 or 2; same box 6.56 / 6.53 / 6.52 ms)
+    static const int wpc = [] {
+      const char* ev = getenv("GM_EDGE_DOT_WARPS");
+      const int v = ev ? atoi(ev) : 2;
+      return (v == 4 || v == 8) ? v : 2;
+    }();
+    const size_t smem = sizeof(float) * kU * stride * wpc;
     GM_TRY_CUDA(cudaFuncSetAttribute(edge_dot_slice_kernel<kU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
     static const int64_t per_warp = [] { const char* ev = getenv("GM_EDGE_DOT_PER_WARP"); return ev ? atoll(ev) : 256; }();
@@ -667,7 +673,7 @@ GM_API gm_status gm_edge_dot_csc(gm_dtype dtype, const gm_csr* csc, const gm_spm
       limit = static_cast<int>(std::floor(4.0 * std::log2(1.0 + hot_rows)));
       if (plan->hot_edge_frac[std::min(limit, GM_PLAN_CLASSES - 1)] >= 0.15) cls = plan->src_class;
     }
-    edge_dot_slice_kernel<kU><<<static_cast<unsigned>(ceil_div(warps, 8)), 256, smem, st>>>(
+    edge_dot_slice_kernel<kU><<<static_cast<unsigned>(ceil_div(warps, wpc)), 32 * wpc, smem, st>>>(
         entry_rows - k0, csc->col, csc->perm, k0, csc->nnz, per_warp, static_cast<const float*>(a_by_dst),
         static_cast<const float*>(b_by_src), f, stride, static_cast<float*>(out), cls, limit);
     GM_CHECK_LAUNCH("edge_dot_slice_kernel");
