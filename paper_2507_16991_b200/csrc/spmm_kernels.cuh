@@ -1102,17 +1102,17 @@ constexpr int kHubStage = 32;
 constexpr int kHubRing = GM_HUB_RING;
 constexpr int kHubMeta = 2 * kHubRing;
 
-template <typename T>
-struct HubLane {  // per-lane storage unit: 4 bytes (f32, bf16x2) or 8 bytes (f64)
-  static constexpr int LE = sizeof(T) == 2 ? 2 : 1;
+template <typename T, int W = 1>
+struct HubLane {  // per-lane storage unit: 4 bytes (f32, bf16x2) or 8 bytes (f64, or f32 x2 with W = 2)
+  static constexpr int LE = (sizeof(T) == 2 ? 2 : 1) * W;
   static constexpr int LB = LE * static_cast<int>(sizeof(T));
   static constexpr int CB = 32 * LB;  // chunk bytes
   using R = typename std::conditional<LB == 8, unsigned long long, uint32_t>::type;
 };
 
-template <typename T>
+template <typename T, int W = 1>
 __host__ __device__ constexpr size_t hub_smem_bytes() {
-  return static_cast<size_t>(kHubRing) * kHubStage * HubLane<T>::CB;
+  return static_cast<size_t>(kHubRing) * kHubStage * HubLane<T, W>::CB;
 }
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -1137,11 +1137,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-template <typename T, int G, int MODE>  // MODE: 0 sum/mean, 2 max, 3 min
+template <typename T, int G, int MODE, int W = 1>  // MODE: 0 sum/mean, 2 max, 3 min; W: lane width x
 __global__ void __launch_bounds__(64) spmm_hub_kernel(const SpmmArgs p) {
   constexpr bool MAXMIN = MODE >= 2;
   constexpr bool IS_MIN = MODE == 3;
-  using HL = HubLane<T>;
+  using HL = HubLane<T, W>;
   using A = typename AccOf<T>::type;
   constexpr int LE = HL::LE;
   constexpr int LB = HL::LB;
@@ -1531,13 +1531,31 @@ gm_status launch_hub(const SpmmArgs& p, int64_t num_heavy, cudaStream_t st) {
   if constexpr (VB < 4) {
     return fail(GM_ERR_INVALID_ARGUMENT, "hub kernel needs >= 4-byte row alignment");
   } else {
-    constexpr int CB = HubLane<T>::CB;
     const int64_t row_bytes = p.f * static_cast<int64_t>(sizeof(T));
+    constexpr int GV = VB > 16 ? 16 : VB;
+    // A/B variant (GM_HUB_LANE8=1): fp32 rows of 8-byte multiples on 8-byte lanes
+    // (W = 2: half the CTAs per hub row). Bit-identical, but slower on C4: hub
+    // kernel alone 0.28 -> 0.44 ms, sum call 4.24 -> 4.39 ms (each CTA's chain
+    // of stages carries twice the copies; ring 8 no better)
+    if constexpr (sizeof(T) == 4 && VB >= 8) {
+      static const bool lane8 = [] { const char* e = getenv("GM_HUB_LANE8"); return e && atoi(e) != 0; }();
+      if (lane8) {
+        constexpr int CB2 = HubLane<T, 2>::CB;
+        const unsigned grid = static_cast<unsigned>(ceil_div(row_bytes, CB2) * num_heavy);
+        auto kern = !MAXMIN ? spmm_hub_kernel<T, GV, 0, 2>
+                    : p.is_min ? spmm_hub_kernel<T, GV, 3, 2> : spmm_hub_kernel<T, GV, 2, 2>;
+        gm_status s_ = ensure_smem(kern, hub_smem_bytes<T, 2>());
+        if (s_ != GM_OK) return s_;
+        kern<<<grid, 64, hub_smem_bytes<T, 2>(), st>>>(p);
+        GM_CHECK_LAUNCH("spmm_hub_kernel");
+        return GM_OK;
+      }
+    }
+    constexpr int CB = HubLane<T>::CB;
     const unsigned grid = static_cast<unsigned>(ceil_div(row_bytes, CB) * num_heavy);
-    // TMA bulk copies need 16-byte aligned rows (VB == 16: x and the row pitch)
-    auto kern = !MAXMIN ? spmm_hub_kernel<T, (VB > 16 ? 16 : VB), 0>
-                : p.is_min ? spmm_hub_kernel<T, (VB > 16 ? 16 : VB), 3>
-                           : spmm_hub_kernel<T, (VB > 16 ? 16 : VB), 2>;
+    auto kern = !MAXMIN ? spmm_hub_kernel<T, GV, 0>
+                : p.is_min ? spmm_hub_kernel<T, GV, 3>
+                           : spmm_hub_kernel<T, GV, 2>;
     gm_status s_ = ensure_smem(kern, hub_smem_bytes<T>());
     if (s_ != GM_OK) return s_;
     kern<<<grid, 64, hub_smem_bytes<T>(), st>>>(p);
