@@ -157,7 +157,9 @@ GM_API size_t gm_spmm_plan_bytes(int64_t num_rows, int64_t num_cols, int64_t nnz
 /* Builds the plan into `buffer` (device, gm_spmm_plan_bytes) and fills
  * *plan_host. On entry plan_host->heavy_threshold may raise the hub-row
  * threshold above the default 1024 (0 = default; rows >= 1 KB wide do best
- * with 4096). Synchronizes once (reads the heavy-row count). */
+ * with 4096) and plan_host->window_edges may fix the window size (0 = auto:
+ * 1024 entries, halved down to 256 until there are >= 8 waves of warps; rows
+ * >= 1 KB wide do best with 256). Synchronizes once (reads the heavy-row count). */
 GM_API gm_status gm_spmm_plan_build(const gm_csr* csr, void* buffer, size_t buffer_bytes,
                                     gm_spmm_plan* plan_host, gm_stream_t stream);
 

@@ -34,7 +34,21 @@ namespace gm {
 // ---------------------------------------------------------------------------
 // Plan: nnz+row balanced windows and the hub list.
 // ---------------------------------------------------------------------------
-constexpr int64_t kWindowCost = 256;    // edges + rows per light window
+// Window size (edges + rows per light window). Larger windows amortise each
+// warp's setup and row-boundary work; too few windows starve the machine. Auto:
+// 1024, halved (down to 256) until the sweep has >= 8 waves of resident warps
+// (148 SMs x 32). C4 same box, window 128 / 256 / 512 / 768 / 1024 / 2048 /
+// 4096: sum 4.28 / 4.24 / 4.22 / 4.21 / 4.20 / 4.21 / 4.34 ms; C5 79.0 -> 76.3
+// ms at 1024; the C3 relation SpMM (7.9 M entries) 0.60 -> 0.64 ms at 1024,
+// hence the wave floor. Rows >= 1 KB wide (C2) keep 256 (plan_host->window_edges,
+// set by the caller: C2 max 68.5 vs 70.1 ms at 1024).
+constexpr int64_t kMinWindowCost = 256;
+constexpr int64_t kMaxWindowCost = 1024;
+static int64_t auto_window_cost(int64_t num_rows, int64_t nnz) {
+  int64_t c = kMaxWindowCost;
+  while (c > kMinWindowCost && (nnz + num_rows) / c < int64_t{kNumSMs} * 32 * 8) c /= 2;
+  return c;
+}
 constexpr int64_t kHeavyThresholdDefault = 1024;
 // Rows longer than this go to the CTA-per-row hub kernel (GM_HEAVY_THR overrides; tuning only).
 static int64_t heavy_threshold() {
@@ -46,7 +60,7 @@ static int64_t heavy_threshold() {
 }
 
 __global__ void plan_windows_kernel(const int64_t* __restrict__ rowptr, int64_t num_rows,
-                                    int64_t num_windows, int32_t* __restrict__ win_row) {
+                                    int64_t num_windows, int64_t cost, int32_t* __restrict__ win_row) {
   const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (g > num_windows) return;
   if (g == num_windows) {
@@ -54,7 +68,7 @@ __global__ void plan_windows_kernel(const int64_t* __restrict__ rowptr, int64_t 
     return;
   }
   // rowptr may be a row slice of a larger CSR: offsets are relative to rowptr[0]
-  const int64_t target = g * kWindowCost + rowptr[0];
+  const int64_t target = g * cost + rowptr[0];
   // first r in [0, num_rows] with rowptr[r] + r >= target
   int64_t lo = 0, hi = num_rows;
   while (lo < hi) {
@@ -96,8 +110,8 @@ __global__ void src_class_kernel(const int32_t* __restrict__ col, int64_t nnz, c
     cls[k] = table[min(deg[col[k]], kDegBuckets - 1)];
 }
 
-static int64_t plan_num_windows(int64_t num_rows, int64_t nnz) {
-  return std::max<int64_t>(1, ceil_div(nnz + num_rows, kWindowCost));
+static int64_t plan_num_windows(int64_t num_rows, int64_t nnz, int64_t cost = kMinWindowCost) {
+  return std::max<int64_t>(1, ceil_div(nnz + num_rows, cost));
 }
 static int64_t plan_heavy_cap(int64_t num_rows, int64_t nnz) {
   return std::min<int64_t>(num_rows, nnz / heavy_threshold() + 1);
@@ -150,7 +164,11 @@ GM_API gm_status gm_spmm_plan_build(const gm_csr* csr, void* buffer, size_t buff
              "gm_spmm_plan_build: buffer too small (" + std::to_string(buffer_bytes) + " < " +
                  std::to_string(need) + ")");
   cudaStream_t st = as_stream(stream);
-  const int64_t g = plan_num_windows(csr->num_rows, csr->nnz);
+  // a caller-set window size (plan_host->window_edges > 0, clamped to [256, 4096]) or the auto rule;
+  // gm_spmm_plan_bytes sized every region for the smallest auto window
+  const int64_t cost = plan->window_edges > 0 ? std::min<int64_t>(4096, std::max<int64_t>(kMinWindowCost, plan->window_edges))
+                                              : auto_window_cost(csr->num_rows, csr->nnz);
+  const int64_t g = plan_num_windows(csr->num_rows, csr->nnz, cost);
   // a caller-set threshold (>= the default) selects fewer hub rows
   const int64_t thr = std::max<int64_t>(heavy_threshold(), plan->heavy_threshold);
   const int64_t cap = plan_heavy_cap(csr->num_rows, csr->nnz);
@@ -174,7 +192,7 @@ GM_API gm_status gm_spmm_plan_build(const gm_csr* csr, void* buffer, size_t buff
   uint8_t* cls = b;
 
   plan_windows_kernel<<<static_cast<unsigned>(ceil_div(g + 1, 256)), 256, 0, st>>>(
-      csr->rowptr, csr->num_rows, g, win_row);
+      csr->rowptr, csr->num_rows, g, cost, win_row);
   GM_CHECK_LAUNCH("plan_windows_kernel");
   GM_TRY_CUDA(cudaMemsetAsync(count, 0, sizeof(unsigned int), st));
   if (csr->num_rows > 0) {
@@ -227,7 +245,7 @@ GM_API gm_status gm_spmm_plan_build(const gm_csr* csr, void* buffer, size_t buff
     GM_TRY_CUDA(cudaStreamSynchronize(st));
   }
   plan->num_windows = g;
-  plan->window_edges = kWindowCost;
+  plan->window_edges = cost;
   plan->num_heavy = nh;
   plan->heavy_threshold = thr;
   plan->win_row = win_row;

@@ -84,9 +84,10 @@ class CsrView:
                         self.rowptr.data_ptr(), self.col.data_ptr(), self.perm.data_ptr())
 
     def plan(self, row_bytes: int = 0):
-        """Scheduling metadata (gm_spmm_plan), built once per hub-threshold
-        class and cached: rows >= 1 KB wide (F=602 fp32) raise the hub
-        threshold to 4096 in-edges, narrower rows keep the default 1024."""
+        """Scheduling metadata (gm_spmm_plan), built once per row-width class
+        and cached: rows >= 1 KB wide (F=602 fp32) raise the hub threshold to
+        4096 in-edges and keep 256-entry windows; narrower rows keep the
+        default 1024 threshold and the library's automatic window size."""
         thr = 4096 if row_bytes >= 1024 else 0
         if self._plan is None:
             self._plan = {}
@@ -96,6 +97,7 @@ class CsrView:
             buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=self.rowptr.device)
             plan = L.gm_spmm_plan()
             plan.heavy_threshold = thr
+            plan.window_edges = 256 if row_bytes >= 1024 else 0  # wide rows: short windows (0 = auto)
             csr = self.c_struct()
             L.check(lib.gm_spmm_plan_build(C.byref(csr), _p(buf), nbytes, C.byref(plan), _stream()),
                     "gm_spmm_plan_build")
