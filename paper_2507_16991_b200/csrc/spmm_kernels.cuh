@@ -1382,6 +1382,9 @@ inline gm_status ensure_smem(K kernel, size_t bytes) {
   return GM_OK;
 }
 
+#ifndef GM_FLAT_SUM_U  // edges per batch of the one-vector sum/mean sweep (16-byte lanes); C4: 6 / 8 / 10 / 12 -> 4.28 / 4.20 / 7.54 / 8.46 ms (10+ spill)
+#define GM_FLAT_SUM_U 8
+#endif
 template <typename T, int VB, bool MAXMIN>
 gm_status launch_flat(const SpmmArgs& p0, int64_t ns, cudaStream_t st) {
   const bool scaled = p0.w != nullptr;
@@ -1444,7 +1447,7 @@ gm_status launch_flat(const SpmmArgs& p0, int64_t ns, cudaStream_t st) {
     } else {
       if (nv == 1) {
         if constexpr (MAXMIN) GM_FLAT(1, GM_FLAT_MAX_U);
-        else GM_FLAT(1, 8);
+        else GM_FLAT(1, GM_FLAT_SUM_U);
       } else if (nv == 2) GM_FLAT(2, 4);
       else if (nv == 4 || kChunk <= 128) GM_FLAT(4, 2);
       else if constexpr (kChunk > 128) GM_FLAT(8, 1);
