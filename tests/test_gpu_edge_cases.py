@@ -137,3 +137,39 @@ def test_host_operands_rejected_on_a_device_index():
         gm.spmm_backward(g, xd, None, "sum", torch.ones(3, 4))
     with pytest.raises(ValueError, match="must be on cuda"):
         gm.gcn_layer(g, xd, torch.ones(4, 4), torch.zeros(4, device="cuda"))
+
+
+@pytest.mark.parametrize("reduce", ["sum", "max"])
+def test_window_size_is_pure_scheduling(reduce):
+    """gm_spmm_plan_build's window size (auto: 1024 entries halved to keep >= 8
+    waves of warps; or caller-set) changes scheduling only: the same output bits
+    (and argmax ids) for auto, 256 and 4096 entry windows."""
+    import ctypes as C
+    import bench
+    n, e, f = 100_000, 20_000_000, 36
+    stream = torch.cuda.current_stream().cuda_stream
+    g, x = bench.make_graph(gm, L, n, e, f, "cuda", stream)
+    csc = g.to_csc()
+    cs = csc.c_struct()
+    lib = L.lib()
+    nbytes = lib.gm_spmm_plan_bytes(cs.num_rows, cs.num_cols, cs.nnz)
+    outs = []
+    for win in (0, 256, 4096):
+        buf = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        plan = L.gm_spmm_plan()
+        plan.window_edges = win
+        L.check(lib.gm_spmm_plan_build(C.byref(cs), C.c_void_p(buf.data_ptr()), nbytes, C.byref(plan),
+                                       C.c_void_p(stream)))
+        # auto: (E + N) / 1024 = 19.6k windows < 8 waves (37,888 warps) -> 512
+        assert plan.window_edges == {0: 512, 256: 256, 4096: 4096}[win]
+        out = torch.empty(n, f, device="cuda")
+        arg = torch.empty(n, f, dtype=torch.int32, device="cuda") if reduce == "max" else None
+        L.check(lib.gm_spmm(C.byref(cs), C.byref(plan), L.GM_F32, C.c_void_p(x.data_ptr()), f, None, None,
+                            L.GM_MAX if reduce == "max" else L.GM_SUM, C.c_void_p(out.data_ptr()),
+                            C.c_void_p(arg.data_ptr()) if arg is not None else None, C.c_void_p(stream)))
+        torch.cuda.synchronize()
+        outs.append((out, arg))
+    for out, arg in outs[1:]:
+        assert torch.equal(out, outs[0][0])
+        if reduce == "max":
+            assert torch.equal(arg, outs[0][1])
